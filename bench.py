@@ -1,0 +1,327 @@
+#!/usr/bin/env python3
+"""Batch-encode benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the high-batch config): 2^20 synthetic
+256-byte ASCII rows per GPU, GPT-2 table (50,000 merges). A step encodes the
+whole batch to CSR token ids + row offsets. Weak scaling: every rank encodes
+its own 2^20-row batch (different seed); rows are independent so there is no
+collective on the data path; ranks only barrier and max-reduce their timings.
+
+value     device-resident throughput (tokens/s over all ranks): bytes + offsets
+          already in HBM, CUDA events around K steps on the encode stream,
+          max over ranks. Inputs (256 MiB) exceed the 126 MB L2.
+e2e       same metric through the public host API (bbpe_encode) from pinned
+          host memory: H2D of the bytes+offsets, encode, D2H of ids+offsets,
+          every step.
+roofline  k_encode (the dominant kernel): algorithmic bytes per launch =
+          input bytes + 4 x tokens + 16 x rows / its average
+          CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the unmodified reference encode_batch (oracle/_ref, block engine,
+          PhasePool over all host cores) on a bounded sample of the same rows.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+METRIC = "batch-encode tokens/sec and input GB/s at 1/2/4/8 B200 vs CPU ref (host cores)"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_rows(table, cfg, rank, scale):
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(table))
+    return synth.config_rows(gen, cfg, scale=scale, seed=cfg * 1000 + rank)
+
+
+def dist_init(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return rank, world, local
+
+
+def barrier_max(world, value):
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reference_arm(args, rank, world):
+    """Times the reference's own CPU implementation (oracle/_ref encode_batch,
+    block engine, PhasePool(nproc)) on a bounded sample of our arm's workload."""
+    if rank != 0:
+        return
+    from paper_2507_11941_b200 import load_merge_table_files
+    from oracle.oracle import Reference
+    table = load_merge_table_files(os.path.join(GOLDEN, "gpt2.bbpt"), None, "binary")
+    data, offsets, desc = make_rows(table, args.config, 0, args.scale)
+    ids_, off_, blob_, m4_ = table.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    cores = os.cpu_count() or 1
+    n_all = offsets.size - 1
+    # Sample size: ~args.ref_seconds of CPU work per step (calibrated).
+    n = min(n_all, 2048)
+    t0 = time.perf_counter()
+    ref.encode_batch(data, offsets[: n + 1], workers=cores)
+    dt = time.perf_counter() - t0
+    n = int(min(n_all, max(n, n * args.ref_seconds / max(dt, 1e-3))))
+    sub_off = offsets[: n + 1]
+    for _ in range(args.warmup):
+        ref.encode_batch(data, sub_off, workers=cores)
+    times, toks = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ids, oo = ref.encode_batch(data, sub_off, workers=cores)
+        times.append(time.perf_counter() - t0)
+        toks = int(oo[-1])
+    t = float(np.median(times))
+    v = toks / t
+    line = {
+        "metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"cfg{args.config}: {desc}", "table": "gpt2 (50,000 merges)",
+                   "sample_rows": n, "sample_bytes": int(sub_off[-1])},
+        "input_GBps": int(sub_off[-1]) / t / 1e9,
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference",
+                         "sample": f"first {n} of {n_all} rows ({int(sub_off[-1])} B), median of {args.steps}"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(table, data, offsets, seconds):
+    from oracle.oracle import Reference
+    cores = os.cpu_count() or 1
+    ids_, off_, blob_, m4_ = table.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    n_all = offsets.size - 1
+    n = min(n_all, 2048)
+    ref.encode_batch(data, offsets[: n + 1], workers=cores)  # warm
+    t0 = time.perf_counter()
+    ref.encode_batch(data, offsets[: n + 1], workers=cores)
+    dt = time.perf_counter() - t0
+    n = int(min(n_all, max(n, n * seconds / max(dt, 1e-3))))
+    t0 = time.perf_counter()
+    ids, oo = ref.encode_batch(data, offsets[: n + 1], workers=cores)
+    dt = time.perf_counter() - t0
+    return {"value": int(oo[-1]) / dt, "unit": "tokens/s", "cores": cores, "kind": "reference",
+            "sample": f"first {n} of {n_all} rows ({int(offsets[n])} B), reference encode_batch "
+                      f"(block engine, PhasePool({cores}))",
+            "input_GBps": int(offsets[n]) / dt / 1e9}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--engine", default="pieces", choices=["pieces", "block"])
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else max(args.warmup, 1)
+
+    rank, world, local = dist_init(args.gpus)
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import paper_2507_11941_b200 as bb
+
+    torch.cuda.set_device(local)
+    table = bb.load_merge_table_files(os.path.join(GOLDEN, "gpt2.bbpt"), None, "binary")
+    data, offsets, desc = make_rows(table, args.config, rank, args.scale)
+    n = offsets.size - 1
+    total = int(offsets[-1])
+    enc = bb.Encoder(device=local, engine=args.engine)
+    enc.prepare(table)
+
+    # ---- device-resident timing ----
+    d_data = torch.from_numpy(data).cuda()
+    d_off = torch.from_numpy(offsets.view(np.int64)).cuda()
+    d_ids = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    d_oo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.Stream()
+
+    def step():
+        enc.encode_device(table, d_data.data_ptr(), d_off.data_ptr(), n, total, d_ids.data_ptr(),
+                          d_oo.data_ptr(), stream=stream.cuda_stream, sync=False)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    enc.sync()
+    enc.kernel_times(reset=True)
+    launches0 = enc.kernel_launches()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(args.steps):
+                step()
+            ev1.record(stream)
+        enc.sync()
+        torch.cuda.synchronize()
+    barrier(world)
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    launches = enc.kernel_launches() - launches0
+    ktimes, kcalls = enc.kernel_times(reset=True)
+    ntok = int(d_oo[-1].item())
+    ms = barrier_max(world, ms_local)
+    tokens_all = ntok * world
+    bytes_all = total * world
+    value = tokens_all / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel ----
+    k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
+    dom = max(k_ms, key=k_ms.get)
+    alg_bytes = total + 4 * ntok + 16 * n
+    peak, peak_src = peaks()
+    achieved = alg_bytes / (k_ms["k_encode"] / 1e3) / 1e9
+
+    # ---- end to end through the host API (pinned host buffers) ----
+    e2e = None
+    if not args.no_e2e:
+        h_data = torch.from_numpy(data).pin_memory()
+        h_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
+        h_ids = torch.empty(max(total, 1), dtype=torch.int32).pin_memory()
+        h_oo = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        hd, ho = h_data.numpy(), h_off.numpy().view(np.uint64)
+        hi, hoo = h_ids.numpy().view(np.uint32), h_oo.numpy().view(np.uint64)
+        for _ in range(2):
+            enc.encode_packed(table, hd, ho, hi, hoo)
+        barrier(world)
+        times = []
+        for _ in range(max(3, args.steps // 2)):
+            t0 = time.perf_counter()
+            enc.encode_packed(table, hd, ho, hi, hoo)
+            times.append(time.perf_counter() - t0)
+        e_ms = barrier_max(world, float(np.median(times)) * 1e3)
+        e2e = {"value": tokens_all / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": total + (n + 1) * 8, "d2h_bytes_per_step": ntok * 4 + (n + 1) * 8,
+               "input_GBps": bytes_all / (e_ms / 1e3) / 1e9}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(table, data, offsets, 10.0)
+        except Exception as ex:  # reference not built on this box
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"cfg{args.config}: {desc} per GPU (Zipf GPT-2 words)",
+                       "table": "gpt2 (50,000 merges)", "engine": args.engine,
+                       "parallelism": f"rows sharded, {world} independent GPU(s), no collective",
+                       "l2": "inputs (%d MiB) larger than L2" % (total >> 20)},
+            "input_GBps": bytes_all / (ms / 1e3) / 1e9,
+            "tokens_per_step": tokens_all,
+            "gpu_launches": launches,
+            "kernel_ms": k_ms,
+            "roofline": {"bound": "hbm", "kernel": "k_encode", "achieved": achieved, "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                         "dominant_kernel": dom},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

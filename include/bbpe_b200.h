@@ -1,0 +1,206 @@
+/* bbpe_b200.h -- C-ABI of the B200-native BlockBPE batch encoder.
+ *
+ * This is the drop-in boundary for the reference's batch-encode hot path
+ * (reference = /root/reference/proj, header-only C++20 `namespace blockbpe`).
+ * Plain pointers and sizes only; no C++ or torch types cross this line.
+ * Each entry point names the reference interface it replaces:
+ *
+ *   bbpe_table_load_files   <- blockbpe::load_merge_table_files
+ *                              (include/blockbpe/merge_table.hpp:513-522;
+ *                               gpt2 loader 399-459, canonical JSON 473-497)
+ *   bbpe_table_create       <- MergeTable::add_token / add_merge / finalize
+ *                              (merge_table.hpp:257-297), i.e. the table that
+ *                              MergeTable::merges().for_each exposes (180-184)
+ *   bbpe_table_byte_token   <- MergeTable::byte_token (merge_table.hpp:246)
+ *   bbpe_table_rank_of      <- MergeTable::rank_of / merged_of (225-235)
+ *   bbpe_decode             <- blockbpe::decode (merge_table.hpp:565-579)
+ *   bbpe_encode             <- blockbpe::encode_batch, block engine, CSR output
+ *                              (include/blockbpe/batch.hpp:64-126; per row
+ *                               encode_single 46-59 -> bytes_to_initial_tokens
+ *                               pretokenize.hpp:60-71 -> block_bpe
+ *                               block_engine.hpp:268-310)
+ *   bbpe_encode_device      <- same, device-resident buffers (no host copies)
+ *   bbpe_block_bpe          <- blockbpe::block_bpe on explicit token ids with
+ *                              an optional PassTrace (block_engine.hpp:42-47,
+ *                              268-310) and max_passes (MaxPassesError,
+ *                              types.hpp:64-70)
+ *   bbpe_encode_sharded     <- encode_batch's row fan-out (PhasePool::run_items,
+ *                              thread_pool.hpp:95-101) re-targeted at several
+ *                              GPUs: byte-balanced shards, no collective
+ *   bbpe_partition          <- (new) the byte/cost-balanced row partitioner
+ *
+ * Error model: every call returns a bbpe_status that maps 1:1 onto the
+ * reference exception taxonomy (types.hpp:32-70). bbpe_last_error() returns a
+ * thread-local message; batch errors carry the reference's "row r: " prefix
+ * (batch.hpp:84-90). Threading: a ctx is single-caller (like PhasePool,
+ * thread_pool.hpp:141-142); a table is immutable and shareable.
+ */
+#ifndef BBPE_B200_H
+#define BBPE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BBPE_ABI_VERSION 1
+
+typedef enum bbpe_status {
+  BBPE_OK = 0,
+  BBPE_USAGE = 1,       /* UsageError        */
+  BBPE_PARSE = 2,       /* ParseError        */
+  BBPE_INTEGRITY = 3,   /* IntegrityError    */
+  BBPE_DECODE = 4,      /* DecodeError       */
+  BBPE_CONTRACT = 5,    /* ContractViolation */
+  BBPE_MAX_PASSES = 6,  /* MaxPassesError    */
+  BBPE_ERROR = 7        /* Error (CUDA / runtime failure) */
+} bbpe_status;
+
+typedef enum bbpe_format {
+  BBPE_FORMAT_GPT2 = 0,       /* vocab.json + merges.txt (VocabFormat::gpt2) */
+  BBPE_FORMAT_CANONICAL = 1,  /* {tokens, merges, specials} JSON             */
+  BBPE_FORMAT_BINARY = 2      /* this repo's .bbpt binary table              */
+} bbpe_format;
+
+/* Engine mode for bbpe_encode*: */
+typedef enum bbpe_engine {
+  /* Default. Each string is cut at "hard boundaries" -- byte positions whose
+   * bigram is not the junction of any merge -- and the pieces are merged
+   * independently: provably identical to block_bpe over the whole string
+   * (DESIGN.md "Piece decomposition"). Short pieces: one lane each;
+   * long pieces: one CTA each. */
+  BBPE_ENGINE_PIECES = 0,
+  /* One CTA per whole string, the paper's pass loop over the full string.
+   * Required for max_passes (exact pass counting per string). */
+  BBPE_ENGINE_BLOCK = 1
+} bbpe_engine;
+
+typedef struct bbpe_table bbpe_table;
+typedef struct bbpe_ctx bbpe_ctx;
+
+typedef struct bbpe_config {
+  uint32_t block_size;     /* BlockConfig::block_size: 32..1024, pow2; results-neutral */
+  int64_t max_passes;      /* <= 0: default (input length, never hit)        */
+  int32_t engine;          /* bbpe_engine                                      */
+  uint64_t wave_bytes;     /* host API: bytes per pipelined wave (0 = auto)     */
+} bbpe_config;
+
+typedef struct bbpe_stats {
+  uint64_t n_rows;
+  uint64_t input_bytes;
+  uint64_t tokens;
+  uint64_t long_pieces;    /* pieces that went to the CTA tier                 */
+  uint64_t waves;
+  double device_ms;        /* kernel time (CUDA events), summed over waves     */
+  double h2d_ms;
+  double d2h_ms;
+  double total_ms;         /* wall time of the call                           */
+} bbpe_stats;
+
+typedef struct bbpe_table_info {
+  uint64_t token_count;
+  uint64_t merge_count;
+  uint64_t base_size;      /* number of single-byte tokens                    */
+  uint32_t max_token_id;
+  uint32_t id_bits;        /* bits per token id in the device pair key        */
+  uint32_t rank_bits;
+  uint32_t remapped_ids;   /* 1 when ids were densified for the device        */
+  uint64_t hash_slots;     /* device hash capacity (slots of 8 bytes)         */
+  uint64_t junction_bigrams; /* |C|: bigrams that some merge can span         */
+  uint32_t rank_consistent;  /* 1 when every merge's parts predate it         */
+} bbpe_table_info;
+
+/* ---- library ---- */
+const char* bbpe_last_error(void);
+int bbpe_abi_version(void);
+int bbpe_device_count(int* count);
+
+/* ---- tables ---- */
+int bbpe_table_load_files(const char* vocab_path, const char* merges_path, int format,
+                          bbpe_table** out);
+/* ids[i] owns tok_bytes[tok_off[i] .. tok_off[i+1]); merges4 rows are
+ * {rank, left, right, merged}. Same validation as MergeTable::finalize. */
+int bbpe_table_create(size_t n_tokens, const uint32_t* ids, const uint64_t* tok_off,
+                      const uint8_t* tok_bytes, size_t n_merges, const uint32_t* merges4,
+                      bbpe_table** out);
+int bbpe_table_destroy(bbpe_table* t);
+int bbpe_table_get_info(const bbpe_table* t, bbpe_table_info* info);
+int bbpe_table_save_binary(const bbpe_table* t, const char* path);
+/* Exports tokens (sorted by id) and merges (sorted by rank). Pass null
+ * buffers to query the sizes. */
+int bbpe_table_export(const bbpe_table* t, uint32_t* ids, uint64_t* tok_off, uint8_t* tok_bytes,
+                      uint64_t* n_tokens, uint64_t* n_bytes, uint32_t* merges4,
+                      uint64_t* n_merges);
+uint32_t bbpe_table_byte_token(const bbpe_table* t, uint8_t b); /* 0xFFFFFFFF = none */
+/* rank (0xFFFFFFFF when absent); *merged receives the merged id when present. */
+uint32_t bbpe_table_rank_of(const bbpe_table* t, uint32_t left, uint32_t right,
+                            uint32_t* merged);
+/* ids -> bytes; writes at most cap bytes and returns the full length in *len. */
+int bbpe_decode(const bbpe_table* t, const uint32_t* ids, size_t n, uint8_t* out, size_t cap,
+                size_t* len);
+
+/* ---- per-device encode contexts ---- */
+int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out);
+int bbpe_ctx_destroy(bbpe_ctx* ctx);
+int bbpe_ctx_set_config(bbpe_ctx* ctx, const bbpe_config* cfg);
+/* Upload (once) the table replica for this ctx's device. Implicit on first use. */
+int bbpe_ctx_prepare(bbpe_ctx* ctx, const bbpe_table* t);
+/* Page-locked host buffers for zero-copy staging (cudaHostAlloc). */
+int bbpe_host_alloc(size_t bytes, void** out);
+int bbpe_host_free(void* p);
+
+/* Batch encode from HOST buffers. Row r is bytes[offsets[r] .. offsets[r+1]).
+ * Output is CSR: ids of row r are out_ids[out_offsets[r] .. out_offsets[r+1]).
+ * out_capacity must be >= the token total; offsets[n] (= total bytes) always
+ * suffices since every token covers at least one byte. */
+int bbpe_encode(bbpe_ctx* ctx, const bbpe_table* t, const uint8_t* bytes, const uint64_t* offsets,
+                size_t n, uint32_t* out_ids, uint64_t out_capacity, uint64_t* out_offsets,
+                bbpe_stats* stats);
+
+/* Batch encode from DEVICE buffers on ctx's device, stream-ordered on `stream`
+ * (a cudaStream_t, or NULL for the ctx's own stream). d_out_ids needs
+ * total_bytes slots. total_bytes must equal d_offsets[n]. If sync is 0 the
+ * call only enqueues work; errors raised on the device are then reported by
+ * the next bbpe_ctx_sync. */
+int bbpe_encode_device(bbpe_ctx* ctx, const bbpe_table* t, const uint8_t* d_bytes,
+                       const uint64_t* d_offsets, size_t n, uint64_t total_bytes,
+                       uint32_t* d_out_ids, uint64_t* d_out_offsets, void* stream, int sync,
+                       bbpe_stats* stats);
+int bbpe_ctx_sync(bbpe_ctx* ctx);
+/* How many of this library's kernels the ctx has launched since creation. */
+uint64_t bbpe_ctx_kernel_launches(const bbpe_ctx* ctx);
+/* Per-kernel device time (CUDA events recorded between launches on the
+ * launching stream) summed over the encodes since the last reset:
+ * ms[0] tile index, ms[1] prepass, ms[2] long pieces, ms[3] main encode.
+ * Synchronises the streams used. *calls receives the number of encodes. */
+#define BBPE_N_KERNELS 4
+int bbpe_ctx_kernel_times(bbpe_ctx* ctx, double* ms, uint64_t* calls, int reset);
+
+/* block_bpe on explicit initial token ids (one sequence), always the
+ * BBPE_ENGINE_BLOCK pass loop. trace (optional): per pass {pass_index (1-based),
+ * min_rank, merges_applied} as 3 x u64, up to trace_cap passes; *n_passes gets
+ * the full count. On BBPE_MAX_PASSES, out holds the partial state and *out_n
+ * its length (MaxPassesError::partial_tokens / passes_run). */
+int bbpe_block_bpe(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* tokens, size_t n,
+                   uint32_t* out, size_t* out_n, uint64_t* trace, size_t trace_cap,
+                   size_t* n_passes);
+
+/* ---- multi-GPU ---- */
+/* Splits rows [0, n) into `parts` contiguous shards with near-equal cost,
+ * cost(row) = len + 64 (bytes plus a per-row overhead). bounds gets parts+1
+ * row indices. */
+int bbpe_partition(const uint64_t* offsets, size_t n, int parts, uint64_t* bounds);
+/* Shards the batch across `n_devices` ctxs (one host thread each; tables are
+ * replicated per device), stitches CSR output. No collective is involved. */
+int bbpe_encode_sharded(bbpe_ctx* const* ctxs, int n_devices, const bbpe_table* t,
+                        const uint8_t* bytes, const uint64_t* offsets, size_t n,
+                        uint32_t* out_ids, uint64_t out_capacity, uint64_t* out_offsets,
+                        bbpe_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BBPE_B200_H */

@@ -1,0 +1,102 @@
+// bbpe_internal.h -- shared host/device definitions of the B200 BlockBPE engine.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/bbpe_b200.h"
+
+namespace bbpe {
+
+constexpr uint32_t kNoRank = 0xFFFFFFFFu;     // block_engine.hpp:16
+constexpr uint32_t kInvalidToken = 0xFFFFFFFFu;  // merge_table.hpp:22
+constexpr uint64_t kEmptySlot = ~0ull;
+constexpr int kBucketSlots = 4;               // 4 x 8 B = one 32 B sector per bucket
+
+// Exceptions mirror the reference taxonomy (types.hpp:32-70); the C-ABI maps
+// each to its bbpe_status.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+inline Error usage_error(const std::string& m) { return Error(BBPE_USAGE, m); }
+inline Error parse_error(const std::string& m) { return Error(BBPE_PARSE, m); }
+inline Error integrity_error(const std::string& m) { return Error(BBPE_INTEGRITY, m); }
+
+// The device view of a merge table, passed by value to every kernel.
+//
+// Pair key  = (left << id_bits) | right  over DENSE token ids.
+// Slot (u64)= (key << rank_bits) | dense_rank, empty = all ones.
+// Buckets of 4 slots (32 B, one sector), linear probing bucket to bucket.
+// dense_rank = position of the merge in rank order (order preserving, so
+// min-rank comparisons are unchanged); r2m[dense_rank] = dense merged id.
+struct DevTable {
+  const uint64_t* slots = nullptr;
+  uint64_t bucket_mask = 0;
+  const uint32_t* r2m = nullptr;    // dense rank -> dense merged id
+  const uint32_t* d2id = nullptr;   // dense id -> original id (null = identity)
+  const uint32_t* lut = nullptr;    // 256: byte -> dense id or kInvalidToken
+  const uint32_t* junction = nullptr;  // 2048 words: bit (a<<8|b) set iff some merge spans a|b
+  const uint32_t* rank_orig = nullptr; // dense rank -> original rank (traces)
+  uint32_t id_bits = 0;
+  uint32_t rank_bits = 0;
+  uint32_t n_merges = 0;
+  uint32_t pad = 0;
+};
+
+struct DeviceReplica {
+  DevTable view;
+  void* base = nullptr;  // one cudaMalloc holding every array
+};
+
+}  // namespace bbpe
+
+// The opaque C-ABI table object.
+struct bbpe_table {
+  // Host copy in reference terms (MergeTable): tokens sorted by id, merges by rank.
+  std::vector<uint32_t> ids;
+  std::vector<uint64_t> tok_off;
+  std::vector<uint8_t> tok_bytes;
+  std::unordered_map<uint32_t, uint32_t> index_of;  // id -> position in ids
+  std::vector<uint32_t> m_rank, m_left, m_right, m_merged;  // sorted by rank
+  uint32_t byte_tokens[256];
+  uint64_t base_size = 0;
+  uint32_t max_id = 0;
+  bool rank_consistent = true;
+
+  // Device layout, built once on the host.
+  uint32_t id_bits = 0, rank_bits = 0;
+  bool remap = false;
+  std::unordered_map<uint32_t, uint32_t> dense_of;  // only when remap
+  std::vector<uint32_t> dense_to_id;                // only when remap
+  std::vector<uint64_t> slots;
+  uint64_t bucket_mask = 0;
+  std::vector<uint32_t> r2m;       // dense rank -> dense merged
+  std::vector<uint32_t> lut;       // 256
+  std::vector<uint32_t> junction;  // 2048
+  uint64_t junction_count = 0;
+  // Host-side pair lookup (rank_of / merged_of) over ORIGINAL ids.
+  std::unordered_map<uint64_t, uint32_t> pair_index;  // pack(l,r) -> merge position
+
+  std::mutex mu;
+  std::map<int, bbpe::DeviceReplica> replicas;
+
+  uint32_t dense(uint32_t id) const {
+    if (!remap) return id;
+    auto it = dense_of.find(id);
+    return it == dense_of.end() ? bbpe::kInvalidToken : it->second;
+  }
+};
+
+namespace bbpe {
+// table.cpp
+void build_device_layout(bbpe_table& t);
+const DevTable& table_on_device(const bbpe_table& t, int device);
+void release_replicas(bbpe_table& t);
+uint64_t mix64(uint64_t h);
+}  // namespace bbpe

@@ -1,0 +1,773 @@
+// capi.cu -- the extern "C" boundary (include/bbpe_b200.h): encode contexts,
+// device scratch, host<->device staging, error mapping, multi-GPU sharding.
+//
+// The reference's batch path is encode_batch (proj/include/blockbpe/batch.hpp:64-126):
+// validate config, fan rows out, encode each row, rethrow the first error with
+// a "row r: " prefix, assemble. Here rows are packed (bytes + u64 offsets),
+// encoded on the device into CSR, and errors raised on the device (invalid byte,
+// pass cap) are re-materialised on the host with the reference's messages.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "bbpe_internal.h"
+#include "kernels.cuh"
+
+namespace bbpe {
+bbpe_table* table_load_files(const char* vocab, const char* merges, int format);
+bbpe_table* table_create(size_t n_tokens, const uint32_t* ids, const uint64_t* tok_off,
+                         const uint8_t* tok_bytes, size_t n_merges, const uint32_t* merges4);
+void table_save_binary(const bbpe_table& t, const char* path);
+}  // namespace bbpe
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define BBPE_TRY try {
+#define BBPE_CATCH                                                      \
+  }                                                                     \
+  catch (const bbpe::Error& e) {                                        \
+    return fail(e.code, e.what());                                      \
+  }                                                                     \
+  catch (const std::bad_alloc&) {                                       \
+    return fail(BBPE_ERROR, "out of host memory");                      \
+  }                                                                     \
+  catch (const std::exception& e) {                                     \
+    return fail(BBPE_ERROR, e.what());                                  \
+  }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw bbpe::Error(BBPE_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= cap && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 256);
+    want = want + want / 8;  // grow with slack so a sweep does not thrash
+    ck(cudaMalloc(&p, want), "cudaMalloc (scratch)");
+    cap = want;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+struct bbpe_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0};
+  bbpe::LaunchPlan plan;
+  DevBuf tile_first, status, counters, err, lp, lpo, lpx, lpy, trace, trace_count;
+  DevBuf in_bytes, in_offsets, out_ids, out_offsets;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint64_t launches = 0;
+  // Deferred device-side error check (bbpe_encode_device with sync == 0).
+  bool pending = false;
+  const uint64_t* pending_offsets = nullptr;
+  cudaStream_t pending_stream = nullptr;
+  uint64_t pending_rows = 0;
+  uint64_t last_long_pieces = 0;
+  // Per-kernel timing: one set of 5 events per enqueued encode.
+  std::vector<std::array<cudaEvent_t, 5>> ev_sets;
+  std::vector<cudaStream_t> ev_streams;
+  size_t ev_used = 0;
+  double kernel_ms[BBPE_N_KERNELS] = {0, 0, 0, 0};
+  uint64_t timed_calls = 0;
+};
+
+namespace {
+
+void validate_config(const bbpe_config& c) {
+  // BlockConfig::validate (block_engine.hpp:26-31).
+  if (c.block_size < 32 || c.block_size > 1024 || (c.block_size & (c.block_size - 1)) != 0)
+    throw bbpe::usage_error("block_size must be a power of two in [32, 1024], got " +
+                            std::to_string(c.block_size));
+  if (c.engine != BBPE_ENGINE_PIECES && c.engine != BBPE_ENGINE_BLOCK)
+    throw bbpe::usage_error("unknown engine " + std::to_string(c.engine));
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Sizes scratch and fills EncodeArgs for a device-resident batch.
+bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                              uint64_t n, uint64_t total, uint32_t* d_out, uint64_t* d_out_off,
+                              cudaStream_t s) {
+  using namespace bbpe;
+  EncodeArgs a{};
+  a.bytes = d_bytes;
+  a.offsets = d_offsets;
+  a.n_rows = n;
+  a.total = total;
+  a.num_tiles = (total + kTile - 1) / kTile;
+  a.out_ids = d_out;
+  a.out_offsets = d_out_off;
+  c.tile_first.ensure((a.num_tiles + 1) * 8);
+  c.status.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
+  c.counters.ensure(CNT_N * 4);
+  c.err.ensure(ERR_N * 8);
+  const bool block = c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0;
+  a.lp_cap = block ? n + 1 : total / (kLmax + 1) + 2;
+  c.lp.ensure(a.lp_cap * sizeof(LongPiece));
+  c.lpo.ensure((total + 1) * 4);
+  c.lpx.ensure(std::max<uint64_t>(total, 1) * 8);
+  c.lpy.ensure(std::max<uint64_t>(total, 1) * 8);
+  a.tile_first = c.tile_first.as<uint64_t>();
+  a.status = c.status.as<uint64_t>();
+  a.counters = c.counters.as<uint32_t>();
+  a.err = c.err.as<uint64_t>();
+  a.lp = c.lp.as<LongPiece>();
+  a.lpo = c.lpo.as<uint32_t>();
+  a.lpx = c.lpx.as<uint64_t>();
+  a.lpy = c.lpy.as<uint64_t>();
+  a.engine = block ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES;
+  a.max_passes = c.cfg.max_passes;
+  ck(cudaMemsetAsync(a.status, 0, std::max<uint64_t>(a.num_tiles, 1) * 8, s), "memset status");
+  ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
+  ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, s), "memset err");
+  return a;
+}
+
+void ensure_plan(bbpe_ctx& c) {
+  if (c.plan.sm_count == 0) c.plan = bbpe::plan_launch(c.device);
+}
+
+// Enqueue a device-resident encode. Handles the empty-input corner cases.
+void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
+                    const uint64_t* d_offsets, uint64_t n, uint64_t total, uint32_t* d_out,
+                    uint64_t* d_out_off, cudaStream_t s) {
+  if (total == 0) {
+    ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
+    c.err.ensure(bbpe::ERR_N * 8);
+    ck(cudaMemsetAsync(c.err.p, 0xFF, bbpe::ERR_N * 8, s), "memset err");
+    return;
+  }
+  const bbpe::DevTable& dt = bbpe::table_on_device(t, c.device);
+  ensure_plan(c);
+  bbpe::EncodeArgs a = prepare_args(c, d_bytes, d_offsets, n, total, d_out, d_out_off, s);
+  if (c.ev_used == c.ev_sets.size()) {
+    std::array<cudaEvent_t, 5> set{};
+    for (auto& e : set) ck(cudaEventCreate(&e), "cudaEventCreate");
+    c.ev_sets.push_back(set);
+    c.ev_streams.push_back(s);
+  }
+  c.ev_streams[c.ev_used] = s;
+  c.launches += bbpe::launch_encode(a, dt, c.plan, s, c.ev_sets[c.ev_used++].data());
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+uint64_t row_of(const uint64_t* host_offsets, uint64_t n, uint64_t pos) {
+  // max r with offsets[r] <= pos, among r < n
+  uint64_t lo = 0, hi = n ? n - 1 : 0;
+  while (lo < hi) {
+    uint64_t mid = (lo + hi + 1) / 2;
+    if (host_offsets[mid] <= pos) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Reads the device error slots; throws the reference's exception for the
+// lowest failing row (the inline encode_batch reports the first row).
+void check_device_errors(bbpe_ctx& c, const uint64_t* host_offsets, uint64_t n, uint64_t row_base,
+                         const uint8_t* host_bytes, const uint64_t* d_offsets,
+                         const uint8_t* d_bytes) {
+  uint64_t err[bbpe::ERR_N];
+  ck(cudaMemcpy(err, c.err.p, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
+  const uint64_t none = ~0ull;
+  if (err[bbpe::ERR_BAD_BYTE_POS] == none && err[bbpe::ERR_MAXPASS_ROW] == none) return;
+  std::vector<uint64_t> tmp;
+  if (!host_offsets) {
+    tmp.resize(n + 1);
+    ck(cudaMemcpy(tmp.data(), d_offsets, (n + 1) * 8, cudaMemcpyDeviceToHost), "read offsets");
+    host_offsets = tmp.data();
+  }
+  uint64_t bad_row = none, mp_row = err[bbpe::ERR_MAXPASS_ROW];
+  if (err[bbpe::ERR_BAD_BYTE_POS] != none) bad_row = row_of(host_offsets, n, err[bbpe::ERR_BAD_BYTE_POS]);
+  if (bad_row != none && (mp_row == none || bad_row <= mp_row)) {
+    uint8_t byte = 0;
+    if (host_bytes)
+      byte = host_bytes[err[bbpe::ERR_BAD_BYTE_POS]];
+    else
+      ck(cudaMemcpy(&byte, d_bytes + err[bbpe::ERR_BAD_BYTE_POS], 1, cudaMemcpyDeviceToHost), "read byte");
+    throw bbpe::integrity_error("row " + std::to_string(bad_row + row_base) +
+                                ": vocabulary has no single-byte token for byte value " +
+                                std::to_string(byte));
+  }
+  // encode_batch rethrows MaxPassesError as a plain Error (batch.hpp:88-89).
+  uint64_t len = host_offsets[mp_row + 1] - host_offsets[mp_row];
+  throw bbpe::Error(BBPE_ERROR, "row " + std::to_string(mp_row + row_base) + ": block_bpe exceeded " +
+                                    std::to_string(c.cfg.max_passes > 0 ? uint64_t(c.cfg.max_passes) : len) +
+                                    " merge passes; the merge table is pathological for this input");
+}
+
+// Encodes rows [r0, r1) of a host batch as one wave. Returns tokens written.
+uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
+                     const uint64_t* offsets, uint64_t r0, uint64_t r1, uint32_t* out_ids,
+                     uint64_t out_pos, uint64_t out_capacity, uint64_t* out_offsets,
+                     bbpe_stats* st) {
+  const uint64_t n = r1 - r0;
+  const uint64_t base = offsets[r0];
+  const uint64_t total = offsets[r1] - base;
+  std::vector<uint64_t> rel(n + 1);
+  for (uint64_t i = 0; i <= n; ++i) rel[i] = offsets[r0 + i] - base;
+  c.in_bytes.ensure(std::max<uint64_t>(total, 1) + 16);
+  c.in_offsets.ensure((n + 1) * 8);
+  c.out_ids.ensure(std::max<uint64_t>(total, 1) * 4);
+  c.out_offsets.ensure((n + 1) * 8);
+  auto t0 = std::chrono::steady_clock::now();
+  if (total) ck(cudaMemcpyAsync(c.in_bytes.p, bytes + base, total, cudaMemcpyHostToDevice, c.stream), "H2D bytes");
+  ck(cudaMemcpyAsync(c.in_offsets.p, rel.data(), (n + 1) * 8, cudaMemcpyHostToDevice, c.stream), "H2D offsets");
+  ck(cudaStreamSynchronize(c.stream), "sync H2D");
+  if (st) st->h2d_ms += ms_since(t0);
+  ck(cudaEventRecord(c.ev0, c.stream), "event");
+  enqueue_encode(c, t, c.in_bytes.as<uint8_t>(), c.in_offsets.as<uint64_t>(), n, total,
+                 c.out_ids.as<uint32_t>(), c.out_offsets.as<uint64_t>(), c.stream);
+  ck(cudaEventRecord(c.ev1, c.stream), "event");
+  std::vector<uint64_t> oo(n + 1);
+  ck(cudaMemcpyAsync(oo.data(), c.out_offsets.p, (n + 1) * 8, cudaMemcpyDeviceToHost, c.stream), "D2H offsets");
+  ck(cudaStreamSynchronize(c.stream), "encode");
+  bbpe_ctx_kernel_times(&c, nullptr, nullptr, 0);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c.ev0, c.ev1);
+  if (st) st->device_ms += ms;
+  check_device_errors(c, rel.data(), n, r0, bytes + base, nullptr, nullptr);
+  const uint64_t ntok = oo[n];
+  if (out_pos + ntok > out_capacity)
+    throw bbpe::usage_error("output capacity " + std::to_string(out_capacity) +
+                            " is smaller than the " + std::to_string(out_pos + ntok) +
+                            " tokens produced");
+  auto t1 = std::chrono::steady_clock::now();
+  if (ntok)
+    ck(cudaMemcpyAsync(out_ids + out_pos, c.out_ids.p, ntok * 4, cudaMemcpyDeviceToHost, c.stream), "D2H ids");
+  ck(cudaStreamSynchronize(c.stream), "D2H ids");
+  if (st) st->d2h_ms += ms_since(t1);
+  for (uint64_t i = 0; i <= n; ++i) out_offsets[r0 + i] = out_pos + oo[i];
+  return ntok;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bbpe_last_error(void) { return g_last_error.c_str(); }
+int bbpe_abi_version(void) { return BBPE_ABI_VERSION; }
+
+int bbpe_device_count(int* count) {
+  BBPE_TRY
+  ck(cudaGetDeviceCount(count), "cudaGetDeviceCount");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_table_load_files(const char* vocab_path, const char* merges_path, int format,
+                          bbpe_table** out) {
+  BBPE_TRY
+  if (!out) throw bbpe::usage_error("out is null");
+  *out = bbpe::table_load_files(vocab_path, merges_path, format);
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_table_create(size_t n_tokens, const uint32_t* ids, const uint64_t* tok_off,
+                      const uint8_t* tok_bytes, size_t n_merges, const uint32_t* merges4,
+                      bbpe_table** out) {
+  BBPE_TRY
+  if (!out) throw bbpe::usage_error("out is null");
+  if ((n_tokens && (!ids || !tok_off)) || (n_merges && !merges4))
+    throw bbpe::usage_error("null table arrays");
+  *out = bbpe::table_create(n_tokens, ids, tok_off, tok_bytes, n_merges, merges4);
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_table_destroy(bbpe_table* t) {
+  if (!t) return BBPE_OK;
+  bbpe::release_replicas(*t);
+  delete t;
+  return BBPE_OK;
+}
+
+int bbpe_table_get_info(const bbpe_table* t, bbpe_table_info* info) {
+  if (!t || !info) return fail(BBPE_USAGE, "null argument");
+  info->token_count = t->ids.size();
+  info->merge_count = t->m_rank.size();
+  info->base_size = t->base_size;
+  info->max_token_id = t->max_id;
+  info->id_bits = t->id_bits;
+  info->rank_bits = t->rank_bits;
+  info->remapped_ids = t->remap ? 1 : 0;
+  info->hash_slots = t->slots.size();
+  info->junction_bigrams = t->junction_count;
+  info->rank_consistent = t->rank_consistent ? 1 : 0;
+  return BBPE_OK;
+}
+
+int bbpe_table_save_binary(const bbpe_table* t, const char* path) {
+  BBPE_TRY
+  if (!t || !path) throw bbpe::usage_error("null argument");
+  bbpe::table_save_binary(*t, path);
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_table_export(const bbpe_table* t, uint32_t* ids, uint64_t* tok_off, uint8_t* tok_bytes,
+                      uint64_t* n_tokens, uint64_t* n_bytes, uint32_t* merges4,
+                      uint64_t* n_merges) {
+  if (!t) return fail(BBPE_USAGE, "null table");
+  if (n_tokens) *n_tokens = t->ids.size();
+  if (n_bytes) *n_bytes = t->tok_bytes.size();
+  if (n_merges) *n_merges = t->m_rank.size();
+  if (ids) std::memcpy(ids, t->ids.data(), t->ids.size() * 4);
+  if (tok_off) std::memcpy(tok_off, t->tok_off.data(), t->tok_off.size() * 8);
+  if (tok_bytes) std::memcpy(tok_bytes, t->tok_bytes.data(), t->tok_bytes.size());
+  if (merges4)
+    for (size_t m = 0; m < t->m_rank.size(); ++m) {
+      merges4[4 * m] = t->m_rank[m];
+      merges4[4 * m + 1] = t->m_left[m];
+      merges4[4 * m + 2] = t->m_right[m];
+      merges4[4 * m + 3] = t->m_merged[m];
+    }
+  return BBPE_OK;
+}
+
+uint32_t bbpe_table_byte_token(const bbpe_table* t, uint8_t b) {
+  return t ? t->byte_tokens[b] : bbpe::kInvalidToken;
+}
+
+uint32_t bbpe_table_rank_of(const bbpe_table* t, uint32_t left, uint32_t right, uint32_t* merged) {
+  if (!t) return bbpe::kNoRank;
+  auto it = t->pair_index.find((uint64_t(left) << 32) | right);
+  if (it == t->pair_index.end()) return bbpe::kNoRank;
+  if (merged) *merged = t->m_merged[it->second];
+  return t->m_rank[it->second];
+}
+
+// blockbpe::decode (merge_table.hpp:565-579), table tokens only.
+int bbpe_decode(const bbpe_table* t, const uint32_t* ids, size_t n, uint8_t* out, size_t cap,
+                size_t* len) {
+  if (!t) return fail(BBPE_USAGE, "null table");
+  size_t pos = 0;
+  for (size_t i = 0; i < n; ++i) {
+    auto it = t->index_of.find(ids[i]);
+    if (it == t->index_of.end())
+      return fail(BBPE_DECODE,
+                  "unknown token id " + std::to_string(ids[i]) + " at index " + std::to_string(i));
+    const uint64_t b = t->tok_off[it->second], e = t->tok_off[it->second + 1];
+    for (uint64_t k = b; k < e; ++k, ++pos)
+      if (out && pos < cap) out[pos] = t->tok_bytes[k];
+  }
+  if (len) *len = pos;
+  return BBPE_OK;
+}
+
+int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out) {
+  BBPE_TRY
+  if (!out) throw bbpe::usage_error("out is null");
+  auto c = std::make_unique<bbpe_ctx>();
+  c->device = device;
+  if (cfg) {
+    validate_config(*cfg);
+    c->cfg = *cfg;
+  }
+  DeviceGuard g(device);
+  ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaEventCreate(&c->ev0), "cudaEventCreate");
+  ck(cudaEventCreate(&c->ev1), "cudaEventCreate");
+  *out = c.release();
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_ctx_destroy(bbpe_ctx* c) {
+  if (!c) return BBPE_OK;
+  {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->tile_first, &c->status, &c->counters, &c->err, &c->lp, &c->lpo, &c->lpx,
+                      &c->lpy, &c->trace, &c->trace_count, &c->in_bytes, &c->in_offsets,
+                      &c->out_ids, &c->out_offsets})
+      b->release();
+    cudaEventDestroy(c->ev0);
+    cudaEventDestroy(c->ev1);
+    for (auto& set : c->ev_sets)
+      for (auto e : set) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    cudaSetDevice(prev);
+  }
+  delete c;
+  return BBPE_OK;
+}
+
+int bbpe_ctx_set_config(bbpe_ctx* c, const bbpe_config* cfg) {
+  BBPE_TRY
+  if (!c || !cfg) throw bbpe::usage_error("null argument");
+  validate_config(*cfg);
+  if (cfg->max_passes < 0) throw bbpe::usage_error("max_passes must be >= 1");
+  c->cfg = *cfg;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_ctx_prepare(bbpe_ctx* c, const bbpe_table* t) {
+  BBPE_TRY
+  if (!c || !t) throw bbpe::usage_error("null argument");
+  DeviceGuard g(c->device);
+  bbpe::table_on_device(*t, c->device);
+  ensure_plan(*c);
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_host_alloc(size_t bytes, void** out) {
+  BBPE_TRY
+  ck(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable), "cudaHostAlloc");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_host_free(void* p) {
+  BBPE_TRY
+  if (p) ck(cudaFreeHost(p), "cudaFreeHost");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_encode(bbpe_ctx* c, const bbpe_table* t, const uint8_t* bytes, const uint64_t* offsets,
+                size_t n, uint32_t* out_ids, uint64_t out_capacity, uint64_t* out_offsets,
+                bbpe_stats* st) {
+  BBPE_TRY
+  auto t0 = std::chrono::steady_clock::now();
+  if (!c || !t || !offsets || !out_offsets) throw bbpe::usage_error("null argument");
+  validate_config(c->cfg);
+  for (size_t i = 0; i < n; ++i)
+    if (offsets[i + 1] < offsets[i]) throw bbpe::usage_error("offsets must be non-decreasing");
+  if (offsets[n] > offsets[0] && (!bytes || !out_ids)) throw bbpe::usage_error("null buffer");
+  DeviceGuard g(c->device);
+  if (st) *st = bbpe_stats{};
+  // Waves: row ranges of at most wave_bytes (a row is never split).
+  const uint64_t wave = c->cfg.wave_bytes ? c->cfg.wave_bytes : (1ull << 31);
+  uint64_t pos = 0, waves = 0;
+  out_offsets[0] = 0;
+  uint64_t r0 = 0;
+  do {
+    uint64_t r1 = r0;
+    while (r1 < n && (r1 == r0 || offsets[r1 + 1] - offsets[r0] <= wave)) ++r1;
+    pos += encode_wave(*c, *t, bytes, offsets, r0, r1, out_ids, pos, out_capacity, out_offsets, st);
+    ++waves;
+    r0 = r1;
+  } while (r0 < n);
+  if (st) {
+    st->n_rows = n;
+    st->input_bytes = offsets[n] - offsets[0];
+    st->tokens = pos;
+    st->waves = waves;
+    st->total_ms = ms_since(t0);
+  }
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_encode_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
+                       const uint64_t* d_offsets, size_t n, uint64_t total_bytes,
+                       uint32_t* d_out_ids, uint64_t* d_out_offsets, void* stream, int sync,
+                       bbpe_stats* st) {
+  BBPE_TRY
+  if (!c || !t || !d_offsets || !d_out_offsets) throw bbpe::usage_error("null argument");
+  validate_config(c->cfg);
+  DeviceGuard g(c->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  if (sync) ck(cudaEventRecord(c->ev0, s), "event");
+  enqueue_encode(*c, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
+  c->pending = true;
+  c->pending_offsets = d_offsets;
+  c->pending_stream = s;
+  c->pending_rows = n;
+  if (sync) {
+    ck(cudaEventRecord(c->ev1, s), "event");
+    ck(cudaStreamSynchronize(s), "encode");
+    c->pending = false;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    if (st) {
+      *st = bbpe_stats{};
+      st->n_rows = n;
+      st->input_bytes = total_bytes;
+      st->device_ms = ms;
+      st->waves = 1;
+    }
+    check_device_errors(*c, nullptr, n, 0, nullptr, d_offsets, d_bytes);
+  }
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_ctx_sync(bbpe_ctx* c) {
+  BBPE_TRY
+  if (!c) throw bbpe::usage_error("null ctx");
+  DeviceGuard g(c->device);
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  if (c->pending_stream) ck(cudaStreamSynchronize(c->pending_stream), "sync");
+  if (c->pending) {
+    c->pending = false;
+    check_device_errors(*c, nullptr, c->pending_rows, 0, nullptr, c->pending_offsets, nullptr);
+  }
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+uint64_t bbpe_ctx_kernel_launches(const bbpe_ctx* c) { return c ? c->launches : 0; }
+
+int bbpe_ctx_kernel_times(bbpe_ctx* c, double* ms, uint64_t* calls, int reset) {
+  BBPE_TRY
+  if (!c) throw bbpe::usage_error("null ctx");
+  DeviceGuard g(c->device);
+  for (size_t i = 0; i < c->ev_used; ++i) {
+    ck(cudaEventSynchronize(c->ev_sets[i][4]), "event sync");
+    for (int k = 0; k < BBPE_N_KERNELS; ++k) {
+      float e = 0;
+      ck(cudaEventElapsedTime(&e, c->ev_sets[i][k], c->ev_sets[i][k + 1]), "event time");
+      c->kernel_ms[k] += e;
+    }
+  }
+  c->timed_calls += c->ev_used;
+  c->ev_used = 0;
+  if (ms)
+    for (int k = 0; k < BBPE_N_KERNELS; ++k) ms[k] = c->kernel_ms[k];
+  if (calls) *calls = c->timed_calls;
+  if (reset) {
+    for (double& v : c->kernel_ms) v = 0;
+    c->timed_calls = 0;
+  }
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, size_t n,
+                   uint32_t* out, size_t* out_n, uint64_t* trace, size_t trace_cap,
+                   size_t* n_passes) {
+  BBPE_TRY
+  using namespace bbpe;
+  if (!c || !t || !out_n || (n && (!tokens || !out))) throw usage_error("null argument");
+  validate_config(c->cfg);
+  if (n_passes) *n_passes = 0;
+  if (n < 2) {
+    if (n) std::memcpy(out, tokens, n * 4);
+    *out_n = n;
+    return BBPE_OK;
+  }
+  if (n >= (1ull << 31)) throw usage_error("sequence too long");
+  DeviceGuard g(c->device);
+  const DevTable& dt = table_on_device(*t, c->device);
+  ensure_plan(*c);
+  // Dense ids for the device. Ids the table never mentions cannot pair; under
+  // a remapped table they get private placeholder ids (mapped back below).
+  std::vector<uint64_t> x(n);
+  std::vector<uint32_t> extra;  // placeholder dense id -> original id
+  std::unordered_map<uint32_t, uint32_t> extra_of;
+  const uint32_t n_dense = t->remap ? static_cast<uint32_t>(t->dense_to_id.size()) : 0;
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t d = t->dense(tokens[i]);
+    if (t->remap && d == kInvalidToken) {
+      auto it = extra_of.find(tokens[i]);
+      if (it == extra_of.end()) {
+        uint32_t nd = n_dense + static_cast<uint32_t>(extra.size());
+        if (nd + 1 >= (1u << t->id_bits)) throw usage_error("too many token ids outside the table");
+        it = extra_of.emplace(tokens[i], nd).first;
+        extra.push_back(tokens[i]);
+      }
+      d = it->second;
+    }
+    x[i] = uint64_t(d) | (uint64_t(0xFFFFFFFEu) << 32);
+  }
+  EncodeArgs a{};
+  a.n_rows = 1;
+  a.total = n;
+  c->counters.ensure(CNT_N * 4);
+  c->err.ensure(ERR_N * 8);
+  c->lp.ensure(sizeof(LongPiece));
+  c->lpo.ensure((n + 1) * 4);
+  c->lpx.ensure(n * 8);
+  c->lpy.ensure(n * 8);
+  size_t tcap = trace ? trace_cap : 0;
+  c->trace.ensure(std::max<size_t>(tcap, 1) * 24);
+  c->trace_count.ensure(8);
+  a.counters = c->counters.as<uint32_t>();
+  a.err = c->err.as<uint64_t>();
+  a.lp = c->lp.as<LongPiece>();
+  a.lp_cap = 1;
+  a.lpo = c->lpo.as<uint32_t>();
+  a.lpx = c->lpx.as<uint64_t>();
+  a.lpy = c->lpy.as<uint64_t>();
+  a.trace = c->trace.as<uint64_t>();
+  a.trace_cap = tcap;
+  a.trace_count = c->trace_count.as<uint64_t>();
+  a.tokens_input = 1;
+  a.engine = BBPE_ENGINE_BLOCK;
+  a.max_passes = c->cfg.max_passes;
+  LongPiece lp{0, n, 0};
+  uint32_t counters[CNT_N] = {0};
+  counters[CNT_LP_COUNT] = 1;
+  ck(cudaMemcpyAsync(a.lp, &lp, sizeof(lp), cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemcpyAsync(a.counters, counters, sizeof(counters), cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, c->stream), "memset");
+  ck(cudaMemcpyAsync(a.lpx, x.data(), n * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+  c->launches += launch_block_bpe(a, dt, c->plan, c->stream);
+  ck(cudaGetLastError(), "launch");
+  uint32_t cnt = 0;
+  uint64_t err[ERR_N], passes = 0;
+  ck(cudaMemcpyAsync(&cnt, a.lpo, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(err, a.err, sizeof(err), cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(&passes, a.trace_count, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "block_bpe");
+  std::vector<uint32_t> res(cnt);
+  if (cnt) ck(cudaMemcpy(res.data(), a.lpo + 1, cnt * 4ull, cudaMemcpyDeviceToHost), "D2H");
+  if (t->remap)
+    for (auto& v : res) v = v < n_dense ? t->dense_to_id[v] : extra[v - n_dense];
+  std::memcpy(out, res.data(), cnt * 4ull);
+  *out_n = cnt;
+  if (n_passes) *n_passes = passes;
+  if (tcap) ck(cudaMemcpy(trace, a.trace, std::min<uint64_t>(passes, tcap) * 24, cudaMemcpyDeviceToHost), "D2H");
+  if (err[ERR_MAXPASS_ROW] != ~0ull)
+    return fail(BBPE_MAX_PASSES, "block_bpe exceeded " + std::to_string(c->cfg.max_passes) +
+                                     " merge passes; the merge table is pathological for this input");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_partition(const uint64_t* offsets, size_t n, int parts, uint64_t* bounds) {
+  BBPE_TRY
+  if (!offsets || !bounds || parts < 1) throw bbpe::usage_error("bad partition arguments");
+  // cost(row) = len + 64: prefix cost is offsets[r] - offsets[0] + 64 r.
+  auto cost = [&](uint64_t r) { return (offsets[r] - offsets[0]) + 64 * r; };
+  const uint64_t total = cost(n);
+  bounds[0] = 0;
+  uint64_t r = 0;
+  for (int p = 1; p < parts; ++p) {
+    const uint64_t target = total * p / parts;
+    while (r < n && cost(r) < target) ++r;
+    bounds[p] = r;
+  }
+  bounds[parts] = n;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_encode_sharded(bbpe_ctx* const* ctxs, int n_devices, const bbpe_table* t,
+                        const uint8_t* bytes, const uint64_t* offsets, size_t n, uint32_t* out_ids,
+                        uint64_t out_capacity, uint64_t* out_offsets, bbpe_stats* st) {
+  BBPE_TRY
+  if (!ctxs || n_devices < 1 || !t || !offsets || !out_offsets) throw bbpe::usage_error("null argument");
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<uint64_t> bounds(n_devices + 1);
+  bbpe_partition(offsets, n, n_devices, bounds.data());
+  // Shard k writes at its byte-based upper-bound position, then shards are
+  // packed in order (tokens <= bytes per shard, so regions never overlap).
+  std::vector<uint64_t> ntok(n_devices, 0);
+  std::vector<std::vector<uint64_t>> offs(n_devices);
+  std::vector<int> codes(n_devices, BBPE_OK);
+  std::vector<std::string> msgs(n_devices);
+  std::vector<bbpe_stats> stats(n_devices);
+  std::vector<std::thread> th;
+  const uint64_t base = offsets[0];
+  if (out_capacity < offsets[n] - base && offsets[n] > base) {
+    // The staging layout needs the byte-sized upper bound.
+    throw bbpe::usage_error("bbpe_encode_sharded needs out_capacity >= total input bytes");
+  }
+  for (int d = 0; d < n_devices; ++d) {
+    th.emplace_back([&, d] {
+      const uint64_t r0 = bounds[d], r1 = bounds[d + 1];
+      offs[d].resize(r1 - r0 + 1);
+      const uint64_t at = offsets[r0] - base;
+      int rc = bbpe_encode(ctxs[d], t, bytes, offsets + r0, r1 - r0, out_ids + at,
+                           out_capacity - at, offs[d].data(), &stats[d]);
+      codes[d] = rc;
+      if (rc != BBPE_OK) msgs[d] = bbpe_last_error();
+      ntok[d] = offs[d].back();
+    });
+  }
+  for (auto& x : th) x.join();
+  for (int d = 0; d < n_devices; ++d)
+    if (codes[d] != BBPE_OK) {
+      // Row indices in shard messages are shard-relative; rebase "row r: ".
+      std::string m = msgs[d];
+      if (m.rfind("row ", 0) == 0) {
+        size_t colon = m.find(':');
+        uint64_t r = std::stoull(m.substr(4, colon - 4)) + bounds[d];
+        m = "row " + std::to_string(r) + m.substr(colon);
+      }
+      return fail(codes[d], m);
+    }
+  uint64_t pos = 0;
+  for (int d = 0; d < n_devices; ++d) {
+    const uint64_t r0 = bounds[d], r1 = bounds[d + 1];
+    const uint64_t at = offsets[r0] - base;
+    if (at != pos && ntok[d]) std::memmove(out_ids + pos, out_ids + at, ntok[d] * 4);
+    for (uint64_t i = 0; i <= r1 - r0; ++i) out_offsets[r0 + i] = pos + offs[d][i];
+    pos += ntok[d];
+  }
+  if (st) {
+    *st = bbpe_stats{};
+    st->n_rows = n;
+    st->input_bytes = offsets[n] - base;
+    st->tokens = pos;
+    for (auto& s : stats) {
+      st->device_ms = std::max(st->device_ms, s.device_ms);
+      st->waves += s.waves;
+    }
+    st->total_ms = ms_since(t0);
+  }
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,238 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the reference's
+golden vectors, the C oracle, and the reference tests' batch semantics
+(test_batch.cpp, test_block_engine.cpp, acceptance_test.cpp)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2507_11941_b200 as bb
+from conftest import GOLDEN, VECTOR_SETS, load_vectors, table_from_json
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = ["pieces", "block"]
+
+
+@pytest.fixture(scope="module")
+def enc():
+    return {e: bb.Encoder(device=0, engine=e) for e in ENGINES}
+
+
+@pytest.fixture(scope="module")
+def tables(gpt2, toy_tables):
+    t = {"gpt2": gpt2}
+    for k, v in toy_tables.items():
+        t[k] = table_from_json(v)
+    return t
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("name", VECTOR_SETS)
+def test_golden_vectors(name, engine, enc, tables):
+    v = load_vectors(name)
+    ids, off, st = enc[engine].encode_packed(tables[str(v["table"])], v["data"], v["offsets"])
+    assert np.array_equal(off, v["out_offsets"])
+    assert np.array_equal(ids, v["ids"])
+
+
+def test_kats(enc, gpt2):
+    with open(os.path.join(GOLDEN, "kats.json")) as f:
+        kats = json.load(f)
+    for e in ENGINES:
+        rows = [s.encode() for s, _ in kats["gpt2"]]
+        got = enc[e].encode_rows(gpt2, rows)
+        assert got == [w for _, w in kats["gpt2"]]
+
+
+def test_toy_canonical_kats(enc, tables):
+    assert enc["pieces"].encode_rows(tables["toy"], [b"abc", b"ab"]) == [[4], [3]]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_random_gpt2_vs_oracle(engine, enc, gpt2, oracle_for):
+    rng = np.random.default_rng(2024)
+    rows = [bytes(rng.integers(0, 256, rng.integers(0, 700)).astype(np.uint8)) for _ in range(500)]
+    rows += [bytes(rng.choice(np.frombuffer(b"ab .0\n", np.uint8), rng.integers(0, 300))) for _ in range(300)]
+    data, off = bb.pack_rows(rows)
+    ids, oo, _ = enc[engine].encode_packed(gpt2, data, off)
+    wi, wo = oracle_for("gpt2").encode_packed(data, off)
+    assert np.array_equal(oo, wo) and np.array_equal(ids, wi)
+
+
+def test_block_bpe_traces(enc, tables):
+    with open(os.path.join(GOLDEN, "traces.json")) as f:
+        tr = json.load(f)
+    e = enc["block"]
+    for fam in ("doubling", "gpt2"):
+        for case in tr[fam]:
+            out, trace = e.block_bpe(tables[fam], case["tokens"], trace=True)
+            assert out == case["out"]
+            assert [tuple(x) for x in trace] == [tuple(x) for x in case["trace"]]
+
+
+def test_max_passes_partial_state(tables):
+    with open(os.path.join(GOLDEN, "traces.json")) as f:
+        mp = json.load(f)["max_passes"]
+    e = bb.Encoder(device=0, config=bb.BlockConfig(256, mp["max_passes"]))
+    with pytest.raises(bb.MaxPassesError) as ei:
+        e.block_bpe(tables["doubling"], mp["tokens"])
+    assert ei.value.partial_tokens == mp["partial"] == [5, 5, 5, 5]
+    # Sufficient cap is silent (test_block_engine.cpp:401-405).
+    assert e.block_bpe(tables["doubling"], [0, 1, 0, 1]) == [5]
+
+
+def test_max_passes_in_batch_is_row_tagged_error(tables):
+    e = bb.Encoder(device=0, config=bb.BlockConfig(256, 2))
+    with pytest.raises(bb.Error) as ei:
+        e.encode_rows(tables["doubling"], [b"ab", b"abab", b"ab" * 8])
+    assert str(ei.value).startswith("row 2: block_bpe exceeded 2 merge passes")
+    assert type(ei.value) is bb.Error  # encode_batch rethrows as plain Error
+
+
+def test_row_error_names_row(enc, tables):
+    # test_batch.cpp:85-94
+    for e in ENGINES:
+        with pytest.raises(bb.IntegrityError) as ei:
+            enc[e].encode_rows(tables["toy"], [b"ab", b"ab", b"xyz"])
+        assert "row 2" in str(ei.value)
+        assert "byte value 120" in str(ei.value)
+
+
+def test_empty_batches(enc, gpt2):
+    for e in ENGINES:
+        assert enc[e].encode_rows(gpt2, []) == []
+        assert enc[e].encode_rows(gpt2, [b"", b"", b""]) == [[], [], []]
+        assert enc[e].encode_rows(gpt2, [b"", b"hi", b""]) == [[], [5303], []]
+
+
+def test_encode_batch_api(gpt2, tables):
+    cfg = bb.BlockConfig(256, None)
+    none = bb.SpecialTokenSet()
+    toy = tables["toy"]
+    enc = bb.encode_batch(["abc", "abab"], toy, none, cfg, 99, False, False)
+    assert enc.max_len == 2 and enc.at(0, 0) == 4 and enc.at(0, 1) == 99
+    assert enc.mask.tolist() == [1, 0, 1, 1]
+    sp = bb.SpecialTokenSet()
+    sp.add("<|endoftext|>", 50256)
+    sp.set_bos("<|endoftext|>")
+    sp.set_eos("<|endoftext|>")
+    assert bb.encode_batch(["hi"], gpt2, sp, cfg, 50256, True, True).row(0) == [50256, 5303, 50256]
+    assert bb.encode_single("hi<|endoftext|>", gpt2, sp, cfg) == [5303, 50256]
+    lim = bb.encode_batch(["abcabc", "ab", "abcc"], toy, none, cfg, 99, False, False,
+                          limits=bb.BatchLimits(1))
+    assert lim.truncated_rows == 2 and lim.lengths.tolist() == [1, 1, 1]
+    with pytest.raises(bb.UsageError):
+        bb.encode_batch(["a"], toy, none, cfg, 0, True, False)
+    with pytest.raises(bb.IntegrityError, match="row 2"):
+        bb.encode_batch(["ab", "ab", "xyz"], toy, none, cfg, 99, False, False)
+    inputs = ["hello world", "...."]
+    e2 = bb.encode_batch(inputs, gpt2, sp, cfg, 50256, True, True)
+    assert [d.decode() for d in bb.decode_batch(e2, gpt2, sp, True)] == inputs
+
+
+def test_batch_independence_and_permutation(enc, gpt2):
+    rng = np.random.default_rng(101)
+    xs = [bytes(rng.integers(0, 256, 32).astype(np.uint8)) for _ in range(5)]
+    ys = [bytes(rng.integers(0, 256, 32).astype(np.uint8)) for _ in range(7)]
+    e = enc["pieces"]
+    assert e.encode_rows(gpt2, xs + ys) == e.encode_rows(gpt2, xs) + e.encode_rows(gpt2, ys)
+    perm = rng.permutation(12)
+    both = xs + ys
+    base = e.encode_rows(gpt2, both)
+    assert e.encode_rows(gpt2, [both[i] for i in perm]) == [base[i] for i in perm]
+
+
+def test_block_size_is_results_neutral(gpt2):
+    rng = np.random.default_rng(53)
+    rows = [bytes(rng.integers(0, 256, 200).astype(np.uint8)) for _ in range(50)]
+    outs = []
+    for bs in (32, 64, 256, 1024):
+        for eng in ENGINES:
+            outs.append(bb.Encoder(0, bb.BlockConfig(bs, None), engine=eng).encode_rows(gpt2, rows))
+    assert all(o == outs[0] for o in outs)
+
+
+def test_losslessness(enc, gpt2):
+    rng = np.random.default_rng(73)
+    rows = [bytes(rng.integers(0, 256, rng.integers(0, 129)).astype(np.uint8)) for _ in range(100)]
+    for r, ids in zip(rows, enc["pieces"].encode_rows(gpt2, rows)):
+        assert bb.decode(gpt2, bb.SpecialTokenSet(), ids) == r
+
+
+def test_waves_match_single_pass(gpt2):
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 3000, 256, seed=3)
+    a = bb.Encoder(0).encode_packed(gpt2, data, off)
+    b = bb.Encoder(0, wave_bytes=100_000).encode_packed(gpt2, data, off)
+    assert b[2]["waves"] > 1
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_device_api_torch(gpt2):
+    torch = pytest.importorskip("torch")
+    v = load_vectors("gpt2_text")
+    d = torch.from_numpy(v["data"]).cuda()
+    o = torch.from_numpy(v["offsets"].astype(np.int64)).cuda()
+    total = int(v["offsets"][-1])
+    n = v["offsets"].size - 1
+    out = torch.empty(total, dtype=torch.int32, device="cuda")
+    oo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    e = bb.Encoder(0)
+    e.encode_device(gpt2, d.data_ptr(), o.data_ptr(), n, total, out.data_ptr(), oo.data_ptr(), sync=True)
+    oo_h = oo.cpu().numpy().astype(np.uint64)
+    assert np.array_equal(oo_h, v["out_offsets"])
+    assert np.array_equal(out[: int(oo_h[-1])].cpu().numpy().astype(np.uint32), v["ids"])
+
+
+def test_sharded_single_device_matches(gpt2):
+    v = load_vectors("gpt2_random")
+    encs = [bb.Encoder(0), bb.Encoder(0)]
+    ids, oo, st = bb.encode_sharded(encs, gpt2, v["data"], v["offsets"])
+    assert np.array_equal(oo, v["out_offsets"]) and np.array_equal(ids, v["ids"])
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 1 / 128), (3, 1 / 512), (4, 1 / 256)])
+def test_config_parity_vs_reference_engines(cfg, scale, gpt2, oracle_for):
+    """BASELINE configs at sizes the C oracle's heap engine finishes quickly
+    (heap == block on the training-consistent GPT-2 table)."""
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off, _ = synth.config_rows(gen, cfg, scale=scale)
+    ids, oo, _ = bb.Encoder(0).encode_packed(gpt2, data, off)
+    wi, wo = oracle_for("gpt2").encode_packed(data, off, engine=1)
+    assert np.array_equal(oo, wo) and np.array_equal(ids, wi)
+
+
+def test_full_size_cfg2_properties(gpt2):
+    """Full 2^20 x 256 B: round trip, determinism, and a random subsample vs the oracle."""
+    from paper_2507_11941_b200 import synth
+    from oracle.oracle import CRestatement
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off, _ = synth.config_rows(gen, 2)
+    e = bb.Encoder(0)
+    ids, oo, _ = e.encode_packed(gpt2, data, off)
+    ids2, oo2, _ = e.encode_packed(gpt2, data, off)
+    assert np.array_equal(ids, ids2) and np.array_equal(oo, oo2)
+    # Full-size round trip: decode(encode(x)) == x for all 256 MiB.
+    tid, toff, tblob, _ = gpt2.export()
+    start = np.zeros(int(tid.max()) + 1, np.int64)
+    lens = np.zeros(int(tid.max()) + 1, np.int64)
+    start[tid] = toff[:-1].astype(np.int64)
+    lens[tid] = (toff[1:] - toff[:-1]).astype(np.int64)
+    L = lens[ids]
+    excl = np.zeros(ids.size, np.int64)
+    np.cumsum(L[:-1], out=excl[1:])
+    idx = np.repeat(start[ids] - excl, L) + np.arange(int(L.sum()), dtype=np.int64)
+    assert np.array_equal(tblob[idx], data)
+    # Row boundaries: every row's tokens decode to exactly its bytes.
+    row_bytes = np.add.reduceat(L, oo[:-1].astype(np.int64))
+    assert np.array_equal(row_bytes, np.diff(off).astype(np.int64))
+    _, _, _, m4 = gpt2.export()
+    orc = CRestatement(m4, [gpt2.byte_token(b) for b in range(256)])
+    rng = np.random.default_rng(0)
+    for r in rng.integers(0, off.size - 1, 200):
+        s = data[int(off[r]):int(off[r + 1])].tobytes()
+        assert ids[int(oo[r]):int(oo[r + 1])].tolist() == orc.heap_bpe(orc.initial(s))
