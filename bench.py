@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-merge-only", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else max(args.warmup, 1)
 
@@ -259,12 +260,38 @@ def main():
     bytes_all = total * world
     value = tokens_all / (ms / 1e3)
 
+    # ---- the same, merge passes only (piece memo off), for reference ----
+    merge_only = None
+    if args.engine == "pieces" and not args.no_merge_only:
+        enc.set_config(piece_memo=False)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                step()
+        enc.sync()
+        enc.kernel_times(reset=True)
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+        enc.sync()
+        torch.cuda.synchronize()
+        mo_ms = barrier_max(world, e0.elapsed_time(e1) / args.steps)
+        kt, kc = enc.kernel_times(reset=True)
+        assert int(d_oo[-1].item()) == ntok
+        merge_only = {"value": tokens_all / (mo_ms / 1e3), "unit": "tokens/s", "ms_per_step": mo_ms,
+                      "kernel_ms": {k: v / max(kc, 1) for k, v in kt.items()}}
+        enc.set_config(piece_memo=True)
+
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
     dom = max(k_ms, key=k_ms.get)
     alg_bytes = total + 4 * ntok + 16 * n
     peak, peak_src = peaks()
-    achieved = alg_bytes / (k_ms["k_encode"] / 1e3) / 1e9
+    achieved = alg_bytes / (k_ms["k_pieces"] / 1e3) / 1e9
 
     # ---- end to end through the host API (pinned host buffers) ----
     e2e = None
@@ -309,12 +336,13 @@ def main():
             "tokens_per_step": tokens_all,
             "gpu_launches": launches,
             "kernel_ms": k_ms,
-            "roofline": {"bound": "hbm", "kernel": "k_encode", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": "k_pieces", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "alg_bytes_per_launch": alg_bytes,
                          "dominant_kernel": dom},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "merge_only": merge_only,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

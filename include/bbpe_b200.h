@@ -85,6 +85,11 @@ typedef struct bbpe_config {
   int64_t max_passes;      /* <= 0: default (input length, never hit)        */
   int32_t engine;          /* bbpe_engine                                      */
   uint64_t wave_bytes;     /* host API: bytes per pipelined wave (0 = auto)     */
+  int32_t piece_memo;      /* 1 (default): whole pieces equal to a vocabulary
+                              token's bytes take that token's precomputed
+                              encoding (exact; built from the table by this
+                              engine on first use per device). 0: always run
+                              the merge passes. Ignored by BBPE_ENGINE_BLOCK. */
 } bbpe_config;
 
 typedef struct bbpe_stats {
@@ -173,9 +178,10 @@ int bbpe_ctx_sync(bbpe_ctx* ctx);
 uint64_t bbpe_ctx_kernel_launches(const bbpe_ctx* ctx);
 /* Per-kernel device time (CUDA events recorded between launches on the
  * launching stream) summed over the encodes since the last reset:
- * ms[0] tile index, ms[1] prepass, ms[2] long pieces, ms[3] main encode.
- * Synchronises the streams used. *calls receives the number of encodes. */
-#define BBPE_N_KERNELS 4
+ * ms[0] k_tile_first, ms[1] k_pieces, ms[2] k_long_pieces, ms[3] k_tile_scan,
+ * ms[4] k_gather. Synchronises the streams used. *calls receives the number
+ * of encodes. */
+#define BBPE_N_KERNELS 5
 int bbpe_ctx_kernel_times(bbpe_ctx* ctx, double* ms, uint64_t* calls, int reset);
 
 /* block_bpe on explicit initial token ids (one sequence), always the

@@ -23,6 +23,7 @@ class Config(C.Structure):
         ("max_passes", C.c_int64),
         ("engine", C.c_int32),
         ("wave_bytes", C.c_uint64),
+        ("piece_memo", C.c_int32),
     ]
 
 

@@ -368,11 +368,12 @@ class Encoder:
     """One encode context on one GPU (bbpe_ctx). Single-caller, like PhasePool."""
 
     def __init__(self, device: int = 0, config: Optional[BlockConfig] = None, engine: str = "pieces",
-                 wave_bytes: int = 0):
+                 wave_bytes: int = 0, piece_memo: bool = True):
         self.device = device
         self.config = config or BlockConfig()
         self.engine = engine
         self.wave_bytes = wave_bytes
+        self.piece_memo = piece_memo
         self._h = C.c_void_p()
         _check(LIB.bbpe_ctx_create(device, C.byref(self._cfg()), C.byref(self._h)))
 
@@ -380,15 +381,19 @@ class Encoder:
         self.config.validate()
         if self.engine not in ENGINES:
             raise UsageError(f'unknown engine "{self.engine}"')
-        return Config(self.config.block_size, self.config.max_passes or 0, ENGINES[self.engine], self.wave_bytes)
+        return Config(self.config.block_size, self.config.max_passes or 0, ENGINES[self.engine], self.wave_bytes,
+                      1 if self.piece_memo else 0)
 
-    def set_config(self, config: BlockConfig = None, engine: str = None, wave_bytes: int = None):
+    def set_config(self, config: BlockConfig = None, engine: str = None, wave_bytes: int = None,
+                   piece_memo: bool = None):
         if config is not None:
             self.config = config
         if engine is not None:
             self.engine = engine
         if wave_bytes is not None:
             self.wave_bytes = wave_bytes
+        if piece_memo is not None:
+            self.piece_memo = piece_memo
         _check(LIB.bbpe_ctx_set_config(self._h, C.byref(self._cfg())))
 
     def __del__(self):
@@ -407,12 +412,12 @@ class Encoder:
     def kernel_launches(self) -> int:
         return LIB.bbpe_ctx_kernel_launches(self._h)
 
-    KERNELS = ("k_tile_first", "k_prepass", "k_long_pieces", "k_encode")
+    KERNELS = ("k_tile_first", "k_pieces", "k_long_pieces", "k_tile_scan", "k_gather")
 
     def kernel_times(self, reset: bool = True) -> Tuple[dict, int]:
         """Per-kernel device ms (CUDA events on the launching stream) summed
         over the encodes since the last reset, and the number of encodes."""
-        ms = (C.c_double * 4)()
+        ms = (C.c_double * len(self.KERNELS))()
         calls = C.c_uint64()
         _check(LIB.bbpe_ctx_kernel_times(self._h, ms, C.byref(calls), 1 if reset else 0))
         return dict(zip(self.KERNELS, list(ms))), calls.value

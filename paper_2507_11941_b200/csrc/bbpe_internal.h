@@ -9,6 +9,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "../../include/bbpe_b200.h"
 
 namespace bbpe {
@@ -43,15 +45,46 @@ struct DevTable {
   const uint32_t* lut = nullptr;    // 256: byte -> dense id or kInvalidToken
   const uint32_t* junction = nullptr;  // 2048 words: bit (a<<8|b) set iff some merge spans a|b
   const uint32_t* rank_orig = nullptr; // dense rank -> original rank (traces)
+  // Piece memo (optional): exact encodings of whole pieces that equal a
+  // vocabulary token's bytes, computed by this engine at table upload.
+  const struct MemoEntry* memo = nullptr;
+  uint64_t memo_mask = 0;
   uint32_t id_bits = 0;
   uint32_t rank_bits = 0;
   uint32_t n_merges = 0;
   uint32_t pad = 0;
 };
 
+// 32-byte memo entry: piece bytes (zero padded), length, 1-2 result tokens
+// (dense ids). len == 0 marks an empty slot.
+constexpr int kMemoMaxLen = 20;
+struct MemoEntry {
+  uint32_t w[5];
+  uint8_t len;
+  uint8_t nres;
+  uint16_t pad;
+  uint32_t res[2];
+};
+static_assert(sizeof(MemoEntry) == 32, "memo entry is one sector");
+
+// Hash of a piece given as 5 little-endian words (bytes past len are zero).
+__host__ __device__ inline uint32_t memo_hash(const uint32_t* w, uint32_t len) {
+  uint32_t h = 0x9E3779B9u ^ len;
+  for (int i = 0; i < 5; ++i) {
+    h ^= w[i];
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 15;
+  }
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
 struct DeviceReplica {
   DevTable view;
   void* base = nullptr;  // one cudaMalloc holding every array
+  void* memo = nullptr;  // memo slots (separate allocation)
+  int memo_state = 0;    // 0 not built, 1 building, 2 built (or not applicable)
 };
 
 }  // namespace bbpe
@@ -72,6 +105,7 @@ struct bbpe_table {
   // Device layout, built once on the host.
   uint32_t id_bits = 0, rank_bits = 0;
   bool remap = false;
+  bool narrow = false;  // 16-bit device working arrays suffice
   std::unordered_map<uint32_t, uint32_t> dense_of;  // only when remap
   std::vector<uint32_t> dense_to_id;                // only when remap
   std::vector<uint64_t> slots;
@@ -97,6 +131,7 @@ namespace bbpe {
 // table.cpp
 void build_device_layout(bbpe_table& t);
 const DevTable& table_on_device(const bbpe_table& t, int device);
+DeviceReplica& replica_of(const bbpe_table& t, int device);  // after table_on_device
 void release_replicas(bbpe_table& t);
 uint64_t mix64(uint64_t h);
 }  // namespace bbpe

@@ -97,9 +97,10 @@ bool is_pinned(const void* p) {
 struct bbpe_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0};
+  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1};
   bbpe::LaunchPlan plan;
-  DevBuf tile_first, status, counters, err, lp, lpo, lpx, lpy, trace, trace_count;
+  DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
+  DevBuf staging, tile_count, tile_lrec, lrec, tile_base;
   DevBuf in_bytes, in_offsets, out_ids, out_offsets;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
@@ -110,10 +111,10 @@ struct bbpe_ctx {
   uint64_t pending_rows = 0;
   uint64_t last_long_pieces = 0;
   // Per-kernel timing: one set of 5 events per enqueued encode.
-  std::vector<std::array<cudaEvent_t, 5>> ev_sets;
+  std::vector<std::array<cudaEvent_t, BBPE_N_KERNELS + 1>> ev_sets;
   std::vector<cudaStream_t> ev_streams;
   size_t ev_used = 0;
-  double kernel_ms[BBPE_N_KERNELS] = {0, 0, 0, 0};
+  double kernel_ms[BBPE_N_KERNELS] = {};
   uint64_t timed_calls = 0;
 };
 
@@ -150,27 +151,36 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   a.num_tiles = (total + kTile - 1) / kTile;
   a.out_ids = d_out;
   a.out_offsets = d_out_off;
+  a.num_groups = (a.num_tiles + kScanTilesPerCta - 1) / kScanTilesPerCta;
   c.tile_first.ensure((a.num_tiles + 1) * 8);
-  c.status.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
+  c.status.ensure(std::max<uint64_t>(a.num_groups, 1) * 8);
+  c.staging.ensure(std::max<uint64_t>(a.num_tiles, 1) * kStage * 4);
+  c.tile_count.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
+  c.tile_lrec.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
+  c.tile_base.ensure((a.num_tiles + 1) * 8);
   c.counters.ensure(CNT_N * 4);
   c.err.ensure(ERR_N * 8);
   const bool block = c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0;
   a.lp_cap = block ? n + 1 : total / (kLmax + 1) + 2;
-  c.lp.ensure(a.lp_cap * sizeof(LongPiece));
+  c.lrec.ensure(a.lp_cap * sizeof(LongRec));
   c.lpo.ensure((total + 1) * 4);
   c.lpx.ensure(std::max<uint64_t>(total, 1) * 8);
   c.lpy.ensure(std::max<uint64_t>(total, 1) * 8);
   a.tile_first = c.tile_first.as<uint64_t>();
   a.status = c.status.as<uint64_t>();
+  a.staging = c.staging.as<uint32_t>();
+  a.tile_count = c.tile_count.as<uint32_t>();
+  a.tile_lrec = c.tile_lrec.as<uint64_t>();
+  a.tile_base = c.tile_base.as<uint64_t>();
+  a.lrec = c.lrec.as<LongRec>();
   a.counters = c.counters.as<uint32_t>();
   a.err = c.err.as<uint64_t>();
-  a.lp = c.lp.as<LongPiece>();
   a.lpo = c.lpo.as<uint32_t>();
   a.lpx = c.lpx.as<uint64_t>();
   a.lpy = c.lpy.as<uint64_t>();
   a.engine = block ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES;
   a.max_passes = c.cfg.max_passes;
-  ck(cudaMemsetAsync(a.status, 0, std::max<uint64_t>(a.num_tiles, 1) * 8, s), "memset status");
+  ck(cudaMemsetAsync(a.status, 0, std::max<uint64_t>(a.num_groups, 1) * 8, s), "memset status");
   ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
   ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, s), "memset err");
   return a;
@@ -180,21 +190,30 @@ void ensure_plan(bbpe_ctx& c) {
   if (c.plan.sm_count == 0) c.plan = bbpe::plan_launch(c.device);
 }
 
+void ensure_memo(bbpe_ctx& c, const bbpe_table& t);
+
 // Enqueue a device-resident encode. Handles the empty-input corner cases.
 void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
                     const uint64_t* d_offsets, uint64_t n, uint64_t total, uint32_t* d_out,
-                    uint64_t* d_out_off, cudaStream_t s) {
+                    uint64_t* d_out_off, cudaStream_t s, bool allow_memo = true) {
   if (total == 0) {
     ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
     c.err.ensure(bbpe::ERR_N * 8);
     ck(cudaMemsetAsync(c.err.p, 0xFF, bbpe::ERR_N * 8, s), "memset err");
     return;
   }
-  const bbpe::DevTable& dt = bbpe::table_on_device(t, c.device);
+  bbpe::table_on_device(t, c.device);
   ensure_plan(c);
+  const bool memo = allow_memo && c.cfg.piece_memo && c.cfg.engine == BBPE_ENGINE_PIECES &&
+                    c.cfg.max_passes <= 0;
+  // The memo itself is built at API entry (maybe_build_memo), never here:
+  // building encodes through the ctx's own staging buffers.
+  const bbpe::DevTable dt = bbpe::table_on_device(t, c.device);
   bbpe::EncodeArgs a = prepare_args(c, d_bytes, d_offsets, n, total, d_out, d_out_off, s);
+  a.narrow = t.narrow ? 1 : 0;
+  a.use_memo = memo && dt.memo ? 1 : 0;
   if (c.ev_used == c.ev_sets.size()) {
-    std::array<cudaEvent_t, 5> set{};
+    std::array<cudaEvent_t, BBPE_N_KERNELS + 1> set{};
     for (auto& e : set) ck(cudaEventCreate(&e), "cudaEventCreate");
     c.ev_sets.push_back(set);
     c.ev_streams.push_back(s);
@@ -202,6 +221,14 @@ void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
   c.ev_streams[c.ev_used] = s;
   c.launches += bbpe::launch_encode(a, dt, c.plan, s, c.ev_sets[c.ev_used++].data());
   ck(cudaGetLastError(), "kernel launch");
+}
+
+void maybe_build_memo(bbpe_ctx& c, const bbpe_table& t) {
+  if (c.cfg.piece_memo && c.cfg.engine == BBPE_ENGINE_PIECES && c.cfg.max_passes <= 0) {
+    bbpe::table_on_device(t, c.device);
+    ensure_plan(c);
+    ensure_memo(c, t);
+  }
 }
 
 uint64_t row_of(const uint64_t* host_offsets, uint64_t n, uint64_t pos) {
@@ -252,7 +279,7 @@ void check_device_errors(bbpe_ctx& c, const uint64_t* host_offsets, uint64_t n, 
 uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
                      const uint64_t* offsets, uint64_t r0, uint64_t r1, uint32_t* out_ids,
                      uint64_t out_pos, uint64_t out_capacity, uint64_t* out_offsets,
-                     bbpe_stats* st) {
+                     bbpe_stats* st, bool allow_memo = true) {
   const uint64_t n = r1 - r0;
   const uint64_t base = offsets[r0];
   const uint64_t total = offsets[r1] - base;
@@ -269,7 +296,7 @@ uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
   if (st) st->h2d_ms += ms_since(t0);
   ck(cudaEventRecord(c.ev0, c.stream), "event");
   enqueue_encode(c, t, c.in_bytes.as<uint8_t>(), c.in_offsets.as<uint64_t>(), n, total,
-                 c.out_ids.as<uint32_t>(), c.out_offsets.as<uint64_t>(), c.stream);
+                 c.out_ids.as<uint32_t>(), c.out_offsets.as<uint64_t>(), c.stream, allow_memo);
   ck(cudaEventRecord(c.ev1, c.stream), "event");
   std::vector<uint64_t> oo(n + 1);
   ck(cudaMemcpyAsync(oo.data(), c.out_offsets.p, (n + 1) * 8, cudaMemcpyDeviceToHost, c.stream), "D2H offsets");
@@ -291,6 +318,76 @@ uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
   if (st) st->d2h_ms += ms_since(t1);
   for (uint64_t i = 0; i <= n; ++i) out_offsets[r0 + i] = out_pos + oo[i];
   return ntok;
+}
+
+// Builds the piece memo for (table, ctx device) once: every vocabulary token of
+// 2..kMemoMaxLen bytes that forms a single piece (all internal bigrams are
+// merge junctions) is encoded by this engine with the memo off; encodings of
+// at most two tokens are stored in an open-addressing table keyed by the
+// bytes. Entries depend on the table only, never on the input being encoded.
+void ensure_memo(bbpe_ctx& c, const bbpe_table& t) {
+  using namespace bbpe;
+  DeviceReplica& rep = replica_of(t, c.device);
+  {
+    std::lock_guard<std::mutex> lock(const_cast<bbpe_table&>(t).mu);
+    if (rep.memo_state != 0) return;
+    rep.memo_state = 1;
+  }
+  std::vector<uint32_t> cand;  // token positions
+  std::vector<uint8_t> blob;
+  std::vector<uint64_t> offs{0};
+  for (size_t i = 0; i < t.ids.size(); ++i) {
+    const uint64_t b = t.tok_off[i], e = t.tok_off[i + 1];
+    const uint64_t len = e - b;
+    if (len < 2 || len > uint64_t(kMemoMaxLen)) continue;
+    bool ok = true;
+    for (uint64_t k = b; k < e && ok; ++k) ok = t.lut[t.tok_bytes[k]] != kInvalidToken;
+    for (uint64_t k = b + 1; k < e && ok; ++k) {
+      const uint32_t bit = (uint32_t(t.tok_bytes[k - 1]) << 8) | t.tok_bytes[k];
+      ok = (t.junction[bit >> 5] >> (bit & 31)) & 1u;
+    }
+    if (!ok) continue;
+    cand.push_back(static_cast<uint32_t>(i));
+    blob.insert(blob.end(), t.tok_bytes.begin() + b, t.tok_bytes.begin() + e);
+    offs.push_back(blob.size());
+  }
+  std::vector<MemoEntry> slots;
+  uint64_t mask = 0;
+  if (!cand.empty()) {
+    std::vector<uint32_t> ids(blob.size());
+    std::vector<uint64_t> oo(cand.size() + 1);
+    encode_wave(c, t, blob.data(), offs.data(), 0, cand.size(), ids.data(), 0, ids.size(), oo.data(),
+                nullptr, /*allow_memo=*/false);
+    uint64_t cap = 16;
+    while (cap < cand.size() * 5 / 2) cap <<= 1;
+    mask = cap - 1;
+    slots.assign(cap, MemoEntry{});
+    for (size_t j = 0; j < cand.size(); ++j) {
+      const uint64_t nres = oo[j + 1] - oo[j];
+      if (nres < 1 || nres > 2) continue;
+      MemoEntry m{};
+      const uint64_t len = offs[j + 1] - offs[j];
+      std::memcpy(m.w, blob.data() + offs[j], len);
+      m.len = static_cast<uint8_t>(len);
+      m.nres = static_cast<uint8_t>(nres);
+      m.res[0] = t.dense(ids[oo[j]]);
+      m.res[1] = nres > 1 ? t.dense(ids[oo[j] + 1]) : 0;
+      uint64_t b = memo_hash(m.w, m.len) & mask;
+      while (slots[b].len != 0) b = (b + 1) & mask;
+      slots[b] = m;
+    }
+  }
+  void* dptr = nullptr;
+  if (!slots.empty()) {
+    ck(cudaMalloc(&dptr, slots.size() * sizeof(MemoEntry)), "cudaMalloc (memo)");
+    ck(cudaMemcpy(dptr, slots.data(), slots.size() * sizeof(MemoEntry), cudaMemcpyHostToDevice),
+       "memo upload");
+  }
+  std::lock_guard<std::mutex> lock(const_cast<bbpe_table&>(t).mu);
+  rep.memo = dptr;
+  rep.view.memo = static_cast<const MemoEntry*>(dptr);
+  rep.view.memo_mask = mask;
+  rep.memo_state = 2;
 }
 
 }  // namespace
@@ -433,7 +530,7 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->tile_first, &c->status, &c->counters, &c->err, &c->lp, &c->lpo, &c->lpx,
+    for (DevBuf* b : {&c->staging, &c->tile_count, &c->tile_lrec, &c->lrec, &c->tile_base, &c->tile_first, &c->status, &c->counters, &c->err, &c->lpo, &c->lpx,
                       &c->lpy, &c->trace, &c->trace_count, &c->in_bytes, &c->in_offsets,
                       &c->out_ids, &c->out_offsets})
       b->release();
@@ -464,6 +561,7 @@ int bbpe_ctx_prepare(bbpe_ctx* c, const bbpe_table* t) {
   DeviceGuard g(c->device);
   bbpe::table_on_device(*t, c->device);
   ensure_plan(*c);
+  maybe_build_memo(*c, *t);
   return BBPE_OK;
   BBPE_CATCH
 }
@@ -493,6 +591,7 @@ int bbpe_encode(bbpe_ctx* c, const bbpe_table* t, const uint8_t* bytes, const ui
     if (offsets[i + 1] < offsets[i]) throw bbpe::usage_error("offsets must be non-decreasing");
   if (offsets[n] > offsets[0] && (!bytes || !out_ids)) throw bbpe::usage_error("null buffer");
   DeviceGuard g(c->device);
+  maybe_build_memo(*c, *t);
   if (st) *st = bbpe_stats{};
   // Waves: row ranges of at most wave_bytes (a row is never split).
   const uint64_t wave = c->cfg.wave_bytes ? c->cfg.wave_bytes : (1ull << 31);
@@ -525,6 +624,7 @@ int bbpe_encode_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
   if (!c || !t || !d_offsets || !d_out_offsets) throw bbpe::usage_error("null argument");
   validate_config(c->cfg);
   DeviceGuard g(c->device);
+  maybe_build_memo(*c, *t);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   if (sync) ck(cudaEventRecord(c->ev0, s), "event");
   enqueue_encode(*c, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
@@ -572,7 +672,7 @@ int bbpe_ctx_kernel_times(bbpe_ctx* c, double* ms, uint64_t* calls, int reset) {
   if (!c) throw bbpe::usage_error("null ctx");
   DeviceGuard g(c->device);
   for (size_t i = 0; i < c->ev_used; ++i) {
-    ck(cudaEventSynchronize(c->ev_sets[i][4]), "event sync");
+    ck(cudaEventSynchronize(c->ev_sets[i][BBPE_N_KERNELS]), "event sync");
     for (int k = 0; k < BBPE_N_KERNELS; ++k) {
       float e = 0;
       ck(cudaEventElapsedTime(&e, c->ev_sets[i][k], c->ev_sets[i][k + 1]), "event time");
@@ -634,7 +734,7 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   a.total = n;
   c->counters.ensure(CNT_N * 4);
   c->err.ensure(ERR_N * 8);
-  c->lp.ensure(sizeof(LongPiece));
+  c->lrec.ensure(sizeof(LongRec));
   c->lpo.ensure((n + 1) * 4);
   c->lpx.ensure(n * 8);
   c->lpy.ensure(n * 8);
@@ -643,7 +743,7 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   c->trace_count.ensure(8);
   a.counters = c->counters.as<uint32_t>();
   a.err = c->err.as<uint64_t>();
-  a.lp = c->lp.as<LongPiece>();
+  a.lrec = c->lrec.as<LongRec>();
   a.lp_cap = 1;
   a.lpo = c->lpo.as<uint32_t>();
   a.lpx = c->lpx.as<uint64_t>();
@@ -654,10 +754,10 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   a.tokens_input = 1;
   a.engine = BBPE_ENGINE_BLOCK;
   a.max_passes = c->cfg.max_passes;
-  LongPiece lp{0, n, 0};
+  LongRec lp{0, n, 0, 0u, 0u};
   uint32_t counters[CNT_N] = {0};
-  counters[CNT_LP_COUNT] = 1;
-  ck(cudaMemcpyAsync(a.lp, &lp, sizeof(lp), cudaMemcpyHostToDevice, c->stream), "H2D");
+  counters[CNT_LREC] = 1;
+  ck(cudaMemcpyAsync(a.lrec, &lp, sizeof(lp), cudaMemcpyHostToDevice, c->stream), "H2D");
   ck(cudaMemcpyAsync(a.counters, counters, sizeof(counters), cudaMemcpyHostToDevice, c->stream), "H2D");
   ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, c->stream), "memset");
   ck(cudaMemcpyAsync(a.lpx, x.data(), n * 8, cudaMemcpyHostToDevice, c->stream), "H2D");

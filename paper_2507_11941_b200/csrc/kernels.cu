@@ -18,10 +18,11 @@
 //
 // Kernels (one stream, no host sync in between):
 //   k_tile_first  : row index of the first row starting at or after each tile
-//   k_prepass     : invalid-byte check, long-piece discovery
-//   k_long_pieces : CTA-per-piece pass loop (the paper's block engine)
-//   k_encode      : warp-per-tile piece split + lane-per-piece pass loop +
-//                   decoupled look-back -> CSR ids and row offsets, written once
+//   k_pieces      : warp-per-tile piece split + lane-per-piece pass loops ->
+//                   tokens staged per tile (no ordering wait)
+//   k_long_pieces : CTA-per-piece pass loop over the long pieces k_pieces found
+//                   (the paper's block engine; every row under BBPE_ENGINE_BLOCK)
+//   k_gather      : decoupled look-back over tile groups -> CSR ids + row offsets
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -37,7 +38,6 @@ constexpr uint32_t kMergeMark = 0xFFFFFFFDu;
 constexpr uint32_t kUnchanged = 0x80000000u;  // lpo flag: piece merged nothing
 constexpr int kWords = (kWin + 31) / 32;
 constexpr int kTileWords = kTile / 32;
-constexpr int kMaxLongPerTile = kTile / (kLmax + 1) + 2;
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
@@ -111,40 +111,48 @@ __global__ void k_tile_first(EncodeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Per-warp window over [b0-1, b0+kWin): bytes, row starts, hard boundaries.
+// Per-warp window over [b0-4, b0+kWin+4): bytes, row starts, hard boundaries.
+// Bytes are copied as aligned words: wb[q + 4] is the byte at b0 + q.
+constexpr int kWinWordsB = (kWin + 8 + 15) / 16 * 4;  // u32 words of bytes
 struct Window {
-  uint8_t wb[kWin + 8];    // wb[q+1] = byte at b0+q, wb[0] = byte at b0-1
-  uint32_t sb[kWords];     // row-start bits
-  uint32_t bd[kWords];     // piece-boundary bits
+  uint32_t wbw[kWinWordsB];  // window bytes (as words)
+  uint32_t sb[kWords];       // row-start bits
+  uint32_t bd[kWords];       // piece-boundary bits
+  __device__ __forceinline__ uint32_t byte(int q) const {  // byte at b0 + q, q >= -4
+    return reinterpret_cast<const uint8_t*>(wbw)[q + 4];
+  }
+  __device__ __forceinline__ const uint8_t* bytes() const {
+    return reinterpret_cast<const uint8_t*>(wbw);
+  }
 };
 
-__device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc, uint64_t tile,
-                            int lane, bool block_engine) {
+// Loads the window and computes boundaries; returns (lane 0's view of) the
+// first invalid byte position found in [b0, b0 + tlen), or ~0.
+__device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc, const uint32_t* lut,
+                            uint64_t tile, int lane, int tlen) {
   const uint64_t b0 = tile * kTile;
-  // Bytes. Aligned 4-byte words covering [b0-4, b0+kWin+4).
   const uint64_t wbase = b0 >= 4 ? b0 - 4 : 0;
-  for (int i = lane; i < (kWin + 12) / 4; i += 32) {
-    uint64_t pos = wbase + 4ull * i;
+  const int wofs = b0 >= 4 ? 0 : 1;  // tile 0: word 0 of the window is before the input
+  for (int i = lane; i < kWinWordsB; i += 32) {
+    const int gi = i - wofs;
     uint32_t v = 0;
-    if (pos + 4 <= a.total) {
-      v = __ldg(reinterpret_cast<const uint32_t*>(a.bytes + pos));
-    } else {
-      for (int k = 0; k < 4; ++k)
-        if (pos + k < a.total) v |= uint32_t(a.bytes[pos + k]) << (8 * k);
+    if (gi >= 0) {
+      const uint64_t pos = wbase + 4ull * gi;
+      if (pos + 4 <= a.total) {
+        v = __ldg(reinterpret_cast<const uint32_t*>(a.bytes + pos));
+      } else {
+        for (int k = 0; k < 4; ++k)
+          if (pos + k < a.total) v |= uint32_t(a.bytes[pos + k]) << (8 * k);
+      }
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int64_t q = int64_t(pos + k) - int64_t(b0);  // relative position
-      if (q >= -1 && q < kWin) w.wb[q + 1] = uint8_t(v >> (8 * k));
-    }
+    w.wbw[i] = v;
   }
-  if (b0 == 0 && lane == 0) w.wb[0] = 0;
   for (int i = lane; i < kWords; i += 32) w.sb[i] = 0;
   __syncwarp();
   // Row starts inside the window.
-  uint64_t s0 = a.tile_first[tile];
+  const uint64_t s0 = a.tile_first[tile];
   for (uint64_t s = s0;; s += 32) {
-    uint64_t my = s + lane;
+    const uint64_t my = s + lane;
     bool in = false;
     uint64_t o = 0;
     if (my <= a.n_rows) {
@@ -155,18 +163,25 @@ __device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc
     if (__ballot_sync(kFull, in) != kFull) break;
   }
   __syncwarp();
-  // Boundaries.
+  // Boundaries, and the invalid-byte check (pretokenize.hpp:64-67).
+  uint32_t badw = 0xFFFFFFFFu;
   for (int wd = 0; wd < kWords; ++wd) {
-    int q = wd * 32 + lane;
-    uint64_t abs = b0 + q;
+    const int q = wd * 32 + lane;
+    const uint64_t abs = b0 + q;
     bool b = true;
     if (q < kWin && abs < a.total) {
+      const uint32_t cur = w.byte(q);
       b = (w.sb[wd] >> lane) & 1u;
-      if (!b && !block_engine) b = !is_junction(junc, w.wb[q], w.wb[q + 1]);
+      if (!b) b = !is_junction(junc, w.byte(q - 1), cur);
+      if (q < tlen && lut[cur] == kInvalidToken && badw == 0xFFFFFFFFu) badw = uint32_t(q);
     }
-    unsigned m = __ballot_sync(kFull, b);
+    const unsigned m = __ballot_sync(kFull, b);
     if (lane == 0) w.bd[wd] = m;
   }
+  const uint32_t bad = __reduce_min_sync(kFull, badw);
+  if (bad != 0xFFFFFFFFu && lane == 0)
+    atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
+              (unsigned long long)(b0 + bad));
   __syncwarp();
 }
 
@@ -184,98 +199,6 @@ __device__ __forceinline__ int next_boundary(const uint32_t* bd, int q, int limi
     p = (p | 31) + 1;
   }
   return last + 1;
-}
-
-// ---------------------------------------------------------------------------
-// k_prepass: invalid bytes (IntegrityError, pretokenize.hpp:64-67) and long
-// pieces (> kLmax bytes, or every row under BBPE_ENGINE_BLOCK).
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_prepass(EncodeArgs a, DevTable T) {
-  __shared__ uint32_t s_lut[256];
-  __shared__ uint32_t s_junc[2048];
-  __shared__ Window s_win[kWarpsPerCta];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_junc[i] = T.junction[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  Window& w = s_win[wid];
-  const bool block_engine = a.engine == BBPE_ENGINE_BLOCK;
-  const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
-  for (uint64_t tile = blockIdx.x * uint64_t(kWarpsPerCta) + wid; tile < a.num_tiles;
-       tile += nwarps) {
-    const uint64_t b0 = tile * kTile;
-    const int tlen = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
-    if (block_engine) {
-      // Every non-empty row starting in this tile is one long piece.
-      uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
-      for (uint64_t s = s0 + lane; s < s1 && s < a.n_rows; s += 32) {
-        uint64_t o = a.offsets[s], e = a.offsets[s + 1];
-        if (e > o) {
-          uint32_t slot = atomicAdd(&a.counters[CNT_LP_COUNT], 1u);
-          if (slot < a.lp_cap) a.lp[slot] = LongPiece{o, e - o, s};
-        }
-      }
-      // Invalid bytes still need checking.
-      for (int q = lane; q < tlen; q += 32) {
-        uint8_t byte = a.bytes[b0 + q];
-        unsigned bad = __ballot_sync(__activemask(), s_lut[byte] == kInvalidToken);
-        if (bad && lane == __ffs(bad) - 1) atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]), b0 + q);
-      }
-      continue;
-    }
-    load_window(w, a, s_junc, tile, lane, false);
-    // Invalid bytes.
-    for (int wd = 0; wd * 32 < tlen; ++wd) {
-      int q = wd * 32 + lane;
-      bool bad = q < tlen && s_lut[w.wb[q + 1]] == kInvalidToken;
-      unsigned m = __ballot_sync(kFull, bad);
-      if (m && lane == 0) {
-        atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
-                  (unsigned long long)(b0 + wd * 32 + __ffs(m) - 1));
-      }
-    }
-    // Long pieces: starts in [0, tlen) with no boundary within kLmax bytes.
-    for (int wd = 0; wd * 32 < tlen; ++wd) {
-      int q = wd * 32 + lane;
-      bool start = q < tlen && ((w.bd[wd] >> lane) & 1u);
-      bool longp = start && next_boundary(w.bd, q, kLmax) > q + kLmax;
-      unsigned lm = __ballot_sync(kFull, longp);
-      while (lm) {
-        int src = __ffs(lm) - 1;
-        lm &= lm - 1;
-        int lq = __shfl_sync(kFull, q, src);
-        uint64_t abs = b0 + lq;
-        // Row of the piece (rare path): binary search on offsets.
-        uint64_t row = 0, row_end = 0;
-        if (lane == 0) {
-          uint64_t lo = 0, hi = a.n_rows;  // find max s with offsets[s] <= abs
-          while (lo < hi) {
-            uint64_t mid = (lo + hi + 1) >> 1;
-            if (a.offsets[mid] <= abs) lo = mid; else hi = mid - 1;
-          }
-          row = lo;
-          row_end = a.offsets[row + 1];
-        }
-        row = __shfl_sync(kFull, row, 0);
-        row_end = __shfl_sync(kFull, row_end, 0);
-        // Scan forward for the first hard boundary (pieces never cross rows).
-        uint64_t end = row_end;
-        for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
-          uint64_t y = x + lane;
-          bool b = y < row_end && !is_junction(s_junc, a.bytes[y - 1], a.bytes[y]);
-          unsigned bm = __ballot_sync(kFull, b);
-          if (bm) {
-            end = x + __ffs(bm) - 1;
-            break;
-          }
-        }
-        if (lane == 0) {
-          uint32_t slot = atomicAdd(&a.counters[CNT_LP_COUNT], 1u);
-          if (slot < a.lp_cap) a.lp[slot] = LongPiece{abs, end - abs, row};
-        }
-      }
-    }
-    __syncwarp();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -382,9 +305,9 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
     if (tid == 0) s_idx = atomicAdd(&a.counters[CNT_LP_NEXT], 1u);
     __syncthreads();
     const uint32_t idx = s_idx;
-    const uint32_t count = min((uint64_t)a.counters[CNT_LP_COUNT], (uint64_t)a.lp_cap);
+    const uint32_t count = min((uint64_t)a.counters[CNT_LREC], (uint64_t)a.lp_cap);
     if (idx >= count) return;
-    const LongPiece P = a.lp[idx];
+    const LongRec P = a.lrec[idx];
     const int32_t len = static_cast<int32_t>(P.len);
     uint64_t* X = a.lpx + P.start;
     uint64_t* Y = a.lpy + P.start;
@@ -484,58 +407,211 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
     if (a.trace && tid == 0 && a.trace_count) *a.trace_count = pass;
     // Result: lpo[start] = count, tokens follow when anything merged (or on token input).
     uint32_t* O = a.lpo + P.start;
-    if (tid == 0) O[0] = static_cast<uint32_t>(n) | ((n == len && !a.tokens_input) ? kUnchanged : 0u);
+    if (tid == 0) {
+      O[0] = static_cast<uint32_t>(n) | ((n == len && !a.tokens_input) ? kUnchanged : 0u);
+      a.lrec[idx].count = static_cast<uint32_t>(n);
+    }
     if (n < len || a.tokens_input)
       for (int32_t i = tid; i < n; i += NT) O[1 + i] = tok_of(X[i]);
   }
 }
 
 // ---------------------------------------------------------------------------
-// k_encode: warp-per-tile. Per tile: window -> pieces -> lane-per-piece pass
-// loops -> tile token count -> decoupled look-back -> CSR writes.
-struct WarpSmem {
-  Window w;
-  uint16_t plist[kTile];
-  uint32_t pref[kTile + 1];
-  uint32_t tok[kWin + 1];
-  uint32_t rnk[kWin + 1];
-  uint32_t nlong;
-  uint32_t longk[kMaxLongPerTile];
-  uint64_t tile;
+// k_pieces: warp-per-tile merge of all short pieces starting in the tile.
+// Per tile: window -> piece list -> initial tokens -> warp-parallel, batched
+// initial pair probes -> sub-warp "blocks" run the reference pass loop, one
+// piece per group of W lanes (one token per lane) -> tokens staged per tile
+// (no ordering wait; k_gather assembles the CSR afterwards).
+//
+// This is the paper's one-block-per-string engine scaled to the piece: a
+// pass is a W-lane shuffle min-reduction, a ballot of the pairs at the
+// minimum (left-greedy over runs), a ballot/popc compaction, and re-probes
+// of only the pairs that touch a merged token.
+template <typename Tk>
+struct Marks {
+  static constexpr uint32_t kNone = Tk(~Tk(0));  // no rank / uncovered position
 };
 
-// One lane: the reference pass loop over a piece of n <= kLmax tokens held at
-// tok[0..n) / rnk[0..n-1) (shared memory). Returns when no pair remains.
-// Per pass: min over cached ranks, sweep-compact in place (left-greedy:
-// a pair at the current minimum merges unless its left token was just
-// consumed -- exactly flags[i+1] = (ranks[i] == m && !flags[i])), then
-// re-probe only the pairs touching a merged token.
-__device__ __forceinline__ int lane_pass(const DevTable& T, uint32_t* tok, uint32_t* rnk, int n) {
-  uint32_t m = kNoRank;
-  for (int i = 0; i < n - 1; ++i) m = min(m, rnk[i]);
-  if (m == kNoRank) return -1;
-  const uint32_t M = __ldg(T.r2m + m);
-  int j = 0, i = 0;
-  while (i < n) {
-    uint32_t ri = (i < n - 1) ? rnk[i] : kNoRank;
-    if (ri == m) {
-      tok[j] = M;
-      rnk[j] = kProbe;
-      if (j > 0) rnk[j - 1] = kProbe;
-      i += 2;
-    } else {
-      tok[j] = tok[i];
-      rnk[j] = ri;
-      i += 1;
-    }
-    ++j;
+constexpr int kMemoDone = 0x40;  // plen flag: piece resolved by the memo
+
+template <typename Tk>
+struct PieceSmem {
+  Window w;
+  uint16_t plist[kTile];      // piece starts (window-relative), in order
+  uint8_t plen[kTile];        // piece length, 0xFF = long (> kLmax)
+  uint16_t clist[kTile];      // pieces that need merge passes
+  uint16_t clist2[kTile];     // the same, <= 8 tokens first
+  uint16_t cnt[kTile + 1];    // short tokens per piece -> exclusive prefix
+  Tk tok[kWin + 1];
+  Tk rnk[kWin + 1];
+  uint32_t sct[32];           // pass compaction scratch: token
+  uint32_t scr[32];           //                          rank
+  uint8_t scf[32];            //                          merged flag
+  uint64_t llen[kTile / (kLmax + 1) + 2];    // byte length of each long piece, in order
+  uint16_t lk[kTile / (kLmax + 1) + 2];      // their piece indices
+};
+
+// Batched probe: issue the bucket loads, resolve later.
+struct ProbeReq {
+  uint64_t key, b;
+  ulonglong2 s01, s23;
+};
+__device__ __forceinline__ void probe_issue(ProbeReq& q, const DevTable& T, uint32_t l, uint32_t r) {
+  q.key = (uint64_t(l) << T.id_bits) | uint64_t(r);
+  q.b = dmix64(q.key) & T.bucket_mask;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + q.b * kBucketSlots);
+  q.s01 = __ldg(p);
+  q.s23 = __ldg(p + 1);
+}
+__device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTable& T) {
+  const uint64_t rmask = (1ull << T.rank_bits) - 1;
+  uint64_t s[4] = {q.s01.x, q.s01.y, q.s23.x, q.s23.y};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (s[j] == kEmptySlot) return kNoRank;
+    if ((s[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(s[j] & rmask);
   }
-  for (int k = 0; k < j - 1; ++k)
-    if (rnk[k] == kProbe) rnk[k] = probe(T, tok[k], tok[k + 1]);
-  return j;
+  // Bucket full without a hit: continue linearly (rare at load <= 0.5).
+  uint64_t b = q.b;
+  for (;;) {
+    b = (b + 1) & T.bucket_mask;
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + b * kBucketSlots);
+    ulonglong2 a = __ldg(p), c = __ldg(p + 1);
+    uint64_t t[4] = {a.x, a.y, c.x, c.y};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (t[j] == kEmptySlot) return kNoRank;
+      if ((t[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(t[j] & rmask);
+    }
+  }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_encode(EncodeArgs a, DevTable T) {
+template <typename Tk>
+__device__ __forceinline__ uint32_t tk_rank(uint32_t r) {
+  return r == kNoRank ? Marks<Tk>::kNone : r;
+}
+
+// Left-greedy marking over W candidate bits (block_engine.hpp:107-109):
+// pair b merges iff it is at the minimum and pair b-1 did not merge.
+template <int W>
+__device__ __forceinline__ unsigned left_greedy(unsigned E) {
+  if (!(E & (E << 1))) return E;  // no adjacent candidates: every one merges
+  unsigned F = 0;
+#pragma unroll
+  for (int b = 0; b < W; ++b)
+    if (((E >> b) & 1u) && !(b > 0 && ((F >> (b - 1)) & 1u))) F |= 1u << b;
+  return F;
+}
+
+// Runs every piece in `list` (pieces of 2..W tokens) through the pass loop,
+// 32/W pieces at a time, refilling groups as their pieces finish.
+template <typename Tk, int W>
+__device__ void run_class(PieceSmem<Tk>& S, const DevTable& T, const uint16_t* list, int count,
+                          int lane) {
+  constexpr uint32_t NONE = Marks<Tk>::kNone;
+  const int g = lane / W, gl = lane % W, gbase = g * W;
+  const unsigned wmask = W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u);
+  int next = 0, pk = 0, q = 0, n = 0;
+  uint32_t t = NONE, r = NONE;
+  for (;;) {
+    const bool idle = n == 0;
+    const unsigned lead = __ballot_sync(kFull, idle && gl == 0);
+    if (idle) {
+      const int k = next + __popc(lead & ((1u << gbase) - 1u));
+      if (k < count) {
+        pk = list[k];
+        q = S.plist[pk];
+        n = S.plen[pk];
+        t = gl < n ? uint32_t(S.tok[q + gl]) : NONE;
+        r = gl < n - 1 ? uint32_t(S.rnk[q + gl]) : NONE;
+      }
+    }
+    next += __popc(lead);
+    const bool active = n >= 2;
+    if (!__any_sync(kFull, active) && next >= count) break;
+
+    // ---- one pass of every active group (warp-convergent) ----
+    uint32_t m = active ? r : NONE;
+#pragma unroll
+    for (int d = W / 2; d >= 1; d >>= 1) m = min(m, __shfl_xor_sync(kFull, m, d));
+    const bool has = m != NONE;
+    const unsigned E = (__ballot_sync(kFull, has && r == m) >> gbase) & wmask;
+    const unsigned F = left_greedy<W>(E);
+    const bool f = (F >> gl) & 1u;
+    const unsigned nmask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
+    const unsigned K = ~(F << 1) & nmask;  // surviving tokens
+    const int n2 = __popc(K);
+    if (has && ((K >> gl) & 1u)) {
+      const int j = __popc(K & ((1u << gl) - 1u));
+      S.sct[gbase + j] = f ? __ldg(T.r2m + m) : t;
+      S.scr[gbase + j] = r;
+      S.scf[gbase + j] = f;
+    }
+    __syncwarp();
+    if (has) {
+      uint32_t nt = NONE, nr = NONE;
+      if (gl < n2) {
+        nt = S.sct[gbase + gl];
+        if (gl < n2 - 1) {
+          const uint32_t nt1 = S.sct[gbase + gl + 1];
+          if (S.scf[gbase + gl] | S.scf[gbase + gl + 1]) {
+            ProbeReq pr;
+            probe_issue(pr, T, nt, nt1);
+            nr = tk_rank<Tk>(probe_resolve(pr, T));
+          } else {
+            nr = S.scr[gbase + gl];  // both tokens unchanged: cached rank holds
+          }
+        }
+      }
+      t = nt;
+      r = nr;
+      n = n2;
+    }
+    __syncwarp();
+    if (active && (!has || n < 2)) {
+      if (gl < n) S.tok[q + gl] = Tk(t);
+      if (gl == 0) S.cnt[pk] = static_cast<uint16_t>(n);
+      n = 0;
+    }
+  }
+}
+
+// Whole-piece memo lookup (exact: the entry holds this engine's own encoding
+// of the same bytes, computed from the table alone at upload time).
+__device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* ww, int q, int len,
+                                            uint32_t& r0, uint32_t& r1, uint32_t& nres) {
+  const int start = q + 4, a = start >> 2, sh = (start & 3) * 8;
+  uint32_t x[6], w[5];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = ww[a + i];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    uint32_t v = sh ? __funnelshift_r(x[i], x[i + 1], sh) : x[i];
+    const int nb = len - 4 * i;
+    v &= nb >= 4 ? 0xFFFFFFFFu : (nb <= 0 ? 0u : ((1u << (8 * nb)) - 1u));
+    w[i] = v;
+  }
+  uint64_t b = memo_hash(w, uint32_t(len)) & T.memo_mask;
+  for (;;) {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
+    const ulonglong2 lo = __ldg(p), hi = __ldg(p + 1);
+    const uint32_t e0 = uint32_t(lo.x), e1 = uint32_t(lo.x >> 32), e2 = uint32_t(lo.y),
+                   e3 = uint32_t(lo.y >> 32), e4 = uint32_t(hi.x), meta = uint32_t(hi.x >> 32);
+    const uint32_t elen = meta & 0xFF;
+    if (elen == 0) return false;
+    if (elen == uint32_t(len) && e0 == w[0] && e1 == w[1] && e2 == w[2] && e3 == w[3] && e4 == w[4]) {
+      nres = (meta >> 8) & 0xFF;
+      r0 = uint32_t(hi.y);
+      r1 = uint32_t(hi.y >> 32);
+      return true;
+    }
+    b = (b + 1) & T.memo_mask;
+  }
+}
+
+template <typename Tk>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, DevTable T) {
+  constexpr uint32_t NONE = Marks<Tk>::kNone;
   __shared__ uint32_t s_lut[256];
   __shared__ uint32_t s_junc[2048];
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -543,8 +619,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_encode(EncodeArgs a, DevT
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_junc[i] = T.junction[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpSmem& S = reinterpret_cast<WarpSmem*>(s_dyn)[wid];
+  PieceSmem<Tk>& S = reinterpret_cast<PieceSmem<Tk>*>(s_dyn)[wid];
   const bool block_engine = a.engine == BBPE_ENGINE_BLOCK;
+  const uint32_t* d2id = T.d2id;
 
   for (;;) {
     uint64_t tile = 0;
@@ -552,178 +629,415 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_encode(EncodeArgs a, DevT
     tile = __shfl_sync(kFull, tile, 0);
     if (tile >= a.num_tiles) return;
     const uint64_t b0 = tile * kTile;
-    const int tlen = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
-    load_window(S.w, a, s_junc, tile, lane, block_engine);
+    const uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
 
-    // Piece list (ordered).
+    if (block_engine) {
+      // Every non-empty row is one long piece for k_long_pieces; the tile's
+      // output is its rows' results in order.
+      const int tl = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
+      for (int q0 = 0; q0 < tl; q0 += 32) {  // invalid bytes (pretokenize.hpp:64-67)
+        const int q = q0 + lane;
+        const bool bad = q < tl && s_lut[a.bytes[b0 + q]] == kInvalidToken;
+        const unsigned bm = __ballot_sync(kFull, bad);
+        if (bm && lane == 0)
+          atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
+                    (unsigned long long)(b0 + q0 + __ffs(bm) - 1));
+      }
+      uint32_t ne = 0;
+      for (uint64_t s = s0 + lane; s < s1 && s < a.n_rows; s += 32)
+        ne += a.offsets[s + 1] > a.offsets[s] ? 1u : 0u;
+      ne = __reduce_add_sync(kFull, ne);
+      uint64_t first = 0;
+      if (lane == 0 && ne) first = atomicAdd(&a.counters[CNT_LREC], ne);
+      first = __shfl_sync(kFull, first, 0);
+      uint32_t ri = 0;
+      for (uint64_t sb = s0; sb < s1 && sb <= a.n_rows; sb += 32) {
+        const uint64_t s = sb + lane;
+        bool ne_row = false;
+        uint64_t o = 0, e = 0;
+        if (s < s1 && s < a.n_rows) {
+          o = a.offsets[s];
+          e = a.offsets[s + 1];
+          ne_row = e > o;
+        }
+        const unsigned nm = __ballot_sync(kFull, ne_row);
+        const uint32_t before = ri + __popc(nm & lanemask_lt(lane));
+        if (s < s1 && s <= a.n_rows) a.out_offsets[s] = uint64_t(before) << 40;
+        if (ne_row && first + before < a.lp_cap)
+          a.lrec[first + before] = LongRec{o, e - o, s, 0u, 0u};
+        ri += __popc(nm);
+      }
+      if (lane == 0) {
+        a.tile_lrec[tile] = ne ? ((first << 24) | ne) : 0;
+        a.tile_count[tile] = 0;
+      }
+      continue;
+    }
+
+    const int tlen = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
+    load_window(S.w, a, s_junc, s_lut, tile, lane, tlen);
+
+    // (1) Piece list with lengths (distance to the next piece start; the
+    // last piece of the tile searches the boundary bits past the tile).
     int npieces = 0;
-    for (int wd = 0; wd < kTileWords; ++wd) {
-      int q = wd * 32 + lane;
-      bool st = q < tlen && ((S.w.bd[wd] >> lane) & 1u);
-      unsigned m = __ballot_sync(kFull, st);
+    for (int wd = 0; wd * 32 < tlen; ++wd) {
+      const int q = wd * 32 + lane;
+      const bool st = q < tlen && ((S.w.bd[wd] >> lane) & 1u);
+      const unsigned m = __ballot_sync(kFull, st);
       if (st) S.plist[npieces + __popc(m & lanemask_lt(lane))] = static_cast<uint16_t>(q);
       npieces += __popc(m);
     }
-    if (lane == 0) S.nlong = 0;
     __syncwarp();
-
-    // Lane-per-piece pass loops with dynamic piece assignment.
-    int my_k = -1, my_n = 0, my_q = 0;
-    int next_k = 0;
-    for (;;) {
-      const bool idle = my_n == 0;
-      const unsigned im = __ballot_sync(kFull, idle);
-      if (idle) {
-        const int k = next_k + __popc(im & lanemask_lt(lane));
-        my_k = -1;
-        if (k < npieces) {
-          my_k = k;
-          my_q = S.plist[k];
-          int len = block_engine ? kLmax + 2 : next_boundary(S.w.bd, my_q, kLmax) - my_q;
-          if (len > kLmax) {
-            // Long piece: merged by k_long_pieces; its count is in lpo[start].
-            S.pref[k] = __ldcg(a.lpo + b0 + my_q) & ~kUnchanged;
-            uint32_t slot = atomicAdd(&S.nlong, 1u);
-            if (slot < kMaxLongPerTile) S.longk[slot] = k;
-            my_n = 0;
-          } else {
-            uint32_t* tk = S.tok + my_q;
-            uint32_t* rk = S.rnk + my_q;
-            for (int i = 0; i < len; ++i) tk[i] = s_lut[S.w.wb[my_q + 1 + i]];
-            for (int i = 0; i < len - 1; ++i) rk[i] = probe(T, tk[i], tk[i + 1]);
-            if (len < 2) {
-              S.pref[k] = len;
-              my_n = 0;
-            } else {
-              my_n = len;
-            }
-          }
-        }
-      }
-      next_k += __popc(im);
-      const bool active = my_n >= 2;
-      if (!__any_sync(kFull, active) && next_k >= npieces) break;
-      if (active) {
-        int r = lane_pass(T, S.tok + my_q, S.rnk + my_q, my_n);
-        if (r < 0) {
-          S.pref[my_k] = my_n;
-          my_n = 0;
-        } else {
-          my_n = r;
-          if (my_n < 2) {
-            S.pref[my_k] = my_n;
-            my_n = 0;
-          }
-        }
-      }
+    for (int k = lane; k < npieces; k += 32) {
+      const int q = S.plist[k];
+      const int len = (k + 1 < npieces) ? S.plist[k + 1] - q : next_boundary(S.w.bd, q, kLmax) - q;
+      S.plen[k] = len > kLmax ? 0xFF : static_cast<uint8_t>(len);
     }
     __syncwarp();
 
-    // Exclusive scan of piece counts -> pref (in place), tile total.
-    uint32_t run = 0;
+    // (2) Piece memo: a piece equal to a vocabulary token's bytes takes its
+    // precomputed encoding (1-2 tokens, parked in rnk[q..] until staging).
+    // Everything else of 2..kLmax bytes goes on the merge list.
+    int nmerge = 0;
     for (int k0 = 0; k0 < npieces; k0 += 32) {
-      int k = k0 + lane;
-      uint32_t c = k < npieces ? S.pref[k] : 0;
-      uint32_t inc = warp_incl_sum(c, lane);
-      if (k < npieces) S.pref[k] = run + inc - c;
+      const int k = k0 + lane;
+      int len = k < npieces ? S.plen[k] : 0;
+      bool merge = false;
+      if (k < npieces) {
+        if (len == 0xFF) {
+          S.cnt[k] = 0;
+        } else if (len < 2) {
+          S.cnt[k] = static_cast<uint16_t>(len);
+          S.tok[S.plist[k]] = Tk(s_lut[S.w.byte(S.plist[k])]);
+        } else {
+          merge = true;
+          const int q = S.plist[k];
+          uint32_t r0, r1, nres;
+          if (a.use_memo && len <= kMemoMaxLen && memo_lookup(T, S.w.wbw, q, len, r0, r1, nres)) {
+            S.plen[k] = static_cast<uint8_t>(len | kMemoDone);
+            S.cnt[k] = static_cast<uint16_t>(nres);
+            S.rnk[q] = Tk(r0);
+            S.rnk[q + 1] = Tk(r1);
+            merge = false;
+          }
+        }
+      }
+      const unsigned mm = __ballot_sync(kFull, merge);
+      if (merge) S.clist[nmerge + __popc(mm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+      nmerge += __popc(mm);
+    }
+    __syncwarp();
+
+    if (nmerge) {
+      // (3) Initial tokens and pair ranks of the merge list (lane per piece,
+      // two probes in flight).
+      for (int i = lane; i < nmerge; i += 32) {
+        const int k = S.clist[i];
+        const int q = S.plist[k], len = S.plen[k];
+        for (int j = 0; j < len; ++j) S.tok[q + j] = Tk(s_lut[S.w.byte(q + j)]);
+        for (int j = 0; j < len - 1; j += 2) {
+          ProbeReq p0, p1;
+          probe_issue(p0, T, S.tok[q + j], S.tok[q + j + 1]);
+          const bool two = j + 2 < len;
+          if (two) probe_issue(p1, T, S.tok[q + j + 1], S.tok[q + j + 2]);
+          S.rnk[q + j] = Tk(tk_rank<Tk>(probe_resolve(p0, T)));
+          if (two) S.rnk[q + j + 1] = Tk(tk_rank<Tk>(probe_resolve(p1, T)));
+        }
+      }
+      // (4) Pass loops: pieces of <= 8 tokens in 8-lane groups, longer ones
+      // in 32-lane groups. The list is split in place (short first).
+      int nsmall = 0;
+      for (int i0 = 0; i0 < nmerge; i0 += 32) {
+        const int i = i0 + lane;
+        const int k = i < nmerge ? S.clist[i] : 0;
+        const bool small = i < nmerge && S.plen[k] <= 8;
+        const unsigned sm = __ballot_sync(kFull, small);
+        const unsigned bm = __ballot_sync(kFull, i < nmerge && !small);
+        __syncwarp();
+        if (small) S.clist2[nsmall + __popc(sm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+        nsmall += __popc(sm);
+        (void)bm;
+      }
+      int nbig = 0;
+      for (int i0 = 0; i0 < nmerge; i0 += 32) {
+        const int i = i0 + lane;
+        const int k = i < nmerge ? S.clist[i] : 0;
+        const bool big = i < nmerge && S.plen[k] > 8;
+        const unsigned bm = __ballot_sync(kFull, big);
+        if (big) S.clist2[nsmall + nbig + __popc(bm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+        nbig += __popc(bm);
+      }
+      __syncwarp();
+      run_class<Tk, 8>(S, T, S.clist2, nsmall, lane);
+      if (nbig) run_class<Tk, 32>(S, T, S.clist2 + nsmall, nbig, lane);
+      __syncwarp();
+    }
+
+    // (5) Exclusive scan of short counts; long pieces listed in order.
+    uint32_t run = 0, nlong = 0;
+    for (int k0 = 0; k0 < npieces; k0 += 32) {
+      const int k = k0 + lane;
+      const uint32_t c = k < npieces ? S.cnt[k] : 0;
+      const uint32_t inc = warp_incl_sum(c, lane);
+      const bool lg = k < npieces && S.plen[k] == 0xFF;
+      const unsigned lm = __ballot_sync(kFull, lg);
+      if (lg) S.lk[nlong + __popc(lm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+      nlong += __popc(lm);
+      __syncwarp();
+      if (k < npieces) S.cnt[k] = static_cast<uint16_t>(run + inc - c);
       run += __shfl_sync(kFull, inc, 31);
     }
-    if (lane == 0) S.pref[npieces] = run;
+    if (lane == 0) S.cnt[npieces] = static_cast<uint16_t>(run);
     __syncwarp();
-    const uint64_t agg = run;
-
-    // Decoupled look-back over tiles (tickets are handed out in order, so every
-    // predecessor is owned by a running warp).
-    uint64_t excl = 0;
-    if (tile == 0) {
-      if (lane == 0) st_release(&a.status[0], kFlagPrefix | agg);
-    } else {
-      if (lane == 0) st_release(&a.status[tile], kFlagAgg | agg);
-      int64_t look = int64_t(tile) - 1;
-      for (;;) {
-        const int64_t idx = look - lane;
-        uint64_t v = kFlagPrefix;
-        for (;;) {
-          if (idx >= 0) v = ld_acquire(&a.status[idx]);
-          if (__all_sync(kFull, (v >> 62) != 0)) break;
-          __nanosleep(64);
-        }
-        const unsigned pm = __ballot_sync(kFull, (v >> 62) == 2);
-        const int first_p = pm ? __ffs(pm) - 1 : 31;
-        uint64_t contrib = lane <= first_p ? (v & kValMask) : 0;
-        excl += warp_sum64(contrib);
-        if (pm) break;
-        look -= 32;
-      }
-      if (lane == 0) st_release(&a.status[tile], kFlagPrefix | (excl + agg));
-    }
-    const uint64_t base = excl;
-
-    // Token writes (short pieces by their lane; long pieces cooperatively).
-    const uint32_t* d2id = T.d2id;
-    for (int k0 = 0; k0 < npieces; k0 += 32) {
-      int k = k0 + lane;
-      if (k < npieces) {
-        const uint32_t c = S.pref[k + 1] - S.pref[k];
-        const int q = S.plist[k];
-        const int len = block_engine ? kLmax + 2 : next_boundary(S.w.bd, q, kLmax) - q;
-        if (len <= kLmax) {
-          uint32_t* dst = a.out_ids + base + S.pref[k];
-          for (uint32_t i = 0; i < c; ++i) {
-            uint32_t v = S.tok[q + i];
-            dst[i] = d2id ? __ldg(d2id + v) : v;
-          }
-        }
-      }
-    }
-    __syncwarp();
-    const uint32_t nlong = min((uint32_t)S.nlong, (uint32_t)kMaxLongPerTile);
+    // Long pieces (rare): full length = distance to the next hard boundary or
+    // the end of the row; k_long_pieces merges them after this kernel.
     for (uint32_t li = 0; li < nlong; ++li) {
-      const int k = S.longk[li];
-      const uint64_t start = b0 + S.plist[k];
-      const uint32_t c = S.pref[k + 1] - S.pref[k];
-      uint32_t* dst = a.out_ids + base + S.pref[k];
-      // k_long_pieces flags a piece that merged nothing (tokens = byte LUT).
-      const bool unchanged = (__ldcg(a.lpo + start) & kUnchanged) != 0;
-      const uint32_t* src = a.lpo + start + 1;
-      for (uint32_t i = lane; i < c; i += 32) {
-        uint32_t v = unchanged ? s_lut[a.bytes[start + i]] : __ldcg(src + i);
+      const uint64_t abs = b0 + S.plist[S.lk[li]];
+      uint64_t row_end = 0;
+      if (lane == 0) {
+        uint64_t lo = 0, hi = a.n_rows;  // max s with offsets[s] <= abs
+        while (lo < hi) {
+          const uint64_t mid = (lo + hi + 1) >> 1;
+          if (a.offsets[mid] <= abs) lo = mid; else hi = mid - 1;
+        }
+        row_end = a.offsets[lo + 1];
+      }
+      row_end = __shfl_sync(kFull, row_end, 0);
+      uint64_t end = row_end;
+      for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
+        const uint64_t y = x + lane;
+        const bool bnd = y < row_end && !is_junction(s_junc, a.bytes[y - 1], a.bytes[y]);
+        const unsigned bm = __ballot_sync(kFull, bnd);
+        if (bm) {
+          end = x + __ffs(bm) - 1;
+          break;
+        }
+      }
+      if (lane == 0) S.llen[li] = end - abs;
+    }
+    __syncwarp();
+
+    // (6) Stage short tokens in piece order (final ids).
+    uint32_t* stage = a.staging + tile * kStage;
+    for (int k = lane; k < npieces; k += 32) {
+      const int pl = S.plen[k];
+      if (pl == 0xFF) continue;
+      const int q = S.plist[k];
+      const uint32_t c = S.cnt[k + 1] - S.cnt[k];
+      uint32_t* dst = stage + S.cnt[k];
+      const Tk* src = (pl != 0xFF && (pl & kMemoDone)) ? S.rnk + q : S.tok + q;
+      for (uint32_t i = 0; i < c; ++i) {
+        const uint32_t v = src[i];
         dst[i] = d2id ? __ldg(d2id + v) : v;
       }
     }
-
-    // Row offsets for rows starting in this tile (the last tile also owns rows
-    // starting exactly at the end of the input, including offsets[n_rows]).
-    const uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
+    // (7) Long-piece records, tile short total.
+    if (lane == 0) {
+      uint64_t rec = 0;
+      if (nlong) {
+        const uint32_t first = atomicAdd(&a.counters[CNT_LREC], nlong);
+        for (uint32_t li = 0; li < nlong && first + li < a.lp_cap; ++li) {
+          const int k = S.lk[li];
+          a.lrec[first + li] = LongRec{b0 + S.plist[k], S.llen[li], 0, S.cnt[k], 0u};
+        }
+        rec = (uint64_t(first) << 24) | nlong;
+      }
+      a.tile_lrec[tile] = rec;
+      a.tile_count[tile] = run;
+    }
+    // (8) Row offsets relative to the tile: short tokens before the row in
+    // the low 40 bits, long pieces before it above; k_gather resolves them.
     for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
       const int o = static_cast<int>(a.offsets[s] - b0);
       int lo = 0, hi = npieces;  // first piece with plist >= o
       while (lo < hi) {
-        int mid = (lo + hi) >> 1;
+        const int mid = (lo + hi) >> 1;
         if (S.plist[mid] < o) lo = mid + 1; else hi = mid;
       }
-      a.out_offsets[s] = base + S.pref[lo];
+      uint64_t lb = 0;
+      while (lb < nlong && S.lk[lb] < lo) ++lb;
+      a.out_offsets[s] = uint64_t(S.cnt[lo]) | (lb << 40);
     }
     __syncwarp();
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_tile_scan: exclusive scan of tile token totals (short + long pieces) into
+// tile_base[0..num_tiles]. One CTA per kScanTiles tiles, CTAs chained by a
+// decoupled look-back (a few hundred CTAs even for GB inputs).
+constexpr int kScanThreads = 512;
+constexpr int kScanPer = 8;
+constexpr int kScanTiles = kScanThreads * kScanPer;
+static_assert(kScanTiles == kScanTilesPerCta, "scan geometry");
+
+__global__ void __launch_bounds__(kScanThreads) k_tile_scan(EncodeArgs a) {
+  __shared__ uint64_t s_warp[kScanThreads / 32];
+  __shared__ uint64_t s_base;
+  __shared__ uint32_t s_cta;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_cta = atomicAdd(&a.counters[CNT_GROUP_TICKET], 1u);
+  __syncthreads();
+  const uint64_t cta = s_cta;
+  const uint64_t t0 = cta * kScanTiles + uint64_t(tid) * kScanPer;
+  uint64_t v[kScanPer];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    const uint64_t t = t0 + i;
+    uint64_t c = 0;
+    if (t < a.num_tiles) {
+      c = __ldcg(a.tile_count + t);
+      const uint64_t rec = __ldcg(a.tile_lrec + t);
+      if (rec) {
+        const uint64_t first = rec >> 24;
+        const uint32_t nl = uint32_t(rec & 0xFFFFFF);
+        for (uint32_t li = 0; li < nl; ++li) c += __ldcg(&a.lrec[first + li].count);
+      }
+    }
+    v[i] = c;
+    sum += c;
+  }
+  // Block exclusive scan of per-thread sums.
+  uint64_t inc = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t u = __shfl_up_sync(kFull, inc, d);
+    if (lane >= d) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t x = lane < kScanThreads / 32 ? s_warp[lane] : 0;
+    uint64_t xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(kFull, xi, d);
+      if (lane >= d) xi += u;
+    }
+    if (lane < kScanThreads / 32) s_warp[lane] = xi - x;
+    const uint64_t agg = __shfl_sync(kFull, xi, 31);
+    // Look-back across CTAs (warp 0).
+    uint64_t excl = 0;
+    if (cta == 0) {
+      if (lane == 0) st_release(&a.status[0], kFlagPrefix | agg);
+    } else {
+      if (lane == 0) st_release(&a.status[cta], kFlagAgg | agg);
+      int64_t look = int64_t(cta) - 1;
+      for (;;) {
+        const int64_t idx = look - lane;
+        uint64_t sv = kFlagPrefix;
+        unsigned pm, xm;
+        for (;;) {
+          if (idx >= 0) sv = ld_acquire(&a.status[idx]);
+          pm = __ballot_sync(kFull, (sv >> 62) == 2);
+          xm = __ballot_sync(kFull, (sv >> 62) == 0);
+          const unsigned first_p = pm ? __ffs(pm) : 33, first_x = xm ? __ffs(xm) : 33;
+          if (first_x > first_p) break;
+          __nanosleep(64);
+        }
+        const int first_p = pm ? __ffs(pm) - 1 : 31;
+        excl += warp_sum64(lane <= first_p ? (sv & kValMask) : 0);
+        if (pm) break;
+        look -= 32;
+      }
+      if (lane == 0) st_release(&a.status[cta], kFlagPrefix | (excl + agg));
+    }
+    if (lane == 0) s_base = excl;
+  }
+  __syncthreads();
+  uint64_t run = s_base + s_warp[wid] + inc - sum;
+#pragma unroll
+  for (int i = 0; i < kScanPer; ++i) {
+    const uint64_t t = t0 + i;
+    if (t < a.num_tiles) a.tile_base[t] = run;
+    if (t == a.num_tiles - 1) a.tile_base[a.num_tiles] = run + v[i];
+    run += v[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_gather: warp per tile, fully parallel. Copies the tile's staged short
+// tokens and its long pieces (in piece order) to their final CSR place and
+// resolves the row offsets written by k_pieces.
+__device__ __forceinline__ void copy_tokens(uint32_t* dst, const uint32_t* src, uint32_t n, int lane) {
+  for (uint32_t i = lane; i < n; i += 32) dst[i] = __ldcg(src + i);
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevTable T) {
+  __shared__ uint32_t s_lut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t* d2id = T.d2id;
+  const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
+  for (uint64_t t = blockIdx.x * uint64_t(kWarpsPerCta) + (threadIdx.x >> 5); t < a.num_tiles; t += nwarps) {
+    const uint64_t tbase = __ldcg(a.tile_base + t);
+    const uint64_t rec = __ldcg(a.tile_lrec + t);
+    const uint32_t nshort = __ldcg(a.tile_count + t);
+    const uint32_t* stage = a.staging + t * kStage;
+    uint32_t* out = a.out_ids + tbase;
+    if (rec == 0) {
+      copy_tokens(out, stage, nshort, lane);
+    } else {
+      const uint64_t first = rec >> 24;
+      const uint32_t nl = uint32_t(rec & 0xFFFFFF);
+      uint64_t pos = 0;
+      uint32_t sp = 0;
+      for (uint32_t li = 0; li < nl; ++li) {
+        const LongRec lr = a.lrec[first + li];
+        copy_tokens(out + pos, stage + sp, lr.spref - sp, lane);
+        pos += lr.spref - sp;
+        sp = lr.spref;
+        const bool unchanged = (__ldcg(a.lpo + lr.start) & kUnchanged) != 0;
+        for (uint32_t i = lane; i < lr.count; i += 32) {
+          const uint32_t v = unchanged ? s_lut[a.bytes[lr.start + i]] : __ldcg(a.lpo + lr.start + 1 + i);
+          out[pos + i] = d2id ? __ldg(d2id + v) : v;
+        }
+        pos += lr.count;
+      }
+      copy_tokens(out + pos, stage + sp, nshort - sp, lane);
+    }
+    // Row offsets: short tokens before the row (low 40 bits) plus the first
+    // (v >> 40) long pieces of the tile.
+    const uint64_t s0 = a.tile_first[t], s1 = a.tile_first[t + 1];
+    for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
+      const uint64_t v = __ldcg(a.out_offsets + s);
+      const uint32_t lb = uint32_t(v >> 40);
+      uint64_t lsum = 0;
+      for (uint32_t li = 0; li < lb; ++li) lsum += __ldcg(&a.lrec[(rec >> 24) + li].count);
+      a.out_offsets[s] = tbase + (v & ((1ull << 40) - 1)) + lsum;
+    }
+  }
+}
+
 }  // namespace
+
+template <typename Tk>
+size_t pieces_smem() {
+  return sizeof(PieceSmem<Tk>) * kWarpsPerCta;
+}
 
 LaunchPlan plan_launch(int device) {
   LaunchPlan p;
   cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, device);
-  const size_t dyn = sizeof(WarpSmem) * kWarpsPerCta;
-  cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_encode, kWarpsPerCta * 32, dyn);
+  cudaFuncSetAttribute(k_pieces<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(pieces_smem<uint16_t>()));
+  cudaFuncSetAttribute(k_pieces<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(pieces_smem<uint32_t>()));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pieces<uint16_t>, kWarpsPerCta * 32,
+                                                pieces_smem<uint16_t>());
   p.main_grid = p.sm_count * (per_sm > 0 ? per_sm : 1);
-  int pre_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pre_sm, k_prepass, kWarpsPerCta * 32, 0);
-  p.prepass_grid = p.sm_count * (pre_sm > 0 ? pre_sm : 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pieces<uint32_t>, kWarpsPerCta * 32,
+                                                pieces_smem<uint32_t>());
+  p.main_grid_wide = p.sm_count * (per_sm > 0 ? per_sm : 1);
   int lp_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lp_sm, k_long_pieces<kLpThreads>, kLpThreads, 0);
   p.lp_grid = p.sm_count * (lp_sm > 0 ? lp_sm : 1);
+  int g_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_sm, k_gather, kWarpsPerCta * 32, 0);
+  p.gather_grid = p.sm_count * (g_sm > 0 ? g_sm : 1);
   return p;
 }
 
@@ -738,16 +1052,21 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     ++launched;
   }
   if (ev) cudaEventRecord(ev[1], stream);
-  k_prepass<<<p.prepass_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
+  if (a.narrow)
+    k_pieces<uint16_t><<<p.main_grid, kWarpsPerCta * 32, pieces_smem<uint16_t>(), stream>>>(a, t);
+  else
+    k_pieces<uint32_t><<<p.main_grid_wide, kWarpsPerCta * 32, pieces_smem<uint32_t>(), stream>>>(a, t);
   ++launched;
   if (ev) cudaEventRecord(ev[2], stream);
   k_long_pieces<kLpThreads><<<p.lp_grid, kLpThreads, 0, stream>>>(a, t);
   ++launched;
   if (ev) cudaEventRecord(ev[3], stream);
-  const size_t dyn = sizeof(WarpSmem) * kWarpsPerCta;
-  k_encode<<<p.main_grid, kWarpsPerCta * 32, dyn, stream>>>(a, t);
+  k_tile_scan<<<unsigned((a.num_tiles + kScanTiles - 1) / kScanTiles), kScanThreads, 0, stream>>>(a);
   ++launched;
   if (ev) cudaEventRecord(ev[4], stream);
+  k_gather<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
+  ++launched;
+  if (ev) cudaEventRecord(ev[5], stream);
   return launched;
 }
 

@@ -12,18 +12,26 @@ namespace bbpe {
 constexpr int kTile = 512;          // input bytes owned by one warp-tile
 constexpr int kLmax = 32;           // longest piece merged by a single lane
 constexpr int kWin = kTile + kLmax + 1;  // window positions [0, kWin) after b0
+constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece tokens)
+constexpr int kScanTilesPerCta = 4096;  // k_tile_scan: 512 threads x 8 tiles
 constexpr int kWarpsPerCta = 8;
 constexpr int kLpThreads = 512;     // CTA size of the long-piece (block engine) kernel
 
 // Counter slots (u32).
-enum { CNT_TILE_TICKET = 0, CNT_LP_COUNT = 1, CNT_LP_NEXT = 2, CNT_N = 8 };
+enum { CNT_TILE_TICKET = 0, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4, CNT_N = 8 };
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_N = 4 };
 
-struct LongPiece {
-  uint64_t start;  // absolute byte position (or token position for token input)
+// A long piece (> kLmax bytes, or a whole row under BBPE_ENGINE_BLOCK): found
+// by k_pieces, merged by k_long_pieces, placed by k_gather. Records of one
+// tile are contiguous and in piece order; `spref` short tokens of the tile
+// precede the piece.
+struct LongRec {
+  uint64_t start;  // absolute byte position (token position for token input)
   uint64_t len;
-  uint64_t row;
+  uint64_t row;    // row index (MaxPassesError reporting)
+  uint32_t spref;
+  uint32_t count;  // tokens out, written by k_long_pieces
 };
 
 struct EncodeArgs {
@@ -36,10 +44,15 @@ struct EncodeArgs {
   uint64_t* out_offsets;
   // scratch
   uint64_t* tile_first;     // num_tiles + 1
-  uint64_t* status;         // num_tiles look-back words
+  uint64_t* status;         // look-back words of k_tile_scan's CTAs
+  uint64_t num_groups;      // k_tile_scan CTAs
+  uint64_t* tile_base;      // num_tiles + 1: first output token of each tile
+  uint32_t* staging;        // num_tiles * kStage: each tile's short-piece tokens, in order
+  uint32_t* tile_count;     // num_tiles: tokens produced by the tile (short + long)
+  uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n, 0 when none
+  LongRec* lrec;            // lp_cap records (CNT_LREC used)
   uint32_t* counters;       // CNT_N
   uint64_t* err;            // ERR_N
-  LongPiece* lp;
   uint64_t lp_cap;
   uint32_t* lpo;            // total + 1: long-piece results {count, tokens...} at start
   uint64_t* lpx;            // total: long-piece working set {token | rank << 32}
@@ -48,20 +61,23 @@ struct EncodeArgs {
   uint64_t trace_cap;
   uint64_t* trace_count;
   int engine;               // bbpe_engine
+  int narrow;               // 1: 16-bit working arrays (ids < 0xFFFE, merges < 0xFFFE)
+  int use_memo;             // 1: look whole pieces up in the table's piece memo first
   int tokens_input;         // 1: lpx already holds initial tokens (bbpe_block_bpe)
   int64_t max_passes;       // <= 0: none
 };
 
 struct LaunchPlan {
   int main_grid = 0;
-  int prepass_grid = 0;
+  int main_grid_wide = 0;
+  int gather_grid = 0;
   int lp_grid = 0;
   int sm_count = 0;
 };
 
 LaunchPlan plan_launch(int device);
 // Enqueues the full encode on `stream`; returns the number of kernels launched.
-// ev (optional): 5 events recorded before the first and after each kernel.
+// ev (optional): BBPE_N_KERNELS + 1 events, before the first and after each kernel.
 int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, cudaStream_t stream,
                   cudaEvent_t* ev = nullptr);
 // Long-piece kernel only (token input, used by bbpe_block_bpe).

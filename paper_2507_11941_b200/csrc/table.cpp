@@ -374,6 +374,10 @@ void build_device_layout(bbpe_table& t) {
       throw usage_error("merge table too large for the device pair key");
   }
   t.id_bits = static_cast<uint32_t>(idb);
+  {
+    const uint64_t max_dense = t.remap ? t.dense_to_id.size() : uint64_t(max_dev_id);
+    t.narrow = max_dense < 0xFFFDull && M < 0xFFFDull;
+  }
 
   // Bucketised open addressing, load <= 0.5.
   uint64_t buckets = 1;
@@ -472,6 +476,12 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
   return pos->second.view;
 }
 
+DeviceReplica& replica_of(const bbpe_table& tc, int device) {
+  bbpe_table& t = const_cast<bbpe_table&>(tc);
+  std::lock_guard<std::mutex> lock(t.mu);
+  return t.replicas.at(device);
+}
+
 void release_replicas(bbpe_table& t) {
   std::lock_guard<std::mutex> lock(t.mu);
   int prev = 0;
@@ -479,6 +489,7 @@ void release_replicas(bbpe_table& t) {
   for (auto& [dev, rep] : t.replicas) {
     cudaSetDevice(dev);
     cudaFree(rep.base);
+    if (rep.memo) cudaFree(rep.memo);
   }
   cudaSetDevice(prev);
   t.replicas.clear();

@@ -12,12 +12,18 @@ from conftest import GOLDEN, VECTOR_SETS, load_vectors, table_from_json
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = ["pieces", "block"]
+ENGINES = ["pieces", "nomemo", "block"]
+
+
+def make_encoder(name, **kw):
+    if name == "nomemo":
+        return bb.Encoder(device=0, engine="pieces", piece_memo=False, **kw)
+    return bb.Encoder(device=0, engine=name, **kw)
 
 
 @pytest.fixture(scope="module")
 def enc():
-    return {e: bb.Encoder(device=0, engine=e) for e in ENGINES}
+    return {e: make_encoder(e) for e in ENGINES}
 
 
 @pytest.fixture(scope="module")
@@ -150,7 +156,7 @@ def test_block_size_is_results_neutral(gpt2):
     outs = []
     for bs in (32, 64, 256, 1024):
         for eng in ENGINES:
-            outs.append(bb.Encoder(0, bb.BlockConfig(bs, None), engine=eng).encode_rows(gpt2, rows))
+            outs.append(make_encoder(eng, config=bb.BlockConfig(bs, None)).encode_rows(gpt2, rows))
     assert all(o == outs[0] for o in outs)
 
 
@@ -201,9 +207,10 @@ def test_config_parity_vs_reference_engines(cfg, scale, gpt2, oracle_for):
     from paper_2507_11941_b200 import synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off, _ = synth.config_rows(gen, cfg, scale=scale)
-    ids, oo, _ = bb.Encoder(0).encode_packed(gpt2, data, off)
     wi, wo = oracle_for("gpt2").encode_packed(data, off, engine=1)
-    assert np.array_equal(oo, wo) and np.array_equal(ids, wi)
+    for name in ("pieces", "nomemo"):
+        ids, oo, _ = make_encoder(name).encode_packed(gpt2, data, off)
+        assert np.array_equal(oo, wo) and np.array_equal(ids, wi), name
 
 
 def test_full_size_cfg2_properties(gpt2):
