@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbbpe_b200.so")
+# BBPE_LIB_PATH selects an alternative in-tree build (A/B experiments).
+LIB_PATH = os.environ.get("BBPE_LIB_PATH") or os.path.join(_HERE, "libbbpe_b200.so")
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)

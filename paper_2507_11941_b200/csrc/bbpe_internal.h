@@ -52,8 +52,18 @@ struct DevTable {
   uint32_t id_bits = 0;
   uint32_t rank_bits = 0;
   uint32_t n_merges = 0;
-  uint32_t pad = 0;
+  uint32_t key32 = 0;  // 1: 32-bit pair keys (ids < 2^16): slot = key32 << 32 | rank
 };
+
+// Bucket hash of a 32-bit pair key (murmur3 finaliser).
+__host__ __device__ inline uint32_t mix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h;
+}
 
 // 32-byte memo entry: piece bytes (zero padded), length, 1-2 result tokens
 // (dense ids). len == 0 marks an empty slot.
@@ -105,7 +115,7 @@ struct bbpe_table {
   // Device layout, built once on the host.
   uint32_t id_bits = 0, rank_bits = 0;
   bool remap = false;
-  bool narrow = false;  // 16-bit device working arrays suffice
+  bool narrow = false;  // 16-bit device working arrays and 32-bit pair keys suffice
   std::unordered_map<uint32_t, uint32_t> dense_of;  // only when remap
   std::vector<uint32_t> dense_to_id;                // only when remap
   std::vector<uint64_t> slots;

@@ -92,6 +92,43 @@ bool is_pinned(const void* p) {
   return attr.type == cudaMemoryTypeHost;
 }
 
+
+// One in-flight wave of the pipelined host encode (double-buffered).
+struct WaveSet {
+  DevBuf in_bytes, in_offsets, out_ids, out_offsets, err;
+  uint64_t* h_off = nullptr;  // pinned: the wave's CSR offsets
+  uint64_t* h_rel = nullptr;  // pinned: the wave's input offsets, rebased
+  uint64_t* h_err = nullptr;  // pinned: error slots
+  uint64_t h_cap = 0;
+  cudaEvent_t h2d_done = nullptr, comp_done = nullptr, off_done = nullptr, d2h_done = nullptr;
+  uint64_t r0 = 0, r1 = 0;
+  bool used = false;
+  void init() {
+    if (h2d_done) return;
+    for (cudaEvent_t* e : {&h2d_done, &comp_done, &off_done, &d2h_done})
+      ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_err), bbpe::ERR_N * 8, 0), "cudaHostAlloc");
+  }
+  void reserve_host(uint64_t rows) {
+    if (rows + 1 <= h_cap) return;
+    if (h_off) cudaFreeHost(h_off);
+    if (h_rel) cudaFreeHost(h_rel);
+    h_cap = rows + 1 + (rows + 1) / 4;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_off), h_cap * 8, 0), "cudaHostAlloc");
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&h_rel), h_cap * 8, 0), "cudaHostAlloc");
+  }
+  void release() {
+    for (DevBuf* b : {&in_bytes, &in_offsets, &out_ids, &out_offsets, &err}) b->release();
+    if (h_off) cudaFreeHost(h_off);
+    if (h_rel) cudaFreeHost(h_rel);
+    if (h_err) cudaFreeHost(h_err);
+    for (cudaEvent_t e : {h2d_done, comp_done, off_done, d2h_done})
+      if (e) cudaEventDestroy(e);
+    h_off = h_rel = h_err = nullptr;
+    h2d_done = comp_done = off_done = d2h_done = nullptr;
+  }
+};
+
 }  // namespace
 
 struct bbpe_ctx {
@@ -116,6 +153,11 @@ struct bbpe_ctx {
   size_t ev_used = 0;
   double kernel_ms[BBPE_N_KERNELS] = {};
   uint64_t timed_calls = 0;
+  // Pipelined host encode.
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr, off_stream = nullptr;
+  static constexpr int kSets = 3;
+  WaveSet sets[kSets];
+  DevBuf run_base;
 };
 
 namespace {
@@ -141,7 +183,7 @@ struct DeviceGuard {
 // Sizes scratch and fills EncodeArgs for a device-resident batch.
 bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_t* d_offsets,
                               uint64_t n, uint64_t total, uint32_t* d_out, uint64_t* d_out_off,
-                              cudaStream_t s) {
+                              cudaStream_t s, uint64_t* err = nullptr) {
   using namespace bbpe;
   EncodeArgs a{};
   a.bytes = d_bytes;
@@ -174,7 +216,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   a.tile_base = c.tile_base.as<uint64_t>();
   a.lrec = c.lrec.as<LongRec>();
   a.counters = c.counters.as<uint32_t>();
-  a.err = c.err.as<uint64_t>();
+  a.err = err ? err : c.err.as<uint64_t>();
   a.lpo = c.lpo.as<uint32_t>();
   a.lpx = c.lpx.as<uint64_t>();
   a.lpy = c.lpy.as<uint64_t>();
@@ -195,11 +237,17 @@ void ensure_memo(bbpe_ctx& c, const bbpe_table& t);
 // Enqueue a device-resident encode. Handles the empty-input corner cases.
 void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
                     const uint64_t* d_offsets, uint64_t n, uint64_t total, uint32_t* d_out,
-                    uint64_t* d_out_off, cudaStream_t s, bool allow_memo = true) {
+                    uint64_t* d_out_off, cudaStream_t s, bool allow_memo = true,
+                    uint64_t* err = nullptr, uint64_t* run_base = nullptr) {
   if (total == 0) {
-    ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
+    if (run_base) {
+      bbpe::launch_fill_offsets(d_out_off, n + 1, run_base, s);
+      c.launches += 1;
+    } else {
+      ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
+    }
     c.err.ensure(bbpe::ERR_N * 8);
-    ck(cudaMemsetAsync(c.err.p, 0xFF, bbpe::ERR_N * 8, s), "memset err");
+    ck(cudaMemsetAsync(err ? err : c.err.as<uint64_t>(), 0xFF, bbpe::ERR_N * 8, s), "memset err");
     return;
   }
   bbpe::table_on_device(t, c.device);
@@ -209,9 +257,10 @@ void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
   // The memo itself is built at API entry (maybe_build_memo), never here:
   // building encodes through the ctx's own staging buffers.
   const bbpe::DevTable dt = bbpe::table_on_device(t, c.device);
-  bbpe::EncodeArgs a = prepare_args(c, d_bytes, d_offsets, n, total, d_out, d_out_off, s);
+  bbpe::EncodeArgs a = prepare_args(c, d_bytes, d_offsets, n, total, d_out, d_out_off, s, err);
   a.narrow = t.narrow ? 1 : 0;
   a.use_memo = memo && dt.memo ? 1 : 0;
+  a.run_base = run_base;
   if (c.ev_used == c.ev_sets.size()) {
     std::array<cudaEvent_t, BBPE_N_KERNELS + 1> set{};
     for (auto& e : set) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -220,6 +269,10 @@ void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
   }
   c.ev_streams[c.ev_used] = s;
   c.launches += bbpe::launch_encode(a, dt, c.plan, s, c.ev_sets[c.ev_used++].data());
+  if (run_base) {
+    bbpe::launch_advance_base(run_base, a.tile_base + a.num_tiles, s);
+    c.launches += 1;
+  }
   ck(cudaGetLastError(), "kernel launch");
 }
 
@@ -243,11 +296,22 @@ uint64_t row_of(const uint64_t* host_offsets, uint64_t n, uint64_t pos) {
 
 // Reads the device error slots; throws the reference's exception for the
 // lowest failing row (the inline encode_batch reports the first row).
+void raise_device_errors(bbpe_ctx& c, const uint64_t* err, const uint64_t* host_offsets, uint64_t n,
+                         uint64_t row_base, const uint8_t* host_bytes, const uint64_t* d_offsets,
+                         const uint8_t* d_bytes);
+
 void check_device_errors(bbpe_ctx& c, const uint64_t* host_offsets, uint64_t n, uint64_t row_base,
                          const uint8_t* host_bytes, const uint64_t* d_offsets,
                          const uint8_t* d_bytes) {
   uint64_t err[bbpe::ERR_N];
   ck(cudaMemcpy(err, c.err.p, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
+  raise_device_errors(c, err, host_offsets, n, row_base, host_bytes, d_offsets, d_bytes);
+}
+
+// Throws the reference's exception for the lowest failing row, if any.
+void raise_device_errors(bbpe_ctx& c, const uint64_t* err, const uint64_t* host_offsets, uint64_t n,
+                         uint64_t row_base, const uint8_t* host_bytes, const uint64_t* d_offsets,
+                         const uint8_t* d_bytes) {
   const uint64_t none = ~0ull;
   if (err[bbpe::ERR_BAD_BYTE_POS] == none && err[bbpe::ERR_MAXPASS_ROW] == none) return;
   std::vector<uint64_t> tmp;
@@ -318,6 +382,130 @@ uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
   if (st) st->d2h_ms += ms_since(t1);
   for (uint64_t i = 0; i <= n; ++i) out_offsets[r0 + i] = out_pos + oo[i];
   return ntok;
+}
+
+// Host-buffer encode, pipelined over waves of at most cfg.wave_bytes: the H2D
+// of wave k+1 and the D2H of wave k-1 overlap the kernels of wave k (three
+// streams, three buffer sets). The only host waits are on each wave's row
+// offsets (copied on the compute stream right after its kernels), which size
+// its id copy on the D2H stream.
+uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
+                               const uint64_t* offsets, uint64_t n, uint32_t* out_ids,
+                               uint64_t out_capacity, uint64_t* out_offsets, bbpe_stats* st) {
+  using namespace bbpe;
+  const uint64_t total_all = offsets[n] - offsets[0];
+  uint64_t wave = c.cfg.wave_bytes;
+  if (!wave) wave = std::max<uint64_t>(16ull << 20, std::min<uint64_t>(64ull << 20, total_all / 8 + 1));
+  std::vector<std::pair<uint64_t, uint64_t>> waves;
+  uint64_t max_rows = 0, max_bytes = 0;
+  {
+    uint64_t r0 = 0;
+    do {
+      uint64_t r1 = r0;
+      // Rows of a wave: at least one, then as many as fit in `wave` bytes
+      // (binary search on the offsets: O(log n) per wave).
+      uint64_t lo = r0 + 1, hi = n;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi + 1) / 2;
+        if (offsets[mid] - offsets[r0] <= wave) lo = mid; else hi = mid - 1;
+      }
+      r1 = std::min<uint64_t>(n, std::max<uint64_t>(lo, r0 + 1));
+      if (n == 0) r1 = 0;
+      waves.push_back({r0, r1});
+      max_rows = std::max(max_rows, r1 - r0);
+      max_bytes = std::max(max_bytes, offsets[r1] - offsets[r0]);
+      r0 = r1;
+    } while (r0 < n);
+  }
+  if (!c.h2d_stream) ck(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking), "stream");
+  if (!c.d2h_stream) ck(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking), "stream");
+  if (!c.off_stream) ck(cudaStreamCreateWithFlags(&c.off_stream, cudaStreamNonBlocking), "stream");
+  for (WaveSet& w : c.sets) {
+    w.init();
+    w.in_bytes.ensure(std::max<uint64_t>(max_bytes, 1) + 16);
+    w.in_offsets.ensure((max_rows + 1) * 8);
+    w.out_ids.ensure(std::max<uint64_t>(max_bytes, 1) * 4);
+    w.out_offsets.ensure((max_rows + 1) * 8);
+    w.err.ensure(ERR_N * 8);
+    w.used = false;
+  }
+  c.run_base.ensure(8);
+  ck(cudaMemsetAsync(c.run_base.p, 0, 8, c.stream), "memset run_base");
+  constexpr int K = bbpe_ctx::kSets;
+  auto t0 = std::chrono::steady_clock::now();
+  double k_before = 0;
+  {
+    double ms[BBPE_N_KERNELS];
+    bbpe_ctx_kernel_times(&c, ms, nullptr, 0);
+    for (double v : ms) k_before += v;
+  }
+
+  auto launch = [&](size_t k) {
+    WaveSet& w = c.sets[k % K];
+    if (w.used) ck(cudaStreamWaitEvent(c.h2d_stream, w.d2h_done, 0), "wait");
+    w.used = true;
+    w.r0 = waves[k].first;
+    w.r1 = waves[k].second;
+    const uint64_t nr = w.r1 - w.r0, base = offsets[w.r0], tot = offsets[w.r1] - base;
+    if (tot)
+      ck(cudaMemcpyAsync(w.in_bytes.p, bytes + base, tot, cudaMemcpyHostToDevice, c.h2d_stream), "H2D bytes");
+    ck(cudaMemcpyAsync(w.in_offsets.p, offsets + w.r0, (nr + 1) * 8, cudaMemcpyHostToDevice, c.h2d_stream),
+       "H2D offsets");
+    ck(cudaEventRecord(w.h2d_done, c.h2d_stream), "event");
+    ck(cudaStreamWaitEvent(c.stream, w.h2d_done, 0), "wait");
+    launch_rebase_input(w.in_offsets.as<uint64_t>(), nr + 1, base, c.stream);
+    enqueue_encode(c, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
+                   w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), c.stream, true,
+                   w.err.as<uint64_t>(), c.run_base.as<uint64_t>());
+    // Final (global) row offsets straight into the caller's array, on their
+    // own stream so neither the kernels nor the id copies queue behind them.
+    ck(cudaEventRecord(w.comp_done, c.stream), "event");
+    ck(cudaStreamWaitEvent(c.off_stream, w.comp_done, 0), "wait");
+    ck(cudaMemcpyAsync(out_offsets + w.r0, w.out_offsets.p, (nr + 1) * 8, cudaMemcpyDeviceToHost,
+                       c.off_stream), "D2H offsets");
+    ck(cudaMemcpyAsync(w.h_err, w.err.p, ERR_N * 8, cudaMemcpyDeviceToHost, c.off_stream), "D2H err");
+    ck(cudaEventRecord(w.off_done, c.off_stream), "event");
+  };
+
+  size_t launched = 0;
+  while (launched < waves.size() && launched < size_t(K - 1)) launch(launched++);
+  try {
+    for (size_t k = 0; k < waves.size(); ++k) {
+      if (launched < waves.size()) launch(launched++);
+      WaveSet& w = c.sets[k % K];
+      ck(cudaEventSynchronize(w.off_done), "encode");
+      const uint64_t nr = w.r1 - w.r0, base = offsets[w.r0];
+      if (w.h_err[ERR_BAD_BYTE_POS] != ~0ull || w.h_err[ERR_MAXPASS_ROW] != ~0ull) {
+        std::vector<uint64_t> rel(nr + 1);
+        for (uint64_t i = 0; i <= nr; ++i) rel[i] = offsets[w.r0 + i] - base;
+        raise_device_errors(c, w.h_err, rel.data(), nr, w.r0, bytes + base, nullptr, nullptr);
+      }
+      const uint64_t first = out_offsets[w.r0], ntok = out_offsets[w.r1] - first;
+      if (first + ntok > out_capacity)
+        throw usage_error("output capacity " + std::to_string(out_capacity) + " is smaller than the " +
+                          std::to_string(first + ntok) + " tokens produced");
+      if (ntok)
+        ck(cudaMemcpyAsync(out_ids + first, w.out_ids.p, ntok * 4, cudaMemcpyDeviceToHost, c.d2h_stream),
+           "D2H ids");
+      ck(cudaEventRecord(w.d2h_done, c.d2h_stream), "event");
+    }
+    ck(cudaStreamSynchronize(c.d2h_stream), "D2H ids");
+  } catch (...) {
+    cudaStreamSynchronize(c.h2d_stream);
+    cudaStreamSynchronize(c.stream);
+    cudaStreamSynchronize(c.off_stream);
+    cudaStreamSynchronize(c.d2h_stream);
+    throw;
+  }
+  if (st) {
+    double ms[BBPE_N_KERNELS], k_after = 0;
+    bbpe_ctx_kernel_times(&c, ms, nullptr, 0);
+    for (double v : ms) k_after += v;
+    st->device_ms = k_after - k_before;
+    st->waves = waves.size();
+    st->total_ms = ms_since(t0);
+  }
+  return out_offsets[n];
 }
 
 // Builds the piece memo for (table, ctx device) once: every vocabulary token of
@@ -538,6 +726,11 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaEventDestroy(c->ev1);
     for (auto& set : c->ev_sets)
       for (auto e : set) cudaEventDestroy(e);
+    for (WaveSet& w : c->sets) w.release();
+    c->run_base.release();
+    if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+    if (c->off_stream) cudaStreamDestroy(c->off_stream);
     cudaStreamDestroy(c->stream);
     cudaSetDevice(prev);
   }
@@ -587,29 +780,21 @@ int bbpe_encode(bbpe_ctx* c, const bbpe_table* t, const uint8_t* bytes, const ui
   auto t0 = std::chrono::steady_clock::now();
   if (!c || !t || !offsets || !out_offsets) throw bbpe::usage_error("null argument");
   validate_config(c->cfg);
-  for (size_t i = 0; i < n; ++i)
-    if (offsets[i + 1] < offsets[i]) throw bbpe::usage_error("offsets must be non-decreasing");
+  {
+    bool bad = false;
+    for (size_t i = 0; i < n; ++i) bad |= offsets[i + 1] < offsets[i];
+    if (bad) throw bbpe::usage_error("offsets must be non-decreasing");
+  }
   if (offsets[n] > offsets[0] && (!bytes || !out_ids)) throw bbpe::usage_error("null buffer");
   DeviceGuard g(c->device);
   maybe_build_memo(*c, *t);
   if (st) *st = bbpe_stats{};
-  // Waves: row ranges of at most wave_bytes (a row is never split).
-  const uint64_t wave = c->cfg.wave_bytes ? c->cfg.wave_bytes : (1ull << 31);
-  uint64_t pos = 0, waves = 0;
-  out_offsets[0] = 0;
-  uint64_t r0 = 0;
-  do {
-    uint64_t r1 = r0;
-    while (r1 < n && (r1 == r0 || offsets[r1 + 1] - offsets[r0] <= wave)) ++r1;
-    pos += encode_wave(*c, *t, bytes, offsets, r0, r1, out_ids, pos, out_capacity, out_offsets, st);
-    ++waves;
-    r0 = r1;
-  } while (r0 < n);
+  const uint64_t pos =
+      encode_host_pipelined(*c, *t, bytes, offsets, n, out_ids, out_capacity, out_offsets, st);
   if (st) {
     st->n_rows = n;
     st->input_bytes = offsets[n] - offsets[0];
     st->tokens = pos;
-    st->waves = waves;
     st->total_ms = ms_since(t0);
   }
   return BBPE_OK;

@@ -50,7 +50,24 @@ __device__ __forceinline__ uint64_t dmix64(uint64_t h) {
 }
 
 // Pair -> dense rank (kNoRank when absent). One 32-byte bucket per step.
+__device__ __forceinline__ uint32_t probe32(const DevTable& T, uint32_t l, uint32_t r) {
+  const uint32_t key = (l << 16) | r;
+  uint64_t b = mix32(key) & T.bucket_mask;
+  for (;;) {
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + b * kBucketSlots);
+    const ulonglong2 s01 = __ldg(p), s23 = __ldg(p + 1);
+    const uint64_t s[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (s[j] == kEmptySlot) return kNoRank;
+      if (uint32_t(s[j] >> 32) == key) return uint32_t(s[j]);
+    }
+    b = (b + 1) & T.bucket_mask;
+  }
+}
+
 __device__ __forceinline__ uint32_t probe(const DevTable& T, uint32_t l, uint32_t r) {
+  if (T.key32) return probe32(T, l, r);
   const uint64_t key = (uint64_t(l) << T.id_bits) | uint64_t(r);
   uint64_t b = dmix64(key) & T.bucket_mask;
   const uint64_t rmask = (1ull << T.rank_bits) - 1;
@@ -133,6 +150,7 @@ __device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc
   const uint64_t b0 = tile * kTile;
   const uint64_t wbase = b0 >= 4 ? b0 - 4 : 0;
   const int wofs = b0 >= 4 ? 0 : 1;  // tile 0: word 0 of the window is before the input
+#pragma unroll 1
   for (int i = lane; i < kWinWordsB; i += 32) {
     const int gi = i - wofs;
     uint32_t v = 0;
@@ -165,6 +183,7 @@ __device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc
   __syncwarp();
   // Boundaries, and the invalid-byte check (pretokenize.hpp:64-67).
   uint32_t badw = 0xFFFFFFFFu;
+#pragma unroll 1
   for (int wd = 0; wd < kWords; ++wd) {
     const int q = wd * 32 + lane;
     const uint64_t abs = b0 + q;
@@ -440,50 +459,65 @@ struct PieceSmem {
   uint16_t plist[kTile];      // piece starts (window-relative), in order
   uint8_t plen[kTile];        // piece length, 0xFF = long (> kLmax)
   uint16_t clist[kTile];      // pieces that need merge passes
-  uint16_t clist2[kTile];     // the same, <= 8 tokens first
   uint16_t cnt[kTile + 1];    // short tokens per piece -> exclusive prefix
   Tk tok[kWin + 1];
   Tk rnk[kWin + 1];
-  uint32_t sct[32];           // pass compaction scratch: token
-  uint32_t scr[32];           //                          rank
-  uint8_t scf[32];            //                          merged flag
   uint64_t llen[kTile / (kLmax + 1) + 2];    // byte length of each long piece, in order
   uint16_t lk[kTile / (kLmax + 1) + 2];      // their piece indices
 };
 
-// Batched probe: issue the bucket loads, resolve later.
+// Batched probe: issue the bucket loads, resolve later. K32: narrow tables
+// (ids < 2^16) with 32-bit keys, slot = key32 << 32 | rank.
 struct ProbeReq {
   uint64_t key, b;
   ulonglong2 s01, s23;
 };
+template <bool K32>
 __device__ __forceinline__ void probe_issue(ProbeReq& q, const DevTable& T, uint32_t l, uint32_t r) {
-  q.key = (uint64_t(l) << T.id_bits) | uint64_t(r);
-  q.b = dmix64(q.key) & T.bucket_mask;
+  if (K32) {
+    const uint32_t k32 = (l << 16) | r;
+    q.key = k32;
+    q.b = mix32(k32) & T.bucket_mask;
+  } else {
+    q.key = (uint64_t(l) << T.id_bits) | uint64_t(r);
+    q.b = dmix64(q.key) & T.bucket_mask;
+  }
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + q.b * kBucketSlots);
   q.s01 = __ldg(p);
   q.s23 = __ldg(p + 1);
 }
-__device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTable& T) {
+
+// Bucket full without a hit: keep probing linearly (rare at load <= 0.5).
+template <bool K32>
+__device__ __noinline__ uint32_t probe_overflow(const DevTable& T, uint64_t key, uint64_t b) {
   const uint64_t rmask = (1ull << T.rank_bits) - 1;
-  uint64_t s[4] = {q.s01.x, q.s01.y, q.s23.x, q.s23.y};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (s[j] == kEmptySlot) return kNoRank;
-    if ((s[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(s[j] & rmask);
-  }
-  // Bucket full without a hit: continue linearly (rare at load <= 0.5).
-  uint64_t b = q.b;
   for (;;) {
     b = (b + 1) & T.bucket_mask;
     const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + b * kBucketSlots);
-    ulonglong2 a = __ldg(p), c = __ldg(p + 1);
-    uint64_t t[4] = {a.x, a.y, c.x, c.y};
+    const ulonglong2 x = __ldg(p), y = __ldg(p + 1);
+    const uint64_t t[4] = {x.x, x.y, y.x, y.y};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (t[j] == kEmptySlot) return kNoRank;
-      if ((t[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(t[j] & rmask);
+      if (K32 ? (uint32_t(t[j] >> 32) == uint32_t(key)) : ((t[j] >> T.rank_bits) == key))
+        return K32 ? uint32_t(t[j]) : static_cast<uint32_t>(t[j] & rmask);
     }
   }
+}
+
+template <bool K32>
+__device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTable& T) {
+  const uint64_t s[4] = {q.s01.x, q.s01.y, q.s23.x, q.s23.y};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (s[j] == kEmptySlot) return kNoRank;
+    if (K32) {
+      if (uint32_t(s[j] >> 32) == uint32_t(q.key)) return uint32_t(s[j]);
+    } else {
+      if ((s[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(s[j] & ((1ull << T.rank_bits) - 1));
+    }
+  }
+  return probe_overflow<K32>(T, q.key, q.b);
 }
 
 template <typename Tk>
@@ -491,93 +525,78 @@ __device__ __forceinline__ uint32_t tk_rank(uint32_t r) {
   return r == kNoRank ? Marks<Tk>::kNone : r;
 }
 
-// Left-greedy marking over W candidate bits (block_engine.hpp:107-109):
-// pair b merges iff it is at the minimum and pair b-1 did not merge.
-template <int W>
-__device__ __forceinline__ unsigned left_greedy(unsigned E) {
-  if (!(E & (E << 1))) return E;  // no adjacent candidates: every one merges
-  unsigned F = 0;
-#pragma unroll
-  for (int b = 0; b < W; ++b)
-    if (((E >> b) & 1u) && !(b > 0 && ((F >> (b - 1)) & 1u))) F |= 1u << b;
-  return F;
-}
-
-// Runs every piece in `list` (pieces of 2..W tokens) through the pass loop,
-// 32/W pieces at a time, refilling groups as their pieces finish.
-template <typename Tk, int W>
-__device__ void run_class(PieceSmem<Tk>& S, const DevTable& T, const uint16_t* list, int count,
-                          int lane) {
-  constexpr uint32_t NONE = Marks<Tk>::kNone;
-  const int g = lane / W, gl = lane % W, gbase = g * W;
-  const unsigned wmask = W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u);
-  int next = 0, pk = 0, q = 0, n = 0;
-  uint32_t t = NONE, r = NONE;
-  for (;;) {
-    const bool idle = n == 0;
-    const unsigned lead = __ballot_sync(kFull, idle && gl == 0);
-    if (idle) {
-      const int k = next + __popc(lead & ((1u << gbase) - 1u));
-      if (k < count) {
-        pk = list[k];
-        q = S.plist[pk];
-        n = S.plen[pk];
-        t = gl < n ? uint32_t(S.tok[q + gl]) : NONE;
-        r = gl < n - 1 ? uint32_t(S.rnk[q + gl]) : NONE;
-      }
+// One lane, one pass of the reference loop over a piece of n <= kLmax tokens
+// at tok[0..n) / rnk[0..n-1) (block_engine.hpp:286-307): min over cached
+// ranks, sweep-compact in place (a pair at the minimum merges unless its left
+// token was just consumed -- exactly flags[i+1] = (ranks[i] == m && !flags[i])),
+// then re-probe only the pairs touching a merged token, two in flight.
+// Returns the new length, or -1 when no pair is mergeable.
+template <typename Tk>
+__device__ __forceinline__ int lane_pass(const DevTable& T, Tk* tok, Tk* rnk, int n) {
+  constexpr bool K32 = sizeof(Tk) == 2;  // narrow tables use 32-bit pair keys
+  constexpr uint32_t NONE = Marks<Tk>::kNone, PROBE = Marks<Tk>::kNone - 1;
+  uint32_t m = NONE;
+  for (int i = 0; i < n - 1; ++i) m = min(m, uint32_t(rnk[i]));
+  if (m == NONE) return -1;
+  const Tk M = Tk(__ldg(T.r2m + m));
+  int j = 0, i = 0;
+  while (i < n) {
+    const uint32_t ri = (i < n - 1) ? uint32_t(rnk[i]) : NONE;
+    if (ri == m) {
+      tok[j] = M;
+      rnk[j] = Tk(PROBE);
+      if (j > 0) rnk[j - 1] = Tk(PROBE);
+      i += 2;
+    } else {
+      tok[j] = tok[i];
+      rnk[j] = Tk(ri);
+      i += 1;
     }
-    next += __popc(lead);
-    const bool active = n >= 2;
-    if (!__any_sync(kFull, active) && next >= count) break;
-
-    // ---- one pass of every active group (warp-convergent) ----
-    uint32_t m = active ? r : NONE;
-#pragma unroll
-    for (int d = W / 2; d >= 1; d >>= 1) m = min(m, __shfl_xor_sync(kFull, m, d));
-    const bool has = m != NONE;
-    const unsigned E = (__ballot_sync(kFull, has && r == m) >> gbase) & wmask;
-    const unsigned F = left_greedy<W>(E);
-    const bool f = (F >> gl) & 1u;
-    const unsigned nmask = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
-    const unsigned K = ~(F << 1) & nmask;  // surviving tokens
-    const int n2 = __popc(K);
-    if (has && ((K >> gl) & 1u)) {
-      const int j = __popc(K & ((1u << gl) - 1u));
-      S.sct[gbase + j] = f ? __ldg(T.r2m + m) : t;
-      S.scr[gbase + j] = r;
-      S.scf[gbase + j] = f;
-    }
-    __syncwarp();
-    if (has) {
-      uint32_t nt = NONE, nr = NONE;
-      if (gl < n2) {
-        nt = S.sct[gbase + gl];
-        if (gl < n2 - 1) {
-          const uint32_t nt1 = S.sct[gbase + gl + 1];
-          if (S.scf[gbase + gl] | S.scf[gbase + gl + 1]) {
-            ProbeReq pr;
-            probe_issue(pr, T, nt, nt1);
-            nr = tk_rank<Tk>(probe_resolve(pr, T));
-          } else {
-            nr = S.scr[gbase + gl];  // both tokens unchanged: cached rank holds
-          }
-        }
-      }
-      t = nt;
-      r = nr;
-      n = n2;
-    }
-    __syncwarp();
-    if (active && (!has || n < 2)) {
-      if (gl < n) S.tok[q + gl] = Tk(t);
-      if (gl == 0) S.cnt[pk] = static_cast<uint16_t>(n);
-      n = 0;
-    }
+    ++j;
   }
+  int k = 0;
+  for (;;) {
+    while (k < j - 1 && uint32_t(rnk[k]) != PROBE) ++k;
+    if (k >= j - 1) break;
+    int k2 = k + 1;
+    while (k2 < j - 1 && uint32_t(rnk[k2]) != PROBE) ++k2;
+    ProbeReq pa, pb;
+    probe_issue<K32>(pa, T, tok[k], tok[k + 1]);
+    const bool two = k2 < j - 1;
+    if (two) probe_issue<K32>(pb, T, tok[k2], tok[k2 + 1]);
+    rnk[k] = Tk(tk_rank<Tk>(probe_resolve<K32>(pa, T)));
+    if (two) rnk[k2] = Tk(tk_rank<Tk>(probe_resolve<K32>(pb, T)));
+    k = two ? k2 + 1 : j;
+  }
+  return j;
 }
 
 // Whole-piece memo lookup (exact: the entry holds this engine's own encoding
 // of the same bytes, computed from the table alone at upload time).
+__device__ __forceinline__ int memo_match(const ulonglong2 lo, const ulonglong2 hi, const uint32_t* w,
+                                          int len, uint32_t& r0, uint32_t& r1, uint32_t& nres) {
+  const uint32_t meta = uint32_t(hi.x >> 32), elen = meta & 0xFF;
+  if (elen == 0) return 0;  // empty slot: miss
+  if (elen == uint32_t(len) && uint32_t(lo.x) == w[0] && uint32_t(lo.x >> 32) == w[1] &&
+      uint32_t(lo.y) == w[2] && uint32_t(lo.y >> 32) == w[3] && uint32_t(hi.x) == w[4]) {
+    nres = (meta >> 8) & 0xFF;
+    r0 = uint32_t(hi.y);
+    r1 = uint32_t(hi.y >> 32);
+    return 1;  // hit
+  }
+  return -1;  // occupied by another piece: keep probing
+}
+
+__device__ __noinline__ bool memo_overflow(const DevTable& T, const uint32_t* w, int len, uint64_t b,
+                                           uint32_t& r0, uint32_t& r1, uint32_t& nres) {
+  for (;;) {
+    b = (b + 1) & T.memo_mask;
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
+    const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, r0, r1, nres);
+    if (m >= 0) return m == 1;
+  }
+}
+
 __device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* ww, int q, int len,
                                             uint32_t& r0, uint32_t& r1, uint32_t& nres) {
   const int start = q + 4, a = start >> 2, sh = (start & 3) * 8;
@@ -586,32 +605,46 @@ __device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* w
   for (int i = 0; i < 6; ++i) x[i] = ww[a + i];
 #pragma unroll
   for (int i = 0; i < 5; ++i) {
-    uint32_t v = sh ? __funnelshift_r(x[i], x[i + 1], sh) : x[i];
+    uint32_t v = __funnelshift_r(x[i], x[i + 1], sh);
     const int nb = len - 4 * i;
     v &= nb >= 4 ? 0xFFFFFFFFu : (nb <= 0 ? 0u : ((1u << (8 * nb)) - 1u));
     w[i] = v;
   }
-  uint64_t b = memo_hash(w, uint32_t(len)) & T.memo_mask;
-  for (;;) {
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
-    const ulonglong2 lo = __ldg(p), hi = __ldg(p + 1);
-    const uint32_t e0 = uint32_t(lo.x), e1 = uint32_t(lo.x >> 32), e2 = uint32_t(lo.y),
-                   e3 = uint32_t(lo.y >> 32), e4 = uint32_t(hi.x), meta = uint32_t(hi.x >> 32);
-    const uint32_t elen = meta & 0xFF;
-    if (elen == 0) return false;
-    if (elen == uint32_t(len) && e0 == w[0] && e1 == w[1] && e2 == w[2] && e3 == w[3] && e4 == w[4]) {
-      nres = (meta >> 8) & 0xFF;
-      r0 = uint32_t(hi.y);
-      r1 = uint32_t(hi.y >> 32);
-      return true;
-    }
-    b = (b + 1) & T.memo_mask;
-  }
+  const uint64_t b = memo_hash(w, uint32_t(len)) & T.memo_mask;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
+  const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, r0, r1, nres);
+  if (m >= 0) return m == 1;
+  return memo_overflow(T, w, len, b, r0, r1, nres);
 }
 
+// Length of a long piece starting at abs (warp-cooperative, rare path).
+__device__ __noinline__ uint64_t long_piece_length(const EncodeArgs& a, const uint32_t* junc,
+                                                   uint64_t abs, int lane) {
+  uint64_t row_end = 0;
+  if (lane == 0) {
+    uint64_t lo = 0, hi = a.n_rows;  // max s with offsets[s] <= abs
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (a.offsets[mid] <= abs) lo = mid; else hi = mid - 1;
+    }
+    row_end = a.offsets[lo + 1];
+  }
+  row_end = __shfl_sync(kFull, row_end, 0);
+  for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
+    const uint64_t y = x + lane;
+    const bool bnd = y < row_end && !is_junction(junc, a.bytes[y - 1], a.bytes[y]);
+    const unsigned bm = __ballot_sync(kFull, bnd);
+    if (bm) return x + __ffs(bm) - 1 - abs;
+  }
+  return row_end - abs;
+}
+
+#ifndef BBPE_PIECES_MINB
+#define BBPE_PIECES_MINB 3
+#endif
 template <typename Tk>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, DevTable T) {
-  constexpr uint32_t NONE = Marks<Tk>::kNone;
+__global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(EncodeArgs a, DevTable T) {
+  constexpr bool K32 = sizeof(Tk) == 2;
   __shared__ uint32_t s_lut[256];
   __shared__ uint32_t s_junc[2048];
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -620,7 +653,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, D
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   PieceSmem<Tk>& S = reinterpret_cast<PieceSmem<Tk>*>(s_dyn)[wid];
-  const bool block_engine = a.engine == BBPE_ENGINE_BLOCK;
   const uint32_t* d2id = T.d2id;
 
   for (;;) {
@@ -631,55 +663,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, D
     const uint64_t b0 = tile * kTile;
     const uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
 
-    if (block_engine) {
-      // Every non-empty row is one long piece for k_long_pieces; the tile's
-      // output is its rows' results in order.
-      const int tl = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
-      for (int q0 = 0; q0 < tl; q0 += 32) {  // invalid bytes (pretokenize.hpp:64-67)
-        const int q = q0 + lane;
-        const bool bad = q < tl && s_lut[a.bytes[b0 + q]] == kInvalidToken;
-        const unsigned bm = __ballot_sync(kFull, bad);
-        if (bm && lane == 0)
-          atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
-                    (unsigned long long)(b0 + q0 + __ffs(bm) - 1));
-      }
-      uint32_t ne = 0;
-      for (uint64_t s = s0 + lane; s < s1 && s < a.n_rows; s += 32)
-        ne += a.offsets[s + 1] > a.offsets[s] ? 1u : 0u;
-      ne = __reduce_add_sync(kFull, ne);
-      uint64_t first = 0;
-      if (lane == 0 && ne) first = atomicAdd(&a.counters[CNT_LREC], ne);
-      first = __shfl_sync(kFull, first, 0);
-      uint32_t ri = 0;
-      for (uint64_t sb = s0; sb < s1 && sb <= a.n_rows; sb += 32) {
-        const uint64_t s = sb + lane;
-        bool ne_row = false;
-        uint64_t o = 0, e = 0;
-        if (s < s1 && s < a.n_rows) {
-          o = a.offsets[s];
-          e = a.offsets[s + 1];
-          ne_row = e > o;
-        }
-        const unsigned nm = __ballot_sync(kFull, ne_row);
-        const uint32_t before = ri + __popc(nm & lanemask_lt(lane));
-        if (s < s1 && s <= a.n_rows) a.out_offsets[s] = uint64_t(before) << 40;
-        if (ne_row && first + before < a.lp_cap)
-          a.lrec[first + before] = LongRec{o, e - o, s, 0u, 0u};
-        ri += __popc(nm);
-      }
-      if (lane == 0) {
-        a.tile_lrec[tile] = ne ? ((first << 24) | ne) : 0;
-        a.tile_count[tile] = 0;
-      }
-      continue;
-    }
-
     const int tlen = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
     load_window(S.w, a, s_junc, s_lut, tile, lane, tlen);
 
     // (1) Piece list with lengths (distance to the next piece start; the
     // last piece of the tile searches the boundary bits past the tile).
     int npieces = 0;
+#pragma unroll 1
     for (int wd = 0; wd * 32 < tlen; ++wd) {
       const int q = wd * 32 + lane;
       const bool st = q < tlen && ((S.w.bd[wd] >> lane) & 1u);
@@ -729,47 +719,45 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, D
     __syncwarp();
 
     if (nmerge) {
-      // (3) Initial tokens and pair ranks of the merge list (lane per piece,
-      // two probes in flight).
-      for (int i = lane; i < nmerge; i += 32) {
-        const int k = S.clist[i];
-        const int q = S.plist[k], len = S.plen[k];
-        for (int j = 0; j < len; ++j) S.tok[q + j] = Tk(s_lut[S.w.byte(q + j)]);
-        for (int j = 0; j < len - 1; j += 2) {
-          ProbeReq p0, p1;
-          probe_issue(p0, T, S.tok[q + j], S.tok[q + j + 1]);
-          const bool two = j + 2 < len;
-          if (two) probe_issue(p1, T, S.tok[q + j + 1], S.tok[q + j + 2]);
-          S.rnk[q + j] = Tk(tk_rank<Tk>(probe_resolve(p0, T)));
-          if (two) S.rnk[q + j + 1] = Tk(tk_rank<Tk>(probe_resolve(p1, T)));
+      // (3) Lane-per-piece pass loops over the merge list (pieces refill
+      // lanes as they finish). A new piece gets its initial tokens and pair
+      // ranks (two probes in flight), then one pass per loop iteration.
+      int my_n = 0, my_q = 0, my_k = 0, next = 0;
+      for (;;) {
+        const bool idle = my_n == 0;
+        const unsigned im = __ballot_sync(kFull, idle);
+        if (idle) {
+          const int i = next + __popc(im & lanemask_lt(lane));
+          if (i < nmerge) {
+            my_k = S.clist[i];
+            my_q = S.plist[my_k];
+            my_n = S.plen[my_k];
+            Tk* tk = S.tok + my_q;
+            Tk* rk = S.rnk + my_q;
+            for (int j = 0; j < my_n; ++j) tk[j] = Tk(s_lut[S.w.byte(my_q + j)]);
+            for (int j = 0; j < my_n - 1; j += 2) {
+              ProbeReq p0, p1;
+              probe_issue<K32>(p0, T, tk[j], tk[j + 1]);
+              const bool two = j + 2 < my_n;
+              if (two) probe_issue<K32>(p1, T, tk[j + 1], tk[j + 2]);
+              rk[j] = Tk(tk_rank<Tk>(probe_resolve<K32>(p0, T)));
+              if (two) rk[j + 1] = Tk(tk_rank<Tk>(probe_resolve<K32>(p1, T)));
+            }
+          }
+        }
+        next += __popc(im);
+        const bool active = my_n >= 2;
+        if (!__any_sync(kFull, active) && next >= nmerge) break;
+        if (active) {
+          const int r = lane_pass<Tk>(T, S.tok + my_q, S.rnk + my_q, my_n);
+          if (r < 2) {
+            S.cnt[my_k] = static_cast<uint16_t>(r < 0 ? my_n : r);
+            my_n = 0;
+          } else {
+            my_n = r;
+          }
         }
       }
-      // (4) Pass loops: pieces of <= 8 tokens in 8-lane groups, longer ones
-      // in 32-lane groups. The list is split in place (short first).
-      int nsmall = 0;
-      for (int i0 = 0; i0 < nmerge; i0 += 32) {
-        const int i = i0 + lane;
-        const int k = i < nmerge ? S.clist[i] : 0;
-        const bool small = i < nmerge && S.plen[k] <= 8;
-        const unsigned sm = __ballot_sync(kFull, small);
-        const unsigned bm = __ballot_sync(kFull, i < nmerge && !small);
-        __syncwarp();
-        if (small) S.clist2[nsmall + __popc(sm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-        nsmall += __popc(sm);
-        (void)bm;
-      }
-      int nbig = 0;
-      for (int i0 = 0; i0 < nmerge; i0 += 32) {
-        const int i = i0 + lane;
-        const int k = i < nmerge ? S.clist[i] : 0;
-        const bool big = i < nmerge && S.plen[k] > 8;
-        const unsigned bm = __ballot_sync(kFull, big);
-        if (big) S.clist2[nsmall + nbig + __popc(bm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-        nbig += __popc(bm);
-      }
-      __syncwarp();
-      run_class<Tk, 8>(S, T, S.clist2, nsmall, lane);
-      if (nbig) run_class<Tk, 32>(S, T, S.clist2 + nsmall, nbig, lane);
       __syncwarp();
     }
 
@@ -792,28 +780,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, D
     // Long pieces (rare): full length = distance to the next hard boundary or
     // the end of the row; k_long_pieces merges them after this kernel.
     for (uint32_t li = 0; li < nlong; ++li) {
-      const uint64_t abs = b0 + S.plist[S.lk[li]];
-      uint64_t row_end = 0;
-      if (lane == 0) {
-        uint64_t lo = 0, hi = a.n_rows;  // max s with offsets[s] <= abs
-        while (lo < hi) {
-          const uint64_t mid = (lo + hi + 1) >> 1;
-          if (a.offsets[mid] <= abs) lo = mid; else hi = mid - 1;
-        }
-        row_end = a.offsets[lo + 1];
-      }
-      row_end = __shfl_sync(kFull, row_end, 0);
-      uint64_t end = row_end;
-      for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
-        const uint64_t y = x + lane;
-        const bool bnd = y < row_end && !is_junction(s_junc, a.bytes[y - 1], a.bytes[y]);
-        const unsigned bm = __ballot_sync(kFull, bnd);
-        if (bm) {
-          end = x + __ffs(bm) - 1;
-          break;
-        }
-      }
-      if (lane == 0) S.llen[li] = end - abs;
+      const uint64_t len = long_piece_length(a, s_junc, b0 + S.plist[S.lk[li]], lane);
+      if (lane == 0) S.llen[li] = len;
     }
     __syncwarp();
 
@@ -860,6 +828,62 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_pieces(EncodeArgs a, D
     }
     __syncwarp();
   }
+}
+
+// ---------------------------------------------------------------------------
+// k_block_rows (BBPE_ENGINE_BLOCK): every non-empty row is one long piece for
+// k_long_pieces -- the paper's one-block-per-string engine. Warp per tile:
+// invalid-byte check, records in row order, row offsets relative to the tile.
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_block_rows(EncodeArgs a, DevTable T) {
+  __shared__ uint32_t s_lut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
+  for (uint64_t tile = blockIdx.x * uint64_t(kWarpsPerCta) + (threadIdx.x >> 5); tile < a.num_tiles;
+       tile += nwarps) {
+    const uint64_t b0 = tile * kTile;
+    const uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
+      // Every non-empty row is one long piece for k_long_pieces; the tile's
+      // output is its rows' results in order.
+      const int tl = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
+      for (int q0 = 0; q0 < tl; q0 += 32) {  // invalid bytes (pretokenize.hpp:64-67)
+        const int q = q0 + lane;
+        const bool bad = q < tl && s_lut[a.bytes[b0 + q]] == kInvalidToken;
+        const unsigned bm = __ballot_sync(kFull, bad);
+        if (bm && lane == 0)
+          atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
+                    (unsigned long long)(b0 + q0 + __ffs(bm) - 1));
+      }
+      uint32_t ne = 0;
+      for (uint64_t s = s0 + lane; s < s1 && s < a.n_rows; s += 32)
+        ne += a.offsets[s + 1] > a.offsets[s] ? 1u : 0u;
+      ne = __reduce_add_sync(kFull, ne);
+      uint64_t first = 0;
+      if (lane == 0 && ne) first = atomicAdd(&a.counters[CNT_LREC], ne);
+      first = __shfl_sync(kFull, first, 0);
+      uint32_t ri = 0;
+      for (uint64_t sb = s0; sb < s1 && sb <= a.n_rows; sb += 32) {
+        const uint64_t s = sb + lane;
+        bool ne_row = false;
+        uint64_t o = 0, e = 0;
+        if (s < s1 && s < a.n_rows) {
+          o = a.offsets[s];
+          e = a.offsets[s + 1];
+          ne_row = e > o;
+        }
+        const unsigned nm = __ballot_sync(kFull, ne_row);
+        const uint32_t before = ri + __popc(nm & lanemask_lt(lane));
+        if (s < s1 && s <= a.n_rows) a.out_offsets[s] = uint64_t(before) << 40;
+        if (ne_row && first + before < a.lp_cap)
+          a.lrec[first + before] = LongRec{o, e - o, s, 0u, 0u};
+        ri += __popc(nm);
+      }
+      if (lane == 0) {
+        a.tile_lrec[tile] = ne ? ((first << 24) | ne) : 0;
+        a.tile_count[tile] = 0;
+      }
+        }
 }
 
 // ---------------------------------------------------------------------------
@@ -1001,17 +1025,42 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
     // Row offsets: short tokens before the row (low 40 bits) plus the first
     // (v >> 40) long pieces of the tile.
     const uint64_t s0 = a.tile_first[t], s1 = a.tile_first[t + 1];
+    const uint64_t rb = a.run_base ? *a.run_base : 0;
     for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
       const uint64_t v = __ldcg(a.out_offsets + s);
       const uint32_t lb = uint32_t(v >> 40);
       uint64_t lsum = 0;
       for (uint32_t li = 0; li < lb; ++li) lsum += __ldcg(&a.lrec[(rec >> 24) + li].count);
-      a.out_offsets[s] = tbase + (v & ((1ull << 40) - 1)) + lsum;
+      a.out_offsets[s] = rb + tbase + (v & ((1ull << 40) - 1)) + lsum;
     }
   }
 }
 
+__global__ void k_rebase_input(uint64_t* off, uint64_t n, uint64_t base) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) off[i] -= base;
+}
+__global__ void k_advance_base(uint64_t* run_base, const uint64_t* wave_total) {
+  *run_base += *wave_total;
+}
+__global__ void k_fill_offsets(uint64_t* out, uint64_t n, const uint64_t* run_base) {
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = run_base ? *run_base : 0;
+}
+
 }  // namespace
+
+void launch_rebase_input(uint64_t* d_off, uint64_t n, uint64_t base, cudaStream_t stream) {
+  if (base == 0 || n == 0) return;
+  k_rebase_input<<<unsigned((n + 255) / 256), 256, 0, stream>>>(d_off, n, base);
+}
+void launch_advance_base(uint64_t* run_base, const uint64_t* wave_total, cudaStream_t stream) {
+  k_advance_base<<<1, 1, 0, stream>>>(run_base, wave_total);
+}
+void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_base, cudaStream_t stream) {
+  if (n == 0) return;
+  k_fill_offsets<<<unsigned((n + 255) / 256), 256, 0, stream>>>(d_out_off, n, run_base);
+}
 
 template <typename Tk>
 size_t pieces_smem() {
@@ -1052,7 +1101,9 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     ++launched;
   }
   if (ev) cudaEventRecord(ev[1], stream);
-  if (a.narrow)
+  if (a.engine == BBPE_ENGINE_BLOCK)
+    k_block_rows<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
+  else if (a.narrow)
     k_pieces<uint16_t><<<p.main_grid, kWarpsPerCta * 32, pieces_smem<uint16_t>(), stream>>>(a, t);
   else
     k_pieces<uint32_t><<<p.main_grid_wide, kWarpsPerCta * 32, pieces_smem<uint32_t>(), stream>>>(a, t);

@@ -9,7 +9,10 @@
 
 namespace bbpe {
 
-constexpr int kTile = 512;          // input bytes owned by one warp-tile
+#ifndef BBPE_TILE
+#define BBPE_TILE 512
+#endif
+constexpr int kTile = BBPE_TILE;    // input bytes owned by one warp-tile
 constexpr int kLmax = 32;           // longest piece merged by a single lane
 constexpr int kWin = kTile + kLmax + 1;  // window positions [0, kWin) after b0
 constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece tokens)
@@ -47,6 +50,7 @@ struct EncodeArgs {
   uint64_t* status;         // look-back words of k_tile_scan's CTAs
   uint64_t num_groups;      // k_tile_scan CTAs
   uint64_t* tile_base;      // num_tiles + 1: first output token of each tile
+  const uint64_t* run_base; // optional: added to every row offset (pipelined waves)
   uint32_t* staging;        // num_tiles * kStage: each tile's short-piece tokens, in order
   uint32_t* tile_count;     // num_tiles: tokens produced by the tile (short + long)
   uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n, 0 when none
@@ -80,6 +84,11 @@ LaunchPlan plan_launch(int device);
 // ev (optional): BBPE_N_KERNELS + 1 events, before the first and after each kernel.
 int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, cudaStream_t stream,
                   cudaEvent_t* ev = nullptr);
+// Pipelined-wave helpers: subtract `base` from n input offsets; advance the
+// running output base by the wave's token total; fill n offsets with the base.
+void launch_rebase_input(uint64_t* d_off, uint64_t n, uint64_t base, cudaStream_t stream);
+void launch_advance_base(uint64_t* run_base, const uint64_t* wave_total, cudaStream_t stream);
+void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_base, cudaStream_t stream);
 // Long-piece kernel only (token input, used by bbpe_block_bpe).
 int launch_block_bpe(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p,
                      cudaStream_t stream);

@@ -379,15 +379,23 @@ void build_device_layout(bbpe_table& t) {
     t.narrow = max_dense < 0xFFFDull && M < 0xFFFDull;
   }
 
-  // Bucketised open addressing, load <= 0.5.
+  // Bucketised open addressing, load <= 0.5. Narrow tables (ids < 2^16) use
+  // 32-bit keys: slot = key32 << 32 | rank, bucket = mix32(key32).
   uint64_t buckets = 1;
   while (buckets * kBucketSlots < 2 * M + 8) buckets <<= 1;
   t.bucket_mask = buckets - 1;
   t.slots.assign(buckets * kBucketSlots, kEmptySlot);
   for (size_t i = 0; i < M; ++i) {
-    uint64_t key = (uint64_t(t.dense(t.m_left[i])) << t.id_bits) | t.dense(t.m_right[i]);
-    uint64_t slot = (key << t.rank_bits) | i;
-    uint64_t bk = mix64(key) & t.bucket_mask;
+    uint64_t slot, bk;
+    if (t.narrow) {
+      const uint32_t key = (t.dense(t.m_left[i]) << 16) | t.dense(t.m_right[i]);
+      slot = (uint64_t(key) << 32) | i;
+      bk = mix32(key) & t.bucket_mask;
+    } else {
+      const uint64_t key = (uint64_t(t.dense(t.m_left[i])) << t.id_bits) | t.dense(t.m_right[i]);
+      slot = (key << t.rank_bits) | i;
+      bk = mix64(key) & t.bucket_mask;
+    }
     for (;;) {
       uint64_t* bs = &t.slots[bk * kBucketSlots];
       int j = 0;
@@ -472,6 +480,7 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
   rep.view.id_bits = t.id_bits;
   rep.view.rank_bits = t.rank_bits;
   rep.view.n_merges = static_cast<uint32_t>(M);
+  rep.view.key32 = t.narrow ? 1u : 0u;
   auto [pos, ok] = t.replicas.emplace(device, rep);
   return pos->second.view;
 }
