@@ -1,0 +1,479 @@
+// blockbpe_b200/blockbpe.hpp -- C++ drop-in for the reference's batch-encode API.
+//
+// Header-only wrapper over the C-ABI (include/bbpe_b200.h, libbbpe_b200.so).
+// Names, argument meaning and error behaviour mirror the reference library
+// (namespace blockbpe, /root/reference/proj/include/blockbpe):
+//
+//   errors                 types.hpp:32-70
+//   MergeTable, loaders    merge_table.hpp:223-305, 503-522
+//   SpecialTokenSet        merge_table.hpp:309-369, validate_specials 374-385
+//   split_specials         pretokenize.hpp:32-57
+//   BlockConfig, block_bpe block_engine.hpp:18-32, 268-310 (PassTrace 42-47)
+//   BatchEncoding/Limits   batch.hpp:21-42
+//   encode_single/batch    batch.hpp:46-126
+//   decode/decode_batch    merge_table.hpp:565-579, batch.hpp:128-154
+//
+// A caller switches by replacing `blockbpe::` with `blockbpe_b200::` and the
+// PhasePool* argument with an Encoder* (one per GPU; nullptr = device 0).
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+#include "../bbpe_b200.h"
+
+namespace blockbpe_b200 {
+
+using TokenId = std::uint32_t;
+using Rank = std::uint32_t;
+using TokenSeq = std::vector<TokenId>;
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct UsageError : Error {
+  using Error::Error;
+};
+struct ParseError : Error {
+  using Error::Error;
+};
+struct IntegrityError : Error {
+  using Error::Error;
+};
+struct DecodeError : Error {
+  using Error::Error;
+};
+struct ContractViolation : Error {
+  using Error::Error;
+};
+struct MaxPassesError : Error {
+  MaxPassesError(const std::string& what, TokenSeq partial, std::size_t passes)
+      : Error(what), partial_tokens(std::move(partial)), passes_run(passes) {}
+  TokenSeq partial_tokens;
+  std::size_t passes_run;
+};
+
+namespace detail {
+[[noreturn]] inline void raise(int rc) {
+  const std::string msg = bbpe_last_error();
+  switch (rc) {
+    case BBPE_USAGE: throw UsageError(msg);
+    case BBPE_PARSE: throw ParseError(msg);
+    case BBPE_INTEGRITY: throw IntegrityError(msg);
+    case BBPE_DECODE: throw DecodeError(msg);
+    case BBPE_CONTRACT: throw ContractViolation(msg);
+    case BBPE_MAX_PASSES: throw MaxPassesError(msg, {}, 0);
+    default: throw Error(msg);
+  }
+}
+inline void check(int rc) {
+  if (rc != BBPE_OK) raise(rc);
+}
+}  // namespace detail
+
+inline constexpr TokenId kInvalidToken = 0xFFFFFFFFu;
+
+struct BlockConfig {
+  std::uint32_t block_size = 256;
+  std::optional<std::size_t> max_passes;
+  void validate() const {
+    if (block_size < 32 || block_size > 1024 || (block_size & (block_size - 1)) != 0)
+      throw UsageError("block_size must be a power of two in [32, 1024], got " +
+                       std::to_string(block_size));
+    if (max_passes && *max_passes < 1) throw UsageError("max_passes must be >= 1");
+  }
+};
+
+inline std::uint32_t coarsening_factor(std::size_t seq_len, const BlockConfig& config) {
+  config.validate();
+  return static_cast<std::uint32_t>((seq_len + config.block_size - 1) / config.block_size);
+}
+
+struct PassRecord {
+  std::size_t pass_index;
+  Rank min_rank;
+  std::size_t merges_applied;
+};
+using PassTrace = std::vector<PassRecord>;
+
+enum class VocabFormat { gpt2, canonical_json, binary };
+
+inline VocabFormat parse_vocab_format(std::string_view name) {
+  if (name == "gpt2") return VocabFormat::gpt2;
+  if (name == "json" || name == "canonical_json") return VocabFormat::canonical_json;
+  if (name == "binary" || name == "bbpt") return VocabFormat::binary;
+  throw UsageError("unknown vocab format \"" + std::string(name) + "\"");
+}
+
+// Immutable merge table; device replicas are uploaded on first use per GPU.
+class MergeTable {
+ public:
+  MergeTable() = default;
+  explicit MergeTable(bbpe_table* h) : h_(h, bbpe_table_destroy) {}
+
+  bbpe_table* handle() const { return h_.get(); }
+
+  std::optional<Rank> rank_of(TokenId l, TokenId r) const {
+    const Rank v = bbpe_table_rank_of(h_.get(), l, r, nullptr);
+    if (v == 0xFFFFFFFFu) return std::nullopt;
+    return v;
+  }
+  std::optional<TokenId> merged_of(TokenId l, TokenId r) const {
+    TokenId m = 0;
+    if (bbpe_table_rank_of(h_.get(), l, r, &m) == 0xFFFFFFFFu) return std::nullopt;
+    return m;
+  }
+  TokenId byte_token(unsigned char b) const { return bbpe_table_byte_token(h_.get(), b); }
+  std::size_t token_count() const { return info().token_count; }
+  std::size_t merge_count() const { return info().merge_count; }
+  std::size_t base_size() const { return info().base_size; }
+  bbpe_table_info info() const {
+    bbpe_table_info i{};
+    detail::check(bbpe_table_get_info(h_.get(), &i));
+    return i;
+  }
+  // Bytes of a table token (decode); nullopt for unknown ids.
+  std::optional<std::string> bytes_of(TokenId id) const {
+    std::uint8_t buf[1024];
+    std::size_t len = 0;
+    if (bbpe_decode(h_.get(), &id, 1, buf, sizeof buf, &len) != BBPE_OK) return std::nullopt;
+    if (len <= sizeof buf) return std::string(reinterpret_cast<char*>(buf), len);
+    std::string s(len, '\0');
+    bbpe_decode(h_.get(), &id, 1, reinterpret_cast<std::uint8_t*>(s.data()), len, &len);
+    return s;
+  }
+
+  // Construction mirroring add_token / add_merge / finalize (merge_table.hpp:257-297).
+  static MergeTable build(const std::vector<std::pair<TokenId, std::string>>& tokens,
+                          const std::vector<std::array<std::uint32_t, 4>>& merges);
+
+ private:
+  std::shared_ptr<bbpe_table> h_;
+};
+
+inline MergeTable load_merge_table_files(const std::string& vocab_path, const std::string& merges_path,
+                                         VocabFormat format) {
+  const int f = format == VocabFormat::gpt2 ? BBPE_FORMAT_GPT2
+                : format == VocabFormat::canonical_json ? BBPE_FORMAT_CANONICAL
+                                                        : BBPE_FORMAT_BINARY;
+  bbpe_table* h = nullptr;
+  detail::check(bbpe_table_load_files(vocab_path.c_str(),
+                                      merges_path.empty() ? nullptr : merges_path.c_str(), f, &h));
+  return MergeTable(h);
+}
+
+inline MergeTable MergeTable::build(const std::vector<std::pair<TokenId, std::string>>& tokens,
+                                    const std::vector<std::array<std::uint32_t, 4>>& merges) {
+  std::vector<std::uint32_t> ids;
+  std::vector<std::uint64_t> off{0};
+  std::string blob;
+  for (const auto& [id, b] : tokens) {
+    ids.push_back(id);
+    blob += b;
+    off.push_back(blob.size());
+  }
+  std::vector<std::uint32_t> m4;
+  for (const auto& m : merges) m4.insert(m4.end(), m.begin(), m.end());
+  if (blob.empty()) blob.push_back('\0');
+  bbpe_table* h = nullptr;
+  detail::check(bbpe_table_create(ids.size(), ids.data(), off.data(),
+                                  reinterpret_cast<const std::uint8_t*>(blob.data()), merges.size(),
+                                  m4.empty() ? nullptr : m4.data(), &h));
+  return MergeTable(h);
+}
+
+class SpecialTokenSet {
+ public:
+  void add(std::string bytes, TokenId id) {
+    if (bytes.empty()) throw UsageError("special token byte string may not be empty");
+    for (const auto& e : entries_)
+      if (e.first == bytes) throw UsageError("duplicate special token \"" + bytes + "\"");
+    auto it = entries_.begin();
+    while (it != entries_.end() && it->first.size() >= bytes.size()) ++it;
+    entries_.insert(it, {std::move(bytes), id});
+  }
+  bool empty() const { return entries_.empty(); }
+  std::size_t size() const { return entries_.size(); }
+  const std::vector<std::pair<std::string, TokenId>>& entries() const { return entries_; }
+  const std::string* bytes_of(TokenId id) const {
+    for (const auto& e : entries_)
+      if (e.second == id) return &e.first;
+    return nullptr;
+  }
+  bool contains_id(TokenId id) const { return bytes_of(id) != nullptr; }
+  std::optional<std::pair<std::size_t, TokenId>> match(std::string_view text, std::size_t pos) const {
+    for (const auto& [b, id] : entries_)
+      if (b.size() <= text.size() - pos && text.compare(pos, b.size(), b) == 0)
+        return std::make_pair(b.size(), id);
+    return std::nullopt;
+  }
+  std::optional<TokenId> bos_id() const { return bos_; }
+  std::optional<TokenId> eos_id() const { return eos_; }
+  void set_bos(std::string_view b) { bos_ = require(b, "bos"); }
+  void set_eos(std::string_view b) { eos_ = require(b, "eos"); }
+
+ private:
+  TokenId require(std::string_view b, const char* what) const {
+    for (const auto& [e, id] : entries_)
+      if (e == b) return id;
+    throw UsageError(std::string(what) + " token \"" + std::string(b) +
+                     "\" is not in the special token set");
+  }
+  std::vector<std::pair<std::string, TokenId>> entries_;
+  std::optional<TokenId> bos_, eos_;
+};
+
+struct Segment {
+  enum class Kind { literal, special };
+  Kind kind;
+  std::string bytes;
+  std::optional<TokenId> special_id;
+};
+
+inline std::vector<Segment> split_specials(std::string_view input, const SpecialTokenSet& specials) {
+  std::vector<Segment> out;
+  std::string pending;
+  std::size_t pos = 0;
+  auto flush = [&] {
+    if (!pending.empty()) {
+      out.push_back({Segment::Kind::literal, std::move(pending), std::nullopt});
+      pending.clear();
+    }
+  };
+  while (pos < input.size()) {
+    if (!specials.empty())
+      if (auto m = specials.match(input, pos)) {
+        flush();
+        out.push_back({Segment::Kind::special, std::string(input.substr(pos, m->first)), m->second});
+        pos += m->first;
+        continue;
+      }
+    pending.push_back(input[pos++]);
+  }
+  flush();
+  return out;
+}
+
+// One encode context on one GPU (the PhasePool* of the reference signatures).
+class Encoder {
+ public:
+  explicit Encoder(int device = 0, BlockConfig cfg = {}, bool piece_memo = true) {
+    cfg.validate();
+    bbpe_config c{cfg.block_size, cfg.max_passes ? static_cast<std::int64_t>(*cfg.max_passes) : 0,
+                  BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0};
+    bbpe_ctx* h = nullptr;
+    detail::check(bbpe_ctx_create(device, &c, &h));
+    h_.reset(h);
+  }
+  bbpe_ctx* handle() const { return h_.get(); }
+  void configure(const BlockConfig& cfg, bool block_engine = false, bool piece_memo = true) {
+    cfg.validate();
+    bbpe_config c{cfg.block_size, cfg.max_passes ? static_cast<std::int64_t>(*cfg.max_passes) : 0,
+                  block_engine ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0};
+    detail::check(bbpe_ctx_set_config(h_.get(), &c));
+  }
+  // Packed rows -> CSR.
+  void encode_csr(const MergeTable& t, const std::string& bytes, const std::vector<std::uint64_t>& offsets,
+                  std::vector<TokenId>& ids, std::vector<std::uint64_t>& out_offsets) {
+    const std::size_t n = offsets.empty() ? 0 : offsets.size() - 1;
+    ids.resize(std::max<std::uint64_t>(offsets.empty() ? 0 : offsets.back() - offsets.front(), 1));
+    out_offsets.resize(n + 1);
+    detail::check(bbpe_encode(h_.get(), t.handle(), reinterpret_cast<const std::uint8_t*>(bytes.data()),
+                              offsets.data(), n, ids.data(), ids.size(), out_offsets.data(), nullptr));
+    ids.resize(out_offsets[n]);
+  }
+
+ private:
+  struct Del {
+    void operator()(bbpe_ctx* c) const { bbpe_ctx_destroy(c); }
+  };
+  std::unique_ptr<bbpe_ctx, Del> h_;
+};
+
+inline Encoder& default_encoder() {
+  static Encoder e(0);
+  return e;
+}
+
+struct BatchEncoding {
+  std::size_t batch_size = 0;
+  std::size_t max_len = 0;
+  TokenId pad_id = 0;
+  std::vector<TokenId> ids;
+  std::vector<std::uint32_t> lengths;
+  std::vector<std::uint8_t> mask;
+  std::size_t truncated_rows = 0;
+  TokenId at(std::size_t row, std::size_t col) const { return ids[row * max_len + col]; }
+  TokenSeq row(std::size_t r) const {
+    const TokenId* b = ids.data() + r * max_len;
+    return TokenSeq(b, b + lengths[r]);
+  }
+};
+
+struct BatchLimits {
+  std::optional<std::uint32_t> max_len;
+};
+
+// batch.hpp:64-126 -- specials split on the host, literal segments merged on
+// the GPU, rows assembled with BOS/EOS, padding, mask and truncation.
+inline BatchEncoding encode_batch(const std::vector<std::string>& inputs, const MergeTable& table,
+                                  const SpecialTokenSet& specials, const BlockConfig& config,
+                                  TokenId pad_id, bool add_bos, bool add_eos, Encoder* encoder = nullptr,
+                                  const BatchLimits& limits = {}) {
+  config.validate();
+  if (add_bos && !specials.bos_id()) throw UsageError("add_bos requires a bos entry in the special token set");
+  if (add_eos && !specials.eos_id()) throw UsageError("add_eos requires an eos entry in the special token set");
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  enc.configure(config);
+  // Device rows: literal segments (one per input when there are no specials).
+  std::string blob;
+  std::vector<std::uint64_t> offs{0};
+  std::vector<std::size_t> seg_row;
+  struct Item {
+    bool special;
+    TokenId id;
+    std::size_t seg;
+  };
+  std::vector<std::vector<Item>> plan(inputs.size());
+  for (std::size_t r = 0; r < inputs.size(); ++r) {
+    if (specials.empty()) {
+      plan[r].push_back({false, 0, seg_row.size()});
+      blob += inputs[r];
+      offs.push_back(blob.size());
+      seg_row.push_back(r);
+      continue;
+    }
+    for (auto& s : split_specials(inputs[r], specials)) {
+      if (s.kind == Segment::Kind::special) {
+        plan[r].push_back({true, *s.special_id, 0});
+      } else {
+        plan[r].push_back({false, 0, seg_row.size()});
+        blob += s.bytes;
+        offs.push_back(blob.size());
+        seg_row.push_back(r);
+      }
+    }
+  }
+  std::vector<TokenId> ids;
+  std::vector<std::uint64_t> oo;
+  try {
+    enc.encode_csr(table, blob, offs, ids, oo);
+  } catch (const Error& e) {
+    // Row tags from the device refer to segments; report the input row.
+    std::string m = e.what();
+    if (m.rfind("row ", 0) == 0) {
+      const std::size_t colon = m.find(':');
+      const std::size_t seg = std::stoull(m.substr(4, colon - 4));
+      m = "row " + std::to_string(seg_row.at(seg)) + m.substr(colon);
+    }
+    if (dynamic_cast<const IntegrityError*>(&e)) throw IntegrityError(m);
+    if (dynamic_cast<const UsageError*>(&e)) throw UsageError(m);
+    throw Error(m);
+  }
+  std::vector<TokenSeq> rows(inputs.size());
+  for (std::size_t r = 0; r < inputs.size(); ++r) {
+    TokenSeq& row = rows[r];
+    if (add_bos) row.push_back(*specials.bos_id());
+    for (const Item& it : plan[r]) {
+      if (it.special) row.push_back(it.id);
+      else row.insert(row.end(), ids.begin() + oo[it.seg], ids.begin() + oo[it.seg + 1]);
+    }
+    if (add_eos) row.push_back(*specials.eos_id());
+  }
+  BatchEncoding out;
+  out.batch_size = inputs.size();
+  out.pad_id = pad_id;
+  std::size_t widest = 0;
+  for (auto& row : rows) widest = std::max(widest, row.size());
+  if (limits.max_len) {
+    for (auto& row : rows)
+      if (row.size() > *limits.max_len) {
+        row.resize(*limits.max_len);
+        ++out.truncated_rows;
+      }
+    out.max_len = *limits.max_len;
+  } else {
+    out.max_len = widest;
+  }
+  out.ids.assign(out.batch_size * out.max_len, pad_id);
+  out.mask.assign(out.batch_size * out.max_len, 0);
+  out.lengths.resize(out.batch_size);
+  for (std::size_t r = 0; r < rows.size(); ++r) {
+    out.lengths[r] = static_cast<std::uint32_t>(rows[r].size());
+    for (std::size_t c = 0; c < rows[r].size(); ++c) {
+      out.ids[r * out.max_len + c] = rows[r][c];
+      out.mask[r * out.max_len + c] = 1;
+    }
+  }
+  return out;
+}
+
+inline TokenSeq encode_single(std::string_view input, const MergeTable& table, const SpecialTokenSet& specials,
+                              const BlockConfig& config, Encoder* encoder = nullptr) {
+  return encode_batch({std::string(input)}, table, specials, config, 0, false, false, encoder).row(0);
+}
+
+// block_engine.hpp:268-310 on explicit ids (one CTA pass loop on the GPU).
+inline TokenSeq block_bpe(const TokenSeq& tokens, const MergeTable& table, const BlockConfig& config,
+                          Encoder* encoder = nullptr, PassTrace* trace = nullptr) {
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  enc.configure(config);
+  TokenSeq out(tokens.size() + 1);
+  std::size_t out_n = 0, passes = 0;
+  std::vector<std::uint64_t> tr(trace ? 3 * (tokens.size() + 1) : 3);
+  const int rc = bbpe_block_bpe(enc.handle(), table.handle(), tokens.data(), tokens.size(), out.data(), &out_n,
+                                trace ? tr.data() : nullptr, trace ? tokens.size() + 1 : 0, &passes);
+  out.resize(out_n);
+  if (rc == BBPE_MAX_PASSES) throw MaxPassesError(bbpe_last_error(), out, passes);
+  detail::check(rc);
+  if (trace)
+    for (std::size_t p = 0; p < passes && p <= tokens.size(); ++p)
+      trace->push_back({static_cast<std::size_t>(tr[3 * p]), static_cast<Rank>(tr[3 * p + 1]),
+                        static_cast<std::size_t>(tr[3 * p + 2])});
+  return out;
+}
+
+inline std::string decode(const MergeTable& table, const SpecialTokenSet& specials, const TokenSeq& ids) {
+  std::string out;
+  for (std::size_t i = 0; i < ids.size(); ++i) {
+    if (auto b = table.bytes_of(ids[i])) {
+      out += *b;
+    } else if (const std::string* s = specials.bytes_of(ids[i])) {
+      out += *s;
+    } else {
+      throw DecodeError("unknown token id " + std::to_string(ids[i]) + " at index " + std::to_string(i));
+    }
+  }
+  return out;
+}
+
+inline std::vector<std::string> decode_batch(const BatchEncoding& enc, const MergeTable& table,
+                                             const SpecialTokenSet& specials, bool skip_specials) {
+  std::vector<std::string> out(enc.batch_size);
+  for (std::size_t r = 0; r < enc.batch_size; ++r) {
+    TokenSeq ids = enc.row(r);
+    if (skip_specials) {
+      TokenSeq kept;
+      for (TokenId id : ids)
+        if (!specials.contains_id(id)) kept.push_back(id);
+      ids.swap(kept);
+    }
+    try {
+      out[r] = decode(table, specials, ids);
+    } catch (const DecodeError& e) {
+      throw DecodeError("row " + std::to_string(r) + ": " + e.what());
+    }
+  }
+  return out;
+}
+
+}  // namespace blockbpe_b200

@@ -243,3 +243,28 @@ def test_full_size_cfg2_properties(gpt2):
     for r in rng.integers(0, off.size - 1, 200):
         s = data[int(off[r]):int(off[r + 1])].tobytes()
         assert ids[int(oo[r]):int(oo[r + 1])].tolist() == orc.heap_bpe(orc.initial(s))
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_remapped_ids_and_sparse_ranks(engine, toy_tables, oracle_for):
+    """Canonical tables may use any unique u32 ids and ranks (merge_table.hpp:
+    473-497); the device works on dense ids/ranks and maps back."""
+    from oracle.oracle import CRestatement
+    t = toy_tables["random3"]
+    idmap = lambda i: 3_000_000_000 + 7919 * i
+    toks = [(idmap(i), bytes(b)) for i, b in t["tokens"]]
+    merges = [(10 * r + 5, idmap(l), idmap(rr), idmap(m)) for r, l, rr, m in t["merges"]]
+    table = bb.MergeTable.build(toks, merges)
+    assert table.info()["remapped_ids"] == 1
+    bt = [0xFFFFFFFF] * 256
+    for i, b in toks:
+        if len(b) == 1:
+            bt[b[0]] = i
+    orc = CRestatement(np.array(merges, np.uint32), bt)
+    rng = np.random.default_rng(5)
+    rows = [bytes(rng.choice(np.frombuffer(b"abcd", np.uint8), rng.integers(0, 60))) for _ in range(300)]
+    rows += [b"abcd" * 20, b"a" * 40]
+    data, off = bb.pack_rows(rows)
+    ids, oo, _ = make_encoder(engine).encode_packed(table, data, off)
+    wi, wo = orc.encode_packed(data, off)
+    assert np.array_equal(oo, wo) and np.array_equal(ids, wi)

@@ -1,0 +1,61 @@
+"""Multi-process plumbing of bench.py's N-GPU mode, on CPU with gloo
+(world_size 2, 127.0.0.1): per-rank deterministic shards, no data-path
+collective, max-over-ranks timing, whole-job token totals."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    import paper_2507_11941_b200 as bb
+    table = bb.load_merge_table_files(os.path.join(bench.GOLDEN, "gpt2.bbpt"), None, "binary")
+    data, off, _ = bench.make_rows(table, 2, rank, 1 / 4096)
+    # Each rank's shard is its own (weak scaling): seeds differ per rank.
+    digest = int(np.frombuffer(data.tobytes()[:4096], np.uint8).astype(np.int64).sum())
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # what bench.barrier_max does (nccl on GPU)
+    n = torch.tensor([off.size - 1], dtype=torch.int64)
+    dist.all_reduce(n)
+    q.put((rank, digest, float(t.item()), int(n.item())))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_plan():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] != res[1][1]                 # distinct shards
+    assert res[0][2] == res[1][2] == 2.0          # max over ranks
+    assert res[0][3] == res[1][3] == 2 * 256      # whole-job row count
+
+
+def test_partition_shards_cover_rows():
+    import paper_2507_11941_b200 as bb
+    off = np.arange(0, 1001, dtype=np.uint64) * np.uint64(7)
+    b = bb.partition(off, 8)
+    assert b[0] == 0 and b[-1] == 1000
+    sizes = np.diff(b.astype(np.int64))
+    assert sizes.max() - sizes.min() <= 1
