@@ -292,6 +292,13 @@ def main():
     alg_bytes = total + 4 * ntok + 16 * n
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms["k_pieces"] / 1e3) / 1e9
+    # DRAM traffic of the same kernel on the same command, from the committed
+    # ncu --set full capture (profiles/<round>_k_pieces_cfg<N>.json), if any.
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"r1_k_pieces_cfg{args.config}.json")
+    if os.path.exists(prof) and args.scale == 1.0 and args.engine == "pieces":
+        with open(prof) as f:
+            traffic = json.load(f).get("traffic_bytes")
 
     # ---- end to end through the host API (pinned host buffers) ----
     e2e = None
@@ -338,7 +345,7 @@ def main():
             "kernel_ms": k_ms,
             "roofline": {"bound": "hbm", "kernel": "k_pieces", "achieved": achieved, "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
                          "dominant_kernel": dom},
             "cpu_baseline": cpu,
             "e2e": e2e,
