@@ -91,6 +91,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def load_table(cfg):
+    """GPT-2 (50,000 merges) for configs 1, 2, 3, 5; config 4 extends it to
+    200,000 consistent word-level merges (paper_2507_11941_b200.synth.extend_table)."""
+    from paper_2507_11941_b200 import load_merge_table_files, synth
+    gpt2 = load_merge_table_files(os.path.join(GOLDEN, "gpt2.bbpt"), None, "binary")
+    if cfg == 4:
+        t, _ = synth.extend_table(gpt2, 200000)
+        return t, "gpt2 extended to 200,000 merges (synth.extend_table, seed 4)"
+    return gpt2, "gpt2 (50,000 merges)"
+
+
 def make_rows(table, cfg, rank, scale):
     from paper_2507_11941_b200 import synth
     gen = synth.TextGen(synth.word_list(table))
@@ -130,9 +141,8 @@ def reference_arm(args, rank, world):
     block engine, PhasePool(nproc)) on a bounded sample of our arm's workload."""
     if rank != 0:
         return
-    from paper_2507_11941_b200 import load_merge_table_files
     from oracle.oracle import Reference
-    table = load_merge_table_files(os.path.join(GOLDEN, "gpt2.bbpt"), None, "binary")
+    table, table_desc = load_table(args.config)
     data, offsets, desc = make_rows(table, args.config, 0, args.scale)
     ids_, off_, blob_, m4_ = table.export()
     ref = Reference.from_arrays(ids_, off_, blob_, m4_)
@@ -159,7 +169,7 @@ def reference_arm(args, rank, world):
         "metric": METRIC, "impl": "reference", "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"cfg{args.config}: {desc}", "table": "gpt2 (50,000 merges)",
+        "config": {"workload": f"cfg{args.config}: {desc}", "table": table_desc,
                    "sample_rows": n, "sample_bytes": int(sub_off[-1])},
         "input_GBps": int(sub_off[-1]) / t / 1e9,
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "reference",
@@ -196,7 +206,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--scale", type=float, default=None,
+                    help="row-count scale (default 1; config 5 defaults to 1/16 = 1 GB per GPU)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--engine", default="pieces", choices=["pieces", "block"])
     ap.add_argument("--ref-seconds", type=float, default=10.0)
@@ -205,6 +216,8 @@ def main():
     ap.add_argument("--no-merge-only", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else max(args.warmup, 1)
+    if args.scale is None:
+        args.scale = 1 / 16 if args.config == 5 else 1.0
 
     rank, world, local = dist_init(args.gpus)
     if args.impl == "reference":
@@ -215,7 +228,7 @@ def main():
     import paper_2507_11941_b200 as bb
 
     torch.cuda.set_device(local)
-    table = bb.load_merge_table_files(os.path.join(GOLDEN, "gpt2.bbpt"), None, "binary")
+    table, table_desc = load_table(args.config)
     data, offsets, desc = make_rows(table, args.config, rank, args.scale)
     n = offsets.size - 1
     total = int(offsets[-1])
@@ -335,8 +348,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"cfg{args.config}: {desc} per GPU (Zipf GPT-2 words)",
-                       "table": "gpt2 (50,000 merges)", "engine": args.engine,
+            "config": {"workload": f"cfg{args.config}: {desc} per GPU (Zipf words of the table)",
+                       "table": table_desc, "engine": args.engine,
                        "parallelism": f"rows sharded, {world} independent GPU(s), no collective",
                        "l2": "inputs (%d MiB) larger than L2" % (total >> 20)},
             "input_GBps": bytes_all / (ms / 1e3) / 1e9,

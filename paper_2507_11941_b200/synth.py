@@ -127,3 +127,61 @@ def config_rows(gen: TextGen, cfg: int, scale: float = 1.0, seed: Optional[int] 
         d, o = rows_lengths(gen, L, seed)
         return d, o, f"{n} x logU[128 B, 64 KiB] ({int(o[-1]) / 1e9:.2f} GB)"
     raise ValueError(cfg)
+
+
+_WORDISH_L = re.compile(rb"^ ?[a-z]+$")
+_WORDISH_R = re.compile(rb"^[a-z]+$")
+
+
+def extend_table(table, total_merges: int, seed: int = 4, max_len: int = 16):
+    """Large-vocabulary table for BASELINE config 4 (128k-200k merges).
+
+    Continues a base table with training-consistent, word-like merges: each
+    new merge joins an existing " ?[a-z]+" token with an existing "[a-z]+"
+    token (both created at lower ranks, so the table stays rank-consistent
+    like tests/helpers.hpp:85-114) whose concatenation is not yet a token.
+    Merges stay inside words, as in regex-trained vocabularies, so the
+    junction-bigram set is essentially unchanged. Deterministic in `seed`.
+    Returns (MergeTable, (ids, tok_off, tok_bytes, merges4))."""
+    from .api import MergeTable
+    ids, off, blob, m4 = table.export()
+    raw = blob.tobytes()
+    toks = {int(i): raw[int(off[k]):int(off[k + 1])] for k, i in enumerate(ids)}
+    by_bytes = set(toks.values())
+    left = [i for i, b in toks.items() if _WORDISH_L.match(b) and len(b) <= max_len - 1]
+    right = [i for i, b in toks.items() if _WORDISH_R.match(b) and len(b) <= max_len - 1]
+    left.sort()
+    right.sort()
+    rng = np.random.default_rng(seed)
+    merges = [tuple(int(x) for x in row) for row in m4]
+    pairs = set((m[1], m[2]) for m in merges)
+    next_id = max(toks) + 1
+    rank = max(m[0] for m in merges) + 1 if merges else 0
+    attempts = 0
+    while len(merges) < total_merges and attempts < 40 * total_merges:
+        attempts += 1
+        # Zipf-ish preference for low ids (frequent tokens) on both sides.
+        li = left[min(int(rng.pareto(1.2) * 300), len(left) - 1)]
+        ri = right[min(int(rng.pareto(1.2) * 300), len(right) - 1)]
+        if (li, ri) in pairs:
+            continue
+        w = toks[li] + toks[ri]
+        if len(w) > max_len or w in by_bytes:
+            continue
+        toks[next_id] = w
+        by_bytes.add(w)
+        pairs.add((li, ri))
+        merges.append((rank, li, ri, next_id))
+        if _WORDISH_L.match(w):
+            left.append(next_id)
+        if _WORDISH_R.match(w):
+            right.append(next_id)
+        next_id += 1
+        rank += 1
+    items = sorted(toks.items())
+    nids = np.array([i for i, _ in items], np.uint32)
+    noff = np.zeros(len(items) + 1, np.uint64)
+    np.cumsum([len(b) for _, b in items], out=noff[1:])
+    nblob = np.frombuffer(b"".join(b for _, b in items), np.uint8).copy()
+    nm4 = np.array(merges, np.uint32)
+    return MergeTable.from_arrays(nids, noff, nblob, nm4), (nids, noff, nblob, nm4)

@@ -268,3 +268,31 @@ def test_remapped_ids_and_sparse_ranks(engine, toy_tables, oracle_for):
     ids, oo, _ = make_encoder(engine).encode_packed(table, data, off)
     wi, wo = orc.encode_packed(data, off)
     assert np.array_equal(oo, wo) and np.array_equal(ids, wi)
+
+
+@pytest.fixture(scope="module")
+def big_tables(gpt2):
+    from paper_2507_11941_b200 import synth
+    t200, arrs = synth.extend_table(gpt2, 200000)
+    ids, off, blob, m4 = arrs
+    keep = m4[:, 0] < 128000
+    t128 = bb.MergeTable.from_arrays(ids, off, blob, m4[keep])
+    return {"200k": (t200, m4), "128k": (t128, m4[keep])}
+
+
+@pytest.mark.parametrize("which", ["128k", "200k"])
+@pytest.mark.parametrize("engine", ENGINES)
+def test_large_vocab_cfg4_vs_oracle(which, engine, big_tables):
+    """BASELINE config 4: 128k/200k-merge tables (wide ids, 4 MiB L2-resident
+    hash), log-uniform 128 B-16 KiB rows, against the oracle's heap engine
+    (identical to the block engine on these rank-consistent tables)."""
+    from oracle.oracle import CRestatement
+    from paper_2507_11941_b200 import synth
+    table, m4 = big_tables[which]
+    assert table.info()["rank_consistent"] == 1
+    gen = synth.TextGen(synth.word_list(table))
+    data, off, _ = synth.config_rows(gen, 4, scale=1 / 512)
+    orc = CRestatement(m4, [table.byte_token(b) for b in range(256)])
+    wi, wo = orc.encode_packed(data, off, engine=1)
+    ids, oo, _ = make_encoder(engine).encode_packed(table, data, off)
+    assert np.array_equal(oo, wo) and np.array_equal(ids, wi)

@@ -108,3 +108,15 @@ def test_decode_and_unknown_ids(gpt2):
     assert bb.decode(gpt2, sp, [31373, 995]) == b"hello world"
     with pytest.raises(bb.DecodeError, match="unknown token id 60000 at index 1"):
         bb.decode(gpt2, sp, [31373, 60000])
+
+
+def test_extended_large_tables(gpt2):
+    from paper_2507_11941_b200 import synth
+    t, (ids, off, blob, m4) = synth.extend_table(gpt2, 200000)
+    info = t.info()
+    assert info["merge_count"] == 200000 and info["rank_consistent"] == 1
+    assert info["remapped_ids"] == 0 and info["id_bits"] == 18 and info["hash_slots"] == 524288
+    # regex-like: the junction set barely grows
+    assert info["junction_bigrams"] < 3000
+    t2, _ = synth.extend_table(gpt2, 200000)
+    assert np.array_equal(t2.export()[3], m4)  # deterministic
