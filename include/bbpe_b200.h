@@ -178,10 +178,10 @@ int bbpe_ctx_sync(bbpe_ctx* ctx);
 uint64_t bbpe_ctx_kernel_launches(const bbpe_ctx* ctx);
 /* Per-kernel device time (CUDA events recorded between launches on the
  * launching stream) summed over the encodes since the last reset:
- * ms[0] k_tile_first, ms[1] k_pieces, ms[2] k_long_pieces, ms[3] k_tile_scan,
- * ms[4] k_gather. Synchronises the streams used. *calls receives the number
- * of encodes. */
-#define BBPE_N_KERNELS 5
+ * ms[0] k_tile_first, ms[1] k_pieces (or k_block_rows), ms[2] k_merge,
+ * ms[3] k_long_pieces, ms[4] k_tile_scan, ms[5] k_gather. Synchronises the
+ * streams used. *calls receives the number of encodes. */
+#define BBPE_N_KERNELS 6
 int bbpe_ctx_kernel_times(bbpe_ctx* ctx, double* ms, uint64_t* calls, int reset);
 
 /* block_bpe on explicit initial token ids (one sequence), always the

@@ -412,7 +412,7 @@ class Encoder:
     def kernel_launches(self) -> int:
         return LIB.bbpe_ctx_kernel_launches(self._h)
 
-    KERNELS = ("k_tile_first", "k_pieces", "k_long_pieces", "k_tile_scan", "k_gather")
+    KERNELS = ("k_tile_first", "k_pieces", "k_merge", "k_long_pieces", "k_tile_scan", "k_gather")
 
     def kernel_times(self, reset: bool = True) -> Tuple[dict, int]:
         """Per-kernel device ms (CUDA events on the launching stream) summed

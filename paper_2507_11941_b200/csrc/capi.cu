@@ -137,7 +137,7 @@ struct bbpe_ctx {
   bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1};
   bbpe::LaunchPlan plan;
   DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
-  DevBuf staging, tile_count, tile_lrec, lrec, tile_base;
+  DevBuf staging, tile_count, tile_lrec, lrec, tile_base, long_idx;
   DevBuf in_bytes, in_offsets, out_ids, out_offsets;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
@@ -203,8 +203,13 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   c.counters.ensure(CNT_N * 4);
   c.err.ensure(ERR_N * 8);
   const bool block = c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0;
-  a.lp_cap = block ? n + 1 : total / (kLmax + 1) + 2;
+  // Records: every row (block engine) or, worst case, one per 2 bytes (merge
+  // pieces) plus the long pieces.
+  a.lp_cap = block ? n + 1 : total / 2 + total / (kLmax + 1) + 2;
+  a.long_cap = block ? n + 1 : total / (kLmax + 1) + 2;
   c.lrec.ensure(a.lp_cap * sizeof(LongRec));
+  c.long_idx.ensure(a.long_cap * 4);
+  a.long_idx = c.long_idx.as<uint32_t>();
   c.lpo.ensure((total + 1) * 4);
   c.lpx.ensure(std::max<uint64_t>(total, 1) * 8);
   c.lpy.ensure(std::max<uint64_t>(total, 1) * 8);
@@ -718,7 +723,7 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->staging, &c->tile_count, &c->tile_lrec, &c->lrec, &c->tile_base, &c->tile_first, &c->status, &c->counters, &c->err, &c->lpo, &c->lpx,
+    for (DevBuf* b : {&c->staging, &c->tile_count, &c->tile_lrec, &c->lrec, &c->tile_base, &c->long_idx, &c->tile_first, &c->status, &c->counters, &c->err, &c->lpo, &c->lpx,
                       &c->lpy, &c->trace, &c->trace_count, &c->in_bytes, &c->in_offsets,
                       &c->out_ids, &c->out_offsets})
       b->release();
@@ -920,6 +925,7 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   c->counters.ensure(CNT_N * 4);
   c->err.ensure(ERR_N * 8);
   c->lrec.ensure(sizeof(LongRec));
+  c->long_idx.ensure(4);
   c->lpo.ensure((n + 1) * 4);
   c->lpx.ensure(n * 8);
   c->lpy.ensure(n * 8);
@@ -930,6 +936,8 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   a.err = c->err.as<uint64_t>();
   a.lrec = c->lrec.as<LongRec>();
   a.lp_cap = 1;
+  a.long_idx = c->long_idx.as<uint32_t>();
+  a.long_cap = 1;
   a.lpo = c->lpo.as<uint32_t>();
   a.lpx = c->lpx.as<uint64_t>();
   a.lpy = c->lpy.as<uint64_t>();
@@ -942,7 +950,10 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   LongRec lp{0, n, 0, 0u, 0u};
   uint32_t counters[CNT_N] = {0};
   counters[CNT_LREC] = 1;
+  counters[CNT_LONG] = 1;
+  const uint32_t zero = 0;
   ck(cudaMemcpyAsync(a.lrec, &lp, sizeof(lp), cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemcpyAsync(a.long_idx, &zero, 4, cudaMemcpyHostToDevice, c->stream), "H2D");
   ck(cudaMemcpyAsync(a.counters, counters, sizeof(counters), cudaMemcpyHostToDevice, c->stream), "H2D");
   ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, c->stream), "memset");
   ck(cudaMemcpyAsync(a.lpx, x.data(), n * 8, cudaMemcpyHostToDevice, c->stream), "H2D");

@@ -36,7 +36,7 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr uint32_t kProbe = 0xFFFFFFFEu;   // rank not yet looked up
 constexpr uint32_t kMergeMark = 0xFFFFFFFDu;
 constexpr uint32_t kUnchanged = 0x80000000u;  // lpo flag: piece merged nothing
-constexpr int kWords = (kWin + 31) / 32;
+constexpr int kWords = (kWin + 127) / 128 * 4;  // boundary words, whole 128-position chunks
 constexpr int kTileWords = kTile / 32;
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
@@ -130,7 +130,7 @@ __global__ void k_tile_first(EncodeArgs a) {
 // ---------------------------------------------------------------------------
 // Per-warp window over [b0-4, b0+kWin+4): bytes, row starts, hard boundaries.
 // Bytes are copied as aligned words: wb[q + 4] is the byte at b0 + q.
-constexpr int kWinWordsB = (kWin + 8 + 15) / 16 * 4;  // u32 words of bytes
+constexpr int kWinWordsB = kWords * 8 + 4;  // u32 words of bytes (all boundary positions + 4)
 struct Window {
   uint32_t wbw[kWinWordsB];  // window bytes (as words)
   uint32_t sb[kWords];       // row-start bits
@@ -146,7 +146,7 @@ struct Window {
 // Loads the window and computes boundaries; returns (lane 0's view of) the
 // first invalid byte position found in [b0, b0 + tlen), or ~0.
 __device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc, const uint32_t* lut,
-                            uint64_t tile, int lane, int tlen) {
+                            uint64_t tile, int lane, int tlen, bool full_lut) {
   const uint64_t b0 = tile * kTile;
   const uint64_t wbase = b0 >= 4 ? b0 - 4 : 0;
   const int wofs = b0 >= 4 ? 0 : 1;  // tile 0: word 0 of the window is before the input
@@ -181,26 +181,41 @@ __device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc
     if (__ballot_sync(kFull, in) != kFull) break;
   }
   __syncwarp();
-  // Boundaries, and the invalid-byte check (pretokenize.hpp:64-67).
+  // Boundaries: lane handles 4 consecutive positions per 128-position chunk
+  // (one word of bytes + the byte before), 8 lanes OR their nibbles into a
+  // boundary word. Plus the invalid-byte check (pretokenize.hpp:64-67) when
+  // the table lacks a token for some byte value.
+  const int64_t limit = min((int64_t)kWin, (int64_t)(a.total - b0));  // positions past this are boundaries
   uint32_t badw = 0xFFFFFFFFu;
 #pragma unroll 1
-  for (int wd = 0; wd < kWords; ++wd) {
-    const int q = wd * 32 + lane;
-    const uint64_t abs = b0 + q;
-    bool b = true;
-    if (q < kWin && abs < a.total) {
-      const uint32_t cur = w.byte(q);
-      b = (w.sb[wd] >> lane) & 1u;
-      if (!b) b = !is_junction(junc, w.byte(q - 1), cur);
-      if (q < tlen && lut[cur] == kInvalidToken && badw == 0xFFFFFFFFu) badw = uint32_t(q);
+  for (int c = 0; c < kWords / 4; ++c) {
+    const int q0 = 128 * c + 4 * lane;
+    const uint32_t cur = w.wbw[32 * c + lane + 1];
+    const uint32_t prv = w.wbw[32 * c + lane] >> 24;
+    uint32_t nib = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t pb = j == 0 ? prv : (cur >> (8 * (j - 1))) & 0xFFu;
+      const uint32_t cb = (cur >> (8 * j)) & 0xFFu;
+      if (!is_junction(junc, pb, cb)) nib |= 1u << j;
+      if (!full_lut && q0 + j < tlen && lut[cb] == kInvalidToken && badw == 0xFFFFFFFFu) badw = uint32_t(q0 + j);
     }
-    const unsigned m = __ballot_sync(kFull, b);
-    if (lane == 0) w.bd[wd] = m;
+    nib |= (w.sb[4 * c + (lane >> 3)] >> (4 * (lane & 7))) & 0xFu;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (q0 + j >= limit) nib |= 1u << j;
+    uint32_t v = nib << (4 * (lane & 7));
+    v |= __shfl_xor_sync(kFull, v, 1);
+    v |= __shfl_xor_sync(kFull, v, 2);
+    v |= __shfl_xor_sync(kFull, v, 4);
+    if ((lane & 7) == 0) w.bd[4 * c + (lane >> 3)] = v;
   }
-  const uint32_t bad = __reduce_min_sync(kFull, badw);
-  if (bad != 0xFFFFFFFFu && lane == 0)
-    atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
-              (unsigned long long)(b0 + bad));
+  if (!full_lut) {
+    const uint32_t bad = __reduce_min_sync(kFull, badw);
+    if (bad != 0xFFFFFFFFu && lane == 0)
+      atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
+                (unsigned long long)(b0 + bad));
+  }
   __syncwarp();
 }
 
@@ -324,9 +339,10 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
     if (tid == 0) s_idx = atomicAdd(&a.counters[CNT_LP_NEXT], 1u);
     __syncthreads();
     const uint32_t idx = s_idx;
-    const uint32_t count = min((uint64_t)a.counters[CNT_LREC], (uint64_t)a.lp_cap);
+    const uint32_t count = min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap);
     if (idx >= count) return;
-    const LongRec P = a.lrec[idx];
+    const uint32_t ridx = a.long_idx[idx];
+    const LongRec P = a.lrec[ridx];
     const int32_t len = static_cast<int32_t>(P.len);
     uint64_t* X = a.lpx + P.start;
     uint64_t* Y = a.lpy + P.start;
@@ -428,7 +444,7 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
     uint32_t* O = a.lpo + P.start;
     if (tid == 0) {
       O[0] = static_cast<uint32_t>(n) | ((n == len && !a.tokens_input) ? kUnchanged : 0u);
-      a.lrec[idx].count = static_cast<uint32_t>(n);
+      a.lrec[ridx].count = static_cast<uint32_t>(n);
     }
     if (n < len || a.tokens_input)
       for (int32_t i = tid; i < n; i += NT) O[1 + i] = tok_of(X[i]);
@@ -436,35 +452,12 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
 }
 
 // ---------------------------------------------------------------------------
-// k_pieces: warp-per-tile merge of all short pieces starting in the tile.
-// Per tile: window -> piece list -> initial tokens -> warp-parallel, batched
-// initial pair probes -> sub-warp "blocks" run the reference pass loop, one
-// piece per group of W lanes (one token per lane) -> tokens staged per tile
-// (no ordering wait; k_gather assembles the CSR afterwards).
-//
-// This is the paper's one-block-per-string engine scaled to the piece: a
-// pass is a W-lane shuffle min-reduction, a ballot of the pairs at the
-// minimum (left-greedy over runs), a ballot/popc compaction, and re-probes
-// of only the pairs that touch a merged token.
+// Marks in the per-lane working arrays of k_merge (16- or 32-bit).
 template <typename Tk>
 struct Marks {
   static constexpr uint32_t kNone = Tk(~Tk(0));  // no rank / uncovered position
 };
 
-constexpr int kMemoDone = 0x40;  // plen flag: piece resolved by the memo
-
-template <typename Tk>
-struct PieceSmem {
-  Window w;
-  uint16_t plist[kTile];      // piece starts (window-relative), in order
-  uint8_t plen[kTile];        // piece length, 0xFF = long (> kLmax)
-  uint16_t clist[kTile];      // pieces that need merge passes
-  uint16_t cnt[kTile + 1];    // short tokens per piece -> exclusive prefix
-  Tk tok[kWin + 1];
-  Tk rnk[kWin + 1];
-  uint64_t llen[kTile / (kLmax + 1) + 2];    // byte length of each long piece, in order
-  uint16_t lk[kTile / (kLmax + 1) + 2];      // their piece indices
-};
 
 // Batched probe: issue the bucket loads, resolve later. K32: narrow tables
 // (ids < 2^16) with 32-bit keys, slot = key32 << 32 | rank.
@@ -639,12 +632,24 @@ __device__ __noinline__ uint64_t long_piece_length(const EncodeArgs& a, const ui
   return row_end - abs;
 }
 
+struct PieceSmem {
+  Window w;
+  uint16_t plist[kTile];      // piece starts (window-relative), in order
+  uint8_t plen[kTile];        // piece length, 0xFF = long (> kLmax)
+  uint16_t cnt[kTile + 1];    // staging slot of each piece (exclusive prefix)
+  uint16_t dk[kTile];         // deferred pieces (merge or long), in order
+  uint64_t llen[kTile / (kLmax + 1) + 2];
+};
+
 #ifndef BBPE_PIECES_MINB
-#define BBPE_PIECES_MINB 3
+#define BBPE_PIECES_MINB 4
 #endif
-template <typename Tk>
+// k_pieces: warp per tile. Window -> hard boundaries -> piece list; each piece
+// is resolved in place when it is a single byte or a piece-memo hit, and its
+// tokens go to the tile's staging slots right away; other pieces are deferred
+// (records, in piece order): 2..kLmax-byte pieces to k_merge (slots reserved),
+// longer ones to k_long_pieces.
 __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(EncodeArgs a, DevTable T) {
-  constexpr bool K32 = sizeof(Tk) == 2;
   __shared__ uint32_t s_lut[256];
   __shared__ uint32_t s_junc[2048];
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -652,7 +657,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_junc[i] = T.junction[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  PieceSmem<Tk>& S = reinterpret_cast<PieceSmem<Tk>*>(s_dyn)[wid];
+  PieceSmem& S = reinterpret_cast<PieceSmem*>(s_dyn)[wid];
   const uint32_t* d2id = T.d2id;
 
   for (;;) {
@@ -662,159 +667,106 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     if (tile >= a.num_tiles) return;
     const uint64_t b0 = tile * kTile;
     const uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
-
     const int tlen = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
-    load_window(S.w, a, s_junc, s_lut, tile, lane, tlen);
+    load_window(S.w, a, s_junc, s_lut, tile, lane, tlen, T.full_lut != 0);
 
-    // (1) Piece list with lengths (distance to the next piece start; the
-    // last piece of the tile searches the boundary bits past the tile).
+    // (1) Piece list: lane w expands boundary word w.
     int npieces = 0;
-#pragma unroll 1
-    for (int wd = 0; wd * 32 < tlen; ++wd) {
-      const int q = wd * 32 + lane;
-      const bool st = q < tlen && ((S.w.bd[wd] >> lane) & 1u);
-      const unsigned m = __ballot_sync(kFull, st);
-      if (st) S.plist[npieces + __popc(m & lanemask_lt(lane))] = static_cast<uint16_t>(q);
-      npieces += __popc(m);
-    }
-    __syncwarp();
-    for (int k = lane; k < npieces; k += 32) {
-      const int q = S.plist[k];
-      const int len = (k + 1 < npieces) ? S.plist[k + 1] - q : next_boundary(S.w.bd, q, kLmax) - q;
-      S.plen[k] = len > kLmax ? 0xFF : static_cast<uint8_t>(len);
-    }
-    __syncwarp();
-
-    // (2) Piece memo: a piece equal to a vocabulary token's bytes takes its
-    // precomputed encoding (1-2 tokens, parked in rnk[q..] until staging).
-    // Everything else of 2..kLmax bytes goes on the merge list.
-    int nmerge = 0;
-    for (int k0 = 0; k0 < npieces; k0 += 32) {
-      const int k = k0 + lane;
-      int len = k < npieces ? S.plen[k] : 0;
-      bool merge = false;
-      if (k < npieces) {
-        if (len == 0xFF) {
-          S.cnt[k] = 0;
-        } else if (len < 2) {
-          S.cnt[k] = static_cast<uint16_t>(len);
-          S.tok[S.plist[k]] = Tk(s_lut[S.w.byte(S.plist[k])]);
-        } else {
-          merge = true;
-          const int q = S.plist[k];
-          uint32_t r0, r1, nres;
-          if (a.use_memo && len <= kMemoMaxLen && memo_lookup(T, S.w.wbw, q, len, r0, r1, nres)) {
-            S.plen[k] = static_cast<uint8_t>(len | kMemoDone);
-            S.cnt[k] = static_cast<uint16_t>(nres);
-            S.rnk[q] = Tk(r0);
-            S.rnk[q + 1] = Tk(r1);
-            merge = false;
-          }
-        }
+    {
+      const int nw = (tlen + 31) / 32;
+      uint32_t m = 0;
+      if (lane < nw) {
+        m = S.w.bd[lane];
+        const int rem = tlen - 32 * lane;
+        if (rem < 32) m &= (1u << rem) - 1u;
       }
-      const unsigned mm = __ballot_sync(kFull, merge);
-      if (merge) S.clist[nmerge + __popc(mm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-      nmerge += __popc(mm);
-    }
-    __syncwarp();
-
-    if (nmerge) {
-      // (3) Lane-per-piece pass loops over the merge list (pieces refill
-      // lanes as they finish). A new piece gets its initial tokens and pair
-      // ranks (two probes in flight), then one pass per loop iteration.
-      int my_n = 0, my_q = 0, my_k = 0, next = 0;
-      for (;;) {
-        const bool idle = my_n == 0;
-        const unsigned im = __ballot_sync(kFull, idle);
-        if (idle) {
-          const int i = next + __popc(im & lanemask_lt(lane));
-          if (i < nmerge) {
-            my_k = S.clist[i];
-            my_q = S.plist[my_k];
-            my_n = S.plen[my_k];
-            Tk* tk = S.tok + my_q;
-            Tk* rk = S.rnk + my_q;
-            for (int j = 0; j < my_n; ++j) tk[j] = Tk(s_lut[S.w.byte(my_q + j)]);
-            for (int j = 0; j < my_n - 1; j += 2) {
-              ProbeReq p0, p1;
-              probe_issue<K32>(p0, T, tk[j], tk[j + 1]);
-              const bool two = j + 2 < my_n;
-              if (two) probe_issue<K32>(p1, T, tk[j + 1], tk[j + 2]);
-              rk[j] = Tk(tk_rank<Tk>(probe_resolve<K32>(p0, T)));
-              if (two) rk[j + 1] = Tk(tk_rank<Tk>(probe_resolve<K32>(p1, T)));
-            }
-          }
-        }
-        next += __popc(im);
-        const bool active = my_n >= 2;
-        if (!__any_sync(kFull, active) && next >= nmerge) break;
-        if (active) {
-          const int r = lane_pass<Tk>(T, S.tok + my_q, S.rnk + my_q, my_n);
-          if (r < 2) {
-            S.cnt[my_k] = static_cast<uint16_t>(r < 0 ? my_n : r);
-            my_n = 0;
-          } else {
-            my_n = r;
-          }
-        }
-      }
-      __syncwarp();
-    }
-
-    // (5) Exclusive scan of short counts; long pieces listed in order.
-    uint32_t run = 0, nlong = 0;
-    for (int k0 = 0; k0 < npieces; k0 += 32) {
-      const int k = k0 + lane;
-      const uint32_t c = k < npieces ? S.cnt[k] : 0;
+      const uint32_t c = __popc(m);
       const uint32_t inc = warp_incl_sum(c, lane);
-      const bool lg = k < npieces && S.plen[k] == 0xFF;
-      const unsigned lm = __ballot_sync(kFull, lg);
-      if (lg) S.lk[nlong + __popc(lm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-      nlong += __popc(lm);
-      __syncwarp();
-      if (k < npieces) S.cnt[k] = static_cast<uint16_t>(run + inc - c);
+      int pos = int(inc - c);
+      while (m) {
+        S.plist[pos++] = static_cast<uint16_t>(32 * lane + __ffs(m) - 1);
+        m &= m - 1;
+      }
+      npieces = int(__shfl_sync(kFull, inc, 31));
+    }
+    __syncwarp();
+
+    // (2) Resolve or defer every piece, 32 at a time, staging as we go.
+    uint32_t* stage = a.staging + tile * kStage;
+    uint32_t run = 0, ndef = 0, nlong = 0;
+    for (int k0 = 0; k0 < npieces; k0 += 32) {
+      const int k = k0 + lane;
+      int len = 0, q = 0;
+      uint32_t c = 0, r0 = 0, r1 = 0;
+      bool deferred = false, lg = false;
+      if (k < npieces) {
+        q = S.plist[k];
+        len = (k + 1 < npieces) ? S.plist[k + 1] - q : next_boundary(S.w.bd, q, kLmax) - q;
+        if (len > kLmax) {
+          lg = deferred = true;  // long: k_long_pieces, no staging slots
+        } else if (len == 1) {
+          c = 1;
+          r0 = s_lut[S.w.byte(q)];
+        } else {
+          uint32_t nres;
+          if (a.use_memo && len <= kMemoMaxLen && memo_lookup(T, S.w.wbw, q, len, r0, r1, nres)) {
+            c = nres;
+          } else {
+            deferred = true;  // merge piece: k_merge fills `len` reserved slots
+            c = uint32_t(len);
+          }
+        }
+        S.plen[k] = lg ? 0xFF : static_cast<uint8_t>(len);
+      }
+      const uint32_t inc = warp_incl_sum(c, lane);
+      const uint32_t slot = run + inc - c;
+      if (k < npieces) S.cnt[k] = static_cast<uint16_t>(slot);
+      if (!deferred && c) {
+        stage[slot] = d2id ? __ldg(d2id + r0) : r0;
+        if (c > 1) stage[slot + 1] = d2id ? __ldg(d2id + r1) : r1;
+      }
+      const unsigned dm = __ballot_sync(kFull, deferred);
+      if (deferred) S.dk[ndef + __popc(dm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+      ndef += __popc(dm);
+      nlong += __popc(__ballot_sync(kFull, lg));
       run += __shfl_sync(kFull, inc, 31);
     }
     if (lane == 0) S.cnt[npieces] = static_cast<uint16_t>(run);
     __syncwarp();
-    // Long pieces (rare): full length = distance to the next hard boundary or
-    // the end of the row; k_long_pieces merges them after this kernel.
-    for (uint32_t li = 0; li < nlong; ++li) {
-      const uint64_t len = long_piece_length(a, s_junc, b0 + S.plist[S.lk[li]], lane);
-      if (lane == 0) S.llen[li] = len;
-    }
-    __syncwarp();
 
-    // (6) Stage short tokens in piece order (final ids).
-    uint32_t* stage = a.staging + tile * kStage;
-    for (int k = lane; k < npieces; k += 32) {
-      const int pl = S.plen[k];
-      if (pl == 0xFF) continue;
-      const int q = S.plist[k];
-      const uint32_t c = S.cnt[k + 1] - S.cnt[k];
-      uint32_t* dst = stage + S.cnt[k];
-      const Tk* src = (pl != 0xFF && (pl & kMemoDone)) ? S.rnk + q : S.tok + q;
-      for (uint32_t i = 0; i < c; ++i) {
-        const uint32_t v = src[i];
-        dst[i] = d2id ? __ldg(d2id + v) : v;
+    // (3) Deferred-piece records (contiguous per tile, in piece order).
+    uint64_t first = 0, lfirst = 0;
+    if (lane == 0 && ndef) first = atomicAdd(&a.counters[CNT_LREC], ndef);
+    if (lane == 0 && nlong) lfirst = atomicAdd(&a.counters[CNT_LONG], nlong);
+    first = __shfl_sync(kFull, first, 0);
+    lfirst = __shfl_sync(kFull, lfirst, 0);
+    if (nlong) {
+      // Long pieces (rare): full length to the next hard boundary or row end.
+      uint32_t li = 0;
+      for (uint32_t i = 0; i < ndef; ++i) {
+        const int k = S.dk[i];
+        if (S.plen[k] != 0xFF) continue;
+        const uint64_t abs = b0 + S.plist[k];
+        const uint64_t len = long_piece_length(a, s_junc, abs, lane);
+        if (lane == 0) {
+          if (first + i < a.lp_cap) a.lrec[first + i] = LongRec{abs, len, 0, S.cnt[k], 0u};
+          if (lfirst + li < a.long_cap) a.long_idx[lfirst + li] = uint32_t(first + i);
+        }
+        ++li;
       }
     }
-    // (7) Long-piece records, tile short total.
+    for (uint32_t i = lane; i < ndef; i += 32) {
+      const int k = S.dk[i];
+      if (S.plen[k] == 0xFF) continue;
+      if (first + i < a.lp_cap)
+        a.lrec[first + i] = LongRec{b0 + S.plist[k], S.plen[k], kMergeKind, S.cnt[k], 0u};
+    }
     if (lane == 0) {
-      uint64_t rec = 0;
-      if (nlong) {
-        const uint32_t first = atomicAdd(&a.counters[CNT_LREC], nlong);
-        for (uint32_t li = 0; li < nlong && first + li < a.lp_cap; ++li) {
-          const int k = S.lk[li];
-          a.lrec[first + li] = LongRec{b0 + S.plist[k], S.llen[li], 0, S.cnt[k], 0u};
-        }
-        rec = (uint64_t(first) << 24) | nlong;
-      }
-      a.tile_lrec[tile] = rec;
+      a.tile_lrec[tile] = ndef ? ((first << 24) | ndef) : 0;
       a.tile_count[tile] = run;
     }
-    // (8) Row offsets relative to the tile: short tokens before the row in
-    // the low 40 bits, long pieces before it above; k_gather resolves them.
+    // (4) Row offsets relative to the tile: staging slots before the row (low
+    // 40 bits) and deferred pieces before it (above); k_gather resolves them.
     for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
       const int o = static_cast<int>(a.offsets[s] - b0);
       int lo = 0, hi = npieces;  // first piece with plist >= o
@@ -823,10 +775,139 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         if (S.plist[mid] < o) lo = mid + 1; else hi = mid;
       }
       uint64_t lb = 0;
-      while (lb < nlong && S.lk[lb] < lo) ++lb;
+      while (lb < ndef && S.dk[lb] < lo) ++lb;
       a.out_offsets[s] = uint64_t(S.cnt[lo]) | (lb << 40);
     }
     __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_merge: the deferred 2..kLmax-byte pieces of every tile, lane per piece,
+// lanes refilled as pieces finish. Working arrays live in shared memory in a
+// [slot][lane] layout (bank = lane: conflict-free for any per-lane index).
+// Tokens go to the slots k_pieces reserved in the piece's tile staging.
+template <typename Tk>
+struct MergeSmem {
+  Tk tok[kLmax][32];
+  Tk rnk[kLmax][32];
+};
+
+// One lane, one pass (block_engine.hpp:286-307) over a piece held in a
+// column of the [slot][lane] arrays: min over cached ranks, sweep-compact in
+// place (a pair at the minimum merges unless its left token was just
+// consumed -- flags[i+1] = (ranks[i] == m && !flags[i])), re-probe only the
+// pairs touching a merged token, two in flight. Returns the new length, or -1.
+template <typename Tk>
+__device__ __forceinline__ int lane_pass_col(const DevTable& T, Tk (*tok)[32], Tk (*rnk)[32], int lane,
+                                             int n) {
+  constexpr bool K32 = sizeof(Tk) == 2;
+  constexpr uint32_t NONE = Marks<Tk>::kNone, PROBE = Marks<Tk>::kNone - 1;
+  uint32_t m = NONE;
+  for (int i = 0; i < n - 1; ++i) m = min(m, uint32_t(rnk[i][lane]));
+  if (m == NONE) return -1;
+  const Tk M = Tk(__ldg(T.r2m + m));
+  int j = 0, i = 0;
+  while (i < n) {
+    const uint32_t ri = (i < n - 1) ? uint32_t(rnk[i][lane]) : NONE;
+    if (ri == m) {
+      tok[j][lane] = M;
+      rnk[j][lane] = Tk(PROBE);
+      if (j > 0) rnk[j - 1][lane] = Tk(PROBE);
+      i += 2;
+    } else {
+      tok[j][lane] = tok[i][lane];
+      rnk[j][lane] = Tk(ri);
+      i += 1;
+    }
+    ++j;
+  }
+  int k = 0;
+  for (;;) {
+    while (k < j - 1 && uint32_t(rnk[k][lane]) != PROBE) ++k;
+    if (k >= j - 1) break;
+    int k2 = k + 1;
+    while (k2 < j - 1 && uint32_t(rnk[k2][lane]) != PROBE) ++k2;
+    ProbeReq pa, pb;
+    probe_issue<K32>(pa, T, tok[k][lane], tok[k + 1][lane]);
+    const bool two = k2 < j - 1;
+    if (two) probe_issue<K32>(pb, T, tok[k2][lane], tok[k2 + 1][lane]);
+    rnk[k][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(pa, T)));
+    if (two) rnk[k2][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(pb, T)));
+    k = two ? k2 + 1 : j;
+  }
+  return j;
+}
+
+template <typename Tk>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTable T) {
+  constexpr bool K32 = sizeof(Tk) == 2;
+  __shared__ uint32_t s_lut[256];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  MergeSmem<Tk>* s_m = reinterpret_cast<MergeSmem<Tk>*>(s_dyn);
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tk(*tok)[32] = s_m[wid].tok;
+  Tk(*rnk)[32] = s_m[wid].rnk;
+  const uint32_t nrec = min((uint64_t)a.counters[CNT_LREC], (uint64_t)a.lp_cap);
+  const uint32_t* d2id = T.d2id;
+  uint32_t base = 0, next = 0, avail = 0;  // warp-uniform slice of record indices
+  bool exhausted = false;
+  int n = 0;  // my piece's current length (0 = idle)
+  uint32_t ridx = 0;
+  for (;;) {
+    const bool idle = n == 0;
+    const unsigned im = __ballot_sync(kFull, idle);
+    if (im && next >= avail && !exhausted) {
+      uint32_t c0 = 0;
+      if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MERGE_TICKET], 32u);
+      base = __shfl_sync(kFull, c0, 0);
+      next = 0;
+      avail = base < nrec ? min(32u, nrec - base) : 0u;
+      exhausted = avail == 0;
+    }
+    const uint32_t take = min(uint32_t(__popc(im)), avail - next);
+    const uint32_t rank = __popc(im & lanemask_lt(lane));
+    if (idle && rank < take) {
+      ridx = base + next + rank;
+      const LongRec r = a.lrec[ridx];
+      if (r.row & kMergeKind) {
+        n = int(r.len);
+        const uint8_t* src = a.bytes + r.start;
+        for (int i = 0; i < n; ++i) tok[i][lane] = Tk(s_lut[src[i]]);
+        for (int i = 0; i < n - 1; i += 2) {
+          ProbeReq p0, p1;
+          probe_issue<K32>(p0, T, tok[i][lane], tok[i + 1][lane]);
+          const bool two = i + 2 < n;
+          if (two) probe_issue<K32>(p1, T, tok[i + 1][lane], tok[i + 2][lane]);
+          rnk[i][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(p0, T)));
+          if (two) rnk[i + 1][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(p1, T)));
+        }
+      }
+    }
+    next += take;
+    const bool busy = n > 0;
+    if (!__any_sync(kFull, busy)) {
+      if (exhausted) break;
+      continue;
+    }
+    if (busy) {
+      const int r = lane_pass_col<Tk>(T, tok, rnk, lane, n);
+      if (r < 2) {
+        const int cnt = r < 0 ? n : r;
+        const LongRec& rec = a.lrec[ridx];
+        uint32_t* dst = a.staging + (rec.start / kTile) * kStage + rec.spref;
+        for (int i = 0; i < cnt; ++i) {
+          const uint32_t v = tok[i][lane];
+          dst[i] = d2id ? __ldg(d2id + v) : v;
+        }
+        a.lrec[ridx].count = uint32_t(cnt);
+        n = 0;
+      } else {
+        n = r;
+      }
+    }
   }
 }
 
@@ -859,9 +940,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_block_rows(EncodeArgs a, 
       for (uint64_t s = s0 + lane; s < s1 && s < a.n_rows; s += 32)
         ne += a.offsets[s + 1] > a.offsets[s] ? 1u : 0u;
       ne = __reduce_add_sync(kFull, ne);
-      uint64_t first = 0;
-      if (lane == 0 && ne) first = atomicAdd(&a.counters[CNT_LREC], ne);
+      uint64_t first = 0, lfirst = 0;
+      if (lane == 0 && ne) {
+        first = atomicAdd(&a.counters[CNT_LREC], ne);
+        lfirst = atomicAdd(&a.counters[CNT_LONG], ne);
+      }
       first = __shfl_sync(kFull, first, 0);
+      lfirst = __shfl_sync(kFull, lfirst, 0);
       uint32_t ri = 0;
       for (uint64_t sb = s0; sb < s1 && sb <= a.n_rows; sb += 32) {
         const uint64_t s = sb + lane;
@@ -875,8 +960,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_block_rows(EncodeArgs a, 
         const unsigned nm = __ballot_sync(kFull, ne_row);
         const uint32_t before = ri + __popc(nm & lanemask_lt(lane));
         if (s < s1 && s <= a.n_rows) a.out_offsets[s] = uint64_t(before) << 40;
-        if (ne_row && first + before < a.lp_cap)
+        if (ne_row && first + before < a.lp_cap) {
           a.lrec[first + before] = LongRec{o, e - o, s, 0u, 0u};
+          if (lfirst + before < a.long_cap) a.long_idx[lfirst + before] = uint32_t(first + before);
+        }
         ri += __popc(nm);
       }
       if (lane == 0) {
@@ -913,10 +1000,15 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(EncodeArgs a) {
     if (t < a.num_tiles) {
       c = __ldcg(a.tile_count + t);
       const uint64_t rec = __ldcg(a.tile_lrec + t);
-      if (rec) {
+      if (rec) {  // deferred pieces: long ones add their tokens, merge ones
+                  // replace their reserved slots by their tokens
         const uint64_t first = rec >> 24;
         const uint32_t nl = uint32_t(rec & 0xFFFFFF);
-        for (uint32_t li = 0; li < nl; ++li) c += __ldcg(&a.lrec[first + li].count);
+        for (uint32_t li = 0; li < nl; ++li) {
+          const LongRec& r = a.lrec[first + li];
+          c += __ldcg(&r.count);
+          if (__ldcg(&r.row) & kMergeKind) c -= __ldcg(&r.len);
+        }
       }
     }
     v[i] = c;
@@ -1004,6 +1096,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
     if (rec == 0) {
       copy_tokens(out, stage, nshort, lane);
     } else {
+      // Staged slots in order; at each deferred piece: a merge piece's tokens
+      // sit in its reserved slots (copy `count`, skip `len`), a long piece's
+      // tokens come from lpo (no slots).
       const uint64_t first = rec >> 24;
       const uint32_t nl = uint32_t(rec & 0xFFFFFF);
       uint64_t pos = 0;
@@ -1013,10 +1108,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
         copy_tokens(out + pos, stage + sp, lr.spref - sp, lane);
         pos += lr.spref - sp;
         sp = lr.spref;
-        const bool unchanged = (__ldcg(a.lpo + lr.start) & kUnchanged) != 0;
-        for (uint32_t i = lane; i < lr.count; i += 32) {
-          const uint32_t v = unchanged ? s_lut[a.bytes[lr.start + i]] : __ldcg(a.lpo + lr.start + 1 + i);
-          out[pos + i] = d2id ? __ldg(d2id + v) : v;
+        if (lr.row & kMergeKind) {
+          copy_tokens(out + pos, stage + sp, lr.count, lane);
+          sp += uint32_t(lr.len);
+        } else {
+          const bool unchanged = (__ldcg(a.lpo + lr.start) & kUnchanged) != 0;
+          for (uint32_t i = lane; i < lr.count; i += 32) {
+            const uint32_t v = unchanged ? s_lut[a.bytes[lr.start + i]] : __ldcg(a.lpo + lr.start + 1 + i);
+            out[pos + i] = d2id ? __ldg(d2id + v) : v;
+          }
         }
         pos += lr.count;
       }
@@ -1030,7 +1130,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
       const uint64_t v = __ldcg(a.out_offsets + s);
       const uint32_t lb = uint32_t(v >> 40);
       uint64_t lsum = 0;
-      for (uint32_t li = 0; li < lb; ++li) lsum += __ldcg(&a.lrec[(rec >> 24) + li].count);
+      for (uint32_t li = 0; li < lb; ++li) {
+        const LongRec& r = a.lrec[(rec >> 24) + li];
+        lsum += __ldcg(&r.count);
+        if (__ldcg(&r.row) & kMergeKind) lsum -= __ldcg(&r.len);
+      }
       a.out_offsets[s] = rb + tbase + (v & ((1ull << 40) - 1)) + lsum;
     }
   }
@@ -1062,31 +1166,27 @@ void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_ba
   k_fill_offsets<<<unsigned((n + 255) / 256), 256, 0, stream>>>(d_out_off, n, run_base);
 }
 
-template <typename Tk>
-size_t pieces_smem() {
-  return sizeof(PieceSmem<Tk>) * kWarpsPerCta;
-}
+size_t pieces_smem() { return sizeof(PieceSmem) * kWarpsPerCta; }
 
 LaunchPlan plan_launch(int device) {
   LaunchPlan p;
   cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, device);
-  int per_sm = 0;
-  cudaFuncSetAttribute(k_pieces<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(pieces_smem<uint16_t>()));
-  cudaFuncSetAttribute(k_pieces<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(pieces_smem<uint32_t>()));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pieces<uint16_t>, kWarpsPerCta * 32,
-                                                pieces_smem<uint16_t>());
-  p.main_grid = p.sm_count * (per_sm > 0 ? per_sm : 1);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pieces<uint32_t>, kWarpsPerCta * 32,
-                                                pieces_smem<uint32_t>());
-  p.main_grid_wide = p.sm_count * (per_sm > 0 ? per_sm : 1);
-  int lp_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lp_sm, k_long_pieces<kLpThreads>, kLpThreads, 0);
-  p.lp_grid = p.sm_count * (lp_sm > 0 ? lp_sm : 1);
-  int g_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_sm, k_gather, kWarpsPerCta * 32, 0);
-  p.gather_grid = p.sm_count * (g_sm > 0 ? g_sm : 1);
+  auto grid = [&](auto kern, int threads, size_t smem) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    return p.sm_count * (per_sm > 0 ? per_sm : 1);
+  };
+  cudaFuncSetAttribute(k_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pieces_smem()));
+  p.main_grid = grid(k_pieces, kWarpsPerCta * 32, pieces_smem());
+  p.main_grid_wide = p.main_grid;
+  cudaFuncSetAttribute(k_merge<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(MergeSmem<uint16_t>) * kWarpsPerCta));
+  cudaFuncSetAttribute(k_merge<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(sizeof(MergeSmem<uint32_t>) * kWarpsPerCta));
+  p.merge_grid = grid(k_merge<uint16_t>, kWarpsPerCta * 32, sizeof(MergeSmem<uint16_t>) * kWarpsPerCta);
+  p.merge_grid_wide = grid(k_merge<uint32_t>, kWarpsPerCta * 32, sizeof(MergeSmem<uint32_t>) * kWarpsPerCta);
+  p.lp_grid = grid(k_long_pieces<kLpThreads>, kLpThreads, 0);
+  p.gather_grid = grid(k_gather, kWarpsPerCta * 32, 0);
   return p;
 }
 
@@ -1101,23 +1201,32 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     ++launched;
   }
   if (ev) cudaEventRecord(ev[1], stream);
-  if (a.engine == BBPE_ENGINE_BLOCK)
+  if (a.engine == BBPE_ENGINE_BLOCK) {
     k_block_rows<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
-  else if (a.narrow)
-    k_pieces<uint16_t><<<p.main_grid, kWarpsPerCta * 32, pieces_smem<uint16_t>(), stream>>>(a, t);
-  else
-    k_pieces<uint32_t><<<p.main_grid_wide, kWarpsPerCta * 32, pieces_smem<uint32_t>(), stream>>>(a, t);
-  ++launched;
-  if (ev) cudaEventRecord(ev[2], stream);
+    ++launched;
+    if (ev) cudaEventRecord(ev[2], stream);
+  } else {
+    k_pieces<<<p.main_grid, kWarpsPerCta * 32, pieces_smem(), stream>>>(a, t);
+    ++launched;
+    if (ev) cudaEventRecord(ev[2], stream);
+    if (a.narrow)
+      k_merge<uint16_t><<<p.merge_grid, kWarpsPerCta * 32, sizeof(MergeSmem<uint16_t>) * kWarpsPerCta,
+                          stream>>>(a, t);
+    else
+      k_merge<uint32_t><<<p.merge_grid_wide, kWarpsPerCta * 32, sizeof(MergeSmem<uint32_t>) * kWarpsPerCta,
+                          stream>>>(a, t);
+    ++launched;
+  }
+  if (ev) cudaEventRecord(ev[3], stream);
   k_long_pieces<kLpThreads><<<p.lp_grid, kLpThreads, 0, stream>>>(a, t);
   ++launched;
-  if (ev) cudaEventRecord(ev[3], stream);
+  if (ev) cudaEventRecord(ev[4], stream);
   k_tile_scan<<<unsigned((a.num_tiles + kScanTiles - 1) / kScanTiles), kScanThreads, 0, stream>>>(a);
   ++launched;
-  if (ev) cudaEventRecord(ev[4], stream);
+  if (ev) cudaEventRecord(ev[5], stream);
   k_gather<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
   ++launched;
-  if (ev) cudaEventRecord(ev[5], stream);
+  if (ev) cudaEventRecord(ev[6], stream);
   return launched;
 }
 

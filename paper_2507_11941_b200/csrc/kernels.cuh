@@ -21,21 +21,25 @@ constexpr int kWarpsPerCta = 8;
 constexpr int kLpThreads = 512;     // CTA size of the long-piece (block engine) kernel
 
 // Counter slots (u32).
-enum { CNT_TILE_TICKET = 0, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4, CNT_N = 8 };
+enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
+       CNT_MERGE_TICKET = 5, CNT_N = 8 };
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_N = 4 };
 
-// A long piece (> kLmax bytes, or a whole row under BBPE_ENGINE_BLOCK): found
-// by k_pieces, merged by k_long_pieces, placed by k_gather. Records of one
-// tile are contiguous and in piece order; `spref` short tokens of the tile
-// precede the piece.
+// A deferred piece: found by k_pieces (or k_block_rows), merged later, placed
+// by k_gather. Records of one tile are contiguous and in piece order.
+//  * long piece (> kLmax bytes, or a whole row under BBPE_ENGINE_BLOCK):
+//    merged by k_long_pieces into lpo; takes no staging slots.
+//  * merge piece (2..kLmax bytes, not in the piece memo): merged by k_merge,
+//    tokens written into `len` staging slots reserved at `spref`.
 struct LongRec {
   uint64_t start;  // absolute byte position (token position for token input)
   uint64_t len;
-  uint64_t row;    // row index (MaxPassesError reporting)
-  uint32_t spref;
-  uint32_t count;  // tokens out, written by k_long_pieces
+  uint64_t row;    // row index (MaxPassesError reporting); kMergeKind for merge pieces
+  uint32_t spref;  // staging slots of the tile before this piece
+  uint32_t count;  // tokens out, written by the merging kernel
 };
+constexpr uint64_t kMergeKind = 1ull << 63;
 
 struct EncodeArgs {
   const uint8_t* bytes;
@@ -55,6 +59,8 @@ struct EncodeArgs {
   uint32_t* tile_count;     // num_tiles: tokens produced by the tile (short + long)
   uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n, 0 when none
   LongRec* lrec;            // lp_cap records (CNT_LREC used)
+  uint32_t* long_idx;       // indices of the long records (CNT_LONG used)
+  uint64_t long_cap;
   uint32_t* counters;       // CNT_N
   uint64_t* err;            // ERR_N
   uint64_t lp_cap;
@@ -74,6 +80,8 @@ struct EncodeArgs {
 struct LaunchPlan {
   int main_grid = 0;
   int main_grid_wide = 0;
+  int merge_grid = 0;
+  int merge_grid_wide = 0;
   int gather_grid = 0;
   int lp_grid = 0;
   int sm_count = 0;

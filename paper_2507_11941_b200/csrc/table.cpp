@@ -481,6 +481,9 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
   rep.view.rank_bits = t.rank_bits;
   rep.view.n_merges = static_cast<uint32_t>(M);
   rep.view.key32 = t.narrow ? 1u : 0u;
+  rep.view.full_lut = 1u;
+  for (uint32_t v : t.lut)
+    if (v == kInvalidToken) rep.view.full_lut = 0u;
   auto [pos, ok] = t.replicas.emplace(device, rep);
   return pos->second.view;
 }

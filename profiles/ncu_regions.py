@@ -27,13 +27,17 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[2]
 idx = {h: i for i, h in enumerate(hdr)}
 agg = {}
+samp = {}
 tot = 0
+tots = 0
 for r in rows[3:]:
     if not (r and r[0] and len(r) == len(hdr) and r[0].isdigit()):
         continue
     ln = int(r[0])
     ins = int(r[idx["Instructions Executed"]] or 0)
+    sm = int(r[idx["Warp Stall Sampling (All Samples)"]] or 0)
     tot += ins
+    tots += sm
     name = None
     for i, n in steps:
         if i <= ln:
@@ -44,6 +48,8 @@ for r in rows[3:]:
             if i <= ln:
                 name = n
     agg[name] = agg.get(name, 0) + ins
-for k, v in sorted(agg.items(), key=lambda x: -x[1]):
-    print(f"{k:24s} {v / tiles:10.0f} {100 * v / max(tot, 1):5.1f}%")
+    samp[name] = samp.get(name, 0) + sm
+print(f"{'region':24s} {'instr/unit':>10s} {'instr%':>6s} {'samples%':>8s}")
+for k, v in sorted(agg.items(), key=lambda x: -samp.get(x[0], 0)):
+    print(f"{k:24s} {v / tiles:10.0f} {100 * v / max(tot, 1):5.1f}% {100 * samp.get(k, 0) / max(tots, 1):7.1f}%")
 print(f"{'total':24s} {tot / tiles:10.0f}")
