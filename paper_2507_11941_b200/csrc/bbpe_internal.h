@@ -44,6 +44,8 @@ struct DevTable {
   const uint32_t* d2id = nullptr;   // dense id -> original id (null = identity)
   const uint32_t* lut = nullptr;    // 256: byte -> dense id or kInvalidToken
   const uint32_t* junction = nullptr;  // 2048 words: bit (a<<8|b) set iff some merge spans a|b
+  const uint32_t* junction_t = nullptr;  // the same, transposed: bit (b<<8|a) (k_pieces' byte-pair order)
+  const uint32_t* lut_out = nullptr;   // 256: byte -> ORIGINAL id of its token, or kInvalidToken
   const uint32_t* rank_orig = nullptr; // dense rank -> original rank (traces)
   // Piece memo (optional): exact encodings of whole pieces that equal a
   // vocabulary token's bytes, computed by this engine at table upload.
@@ -67,7 +69,7 @@ __host__ __device__ inline uint32_t mix32(uint32_t h) {
 }
 
 // 32-byte memo entry: piece bytes (zero padded), length, 1-2 result tokens
-// (dense ids). len == 0 marks an empty slot.
+// (original ids: memo results are final output). len == 0 marks an empty slot.
 constexpr int kMemoMaxLen = 20;
 struct MemoEntry {
   uint32_t w[5];
@@ -78,16 +80,14 @@ struct MemoEntry {
 };
 static_assert(sizeof(MemoEntry) == 32, "memo entry is one sector");
 
-// Hash of a piece given as 5 little-endian words (bytes past len are zero).
+// Hash of a piece given as 5 little-endian words (bytes past len are zero):
+// one xor-multiply per word, then a murmur-style finaliser.
 __host__ __device__ inline uint32_t memo_hash(const uint32_t* w, uint32_t len) {
-  uint32_t h = 0x9E3779B9u ^ len;
-  for (int i = 0; i < 5; ++i) {
-    h ^= w[i];
-    h *= 0x85EBCA6Bu;
-    h ^= h >> 15;
-  }
+  uint32_t h = len * 0x9E3779B9u;
+  for (int i = 0; i < 5; ++i) h = (h ^ w[i]) * 0x85EBCA6Bu;
+  h ^= h >> 15;
   h *= 0xC2B2AE35u;
-  h ^= h >> 16;
+  h ^= h >> 13;
   return h;
 }
 

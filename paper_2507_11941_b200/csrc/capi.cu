@@ -12,6 +12,8 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -137,7 +139,7 @@ struct bbpe_ctx {
   bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1};
   bbpe::LaunchPlan plan;
   DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
-  DevBuf staging, tile_count, tile_lrec, lrec, tile_base, long_idx;
+  DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
   DevBuf in_bytes, in_offsets, out_ids, out_offsets;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
@@ -198,15 +200,23 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   c.status.ensure(std::max<uint64_t>(a.num_groups, 1) * 8);
   c.staging.ensure(std::max<uint64_t>(a.num_tiles, 1) * kStage * 4);
   c.tile_count.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
+  c.tile_slots.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
+  const uint64_t rb_words = (a.num_tiles + 1) * (kTile / 32) + kRowWords;
+  c.rowbits.ensure(rb_words * 4);
   c.tile_lrec.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
   c.tile_base.ensure((a.num_tiles + 1) * 8);
   c.counters.ensure(CNT_N * 4);
   c.err.ensure(ERR_N * 8);
   const bool block = c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0;
-  // Records: every row (block engine) or, worst case, one per 2 bytes (merge
-  // pieces) plus the long pieces.
-  a.lp_cap = block ? n + 1 : total / 2 + total / (kLmax + 1) + 2;
-  a.long_cap = block ? n + 1 : total / (kLmax + 1) + 2;
+  // Long records: every row (block engine) or, worst case, one per kLmax+1
+  // bytes. Merge records: at most one per 2 bytes, plus the unused tail of
+  // each warp's record chunk (< 32 per refill of kMrecChunk, and the last
+  // chunk of every warp).
+  a.lp_cap = block ? n + 1 : total / (kLmax + 1) + 2;
+  a.long_cap = a.lp_cap;
+  a.mrec_cap = block ? 1 : total / 2 + total / 14 + uint64_t(std::max(c.plan.main_grid, 1)) * kWarpsPerCta * kMrecChunk;
+  c.mrec.ensure(a.mrec_cap * 8);
+  a.mrec = c.mrec.as<uint64_t>();
   c.lrec.ensure(a.lp_cap * sizeof(LongRec));
   c.long_idx.ensure(a.long_cap * 4);
   a.long_idx = c.long_idx.as<uint32_t>();
@@ -217,6 +227,9 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   a.status = c.status.as<uint64_t>();
   a.staging = c.staging.as<uint32_t>();
   a.tile_count = c.tile_count.as<uint32_t>();
+  a.tile_slots = c.tile_slots.as<uint32_t>();
+  a.rowbits = c.rowbits.as<uint32_t>();
+  a.bytes_aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0 ? 1 : 0;
   a.tile_lrec = c.tile_lrec.as<uint64_t>();
   a.tile_base = c.tile_base.as<uint64_t>();
   a.lrec = c.lrec.as<LongRec>();
@@ -229,6 +242,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   a.max_passes = c.cfg.max_passes;
   ck(cudaMemsetAsync(a.status, 0, std::max<uint64_t>(a.num_groups, 1) * 8, s), "memset status");
   ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
+  ck(cudaMemsetAsync(a.rowbits, 0, rb_words * 4, s), "memset rowbits");
   ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, s), "memset err");
   return a;
 }
@@ -445,9 +459,27 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     for (double v : ms) k_before += v;
   }
 
+  // Opt-in timeline (BBPE_TIMELINE=1): timing events around every copy and
+  // kernel sequence, printed to stderr at the end (diagnostics only).
+  static const bool tl_on = std::getenv("BBPE_TIMELINE") != nullptr;
+  std::vector<std::array<cudaEvent_t, 6>> tl;
+  cudaEvent_t tl0 = nullptr;
+  auto tl_rec = [&](size_t k, int i, cudaStream_t s) {
+    if (tl_on) ck(cudaEventRecord(tl[k][i], s), "event");
+  };
+  if (tl_on) {
+    tl.resize(waves.size());
+    for (auto& a : tl)
+      for (auto& e : a) ck(cudaEventCreate(&e), "cudaEventCreate");
+    ck(cudaEventCreate(&tl0), "cudaEventCreate");
+    ck(cudaEventRecord(tl0, c.stream), "event");
+    ck(cudaStreamWaitEvent(c.h2d_stream, tl0, 0), "wait");
+  }
+
   auto launch = [&](size_t k) {
     WaveSet& w = c.sets[k % K];
     if (w.used) ck(cudaStreamWaitEvent(c.h2d_stream, w.d2h_done, 0), "wait");
+    tl_rec(k, 0, c.h2d_stream);
     w.used = true;
     w.r0 = waves[k].first;
     w.r1 = waves[k].second;
@@ -457,7 +489,9 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     ck(cudaMemcpyAsync(w.in_offsets.p, offsets + w.r0, (nr + 1) * 8, cudaMemcpyHostToDevice, c.h2d_stream),
        "H2D offsets");
     ck(cudaEventRecord(w.h2d_done, c.h2d_stream), "event");
+    tl_rec(k, 1, c.h2d_stream);
     ck(cudaStreamWaitEvent(c.stream, w.h2d_done, 0), "wait");
+    tl_rec(k, 2, c.stream);
     launch_rebase_input(w.in_offsets.as<uint64_t>(), nr + 1, base, c.stream);
     enqueue_encode(c, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
                    w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), c.stream, true,
@@ -465,6 +499,7 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     // Final (global) row offsets straight into the caller's array, on their
     // own stream so neither the kernels nor the id copies queue behind them.
     ck(cudaEventRecord(w.comp_done, c.stream), "event");
+    tl_rec(k, 3, c.stream);
     ck(cudaStreamWaitEvent(c.off_stream, w.comp_done, 0), "wait");
     ck(cudaMemcpyAsync(out_offsets + w.r0, w.out_offsets.p, (nr + 1) * 8, cudaMemcpyDeviceToHost,
                        c.off_stream), "D2H offsets");
@@ -489,12 +524,26 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
       if (first + ntok > out_capacity)
         throw usage_error("output capacity " + std::to_string(out_capacity) + " is smaller than the " +
                           std::to_string(first + ntok) + " tokens produced");
+      tl_rec(k, 4, c.d2h_stream);
       if (ntok)
         ck(cudaMemcpyAsync(out_ids + first, w.out_ids.p, ntok * 4, cudaMemcpyDeviceToHost, c.d2h_stream),
            "D2H ids");
       ck(cudaEventRecord(w.d2h_done, c.d2h_stream), "event");
+      tl_rec(k, 5, c.d2h_stream);
     }
     ck(cudaStreamSynchronize(c.d2h_stream), "D2H ids");
+    if (tl_on) {
+      std::fprintf(stderr, "[bbpe timeline] wave: h2d_start h2d_end comp_start comp_end d2h_start d2h_end (ms)\n");
+      for (size_t k = 0; k < waves.size(); ++k) {
+        float v[6];
+        for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&v[i], tl0, tl[k][i]);
+        std::fprintf(stderr, "[bbpe timeline] %zu: %.3f %.3f %.3f %.3f %.3f %.3f\n", k, v[0], v[1], v[2], v[3],
+                     v[4], v[5]);
+      }
+      for (auto& a : tl)
+        for (auto& e : a) cudaEventDestroy(e);
+      cudaEventDestroy(tl0);
+    }
   } catch (...) {
     cudaStreamSynchronize(c.h2d_stream);
     cudaStreamSynchronize(c.stream);
@@ -563,8 +612,8 @@ void ensure_memo(bbpe_ctx& c, const bbpe_table& t) {
       std::memcpy(m.w, blob.data() + offs[j], len);
       m.len = static_cast<uint8_t>(len);
       m.nres = static_cast<uint8_t>(nres);
-      m.res[0] = t.dense(ids[oo[j]]);
-      m.res[1] = nres > 1 ? t.dense(ids[oo[j] + 1]) : 0;
+      m.res[0] = ids[oo[j]];
+      m.res[1] = nres > 1 ? ids[oo[j] + 1] : 0;
       uint64_t b = memo_hash(m.w, m.len) & mask;
       while (slots[b].len != 0) b = (b + 1) & mask;
       slots[b] = m;

@@ -115,124 +115,398 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
 // ---------------------------------------------------------------------------
-// k_tile_first: F(t) = min{ s : offsets[s] >= t*kTile }, t in [0, num_tiles).
+// k_tile_first: F(t) = min{ s : offsets[s] >= t*kTile }, t in [0, num_tiles),
+// and the row-start bitmap (one bit per input byte, zeroed by the host), which
+// k_pieces copies into shared memory with its window.
 // Row s owns tiles t with offsets[s-1] < t*kTile <= offsets[s].
 __global__ void k_tile_first(EncodeArgs a) {
   uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (s > a.n_rows) return;
-  uint64_t hi = a.offsets[s] / kTile;
+  const uint64_t o = a.offsets[s];
+  uint64_t hi = o / kTile;
   uint64_t lo = (s == 0) ? 0 : a.offsets[s - 1] / kTile + 1;
   if (s == 0) hi = 0;  // offsets[0] == 0
   for (uint64_t t = lo; t <= hi && t < a.num_tiles; ++t) a.tile_first[t] = s;
   if (s == 0) a.tile_first[a.num_tiles] = a.n_rows + 1;
+  if (a.rowbits && s < a.n_rows) atomicOr(&a.rowbits[o >> 5], 1u << (o & 31));
 }
 
 // ---------------------------------------------------------------------------
-// Per-warp window over [b0-4, b0+kWin+4): bytes, row starts, hard boundaries.
-// Bytes are copied as aligned words: wb[q + 4] is the byte at b0 + q.
-constexpr int kWinWordsB = kWords * 8 + 4;  // u32 words of bytes (all boundary positions + 4)
-struct Window {
-  uint32_t wbw[kWinWordsB];  // window bytes (as words)
-  uint32_t sb[kWords];       // row-start bits
-  uint32_t bd[kWords];       // piece-boundary bits
-  __device__ __forceinline__ uint32_t byte(int q) const {  // byte at b0 + q, q >= -4
-    return reinterpret_cast<const uint8_t*>(wbw)[q + 4];
-  }
-  __device__ __forceinline__ const uint8_t* bytes() const {
-    return reinterpret_cast<const uint8_t*>(wbw);
-  }
-};
-
-// Loads the window and computes boundaries; returns (lane 0's view of) the
-// first invalid byte position found in [b0, b0 + tlen), or ~0.
-__device__ void load_window(Window& w, const EncodeArgs& a, const uint32_t* junc, const uint32_t* lut,
-                            uint64_t tile, int lane, int tlen, bool full_lut) {
-  const uint64_t b0 = tile * kTile;
-  const uint64_t wbase = b0 >= 4 ? b0 - 4 : 0;
-  const int wofs = b0 >= 4 ? 0 : 1;  // tile 0: word 0 of the window is before the input
-#pragma unroll 1
-  for (int i = lane; i < kWinWordsB; i += 32) {
-    const int gi = i - wofs;
-    uint32_t v = 0;
-    if (gi >= 0) {
-      const uint64_t pos = wbase + 4ull * gi;
-      if (pos + 4 <= a.total) {
-        v = __ldg(reinterpret_cast<const uint32_t*>(a.bytes + pos));
-      } else {
-        for (int k = 0; k < 4; ++k)
-          if (pos + k < a.total) v |= uint32_t(a.bytes[pos + k]) << (8 * k);
-      }
-    }
-    w.wbw[i] = v;
-  }
-  for (int i = lane; i < kWords; i += 32) w.sb[i] = 0;
-  __syncwarp();
-  // Row starts inside the window.
-  const uint64_t s0 = a.tile_first[tile];
-  for (uint64_t s = s0;; s += 32) {
-    const uint64_t my = s + lane;
-    bool in = false;
-    uint64_t o = 0;
-    if (my <= a.n_rows) {
-      o = a.offsets[my];
-      in = o < b0 + kWin;
-    }
-    if (in) atomicOr(&w.sb[(o - b0) >> 5], 1u << ((o - b0) & 31));
-    if (__ballot_sync(kFull, in) != kFull) break;
-  }
-  __syncwarp();
-  // Boundaries: lane handles 4 consecutive positions per 128-position chunk
-  // (one word of bytes + the byte before), 8 lanes OR their nibbles into a
-  // boundary word. Plus the invalid-byte check (pretokenize.hpp:64-67) when
-  // the table lacks a token for some byte value.
-  const int64_t limit = min((int64_t)kWin, (int64_t)(a.total - b0));  // positions past this are boundaries
-  uint32_t badw = 0xFFFFFFFFu;
-#pragma unroll 1
-  for (int c = 0; c < kWords / 4; ++c) {
-    const int q0 = 128 * c + 4 * lane;
-    const uint32_t cur = w.wbw[32 * c + lane + 1];
-    const uint32_t prv = w.wbw[32 * c + lane] >> 24;
-    uint32_t nib = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t pb = j == 0 ? prv : (cur >> (8 * (j - 1))) & 0xFFu;
-      const uint32_t cb = (cur >> (8 * j)) & 0xFFu;
-      if (!is_junction(junc, pb, cb)) nib |= 1u << j;
-      if (!full_lut && q0 + j < tlen && lut[cb] == kInvalidToken && badw == 0xFFFFFFFFu) badw = uint32_t(q0 + j);
-    }
-    nib |= (w.sb[4 * c + (lane >> 3)] >> (4 * (lane & 7))) & 0xFu;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (q0 + j >= limit) nib |= 1u << j;
-    uint32_t v = nib << (4 * (lane & 7));
-    v |= __shfl_xor_sync(kFull, v, 1);
-    v |= __shfl_xor_sync(kFull, v, 2);
-    v |= __shfl_xor_sync(kFull, v, 4);
-    if ((lane & 7) == 0) w.bd[4 * c + (lane >> 3)] = v;
-  }
-  if (!full_lut) {
-    const uint32_t bad = __reduce_min_sync(kFull, badw);
-    if (bad != 0xFFFFFFFFu && lane == 0)
-      atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
-                (unsigned long long)(b0 + bad));
-  }
-  __syncwarp();
+// Asynchronous global -> shared copies (LDGSTS), zero-filled past src_bytes.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// First boundary strictly after q, searching positions (q, q+limit]; returns
-// q+limit+1 when there is none in range.
-__device__ __forceinline__ int next_boundary(const uint32_t* bd, int q, int limit) {
-  int p = q + 1;
-  int last = q + limit;
-  while (p <= last) {
-    uint32_t bits = bd[p >> 5] >> (p & 31);
-    if (bits) {
-      int r = p + __ffs(bits) - 1;
-      return r <= last ? r : last + 1;
-    }
-    p = (p | 31) + 1;
+// Junction test on the transposed bitmap: bit (c << 8 | a) for the bigram (a, c).
+__device__ __forceinline__ bool is_junction_t(const uint32_t* jt, uint32_t a, uint32_t c) {
+  const uint32_t bit = (c << 8) | a;
+  return (jt[bit >> 5] >> (bit & 31)) & 1u;
+}
+
+// Per-warp shared state of k_pieces (double-buffered input window).
+struct PieceSmem {
+  uint4 win[2][kWinVec];          // bytes [b0-16, b0+kTile+32): position q at byte q+16
+  uint32_t rb[2][kRowWords];      // row-start bits of positions [0, 32*kRowWords)
+  uint32_t bd[kTile / 32 + 1];    // piece-start bits of positions [0, min(kTile, limit)); [16] = 0
+  uint16_t wpre[kTile / 32 + 1];  // pieces starting in words < w
+  uint16_t plist[kTile + 1];      // piece starts in order, then the end of the last piece
+  uint16_t cnt[kTile + 1];        // staging slots before piece k (k <= npieces)
+  uint16_t lk[kTile / (kLmax + 1) + 2];  // long pieces (piece indices), in order
+};
+
+// Issues the window + row-bit copies of `tile` into buffer `buf` (one group).
+__device__ __forceinline__ void issue_window(PieceSmem& S, int buf, const EncodeArgs& a, uint64_t tile,
+                                             int lane) {
+  const int64_t g0 = int64_t(tile) * kTile - 16;
+#pragma unroll
+  for (int i = lane; i < kWinVec; i += 32) {
+    const int64_t pos = g0 + 16 * i;
+    const int64_t rem = int64_t(a.total) - pos;
+    const uint32_t nb = pos < 0 ? 0u : uint32_t(rem >= 16 ? 16 : (rem > 0 ? rem : 0));
+    cp_async16(&S.win[buf][i], nb ? static_cast<const void*>(a.bytes + pos) : a.bytes, nb);
   }
-  return last + 1;
+  if (lane < kRowWords / 4)
+    cp_async16(&S.rb[buf][4 * lane], a.rowbits + tile * (kTile / 32) + 4 * lane, 16);
+}
+
+// Window load without cp.async (input pointer not 16-byte aligned): plain
+// byte loads into the same layout.
+__device__ __noinline__ void load_window_slow(PieceSmem& S, int buf, const uint8_t* bytes, uint64_t total,
+                                              const uint32_t* rowbits, uint64_t tile, int lane) {
+  const int64_t g0 = int64_t(tile) * kTile - 16;
+  uint8_t* w = reinterpret_cast<uint8_t*>(S.win[buf]);
+  for (int i = lane; i < kWinVec * 16; i += 32) {
+    const int64_t pos = g0 + i;
+    w[i] = (pos >= 0 && pos < int64_t(total)) ? bytes[pos] : 0;
+  }
+  for (int i = lane; i < kRowWords; i += 32) S.rb[buf][i] = rowbits[tile * (kTile / 32) + i];
+}
+
+// Length of a long piece starting at abs (warp-cooperative, rare path).
+__device__ __noinline__ uint64_t long_piece_length(const uint64_t* offsets, uint64_t n_rows, const uint8_t* bytes,
+                                                   const uint32_t* jt, uint64_t abs, int lane) {
+  uint64_t row_end = 0;
+  if (lane == 0) {
+    uint64_t lo = 0, hi = n_rows;  // max s with offsets[s] <= abs
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (offsets[mid] <= abs) lo = mid; else hi = mid - 1;
+    }
+    row_end = offsets[lo + 1];
+  }
+  row_end = __shfl_sync(kFull, row_end, 0);
+  for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
+    const uint64_t y = x + lane;
+    const bool bnd = y < row_end && !is_junction_t(jt, bytes[y - 1], bytes[y]);
+    const unsigned bm = __ballot_sync(kFull, bnd);
+    if (bm) return x + __ffs(bm) - 1 - abs;
+  }
+  return row_end - abs;
+}
+
+// Whole-piece memo lookup: the piece's bytes (window byte index `start`,
+// 2..kMemoMaxLen bytes) as 5 zero-padded words, hashed, then linear probing
+// over 32-byte entries. Exact: an entry holds this engine's own encoding of
+// the same bytes, computed from the table alone at upload time.
+__device__ __forceinline__ int memo_match(const ulonglong2 lo, const ulonglong2 hi, const uint32_t* w,
+                                          int len, uint32_t& r0, uint32_t& r1, uint32_t& nres) {
+  const uint32_t meta = uint32_t(hi.x >> 32), elen = meta & 0xFF;
+  if (elen == 0) return 0;  // empty slot: miss
+  if (elen == uint32_t(len) && lo.x == (uint64_t(w[1]) << 32 | w[0]) && lo.y == (uint64_t(w[3]) << 32 | w[2]) &&
+      uint32_t(hi.x) == w[4]) {
+    nres = (meta >> 8) & 0xFF;
+    r0 = uint32_t(hi.y);
+    r1 = uint32_t(hi.y >> 32);
+    return 1;  // hit
+  }
+  return -1;  // occupied by another piece: keep probing
+}
+
+// Everything by value: a pointer would force the caller's key into local memory.
+struct MemoHit {
+  uint32_t r0, r1, nres;  // nres 0: miss
+};
+__device__ __noinline__ MemoHit memo_overflow(const MemoEntry* memo, uint64_t mask, uint32_t w0, uint32_t w1,
+                                              uint32_t w2, uint32_t w3, uint32_t w4, int len, uint64_t b) {
+  const uint32_t w[5] = {w0, w1, w2, w3, w4};
+  for (;;) {
+    b = (b + 1) & mask;
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(memo + b);
+    MemoHit h{0, 0, 0};
+    const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, h.r0, h.r1, h.nres);
+    if (m == 0) return MemoHit{0, 0, 0};
+    if (m == 1) return h;
+  }
+}
+
+__device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* ww, int start, int len,
+                                            uint32_t& r0, uint32_t& r1, uint32_t& nres) {
+  const int a = start >> 2;
+  const uint32_t sh = uint32_t(start & 3) * 8;
+  const int base = 32 - 8 * len;  // mask shift of word i: base + 32 i (clamped to [0, 32])
+  uint32_t x[6], w[5];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) x[i] = ww[a + i];
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    w[i] = __funnelshift_r(x[i], x[i + 1], sh) & __funnelshift_rc(~0u, 0u, uint32_t(max(0, base + 32 * i)));
+  const uint64_t b = memo_hash(w, uint32_t(len)) & T.memo_mask;
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
+  const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, r0, r1, nres);
+  if (m >= 0) return m == 1;
+  const MemoHit h = memo_overflow(T.memo, T.memo_mask, w[0], w[1], w[2], w[3], w[4], len, b);
+  r0 = h.r0;
+  r1 = h.r1;
+  nres = h.nres;
+  return nres != 0;
+}
+
+#ifndef BBPE_PIECES_MINB
+#define BBPE_PIECES_MINB 4
+#endif
+// k_pieces: warp per 512-byte tile, persistent over tiles by ticket, the next
+// tile's window and row bits in flight (cp.async) while the current one is
+// processed.
+//  (1) piece-start bits: lane l tests positions [16l, 16l+16) against the
+//      junction bitmap (a position is a hard boundary when its bigram is not a
+//      merge junction), ORs in row starts; the end of the last
+//      piece comes from a 32-position tail test.
+//  (2) piece list (start positions, in order).
+//  (3) resolve 32 pieces per round: single bytes and piece-memo hits are
+//      final and go to the tile's staging slots; other pieces of <= kLmax
+//      bytes reserve `len` slots and become merge records (k_merge); longer
+//      pieces become long records (k_long_pieces).
+//  (4) row offsets relative to the tile (staging slot | long pieces before).
+__global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(EncodeArgs a, DevTable T) {
+  __shared__ uint32_t s_jt[2048];
+  __shared__ uint32_t s_lo[256];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_jt[i] = T.junction_t[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lo[i] = T.lut_out[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  PieceSmem& S = reinterpret_cast<PieceSmem*>(s_dyn)[wid];
+  const bool async = a.bytes_aligned != 0;
+  const bool chk = T.full_lut == 0;
+
+  uint32_t tk = 0;
+  if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
+  uint64_t tile = __shfl_sync(kFull, tk, 0);
+  if (tile >= a.num_tiles) return;
+  if (async) issue_window(S, 0, a, tile, lane);
+  cp_async_commit();
+  if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
+  uint64_t nxt = __shfl_sync(kFull, tk, 0);
+  uint64_t f = lane < 2 ? a.tile_first[tile + lane] : 0;
+  int buf = 0;
+  uint64_t mbase = 0;
+  uint32_t mleft = 0;
+
+  while (tile < a.num_tiles) {
+    // Prefetch: the next tile's window, the ticket after it, its row range.
+    if (async && nxt < a.num_tiles) issue_window(S, buf ^ 1, a, nxt, lane);
+    cp_async_commit();
+    if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
+    const uint64_t nf = (lane < 2 && nxt < a.num_tiles) ? a.tile_first[nxt + lane] : 0;
+    if (async) {
+      cp_async_wait<1>();
+    } else {
+      load_window_slow(S, buf, a.bytes, a.total, a.rowbits, tile, lane);
+    }
+    __syncwarp();
+
+    const uint64_t b0 = tile * kTile;
+    const int64_t limit = int64_t(a.total - b0);  // positions >= limit are past the input
+    const uint64_t s0 = __shfl_sync(kFull, f, 0), s1 = __shfl_sync(kFull, f, 1);
+    const uint32_t* ww = reinterpret_cast<const uint32_t*>(S.win[buf]);
+    const uint8_t* wb = reinterpret_cast<const uint8_t*>(S.win[buf]);
+    // Row offsets of the rows starting in this tile: loads issued now, used in (4).
+    uint64_t my_off = 0;
+    const uint64_t my_s = s0 + lane;
+    if (my_s < s1 && my_s <= a.n_rows) my_off = a.offsets[my_s];
+
+    // (1) Piece-start bits, 16 positions per lane: bigram (q-1, q) as the
+    // 16-bit little-endian pair at window byte q+15.
+    {
+      const uint32_t y0 = ww[4 * lane + 3];
+      const uint4 yv = S.win[buf][lane + 1];
+      const uint32_t y[5] = {y0, yv.x, yv.y, yv.z, yv.w};
+      uint32_t jm = 0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int r = j + 3;
+        const uint32_t lo = y[r >> 2];
+        const uint32_t hi = ((r & 3) == 3) ? y[(r >> 2) + 1] : lo;
+        const uint32_t v = __byte_perm(lo, hi, uint32_t((r & 3) | (((r & 3) + 1) << 4)));
+        const uint32_t wd = s_jt[(v >> 5) & 0x7FF];
+        jm |= (__funnelshift_r(wd, wd, v) & 1u) << j;
+      }
+      uint32_t m = (~jm) & 0xFFFFu;  // not a junction: boundary
+      if (chk) {
+        uint32_t bad = 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int q = 16 * lane + j;
+          const uint32_t byte = (y[(j + 4) >> 2] >> (8 * ((j + 4) & 3))) & 0xFFu;
+          if (q < limit && s_lo[byte] == kInvalidToken && bad == 0xFFFFFFFFu) bad = uint32_t(q);
+        }
+        bad = __reduce_min_sync(kFull, bad);
+        if (bad != 0xFFFFFFFFu && lane == 0)
+          atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_BYTE_POS]),
+                    (unsigned long long)(b0 + bad));
+      }
+      const uint32_t other = __shfl_down_sync(kFull, m, 1);
+      if ((lane & 1) == 0) {
+        uint32_t wbits = m | (other << 16) | S.rb[buf][lane >> 1];
+        const int64_t q0 = 16 * lane;  // word (lane/2) covers [q0, q0 + 32)
+        if (q0 + 32 > limit) wbits &= limit <= q0 ? 0u : ((1u << (limit - q0)) - 1u);
+        S.bd[lane >> 1] = wbits;
+      }
+    }
+    // Tail: first cut in [kTile, kTile + 32) ends the tile's last piece.
+    int last_end;
+    {
+      const int p = kTile + lane;
+      const uint32_t pa = wb[p + 15], pc = wb[p + 16];
+      const bool cut = p >= limit || ((S.rb[buf][p >> 5] >> (p & 31)) & 1u) || !is_junction_t(s_jt, pa, pc);
+      const unsigned cm = __ballot_sync(kFull, cut);
+      last_end = cm ? kTile + __ffs(cm) - 1 : kTile + 32;
+      if (limit < kTile) last_end = int(limit);
+    }
+    if (lane == 0) S.bd[kTile / 32] = 0;
+    __syncwarp();
+
+    // (2) Piece list.
+    int npieces;
+    {
+      const uint32_t m = lane < kTile / 32 ? S.bd[lane] : 0u;
+      const uint32_t c = __popc(m);
+      const uint32_t inc = warp_incl_sum(c, lane);
+      if (lane <= kTile / 32) S.wpre[lane] = static_cast<uint16_t>(inc - c);
+      int pos = int(inc - c);
+      uint32_t mm = m;
+      while (mm) {
+        S.plist[pos++] = static_cast<uint16_t>(32 * lane + __ffs(mm) - 1);
+        mm &= mm - 1;
+      }
+      npieces = int(__shfl_sync(kFull, inc, 31));
+      if (lane == 0) S.plist[npieces] = static_cast<uint16_t>(last_end);
+    }
+    __syncwarp();
+
+    // (3) Resolve 32 pieces per round.
+    uint32_t* stage = a.staging + tile * kStage;
+    uint32_t run = 0, nlong = 0;
+    for (int k0 = 0; k0 < npieces; k0 += 32) {
+      const int k = k0 + lane;
+      int len = 0, q = 0;
+      uint32_t c = 0, r0 = 0, r1 = 0;
+      bool merge = false, lg = false;
+      if (k < npieces) {
+        q = S.plist[k];
+        len = S.plist[k + 1] - q;
+        if (len > kLmax) {
+          lg = true;  // long: k_long_pieces, no staging slots
+        } else if (len == 1) {
+          c = 1;
+          r0 = s_lo[wb[q + 16]];
+        } else {
+          uint32_t nres = 0;
+          if (a.use_memo && len <= kMemoMaxLen && memo_lookup(T, ww, q + 16, len, r0, r1, nres)) {
+            c = nres;
+          } else {
+            merge = true;  // k_merge fills the `len` reserved slots
+            c = uint32_t(len);
+          }
+        }
+      }
+      const uint32_t inc = warp_incl_sum(c, lane);
+      const uint32_t slot = run + inc - c;
+      if (k < npieces) S.cnt[k] = static_cast<uint16_t>(slot);
+      if (!merge && c) {
+        stage[slot] = r0;
+        if (c > 1) stage[slot + 1] = r1;
+      }
+      const unsigned mm = __ballot_sync(kFull, merge);
+      if (mm) {
+        const uint32_t nm = __popc(mm);
+        if (nm > mleft) {  // new chunk of merge records; the old chunk's tail becomes holes
+          for (uint32_t i = lane; i < mleft; i += 32)
+            if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = ~0ull;
+          uint32_t c0 = 0;
+          if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MREC], uint32_t(kMrecChunk));
+          mbase = __shfl_sync(kFull, c0, 0);
+          mleft = kMrecChunk;
+        }
+        if (merge) {
+          const uint64_t at = mbase + __popc(mm & lanemask_lt(lane));
+          if (at < a.mrec_cap) a.mrec[at] = pack_mrec(b0 + q, slot, uint32_t(len));
+        }
+        mbase += nm;
+        mleft -= nm;
+      }
+      const unsigned lm = __ballot_sync(kFull, lg);
+      if (lg) S.lk[nlong + __popc(lm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+      nlong += __popc(lm);
+      run += __shfl_sync(kFull, inc, 31);
+    }
+    if (lane == 0) S.cnt[npieces] = static_cast<uint16_t>(run);
+    __syncwarp();
+
+    // Long pieces (rare): full length to the next hard boundary or row end.
+    uint64_t lfirst = 0;
+    if (nlong) {
+      uint64_t l0 = 0, x0 = 0;
+      if (lane == 0) {
+        l0 = atomicAdd(&a.counters[CNT_LREC], nlong);
+        x0 = atomicAdd(&a.counters[CNT_LONG], nlong);
+      }
+      lfirst = __shfl_sync(kFull, l0, 0);
+      x0 = __shfl_sync(kFull, x0, 0);
+      for (uint32_t i = 0; i < nlong; ++i) {
+        const int k = S.lk[i];
+        const uint64_t abs = b0 + S.plist[k];
+        const uint64_t len = long_piece_length(a.offsets, a.n_rows, a.bytes, s_jt, abs, lane);
+        if (lane == 0) {
+          if (lfirst + i < a.lp_cap) a.lrec[lfirst + i] = LongRec{abs, len, 0, S.cnt[k], 0u};
+          if (x0 + i < a.long_cap) a.long_idx[x0 + i] = uint32_t(lfirst + i);
+        }
+      }
+    }
+    if (lane == 0) {
+      a.tile_lrec[tile] = nlong ? ((lfirst << 24) | nlong) : 0;
+      a.tile_count[tile] = run;
+      a.tile_slots[tile] = run;
+    }
+    // (4) Row offsets relative to the tile: staging slots before the row's
+    // first piece (low 40 bits) and long pieces before it (above).
+    for (uint64_t s = my_s, o = my_off;;) {
+      if (!(s < s1 && s <= a.n_rows)) break;
+      const int r = int(o - b0);  // in [0, kTile]
+      const int w = r >> 5;
+      const int kk = S.wpre[w] + __popc(S.bd[w] & ((1u << (r & 31)) - 1u));
+      uint64_t lb = 0;
+      while (lb < nlong && S.lk[lb] < kk) ++lb;
+      a.out_offsets[s] = uint64_t(S.cnt[kk]) | (lb << 40);
+      s += 32;
+      if (s < s1 && s <= a.n_rows) o = a.offsets[s];
+    }
+    __syncwarp();
+    tile = nxt;
+    nxt = __shfl_sync(kFull, tk, 0);
+    f = nf;
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+  for (uint32_t i = lane; i < mleft; i += 32)
+    if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = ~0ull;
 }
 
 // ---------------------------------------------------------------------------
@@ -445,6 +719,7 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
     if (tid == 0) {
       O[0] = static_cast<uint32_t>(n) | ((n == len && !a.tokens_input) ? kUnchanged : 0u);
       a.lrec[ridx].count = static_cast<uint32_t>(n);
+      if (!a.tokens_input) atomicAdd(&a.tile_count[P.start / kTile], static_cast<uint32_t>(n));
     }
     if (n < len || a.tokens_input)
       for (int32_t i = tid; i < n; i += NT) O[1 + i] = tok_of(X[i]);
@@ -482,17 +757,18 @@ __device__ __forceinline__ void probe_issue(ProbeReq& q, const DevTable& T, uint
 
 // Bucket full without a hit: keep probing linearly (rare at load <= 0.5).
 template <bool K32>
-__device__ __noinline__ uint32_t probe_overflow(const DevTable& T, uint64_t key, uint64_t b) {
-  const uint64_t rmask = (1ull << T.rank_bits) - 1;
+__device__ __noinline__ uint32_t probe_overflow(const uint64_t* slots, uint64_t bucket_mask, uint32_t rank_bits,
+                                                uint64_t key, uint64_t b) {
+  const uint64_t rmask = (1ull << rank_bits) - 1;
   for (;;) {
-    b = (b + 1) & T.bucket_mask;
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + b * kBucketSlots);
+    b = (b + 1) & bucket_mask;
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(slots + b * kBucketSlots);
     const ulonglong2 x = __ldg(p), y = __ldg(p + 1);
     const uint64_t t[4] = {x.x, x.y, y.x, y.y};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (t[j] == kEmptySlot) return kNoRank;
-      if (K32 ? (uint32_t(t[j] >> 32) == uint32_t(key)) : ((t[j] >> T.rank_bits) == key))
+      if (K32 ? (uint32_t(t[j] >> 32) == uint32_t(key)) : ((t[j] >> rank_bits) == key))
         return K32 ? uint32_t(t[j]) : static_cast<uint32_t>(t[j] & rmask);
     }
   }
@@ -510,276 +786,12 @@ __device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTa
       if ((s[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(s[j] & ((1ull << T.rank_bits) - 1));
     }
   }
-  return probe_overflow<K32>(T, q.key, q.b);
+  return probe_overflow<K32>(T.slots, T.bucket_mask, T.rank_bits, q.key, q.b);
 }
 
 template <typename Tk>
 __device__ __forceinline__ uint32_t tk_rank(uint32_t r) {
   return r == kNoRank ? Marks<Tk>::kNone : r;
-}
-
-// One lane, one pass of the reference loop over a piece of n <= kLmax tokens
-// at tok[0..n) / rnk[0..n-1) (block_engine.hpp:286-307): min over cached
-// ranks, sweep-compact in place (a pair at the minimum merges unless its left
-// token was just consumed -- exactly flags[i+1] = (ranks[i] == m && !flags[i])),
-// then re-probe only the pairs touching a merged token, two in flight.
-// Returns the new length, or -1 when no pair is mergeable.
-template <typename Tk>
-__device__ __forceinline__ int lane_pass(const DevTable& T, Tk* tok, Tk* rnk, int n) {
-  constexpr bool K32 = sizeof(Tk) == 2;  // narrow tables use 32-bit pair keys
-  constexpr uint32_t NONE = Marks<Tk>::kNone, PROBE = Marks<Tk>::kNone - 1;
-  uint32_t m = NONE;
-  for (int i = 0; i < n - 1; ++i) m = min(m, uint32_t(rnk[i]));
-  if (m == NONE) return -1;
-  const Tk M = Tk(__ldg(T.r2m + m));
-  int j = 0, i = 0;
-  while (i < n) {
-    const uint32_t ri = (i < n - 1) ? uint32_t(rnk[i]) : NONE;
-    if (ri == m) {
-      tok[j] = M;
-      rnk[j] = Tk(PROBE);
-      if (j > 0) rnk[j - 1] = Tk(PROBE);
-      i += 2;
-    } else {
-      tok[j] = tok[i];
-      rnk[j] = Tk(ri);
-      i += 1;
-    }
-    ++j;
-  }
-  int k = 0;
-  for (;;) {
-    while (k < j - 1 && uint32_t(rnk[k]) != PROBE) ++k;
-    if (k >= j - 1) break;
-    int k2 = k + 1;
-    while (k2 < j - 1 && uint32_t(rnk[k2]) != PROBE) ++k2;
-    ProbeReq pa, pb;
-    probe_issue<K32>(pa, T, tok[k], tok[k + 1]);
-    const bool two = k2 < j - 1;
-    if (two) probe_issue<K32>(pb, T, tok[k2], tok[k2 + 1]);
-    rnk[k] = Tk(tk_rank<Tk>(probe_resolve<K32>(pa, T)));
-    if (two) rnk[k2] = Tk(tk_rank<Tk>(probe_resolve<K32>(pb, T)));
-    k = two ? k2 + 1 : j;
-  }
-  return j;
-}
-
-// Whole-piece memo lookup (exact: the entry holds this engine's own encoding
-// of the same bytes, computed from the table alone at upload time).
-__device__ __forceinline__ int memo_match(const ulonglong2 lo, const ulonglong2 hi, const uint32_t* w,
-                                          int len, uint32_t& r0, uint32_t& r1, uint32_t& nres) {
-  const uint32_t meta = uint32_t(hi.x >> 32), elen = meta & 0xFF;
-  if (elen == 0) return 0;  // empty slot: miss
-  if (elen == uint32_t(len) && uint32_t(lo.x) == w[0] && uint32_t(lo.x >> 32) == w[1] &&
-      uint32_t(lo.y) == w[2] && uint32_t(lo.y >> 32) == w[3] && uint32_t(hi.x) == w[4]) {
-    nres = (meta >> 8) & 0xFF;
-    r0 = uint32_t(hi.y);
-    r1 = uint32_t(hi.y >> 32);
-    return 1;  // hit
-  }
-  return -1;  // occupied by another piece: keep probing
-}
-
-__device__ __noinline__ bool memo_overflow(const DevTable& T, const uint32_t* w, int len, uint64_t b,
-                                           uint32_t& r0, uint32_t& r1, uint32_t& nres) {
-  for (;;) {
-    b = (b + 1) & T.memo_mask;
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
-    const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, r0, r1, nres);
-    if (m >= 0) return m == 1;
-  }
-}
-
-__device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* ww, int q, int len,
-                                            uint32_t& r0, uint32_t& r1, uint32_t& nres) {
-  const int start = q + 4, a = start >> 2, sh = (start & 3) * 8;
-  uint32_t x[6], w[5];
-#pragma unroll
-  for (int i = 0; i < 6; ++i) x[i] = ww[a + i];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    uint32_t v = __funnelshift_r(x[i], x[i + 1], sh);
-    const int nb = len - 4 * i;
-    v &= nb >= 4 ? 0xFFFFFFFFu : (nb <= 0 ? 0u : ((1u << (8 * nb)) - 1u));
-    w[i] = v;
-  }
-  const uint64_t b = memo_hash(w, uint32_t(len)) & T.memo_mask;
-  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
-  const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, r0, r1, nres);
-  if (m >= 0) return m == 1;
-  return memo_overflow(T, w, len, b, r0, r1, nres);
-}
-
-// Length of a long piece starting at abs (warp-cooperative, rare path).
-__device__ __noinline__ uint64_t long_piece_length(const EncodeArgs& a, const uint32_t* junc,
-                                                   uint64_t abs, int lane) {
-  uint64_t row_end = 0;
-  if (lane == 0) {
-    uint64_t lo = 0, hi = a.n_rows;  // max s with offsets[s] <= abs
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi + 1) >> 1;
-      if (a.offsets[mid] <= abs) lo = mid; else hi = mid - 1;
-    }
-    row_end = a.offsets[lo + 1];
-  }
-  row_end = __shfl_sync(kFull, row_end, 0);
-  for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
-    const uint64_t y = x + lane;
-    const bool bnd = y < row_end && !is_junction(junc, a.bytes[y - 1], a.bytes[y]);
-    const unsigned bm = __ballot_sync(kFull, bnd);
-    if (bm) return x + __ffs(bm) - 1 - abs;
-  }
-  return row_end - abs;
-}
-
-struct PieceSmem {
-  Window w;
-  uint16_t plist[kTile];      // piece starts (window-relative), in order
-  uint8_t plen[kTile];        // piece length, 0xFF = long (> kLmax)
-  uint16_t cnt[kTile + 1];    // staging slot of each piece (exclusive prefix)
-  uint16_t dk[kTile];         // deferred pieces (merge or long), in order
-  uint64_t llen[kTile / (kLmax + 1) + 2];
-};
-
-#ifndef BBPE_PIECES_MINB
-#define BBPE_PIECES_MINB 4
-#endif
-// k_pieces: warp per tile. Window -> hard boundaries -> piece list; each piece
-// is resolved in place when it is a single byte or a piece-memo hit, and its
-// tokens go to the tile's staging slots right away; other pieces are deferred
-// (records, in piece order): 2..kLmax-byte pieces to k_merge (slots reserved),
-// longer ones to k_long_pieces.
-__global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(EncodeArgs a, DevTable T) {
-  __shared__ uint32_t s_lut[256];
-  __shared__ uint32_t s_junc[2048];
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_junc[i] = T.junction[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  PieceSmem& S = reinterpret_cast<PieceSmem*>(s_dyn)[wid];
-  const uint32_t* d2id = T.d2id;
-
-  for (;;) {
-    uint64_t tile = 0;
-    if (lane == 0) tile = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
-    tile = __shfl_sync(kFull, tile, 0);
-    if (tile >= a.num_tiles) return;
-    const uint64_t b0 = tile * kTile;
-    const uint64_t s0 = a.tile_first[tile], s1 = a.tile_first[tile + 1];
-    const int tlen = int(min((uint64_t)kTile, (uint64_t)(a.total - b0)));
-    load_window(S.w, a, s_junc, s_lut, tile, lane, tlen, T.full_lut != 0);
-
-    // (1) Piece list: lane w expands boundary word w.
-    int npieces = 0;
-    {
-      const int nw = (tlen + 31) / 32;
-      uint32_t m = 0;
-      if (lane < nw) {
-        m = S.w.bd[lane];
-        const int rem = tlen - 32 * lane;
-        if (rem < 32) m &= (1u << rem) - 1u;
-      }
-      const uint32_t c = __popc(m);
-      const uint32_t inc = warp_incl_sum(c, lane);
-      int pos = int(inc - c);
-      while (m) {
-        S.plist[pos++] = static_cast<uint16_t>(32 * lane + __ffs(m) - 1);
-        m &= m - 1;
-      }
-      npieces = int(__shfl_sync(kFull, inc, 31));
-    }
-    __syncwarp();
-
-    // (2) Resolve or defer every piece, 32 at a time, staging as we go.
-    uint32_t* stage = a.staging + tile * kStage;
-    uint32_t run = 0, ndef = 0, nlong = 0;
-    for (int k0 = 0; k0 < npieces; k0 += 32) {
-      const int k = k0 + lane;
-      int len = 0, q = 0;
-      uint32_t c = 0, r0 = 0, r1 = 0;
-      bool deferred = false, lg = false;
-      if (k < npieces) {
-        q = S.plist[k];
-        len = (k + 1 < npieces) ? S.plist[k + 1] - q : next_boundary(S.w.bd, q, kLmax) - q;
-        if (len > kLmax) {
-          lg = deferred = true;  // long: k_long_pieces, no staging slots
-        } else if (len == 1) {
-          c = 1;
-          r0 = s_lut[S.w.byte(q)];
-        } else {
-          uint32_t nres;
-          if (a.use_memo && len <= kMemoMaxLen && memo_lookup(T, S.w.wbw, q, len, r0, r1, nres)) {
-            c = nres;
-          } else {
-            deferred = true;  // merge piece: k_merge fills `len` reserved slots
-            c = uint32_t(len);
-          }
-        }
-        S.plen[k] = lg ? 0xFF : static_cast<uint8_t>(len);
-      }
-      const uint32_t inc = warp_incl_sum(c, lane);
-      const uint32_t slot = run + inc - c;
-      if (k < npieces) S.cnt[k] = static_cast<uint16_t>(slot);
-      if (!deferred && c) {
-        stage[slot] = d2id ? __ldg(d2id + r0) : r0;
-        if (c > 1) stage[slot + 1] = d2id ? __ldg(d2id + r1) : r1;
-      }
-      const unsigned dm = __ballot_sync(kFull, deferred);
-      if (deferred) S.dk[ndef + __popc(dm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-      ndef += __popc(dm);
-      nlong += __popc(__ballot_sync(kFull, lg));
-      run += __shfl_sync(kFull, inc, 31);
-    }
-    if (lane == 0) S.cnt[npieces] = static_cast<uint16_t>(run);
-    __syncwarp();
-
-    // (3) Deferred-piece records (contiguous per tile, in piece order).
-    uint64_t first = 0, lfirst = 0;
-    if (lane == 0 && ndef) first = atomicAdd(&a.counters[CNT_LREC], ndef);
-    if (lane == 0 && nlong) lfirst = atomicAdd(&a.counters[CNT_LONG], nlong);
-    first = __shfl_sync(kFull, first, 0);
-    lfirst = __shfl_sync(kFull, lfirst, 0);
-    if (nlong) {
-      // Long pieces (rare): full length to the next hard boundary or row end.
-      uint32_t li = 0;
-      for (uint32_t i = 0; i < ndef; ++i) {
-        const int k = S.dk[i];
-        if (S.plen[k] != 0xFF) continue;
-        const uint64_t abs = b0 + S.plist[k];
-        const uint64_t len = long_piece_length(a, s_junc, abs, lane);
-        if (lane == 0) {
-          if (first + i < a.lp_cap) a.lrec[first + i] = LongRec{abs, len, 0, S.cnt[k], 0u};
-          if (lfirst + li < a.long_cap) a.long_idx[lfirst + li] = uint32_t(first + i);
-        }
-        ++li;
-      }
-    }
-    for (uint32_t i = lane; i < ndef; i += 32) {
-      const int k = S.dk[i];
-      if (S.plen[k] == 0xFF) continue;
-      if (first + i < a.lp_cap)
-        a.lrec[first + i] = LongRec{b0 + S.plist[k], S.plen[k], kMergeKind, S.cnt[k], 0u};
-    }
-    if (lane == 0) {
-      a.tile_lrec[tile] = ndef ? ((first << 24) | ndef) : 0;
-      a.tile_count[tile] = run;
-    }
-    // (4) Row offsets relative to the tile: staging slots before the row (low
-    // 40 bits) and deferred pieces before it (above); k_gather resolves them.
-    for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
-      const int o = static_cast<int>(a.offsets[s] - b0);
-      int lo = 0, hi = npieces;  // first piece with plist >= o
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (S.plist[mid] < o) lo = mid + 1; else hi = mid;
-      }
-      uint64_t lb = 0;
-      while (lb < ndef && S.dk[lb] < lo) ++lb;
-      a.out_offsets[s] = uint64_t(S.cnt[lo]) | (lb << 40);
-    }
-    __syncwarp();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -850,12 +862,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTa
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   Tk(*tok)[32] = s_m[wid].tok;
   Tk(*rnk)[32] = s_m[wid].rnk;
-  const uint32_t nrec = min((uint64_t)a.counters[CNT_LREC], (uint64_t)a.lp_cap);
+  const uint32_t nrec = min((uint64_t)a.counters[CNT_MREC], (uint64_t)a.mrec_cap);
   const uint32_t* d2id = T.d2id;
   uint32_t base = 0, next = 0, avail = 0;  // warp-uniform slice of record indices
   bool exhausted = false;
   int n = 0;  // my piece's current length (0 = idle)
-  uint32_t ridx = 0;
+  uint64_t rec = 0;
   for (;;) {
     const bool idle = n == 0;
     const unsigned im = __ballot_sync(kFull, idle);
@@ -870,11 +882,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTa
     const uint32_t take = min(uint32_t(__popc(im)), avail - next);
     const uint32_t rank = __popc(im & lanemask_lt(lane));
     if (idle && rank < take) {
-      ridx = base + next + rank;
-      const LongRec r = a.lrec[ridx];
-      if (r.row & kMergeKind) {
-        n = int(r.len);
-        const uint8_t* src = a.bytes + r.start;
+      rec = a.mrec[base + next + rank];
+      if (rec != ~0ull) {
+        n = int(rec & 63);
+        const uint8_t* src = a.bytes + (rec >> 16);
         for (int i = 0; i < n; ++i) tok[i][lane] = Tk(s_lut[src[i]]);
         for (int i = 0; i < n - 1; i += 2) {
           ProbeReq p0, p1;
@@ -895,14 +906,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTa
     if (busy) {
       const int r = lane_pass_col<Tk>(T, tok, rnk, lane, n);
       if (r < 2) {
+        // Done: tokens into the reserved slots, kSentinel into the rest; the
+        // tile's token count drops by the slots left empty.
         const int cnt = r < 0 ? n : r;
-        const LongRec& rec = a.lrec[ridx];
-        uint32_t* dst = a.staging + (rec.start / kTile) * kStage + rec.spref;
+        const uint64_t start = rec >> 16;
+        const int len = int(rec & 63);
+        uint32_t* dst = a.staging + (start / kTile) * kStage + ((rec >> 6) & 1023);
         for (int i = 0; i < cnt; ++i) {
           const uint32_t v = tok[i][lane];
           dst[i] = d2id ? __ldg(d2id + v) : v;
         }
-        a.lrec[ridx].count = uint32_t(cnt);
+        for (int i = cnt; i < len; ++i) dst[i] = kSentinel;
+        if (len > cnt) atomicSub(&a.tile_count[start / kTile], uint32_t(len - cnt));
         n = 0;
       } else {
         n = r;
@@ -969,12 +984,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_block_rows(EncodeArgs a, 
       if (lane == 0) {
         a.tile_lrec[tile] = ne ? ((first << 24) | ne) : 0;
         a.tile_count[tile] = 0;
+        a.tile_slots[tile] = 0;
       }
         }
 }
 
 // ---------------------------------------------------------------------------
-// k_tile_scan: exclusive scan of tile token totals (short + long pieces) into
+// k_tile_scan: exclusive scan of the final tile token counts into
 // tile_base[0..num_tiles]. One CTA per kScanTiles tiles, CTAs chained by a
 // decoupled look-back (a few hundred CTAs even for GB inputs).
 constexpr int kScanThreads = 512;
@@ -996,23 +1012,8 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(EncodeArgs a) {
 #pragma unroll
   for (int i = 0; i < kScanPer; ++i) {
     const uint64_t t = t0 + i;
-    uint64_t c = 0;
-    if (t < a.num_tiles) {
-      c = __ldcg(a.tile_count + t);
-      const uint64_t rec = __ldcg(a.tile_lrec + t);
-      if (rec) {  // deferred pieces: long ones add their tokens, merge ones
-                  // replace their reserved slots by their tokens
-        const uint64_t first = rec >> 24;
-        const uint32_t nl = uint32_t(rec & 0xFFFFFF);
-        for (uint32_t li = 0; li < nl; ++li) {
-          const LongRec& r = a.lrec[first + li];
-          c += __ldcg(&r.count);
-          if (__ldcg(&r.row) & kMergeKind) c -= __ldcg(&r.len);
-        }
-      }
-    }
-    v[i] = c;
-    sum += c;
+    v[i] = t < a.num_tiles ? __ldcg(a.tile_count + t) : 0;
+    sum += v[i];
   }
   // Block exclusive scan of per-thread sums.
   uint64_t inc = sum;
@@ -1073,70 +1074,124 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(EncodeArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_gather: warp per tile, fully parallel. Copies the tile's staged short
-// tokens and its long pieces (in piece order) to their final CSR place and
-// resolves the row offsets written by k_pieces.
-__device__ __forceinline__ void copy_tokens(uint32_t* dst, const uint32_t* src, uint32_t n, int lane) {
-  for (uint32_t i = lane; i < n; i += 32) dst[i] = __ldcg(src + i);
+// k_gather: warp per tile. Compacts the tile's staging slots (kSentinel =
+// slot a merge piece left empty) into its final CSR place, interleaving the
+// tile's long pieces (rare) at their slot positions, and resolves the row
+// offsets written by k_pieces. The compacted prefix of every 4-slot group is
+// kept in shared memory for the row offsets.
+constexpr int kStageVec = kStage / 4;
+constexpr int kLongCache = kTile / (kLmax + 1) + 2;  // long pieces of a k_pieces tile
+struct GatherSmem {
+  uint16_t pre[kStageVec + 1];  // valid slots before 4-slot group v
+  uint8_t msk[kStageVec + 1];   // valid-slot mask of group v
+  uint32_t lsp[kLongCache];     // long pieces: slot position
+  uint32_t lcnt[kLongCache];    // long pieces: token count
+};
+// Long-piece slot / count: cached in shared memory, or read from the records
+// when a tile has more than kLongCache of them (block engine: one per row).
+struct LongView {
+  const GatherSmem& G;
+  const LongRec* r;
+  uint32_t n;
+  __device__ __forceinline__ uint32_t sp(uint32_t i) const { return n <= kLongCache ? G.lsp[i] : r[i].spref; }
+  __device__ __forceinline__ uint32_t cnt(uint32_t i) const {
+    return n <= kLongCache ? G.lcnt[i] : __ldcg(&r[i].count);
+  }
+};
+static_assert(kStage % 4 == 0, "staging groups");
+
+__device__ __forceinline__ uint32_t compact_at(const GatherSmem& G, uint32_t slot, uint32_t nslots,
+                                               uint32_t total) {
+  if (slot >= nslots) return total;
+  return G.pre[slot >> 2] + __popc(G.msk[slot >> 2] & ((1u << (slot & 3)) - 1u));
 }
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
+  __shared__ GatherSmem s_g[kWarpsPerCta];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  GatherSmem& G = s_g[threadIdx.x >> 5];
   const uint32_t* d2id = T.d2id;
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
+  const uint64_t rb = a.run_base ? *a.run_base : 0;
   for (uint64_t t = blockIdx.x * uint64_t(kWarpsPerCta) + (threadIdx.x >> 5); t < a.num_tiles; t += nwarps) {
     const uint64_t tbase = __ldcg(a.tile_base + t);
     const uint64_t rec = __ldcg(a.tile_lrec + t);
-    const uint32_t nshort = __ldcg(a.tile_count + t);
-    const uint32_t* stage = a.staging + t * kStage;
-    uint32_t* out = a.out_ids + tbase;
-    if (rec == 0) {
-      copy_tokens(out, stage, nshort, lane);
-    } else {
-      // Staged slots in order; at each deferred piece: a merge piece's tokens
-      // sit in its reserved slots (copy `count`, skip `len`), a long piece's
-      // tokens come from lpo (no slots).
-      const uint64_t first = rec >> 24;
-      const uint32_t nl = uint32_t(rec & 0xFFFFFF);
-      uint64_t pos = 0;
-      uint32_t sp = 0;
-      for (uint32_t li = 0; li < nl; ++li) {
-        const LongRec lr = a.lrec[first + li];
-        copy_tokens(out + pos, stage + sp, lr.spref - sp, lane);
-        pos += lr.spref - sp;
-        sp = lr.spref;
-        if (lr.row & kMergeKind) {
-          copy_tokens(out + pos, stage + sp, lr.count, lane);
-          sp += uint32_t(lr.len);
-        } else {
-          const bool unchanged = (__ldcg(a.lpo + lr.start) & kUnchanged) != 0;
-          for (uint32_t i = lane; i < lr.count; i += 32) {
-            const uint32_t v = unchanged ? s_lut[a.bytes[lr.start + i]] : __ldcg(a.lpo + lr.start + 1 + i);
-            out[pos + i] = d2id ? __ldg(d2id + v) : v;
-          }
-        }
-        pos += lr.count;
-      }
-      copy_tokens(out + pos, stage + sp, nshort - sp, lane);
-    }
-    // Row offsets: short tokens before the row (low 40 bits) plus the first
-    // (v >> 40) long pieces of the tile.
+    const uint32_t nslots = __ldcg(a.tile_slots + t);
     const uint64_t s0 = a.tile_first[t], s1 = a.tile_first[t + 1];
-    const uint64_t rb = a.run_base ? *a.run_base : 0;
+    const uint4* stage = reinterpret_cast<const uint4*>(a.staging + t * kStage);
+    uint32_t* out = a.out_ids + tbase;
+    const uint32_t nl = uint32_t(rec & 0xFFFFFF);
+    const uint64_t lfirst = rec >> 24;
+    const LongView LV{G, a.lrec + lfirst, nl};
+    if (nl && nl <= kLongCache) {  // long pieces: slot positions and counts
+      for (uint32_t i = lane; i < nl; i += 32) {
+        const LongRec& r = a.lrec[lfirst + i];
+        G.lsp[i] = r.spref;
+        G.lcnt[i] = __ldcg(&r.count);
+      }
+      __syncwarp();
+    }
+    // Staged slots, 4 per lane per step: compaction by warp scan.
+    const uint32_t nvec = (nslots + 3) / 4;
+    uint32_t run = 0;
+    for (uint32_t v0 = 0; v0 < nvec; v0 += 32) {
+      const uint32_t v = v0 + lane;
+      uint4 x = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+      if (v < nvec) x = __ldcs(stage + v);
+      const uint32_t e[4] = {x.x, x.y, x.z, x.w};
+      uint32_t m = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (e[i] != kSentinel && 4 * v + i < nslots) m |= 1u << i;
+      const uint32_t c = __popc(m);
+      const uint32_t inc = warp_incl_sum(c, lane);
+      uint32_t pos = run + inc - c;
+      if (v < nvec) {
+        G.pre[v] = static_cast<uint16_t>(pos);
+        G.msk[v] = static_cast<uint8_t>(m);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (m & (1u << i)) {
+          uint32_t o = pos;
+          if (nl) {  // tokens after the long pieces that precede this slot
+            const uint32_t slot = 4 * v + i;
+            for (uint32_t li = 0; li < nl && LV.sp(li) <= slot; ++li) o += LV.cnt(li);
+          }
+          __stcs(out + o, e[i]);
+          ++pos;
+        }
+      }
+      run += __shfl_sync(kFull, inc, 31);
+    }
+    __syncwarp();
+    if (nl) {  // long pieces' tokens (rare path)
+      uint32_t before = 0;
+      for (uint32_t li = 0; li < nl; ++li) {
+        const LongRec& lr = a.lrec[lfirst + li];
+        const uint32_t o = compact_at(G, lr.spref, nslots, run) + before;
+        const uint32_t cnt = LV.cnt(li);
+        const bool unchanged = (__ldcg(a.lpo + lr.start) & kUnchanged) != 0;
+        for (uint32_t i = lane; i < cnt; i += 32) {
+          const uint32_t v = unchanged ? s_lut[a.bytes[lr.start + i]] : __ldcg(a.lpo + lr.start + 1 + i);
+          out[o + i] = d2id ? __ldg(d2id + v) : v;
+        }
+        before += cnt;
+      }
+    }
+    // Row offsets: compacted staging slots before the row plus the tokens of
+    // the first (v >> 40) long pieces of the tile.
     for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
       const uint64_t v = __ldcg(a.out_offsets + s);
       const uint32_t lb = uint32_t(v >> 40);
       uint64_t lsum = 0;
-      for (uint32_t li = 0; li < lb; ++li) {
-        const LongRec& r = a.lrec[(rec >> 24) + li];
-        lsum += __ldcg(&r.count);
-        if (__ldcg(&r.row) & kMergeKind) lsum -= __ldcg(&r.len);
-      }
-      a.out_offsets[s] = rb + tbase + (v & ((1ull << 40) - 1)) + lsum;
+      for (uint32_t li = 0; li < lb; ++li) lsum += LV.cnt(li);
+      a.out_offsets[s] = rb + tbase + compact_at(G, uint32_t(v & ((1ull << 40) - 1)), nslots, run) + lsum;
     }
+    __syncwarp();
   }
 }
 
@@ -1167,6 +1222,7 @@ void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_ba
 }
 
 size_t pieces_smem() { return sizeof(PieceSmem) * kWarpsPerCta; }
+static_assert(sizeof(PieceSmem) % 16 == 0, "per-warp window buffers stay 16-byte aligned");
 
 LaunchPlan plan_launch(int device) {
   LaunchPlan p;

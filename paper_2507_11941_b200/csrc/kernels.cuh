@@ -19,27 +19,36 @@ constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece to
 constexpr int kScanTilesPerCta = 4096;  // k_tile_scan: 512 threads x 8 tiles
 constexpr int kWarpsPerCta = 8;
 constexpr int kLpThreads = 512;     // CTA size of the long-piece (block engine) kernel
+constexpr int kWinVec = (kTile + 48) / 16;  // 16-byte chunks of a tile window: bytes [b0-16, b0+kTile+32)
+constexpr int kRowWords = kTile / 32 + 4;   // row-start bit words copied per tile (whole 16-byte chunks)
+constexpr int kMrecChunk = 256;     // merge records a warp reserves at a time
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // staging slot left empty by a merge piece
 
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
-       CNT_MERGE_TICKET = 5, CNT_N = 8 };
+       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_N = 8 };
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_N = 4 };
 
-// A deferred piece: found by k_pieces (or k_block_rows), merged later, placed
-// by k_gather. Records of one tile are contiguous and in piece order.
-//  * long piece (> kLmax bytes, or a whole row under BBPE_ENGINE_BLOCK):
-//    merged by k_long_pieces into lpo; takes no staging slots.
-//  * merge piece (2..kLmax bytes, not in the piece memo): merged by k_merge,
-//    tokens written into `len` staging slots reserved at `spref`.
+// Deferred pieces, found by k_pieces (or k_block_rows) and merged later:
+//  * long piece (> kLmax bytes, or a whole row under BBPE_ENGINE_BLOCK): a
+//    LongRec, merged by k_long_pieces into lpo; takes no staging slots. The
+//    long records of one tile are contiguous and in piece order (k_gather
+//    interleaves their tokens with the tile's staging slots).
+//  * merge piece (2..kLmax bytes, not in the piece memo): a packed u64
+//    (start << 16 | spref << 6 | len) in `mrec`, merged by k_merge into the
+//    `len` staging slots reserved at `spref`; unused slots get kSentinel and
+//    the tile's token count drops by len - count. ~0 marks an unused record.
 struct LongRec {
   uint64_t start;  // absolute byte position (token position for token input)
   uint64_t len;
-  uint64_t row;    // row index (MaxPassesError reporting); kMergeKind for merge pieces
+  uint64_t row;    // row index (MaxPassesError reporting)
   uint32_t spref;  // staging slots of the tile before this piece
   uint32_t count;  // tokens out, written by the merging kernel
 };
-constexpr uint64_t kMergeKind = 1ull << 63;
+__host__ __device__ inline uint64_t pack_mrec(uint64_t start, uint32_t spref, uint32_t len) {
+  return (start << 16) | (uint64_t(spref) << 6) | len;
+}
 
 struct EncodeArgs {
   const uint8_t* bytes;
@@ -56,8 +65,13 @@ struct EncodeArgs {
   uint64_t* tile_base;      // num_tiles + 1: first output token of each tile
   const uint64_t* run_base; // optional: added to every row offset (pipelined waves)
   uint32_t* staging;        // num_tiles * kStage: each tile's short-piece tokens, in order
-  uint32_t* tile_count;     // num_tiles: tokens produced by the tile (short + long)
-  uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n, 0 when none
+  uint32_t* tile_count;     // num_tiles: tokens produced by the tile (final after k_merge/k_long_pieces)
+  uint32_t* tile_slots;     // num_tiles: staging slots the tile used (incl. reserved)
+  uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n long pieces, 0 when none
+  uint32_t* rowbits;        // (num_tiles + 1) * (kTile/32) + kRowWords words: row-start bit per byte
+  int bytes_aligned;        // bytes pointer is 16-byte aligned (cp.async window loads)
+  uint64_t* mrec;           // mrec_cap packed merge records (CNT_MREC allocated)
+  uint64_t mrec_cap;
   LongRec* lrec;            // lp_cap records (CNT_LREC used)
   uint32_t* long_idx;       // indices of the long records (CNT_LONG used)
   uint64_t long_cap;

@@ -450,7 +450,9 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
   size_t o_d2id = align(o_r2m + std::max<size_t>(M, 1) * 4);
   size_t o_lut = align(o_d2id + std::max<size_t>(t.dense_to_id.size(), 1) * 4);
   size_t o_junc = align(o_lut + 256 * 4);
-  size_t o_rank = align(o_junc + 2048 * 4);
+  size_t o_junct = align(o_junc + 2048 * 4);
+  size_t o_lutout = align(o_junct + 2048 * 4);
+  size_t o_rank = align(o_lutout + 256 * 4);
   size_t total = align(o_rank + std::max<size_t>(M, 1) * 4);
   char* base = nullptr;
   if (cudaMalloc(&base, total) != cudaSuccess) {
@@ -464,6 +466,16 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
     std::memcpy(host.data() + o_d2id, t.dense_to_id.data(), t.dense_to_id.size() * 4);
   std::memcpy(host.data() + o_lut, t.lut.data(), 256 * 4);
   std::memcpy(host.data() + o_junc, t.junction.data(), 2048 * 4);
+  {
+    uint32_t* jt = reinterpret_cast<uint32_t*>(host.data() + o_junct);
+    for (uint32_t bit = 0; bit < 65536; ++bit)
+      if ((t.junction[bit >> 5] >> (bit & 31)) & 1u) {
+        const uint32_t tb = ((bit & 0xFF) << 8) | (bit >> 8);
+        jt[tb >> 5] |= 1u << (tb & 31);
+      }
+    uint32_t* lo = reinterpret_cast<uint32_t*>(host.data() + o_lutout);
+    for (int b = 0; b < 256; ++b) lo[b] = t.byte_tokens[b];
+  }
   if (M) std::memcpy(host.data() + o_rank, t.m_rank.data(), M * 4);
   cudaError_t e = cudaMemcpy(base, host.data(), total, cudaMemcpyHostToDevice);
   cudaSetDevice(prev);
@@ -476,6 +488,8 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
   rep.view.d2id = t.remap ? reinterpret_cast<const uint32_t*>(base + o_d2id) : nullptr;
   rep.view.lut = reinterpret_cast<const uint32_t*>(base + o_lut);
   rep.view.junction = reinterpret_cast<const uint32_t*>(base + o_junc);
+  rep.view.junction_t = reinterpret_cast<const uint32_t*>(base + o_junct);
+  rep.view.lut_out = reinterpret_cast<const uint32_t*>(base + o_lutout);
   rep.view.rank_orig = reinterpret_cast<const uint32_t*>(base + o_rank);
   rep.view.id_bits = t.id_bits;
   rep.view.rank_bits = t.rank_bits;
