@@ -737,20 +737,17 @@ struct Marks {
 // Batched probe: issue the bucket loads, resolve later. K32: narrow tables
 // (ids < 2^16) with 32-bit keys, slot = key32 << 32 | rank.
 struct ProbeReq {
-  uint64_t key, b;
+  uint64_t key;
   ulonglong2 s01, s23;
 };
 template <bool K32>
+__device__ __forceinline__ uint64_t probe_bucket(const DevTable& T, uint64_t key) {
+  return (K32 ? uint64_t(mix32(uint32_t(key))) : dmix64(key)) & T.bucket_mask;
+}
+template <bool K32>
 __device__ __forceinline__ void probe_issue(ProbeReq& q, const DevTable& T, uint32_t l, uint32_t r) {
-  if (K32) {
-    const uint32_t k32 = (l << 16) | r;
-    q.key = k32;
-    q.b = mix32(k32) & T.bucket_mask;
-  } else {
-    q.key = (uint64_t(l) << T.id_bits) | uint64_t(r);
-    q.b = dmix64(q.key) & T.bucket_mask;
-  }
-  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + q.b * kBucketSlots);
+  q.key = K32 ? uint64_t((l << 16) | r) : ((uint64_t(l) << T.id_bits) | uint64_t(r));
+  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + probe_bucket<K32>(T, q.key) * kBucketSlots);
   q.s01 = __ldg(p);
   q.s23 = __ldg(p + 1);
 }
@@ -786,7 +783,7 @@ __device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTa
       if ((s[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(s[j] & ((1ull << T.rank_bits) - 1));
     }
   }
-  return probe_overflow<K32>(T.slots, T.bucket_mask, T.rank_bits, q.key, q.b);
+  return probe_overflow<K32>(T.slots, T.bucket_mask, T.rank_bits, q.key, probe_bucket<K32>(T, q.key));
 }
 
 template <typename Tk>
@@ -802,58 +799,27 @@ __device__ __forceinline__ uint32_t tk_rank(uint32_t r) {
 template <typename Tk>
 struct MergeSmem {
   Tk tok[kLmax][32];
-  Tk rnk[kLmax][32];
+  Tk rnk[kLmax][32];       // rank of pair (i, i+1) once resolved
+  uint8_t pq[kLmax][32];   // pairs waiting for a probe (positions)
 };
 
-// One lane, one pass (block_engine.hpp:286-307) over a piece held in a
-// column of the [slot][lane] arrays: min over cached ranks, sweep-compact in
-// place (a pair at the minimum merges unless its left token was just
-// consumed -- flags[i+1] = (ranks[i] == m && !flags[i])), re-probe only the
-// pairs touching a merged token, two in flight. Returns the new length, or -1.
+// k_merge: every pass of the reference loop (block_engine.hpp:286-307) for a
+// piece held in one lane's column of the [slot][lane] arrays:
+//   probe : resolve the pending pairs, four bucket loads in flight, folding
+//           their ranks into the running minimum m;
+//   stop  : m == NONE (no pair in the table, block_engine.hpp:288-289);
+//   sweep : compact in place -- a pair at rank m merges unless its left token
+//           was just consumed (flags[i+1] = (ranks[i] == m && !flags[i]),
+//           103-128) into M = r2m[m] (ranks are unique per pair, so this is
+//           the merged id compact_into looks up, 173); pairs touching a merged
+//           token become pending, the others keep their rank (cached ranks
+//           are exact: a pair's rank depends on its two tokens only) and
+//           give the next pass's minimum.
+// Lanes refill from the merge-record list as their pieces finish.
 template <typename Tk>
-__device__ __forceinline__ int lane_pass_col(const DevTable& T, Tk (*tok)[32], Tk (*rnk)[32], int lane,
-                                             int n) {
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, DevTable T) {
   constexpr bool K32 = sizeof(Tk) == 2;
-  constexpr uint32_t NONE = Marks<Tk>::kNone, PROBE = Marks<Tk>::kNone - 1;
-  uint32_t m = NONE;
-  for (int i = 0; i < n - 1; ++i) m = min(m, uint32_t(rnk[i][lane]));
-  if (m == NONE) return -1;
-  const Tk M = Tk(__ldg(T.r2m + m));
-  int j = 0, i = 0;
-  while (i < n) {
-    const uint32_t ri = (i < n - 1) ? uint32_t(rnk[i][lane]) : NONE;
-    if (ri == m) {
-      tok[j][lane] = M;
-      rnk[j][lane] = Tk(PROBE);
-      if (j > 0) rnk[j - 1][lane] = Tk(PROBE);
-      i += 2;
-    } else {
-      tok[j][lane] = tok[i][lane];
-      rnk[j][lane] = Tk(ri);
-      i += 1;
-    }
-    ++j;
-  }
-  int k = 0;
-  for (;;) {
-    while (k < j - 1 && uint32_t(rnk[k][lane]) != PROBE) ++k;
-    if (k >= j - 1) break;
-    int k2 = k + 1;
-    while (k2 < j - 1 && uint32_t(rnk[k2][lane]) != PROBE) ++k2;
-    ProbeReq pa, pb;
-    probe_issue<K32>(pa, T, tok[k][lane], tok[k + 1][lane]);
-    const bool two = k2 < j - 1;
-    if (two) probe_issue<K32>(pb, T, tok[k2][lane], tok[k2 + 1][lane]);
-    rnk[k][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(pa, T)));
-    if (two) rnk[k2][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(pb, T)));
-    k = two ? k2 + 1 : j;
-  }
-  return j;
-}
-
-template <typename Tk>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTable T) {
-  constexpr bool K32 = sizeof(Tk) == 2;
+  constexpr uint32_t NONE = Marks<Tk>::kNone;
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   MergeSmem<Tk>* s_m = reinterpret_cast<MergeSmem<Tk>*>(s_dyn);
@@ -862,11 +828,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTa
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   Tk(*tok)[32] = s_m[wid].tok;
   Tk(*rnk)[32] = s_m[wid].rnk;
+  uint8_t(*pq)[32] = s_m[wid].pq;
   const uint32_t nrec = min((uint64_t)a.counters[CNT_MREC], (uint64_t)a.mrec_cap);
   const uint32_t* d2id = T.d2id;
   uint32_t base = 0, next = 0, avail = 0;  // warp-uniform slice of record indices
   bool exhausted = false;
-  int n = 0;  // my piece's current length (0 = idle)
+  int n = 0;      // my piece's current length (0 = idle)
+  int np = 0;     // pending probes
+  uint32_t m = NONE;  // minimum over resolved ranks
   uint64_t rec = 0;
   for (;;) {
     const bool idle = n == 0;
@@ -886,15 +855,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTa
       if (rec != ~0ull) {
         n = int(rec & 63);
         const uint8_t* src = a.bytes + (rec >> 16);
-        for (int i = 0; i < n; ++i) tok[i][lane] = Tk(s_lut[src[i]]);
-        for (int i = 0; i < n - 1; i += 2) {
-          ProbeReq p0, p1;
-          probe_issue<K32>(p0, T, tok[i][lane], tok[i + 1][lane]);
-          const bool two = i + 2 < n;
-          if (two) probe_issue<K32>(p1, T, tok[i + 1][lane], tok[i + 2][lane]);
-          rnk[i][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(p0, T)));
-          if (two) rnk[i + 1][lane] = Tk(tk_rank<Tk>(probe_resolve<K32>(p1, T)));
+        for (int i = 0; i < n; ++i) {
+          tok[i][lane] = Tk(s_lut[src[i]]);
+          pq[i][lane] = static_cast<uint8_t>(i);
         }
+        np = n - 1;
+        m = NONE;
       }
     }
     next += take;
@@ -903,26 +869,71 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_merge(EncodeArgs a, DevTa
       if (exhausted) break;
       continue;
     }
-    if (busy) {
-      const int r = lane_pass_col<Tk>(T, tok, rnk, lane, n);
-      if (r < 2) {
-        // Done: tokens into the reserved slots, kSentinel into the rest; the
-        // tile's token count drops by the slots left empty.
-        const int cnt = r < 0 ? n : r;
-        const uint64_t start = rec >> 16;
-        const int len = int(rec & 63);
-        uint32_t* dst = a.staging + (start / kTile) * kStage + ((rec >> 6) & 1023);
-        for (int i = 0; i < cnt; ++i) {
-          const uint32_t v = tok[i][lane];
-          dst[i] = d2id ? __ldg(d2id + v) : v;
+    if (!busy) continue;
+    // probe: pending pairs, four in flight.
+    for (int p = 0; p < np; p += 4) {
+      ProbeReq r[4];
+      int at[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        at[u] = p + u < np ? int(pq[p + u][lane]) : -1;
+        if (at[u] >= 0) probe_issue<K32>(r[u], T, tok[at[u]][lane], tok[at[u] + 1][lane]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (at[u] >= 0) {
+          const uint32_t rk = tk_rank<Tk>(probe_resolve<K32>(r[u], T));
+          rnk[at[u]][lane] = Tk(rk);
+          m = min(m, rk);
         }
-        for (int i = cnt; i < len; ++i) dst[i] = kSentinel;
-        if (len > cnt) atomicSub(&a.tile_count[start / kTile], uint32_t(len - cnt));
-        n = 0;
-      } else {
-        n = r;
       }
     }
+    if (m == NONE || n < 2) {
+      // Done: tokens into the reserved slots, kSentinel into the rest; the
+      // tile's token count drops by the slots left empty.
+      const uint64_t start = rec >> 16;
+      const int len = int(rec & 63);
+      uint32_t* dst = a.staging + (start / kTile) * kStage + ((rec >> 6) & 1023);
+      for (int i = 0; i < n; ++i) {
+        const uint32_t v = tok[i][lane];
+        dst[i] = d2id ? __ldg(d2id + v) : v;
+      }
+      for (int i = n; i < len; ++i) dst[i] = kSentinel;
+      if (len > n) atomicSub(&a.tile_count[start / kTile], uint32_t(len - n));
+      n = 0;
+      continue;
+    }
+    // sweep at rank m.
+    const Tk M = Tk(__ldg(T.r2m + m));
+    const uint32_t mm = m;
+    int j = 0, i = 0;
+    np = 0;
+    m = NONE;
+    uint32_t hold = NONE;  // rank of pair (j-1, j) if it survives
+    bool prev_merged = false;
+    while (i < n) {
+      const uint32_t ri = (i < n - 1) ? uint32_t(rnk[i][lane]) : NONE;
+      if (ri == mm) {
+        tok[j][lane] = M;
+        if (j > 0 && !prev_merged) pq[np++][lane] = static_cast<uint8_t>(j - 1);
+        pq[np++][lane] = static_cast<uint8_t>(j);
+        prev_merged = true;
+        hold = NONE;
+        i += 2;
+      } else {
+        m = min(m, hold);  // pair (j-1, j) keeps its rank
+        tok[j][lane] = tok[i][lane];
+        rnk[j][lane] = Tk(ri);
+        hold = ri;  // rank of pair (j, j+1), kept unless the next output is a merge
+        prev_merged = false;
+        i += 1;
+      }
+      ++j;
+    }
+    m = min(m, hold);
+    n = j;
+    // The last merged token has no right pair.
+    if (np > 0 && int(pq[np - 1][lane]) >= n - 1) --np;
   }
 }
 
