@@ -98,7 +98,7 @@ typedef struct bbpe_stats {
   uint64_t tokens;
   uint64_t long_pieces;    /* pieces that went to the CTA tier                 */
   uint64_t waves;
-  double device_ms;        /* kernel time (CUDA events), summed over waves     */
+  double device_ms;        /* kernel time (CUDA events); 0 on the pipelined host path (untimed) */
   double h2d_ms;
   double d2h_ms;
   double total_ms;         /* wall time of the call                           */

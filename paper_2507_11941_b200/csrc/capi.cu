@@ -95,9 +95,25 @@ bool is_pinned(const void* p) {
 }
 
 
-// One in-flight wave of the pipelined host encode (double-buffered).
+// Device scratch of one encode in flight (kernels.cuh EncodeArgs).
+struct Scratch {
+  DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
+  DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
+  uint64_t rowbits_zeroed = 0;  // words known to be zero (k_pieces clears what it consumes)
+  void release() {
+    for (DevBuf* b : {&tile_first, &status, &counters, &err, &lpo, &lpx, &lpy, &trace, &trace_count, &staging,
+                      &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &rowbits, &mrec})
+      b->release();
+    rowbits_zeroed = 0;
+  }
+};
+
+// One in-flight wave of the pipelined host encode: buffers, its own device
+// scratch and compute stream (waves of different sets overlap on the device).
 struct WaveSet {
   DevBuf in_bytes, in_offsets, out_ids, out_offsets, err;
+  Scratch sc;
+  cudaStream_t stream = nullptr;
   uint64_t* h_off = nullptr;  // pinned: the wave's CSR offsets
   uint64_t* h_rel = nullptr;  // pinned: the wave's input offsets, rebased
   uint64_t* h_err = nullptr;  // pinned: error slots
@@ -106,6 +122,7 @@ struct WaveSet {
   uint64_t r0 = 0, r1 = 0;
   bool used = false;
   void init() {
+    if (!stream) ck(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
     if (h2d_done) return;
     for (cudaEvent_t* e : {&h2d_done, &comp_done, &off_done, &d2h_done})
       ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
@@ -121,6 +138,9 @@ struct WaveSet {
   }
   void release() {
     for (DevBuf* b : {&in_bytes, &in_offsets, &out_ids, &out_offsets, &err}) b->release();
+    sc.release();
+    if (stream) cudaStreamDestroy(stream);
+    stream = nullptr;
     if (h_off) cudaFreeHost(h_off);
     if (h_rel) cudaFreeHost(h_rel);
     if (h_err) cudaFreeHost(h_err);
@@ -138,8 +158,7 @@ struct bbpe_ctx {
   cudaStream_t stream = nullptr;
   bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1};
   bbpe::LaunchPlan plan;
-  DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
-  DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
+  Scratch sc;  // device API / single-wave encodes (on `stream` or the caller's)
   DevBuf in_bytes, in_offsets, out_ids, out_offsets;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   uint64_t launches = 0;
@@ -157,8 +176,10 @@ struct bbpe_ctx {
   uint64_t timed_calls = 0;
   // Pipelined host encode.
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr, off_stream = nullptr;
-  static constexpr int kSets = 3;
+  static constexpr int kSets = 6;
   WaveSet sets[kSets];
+  uint64_t* h_errs = nullptr;  // pinned: error slots of every wave of the last host encode
+  size_t h_errs_cap = 0;
   DevBuf run_base;
 };
 
@@ -183,7 +204,7 @@ struct DeviceGuard {
 };
 
 // Sizes scratch and fills EncodeArgs for a device-resident batch.
-bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_t* d_offsets,
+bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, const uint64_t* d_offsets,
                               uint64_t n, uint64_t total, uint32_t* d_out, uint64_t* d_out_off,
                               cudaStream_t s, uint64_t* err = nullptr) {
   using namespace bbpe;
@@ -196,17 +217,17 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   a.out_ids = d_out;
   a.out_offsets = d_out_off;
   a.num_groups = (a.num_tiles + kScanTilesPerCta - 1) / kScanTilesPerCta;
-  c.tile_first.ensure((a.num_tiles + 1) * 8);
-  c.status.ensure(std::max<uint64_t>(a.num_groups, 1) * 8);
-  c.staging.ensure(std::max<uint64_t>(a.num_tiles, 1) * kStage * 4);
-  c.tile_count.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
-  c.tile_slots.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
+  sc.tile_first.ensure((a.num_tiles + 1) * 8);
+  sc.status.ensure(std::max<uint64_t>(a.num_groups, 1) * 8);
+  sc.staging.ensure(std::max<uint64_t>(a.num_tiles, 1) * kStage * 4);
+  sc.tile_count.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
+  sc.tile_slots.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
   const uint64_t rb_words = (a.num_tiles + 1) * (kTile / 32) + kRowWords;
-  c.rowbits.ensure(rb_words * 4);
-  c.tile_lrec.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
-  c.tile_base.ensure((a.num_tiles + 1) * 8);
-  c.counters.ensure(CNT_N * 4);
-  c.err.ensure(ERR_N * 8);
+  sc.rowbits.ensure(rb_words * 4);
+  sc.tile_lrec.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
+  sc.tile_base.ensure((a.num_tiles + 1) * 8);
+  sc.counters.ensure(CNT_N * 4);
+  sc.err.ensure(ERR_N * 8);
   const bool block = c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0;
   // Long records: every row (block engine) or, worst case, one per kLmax+1
   // bytes. Merge records: at most one per 2 bytes, plus the unused tail of
@@ -215,34 +236,37 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, const uint8_t* d_bytes, const uint64_
   a.lp_cap = block ? n + 1 : total / (kLmax + 1) + 2;
   a.long_cap = a.lp_cap;
   a.mrec_cap = block ? 1 : total / 2 + total / 14 + uint64_t(std::max(c.plan.main_grid, 1)) * kWarpsPerCta * kMrecChunk;
-  c.mrec.ensure(a.mrec_cap * 8);
-  a.mrec = c.mrec.as<uint64_t>();
-  c.lrec.ensure(a.lp_cap * sizeof(LongRec));
-  c.long_idx.ensure(a.long_cap * 4);
-  a.long_idx = c.long_idx.as<uint32_t>();
-  c.lpo.ensure((total + 1) * 4);
-  c.lpx.ensure(std::max<uint64_t>(total, 1) * 8);
-  c.lpy.ensure(std::max<uint64_t>(total, 1) * 8);
-  a.tile_first = c.tile_first.as<uint64_t>();
-  a.status = c.status.as<uint64_t>();
-  a.staging = c.staging.as<uint32_t>();
-  a.tile_count = c.tile_count.as<uint32_t>();
-  a.tile_slots = c.tile_slots.as<uint32_t>();
-  a.rowbits = c.rowbits.as<uint32_t>();
+  sc.mrec.ensure(a.mrec_cap * 8);
+  a.mrec = sc.mrec.as<uint64_t>();
+  sc.lrec.ensure(a.lp_cap * sizeof(LongRec));
+  sc.long_idx.ensure(a.long_cap * 4);
+  a.long_idx = sc.long_idx.as<uint32_t>();
+  sc.lpo.ensure((total + 1) * 4);
+  sc.lpx.ensure(std::max<uint64_t>(total, 1) * 8);
+  sc.lpy.ensure(std::max<uint64_t>(total, 1) * 8);
+  a.tile_first = sc.tile_first.as<uint64_t>();
+  a.status = sc.status.as<uint64_t>();
+  a.staging = sc.staging.as<uint32_t>();
+  a.tile_count = sc.tile_count.as<uint32_t>();
+  a.tile_slots = sc.tile_slots.as<uint32_t>();
+  a.rowbits = sc.rowbits.as<uint32_t>();
   a.bytes_aligned = (reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0 ? 1 : 0;
-  a.tile_lrec = c.tile_lrec.as<uint64_t>();
-  a.tile_base = c.tile_base.as<uint64_t>();
-  a.lrec = c.lrec.as<LongRec>();
-  a.counters = c.counters.as<uint32_t>();
-  a.err = err ? err : c.err.as<uint64_t>();
-  a.lpo = c.lpo.as<uint32_t>();
-  a.lpx = c.lpx.as<uint64_t>();
-  a.lpy = c.lpy.as<uint64_t>();
+  a.tile_lrec = sc.tile_lrec.as<uint64_t>();
+  a.tile_base = sc.tile_base.as<uint64_t>();
+  a.lrec = sc.lrec.as<LongRec>();
+  a.counters = sc.counters.as<uint32_t>();
+  a.err = err ? err : sc.err.as<uint64_t>();
+  a.lpo = sc.lpo.as<uint32_t>();
+  a.lpx = sc.lpx.as<uint64_t>();
+  a.lpy = sc.lpy.as<uint64_t>();
   a.engine = block ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES;
   a.max_passes = c.cfg.max_passes;
   ck(cudaMemsetAsync(a.status, 0, std::max<uint64_t>(a.num_groups, 1) * 8, s), "memset status");
   ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
-  ck(cudaMemsetAsync(a.rowbits, 0, rb_words * 4, s), "memset rowbits");
+  if (sc.rowbits_zeroed < rb_words || c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0) {
+    ck(cudaMemsetAsync(a.rowbits, 0, sc.rowbits.cap, s), "memset rowbits");
+    sc.rowbits_zeroed = sc.rowbits.cap / 4;
+  }
   ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, s), "memset err");
   return a;
 }
@@ -254,19 +278,14 @@ void ensure_plan(bbpe_ctx& c) {
 void ensure_memo(bbpe_ctx& c, const bbpe_table& t);
 
 // Enqueue a device-resident encode. Handles the empty-input corner cases.
-void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
+void enqueue_encode(bbpe_ctx& c, Scratch& sc, const bbpe_table& t, const uint8_t* d_bytes,
                     const uint64_t* d_offsets, uint64_t n, uint64_t total, uint32_t* d_out,
                     uint64_t* d_out_off, cudaStream_t s, bool allow_memo = true,
-                    uint64_t* err = nullptr, uint64_t* run_base = nullptr) {
+                    uint64_t* err = nullptr, bool timed = true) {
   if (total == 0) {
-    if (run_base) {
-      bbpe::launch_fill_offsets(d_out_off, n + 1, run_base, s);
-      c.launches += 1;
-    } else {
-      ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
-    }
-    c.err.ensure(bbpe::ERR_N * 8);
-    ck(cudaMemsetAsync(err ? err : c.err.as<uint64_t>(), 0xFF, bbpe::ERR_N * 8, s), "memset err");
+    ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
+    sc.err.ensure(bbpe::ERR_N * 8);
+    ck(cudaMemsetAsync(err ? err : sc.err.as<uint64_t>(), 0xFF, bbpe::ERR_N * 8, s), "memset err");
     return;
   }
   bbpe::table_on_device(t, c.device);
@@ -276,21 +295,24 @@ void enqueue_encode(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes,
   // The memo itself is built at API entry (maybe_build_memo), never here:
   // building encodes through the ctx's own staging buffers.
   const bbpe::DevTable dt = bbpe::table_on_device(t, c.device);
-  bbpe::EncodeArgs a = prepare_args(c, d_bytes, d_offsets, n, total, d_out, d_out_off, s, err);
+  bbpe::EncodeArgs a = prepare_args(c, sc, d_bytes, d_offsets, n, total, d_out, d_out_off, s, err);
   a.narrow = t.narrow ? 1 : 0;
   a.use_memo = memo && dt.memo ? 1 : 0;
-  a.run_base = run_base;
-  if (c.ev_used == c.ev_sets.size()) {
-    std::array<cudaEvent_t, BBPE_N_KERNELS + 1> set{};
-    for (auto& e : set) ck(cudaEventCreate(&e), "cudaEventCreate");
-    c.ev_sets.push_back(set);
-    c.ev_streams.push_back(s);
-  }
-  c.ev_streams[c.ev_used] = s;
-  c.launches += bbpe::launch_encode(a, dt, c.plan, s, c.ev_sets[c.ev_used++].data());
-  if (run_base) {
-    bbpe::launch_advance_base(run_base, a.tile_base + a.num_tiles, s);
-    c.launches += 1;
+  a.run_base = nullptr;
+  // Per-kernel timing events (BBPE_NO_KERNEL_TIMING=1 disables them, e.g.
+  // for stream capture into a CUDA graph).
+  static const bool no_timing = std::getenv("BBPE_NO_KERNEL_TIMING") != nullptr;
+  if (no_timing || !timed) {
+    c.launches += bbpe::launch_encode(a, dt, c.plan, s, nullptr);
+  } else {
+    if (c.ev_used == c.ev_sets.size()) {
+      std::array<cudaEvent_t, BBPE_N_KERNELS + 1> set{};
+      for (auto& e : set) ck(cudaEventCreate(&e), "cudaEventCreate");
+      c.ev_sets.push_back(set);
+      c.ev_streams.push_back(s);
+    }
+    c.ev_streams[c.ev_used] = s;
+    c.launches += bbpe::launch_encode(a, dt, c.plan, s, c.ev_sets[c.ev_used++].data());
   }
   ck(cudaGetLastError(), "kernel launch");
 }
@@ -323,7 +345,7 @@ void check_device_errors(bbpe_ctx& c, const uint64_t* host_offsets, uint64_t n, 
                          const uint8_t* host_bytes, const uint64_t* d_offsets,
                          const uint8_t* d_bytes) {
   uint64_t err[bbpe::ERR_N];
-  ck(cudaMemcpy(err, c.err.p, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
+  ck(cudaMemcpy(err, c.sc.err.p, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
   raise_device_errors(c, err, host_offsets, n, row_base, host_bytes, d_offsets, d_bytes);
 }
 
@@ -332,6 +354,7 @@ void raise_device_errors(bbpe_ctx& c, const uint64_t* err, const uint64_t* host_
                          uint64_t row_base, const uint8_t* host_bytes, const uint64_t* d_offsets,
                          const uint8_t* d_bytes) {
   const uint64_t none = ~0ull;
+  if (err[bbpe::ERR_BAD_OFFSETS] != none) throw bbpe::usage_error("offsets must be non-decreasing");
   if (err[bbpe::ERR_BAD_BYTE_POS] == none && err[bbpe::ERR_MAXPASS_ROW] == none) return;
   std::vector<uint64_t> tmp;
   if (!host_offsets) {
@@ -378,7 +401,7 @@ uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
   ck(cudaStreamSynchronize(c.stream), "sync H2D");
   if (st) st->h2d_ms += ms_since(t0);
   ck(cudaEventRecord(c.ev0, c.stream), "event");
-  enqueue_encode(c, t, c.in_bytes.as<uint8_t>(), c.in_offsets.as<uint64_t>(), n, total,
+  enqueue_encode(c, c.sc, t, c.in_bytes.as<uint8_t>(), c.in_offsets.as<uint64_t>(), n, total,
                  c.out_ids.as<uint32_t>(), c.out_offsets.as<uint64_t>(), c.stream, allow_memo);
   ck(cudaEventRecord(c.ev1, c.stream), "event");
   std::vector<uint64_t> oo(n + 1);
@@ -403,39 +426,86 @@ uint64_t encode_wave(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
   return ntok;
 }
 
-// Host-buffer encode, pipelined over waves of at most cfg.wave_bytes: the H2D
-// of wave k+1 and the D2H of wave k-1 overlap the kernels of wave k (three
-// streams, three buffer sets). The only host waits are on each wave's row
-// offsets (copied on the compute stream right after its kernels), which size
-// its id copy on the D2H stream.
+// Wave plan of a host batch: rows cut into waves whose byte sizes ramp up
+// from 1 MiB (the first ids leave the device early), stay at `wave` bytes,
+// and ramp down at the end (short drain). Every wave has at least one row.
+std::vector<std::pair<uint64_t, uint64_t>> plan_waves(const uint64_t* offsets, uint64_t n, uint64_t wave) {
+  const uint64_t total = offsets[n] - offsets[0];
+  std::vector<uint64_t> front, back;
+  uint64_t rem = total, f = std::min<uint64_t>(wave, 1ull << 20);
+  while (rem > 0) {
+    const uint64_t take = std::min(f, rem);
+    front.push_back(take);
+    rem -= take;
+    if (f < wave && rem > 0) {
+      const uint64_t b = std::min(f, rem);
+      back.push_back(b);
+      rem -= b;
+    }
+    f = std::min(wave, f * 2);
+  }
+  front.insert(front.end(), back.rbegin(), back.rend());
+  std::vector<std::pair<uint64_t, uint64_t>> waves;
+  uint64_t r0 = 0;
+  size_t k = 0;
+  do {
+    const uint64_t target = k < front.size() ? front[k] : wave;
+    ++k;
+    // Rows of a wave: at least one, then as many as fit in `target` bytes
+    // (binary search on the offsets: O(log n) per wave).
+    uint64_t lo = r0 + 1, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) / 2;
+      if (offsets[mid] - offsets[r0] <= target) lo = mid; else hi = mid - 1;
+    }
+    const uint64_t r1 = n == 0 ? 0 : std::min<uint64_t>(n, std::max<uint64_t>(lo, r0 + 1));
+    waves.push_back({r0, r1});
+    r0 = r1;
+  } while (r0 < n);
+  return waves;
+}
+
+// Host-buffer encode, pipelined over waves (plan_waves) with bbpe_ctx::kSets
+// buffer sets, each with its own device scratch and compute stream: the H2D
+// copies (one stream), the waves' kernels (overlapping across sets) and the
+// D2H copies (one stream) run concurrently.
+//  * Default: the host waits for each wave's row offsets (pinned staging),
+//    rebases them into the caller's array and enqueues the wave's id copy
+//    (copy engine) -- its size is only known once the wave is encoded.
+//  * BBPE_COPY_OUT=kernel and pinned (device-mapped) outputs: everything is
+//    enqueued up front and k_copy_out writes offsets and ids through the
+//    mappings, carrying the running base on the copy stream (no host round
+//    trip per wave; slower than the copy engines on the measured box).
 uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* bytes,
                                const uint64_t* offsets, uint64_t n, uint32_t* out_ids,
                                uint64_t out_capacity, uint64_t* out_offsets, bbpe_stats* st) {
   using namespace bbpe;
   const uint64_t total_all = offsets[n] - offsets[0];
   uint64_t wave = c.cfg.wave_bytes;
-  if (!wave) wave = std::max<uint64_t>(16ull << 20, std::min<uint64_t>(64ull << 20, total_all / 8 + 1));
-  std::vector<std::pair<uint64_t, uint64_t>> waves;
+  if (!wave) wave = std::max<uint64_t>(4ull << 20, std::min<uint64_t>(16ull << 20, total_all / 16 + 1));
+  const std::vector<std::pair<uint64_t, uint64_t>> waves = plan_waves(offsets, n, wave);
   uint64_t max_rows = 0, max_bytes = 0;
-  {
-    uint64_t r0 = 0;
-    do {
-      uint64_t r1 = r0;
-      // Rows of a wave: at least one, then as many as fit in `wave` bytes
-      // (binary search on the offsets: O(log n) per wave).
-      uint64_t lo = r0 + 1, hi = n;
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi + 1) / 2;
-        if (offsets[mid] - offsets[r0] <= wave) lo = mid; else hi = mid - 1;
-      }
-      r1 = std::min<uint64_t>(n, std::max<uint64_t>(lo, r0 + 1));
-      if (n == 0) r1 = 0;
-      waves.push_back({r0, r1});
-      max_rows = std::max(max_rows, r1 - r0);
-      max_bytes = std::max(max_bytes, offsets[r1] - offsets[r0]);
-      r0 = r1;
-    } while (r0 < n);
+  for (const auto& w : waves) {
+    max_rows = std::max(max_rows, w.second - w.first);
+    max_bytes = std::max(max_bytes, offsets[w.second] - offsets[w.first]);
   }
+  // Device-mapped views of the caller's output buffers (pinned memory only).
+  uint32_t* d_out_ids = nullptr;
+  uint64_t* d_out_off = nullptr;
+  if (is_pinned(out_offsets) && (total_all == 0 || is_pinned(out_ids))) {
+    void* p = nullptr;
+    if (total_all && cudaHostGetDevicePointer(&p, out_ids, 0) == cudaSuccess) d_out_ids = static_cast<uint32_t*>(p);
+    if (cudaHostGetDevicePointer(&p, out_offsets, 0) == cudaSuccess) d_out_off = static_cast<uint64_t*>(p);
+    cudaGetLastError();
+  }
+  // Device-driven copy-out is opt-in (BBPE_COPY_OUT=kernel): on B200 + PCIe
+  // Gen5 the copy engines move D2H data faster than SM stores to host memory
+  // and do not take SM time from the overlapping waves.
+  static const bool copy_kernel = [] {
+    const char* v = std::getenv("BBPE_COPY_OUT");
+    return v && std::string(v) == "kernel";
+  }();
+  const bool async = copy_kernel && d_out_off && (total_all == 0 || d_out_ids);
   if (!c.h2d_stream) ck(cudaStreamCreateWithFlags(&c.h2d_stream, cudaStreamNonBlocking), "stream");
   if (!c.d2h_stream) ck(cudaStreamCreateWithFlags(&c.d2h_stream, cudaStreamNonBlocking), "stream");
   if (!c.off_stream) ck(cudaStreamCreateWithFlags(&c.off_stream, cudaStreamNonBlocking), "stream");
@@ -448,8 +518,15 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     w.err.ensure(ERR_N * 8);
     w.used = false;
   }
+  if (c.h_errs_cap < waves.size()) {
+    if (c.h_errs) cudaFreeHost(c.h_errs);
+    c.h_errs = nullptr;
+    c.h_errs_cap = 0;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&c.h_errs), waves.size() * ERR_N * 8, 0), "cudaHostAlloc");
+    c.h_errs_cap = waves.size();
+  }
   c.run_base.ensure(8);
-  ck(cudaMemsetAsync(c.run_base.p, 0, 8, c.stream), "memset run_base");
+  ck(cudaMemsetAsync(c.run_base.p, 0, 8, c.d2h_stream), "memset run_base");
   constexpr int K = bbpe_ctx::kSets;
   auto t0 = std::chrono::steady_clock::now();
   double k_before = 0;
@@ -472,15 +549,15 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     for (auto& a : tl)
       for (auto& e : a) ck(cudaEventCreate(&e), "cudaEventCreate");
     ck(cudaEventCreate(&tl0), "cudaEventCreate");
-    ck(cudaEventRecord(tl0, c.stream), "event");
+    ck(cudaEventRecord(tl0, c.d2h_stream), "event");
     ck(cudaStreamWaitEvent(c.h2d_stream, tl0, 0), "wait");
   }
 
   auto launch = [&](size_t k) {
     WaveSet& w = c.sets[k % K];
-    if (w.used) ck(cudaStreamWaitEvent(c.h2d_stream, w.d2h_done, 0), "wait");
+    // Input buffers are free once the wave K back has been encoded.
+    if (w.used) ck(cudaStreamWaitEvent(c.h2d_stream, w.comp_done, 0), "wait");
     tl_rec(k, 0, c.h2d_stream);
-    w.used = true;
     w.r0 = waves[k].first;
     w.r1 = waves[k].second;
     const uint64_t nr = w.r1 - w.r0, base = offsets[w.r0], tot = offsets[w.r1] - base;
@@ -490,55 +567,98 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
        "H2D offsets");
     ck(cudaEventRecord(w.h2d_done, c.h2d_stream), "event");
     tl_rec(k, 1, c.h2d_stream);
-    ck(cudaStreamWaitEvent(c.stream, w.h2d_done, 0), "wait");
-    tl_rec(k, 2, c.stream);
-    launch_rebase_input(w.in_offsets.as<uint64_t>(), nr + 1, base, c.stream);
-    enqueue_encode(c, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
-                   w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), c.stream, true,
-                   w.err.as<uint64_t>(), c.run_base.as<uint64_t>());
-    // Final (global) row offsets straight into the caller's array, on their
-    // own stream so neither the kernels nor the id copies queue behind them.
-    ck(cudaEventRecord(w.comp_done, c.stream), "event");
-    tl_rec(k, 3, c.stream);
-    ck(cudaStreamWaitEvent(c.off_stream, w.comp_done, 0), "wait");
-    ck(cudaMemcpyAsync(out_offsets + w.r0, w.out_offsets.p, (nr + 1) * 8, cudaMemcpyDeviceToHost,
-                       c.off_stream), "D2H offsets");
-    ck(cudaMemcpyAsync(w.h_err, w.err.p, ERR_N * 8, cudaMemcpyDeviceToHost, c.off_stream), "D2H err");
-    ck(cudaEventRecord(w.off_done, c.off_stream), "event");
-  };
-
-  size_t launched = 0;
-  while (launched < waves.size() && launched < size_t(K - 1)) launch(launched++);
-  try {
-    for (size_t k = 0; k < waves.size(); ++k) {
-      if (launched < waves.size()) launch(launched++);
-      WaveSet& w = c.sets[k % K];
-      ck(cudaEventSynchronize(w.off_done), "encode");
-      const uint64_t nr = w.r1 - w.r0, base = offsets[w.r0];
-      if (w.h_err[ERR_BAD_BYTE_POS] != ~0ull || w.h_err[ERR_MAXPASS_ROW] != ~0ull) {
-        std::vector<uint64_t> rel(nr + 1);
-        for (uint64_t i = 0; i <= nr; ++i) rel[i] = offsets[w.r0 + i] - base;
-        raise_device_errors(c, w.h_err, rel.data(), nr, w.r0, bytes + base, nullptr, nullptr);
-      }
-      const uint64_t first = out_offsets[w.r0], ntok = out_offsets[w.r1] - first;
-      if (first + ntok > out_capacity)
-        throw usage_error("output capacity " + std::to_string(out_capacity) + " is smaller than the " +
-                          std::to_string(first + ntok) + " tokens produced");
+    // The set's compute stream: waves of different sets overlap on the device.
+    ck(cudaStreamWaitEvent(w.stream, w.h2d_done, 0), "wait");
+    // Output buffers are free once the wave K back has been copied out.
+    if (w.used) ck(cudaStreamWaitEvent(w.stream, w.d2h_done, 0), "wait");
+    w.used = true;
+    tl_rec(k, 2, w.stream);
+    launch_rebase_input(w.in_offsets.as<uint64_t>(), nr + 1, base, w.stream);
+    enqueue_encode(c, w.sc, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
+                   w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), w.stream, true, w.err.as<uint64_t>(),
+                   /*timed=*/false);
+    ck(cudaEventRecord(w.comp_done, w.stream), "event");
+    tl_rec(k, 3, w.stream);
+    if (async) {
+      // Copy-out in wave order on one stream (it carries the running base).
+      ck(cudaStreamWaitEvent(c.d2h_stream, w.comp_done, 0), "wait");
       tl_rec(k, 4, c.d2h_stream);
-      if (ntok)
-        ck(cudaMemcpyAsync(out_ids + first, w.out_ids.p, ntok * 4, cudaMemcpyDeviceToHost, c.d2h_stream),
-           "D2H ids");
+      ck(cudaMemcpyAsync(c.h_errs + k * ERR_N, w.err.p, ERR_N * 8, cudaMemcpyDeviceToHost, c.d2h_stream),
+         "D2H err");
+      launch_copy_out(w.out_ids.as<uint32_t>(), d_out_ids, w.out_offsets.as<uint64_t>(), d_out_off + w.r0, nr,
+                      c.run_base.as<uint64_t>(), d_out_ids ? out_capacity : 0, c.plan.sm_count, c.d2h_stream);
+      c.launches += 2;
       ck(cudaEventRecord(w.d2h_done, c.d2h_stream), "event");
       tl_rec(k, 5, c.d2h_stream);
+    } else {
+      // Wave-relative row offsets to pinned staging; the host rebases them.
+      w.reserve_host(nr);
+      ck(cudaStreamWaitEvent(c.off_stream, w.comp_done, 0), "wait");
+      ck(cudaMemcpyAsync(w.h_off, w.out_offsets.p, (nr + 1) * 8, cudaMemcpyDeviceToHost, c.off_stream),
+         "D2H offsets");
+      ck(cudaMemcpyAsync(w.h_err, w.err.p, ERR_N * 8, cudaMemcpyDeviceToHost, c.off_stream), "D2H err");
+      ck(cudaEventRecord(w.off_done, c.off_stream), "event");
     }
-    ck(cudaStreamSynchronize(c.d2h_stream), "D2H ids");
+  };
+
+  auto raise_wave_errors = [&](const uint64_t* err, size_t k) {
+    if (err[ERR_BAD_OFFSETS] != ~0ull) throw usage_error("offsets must be non-decreasing");
+    if (err[ERR_BAD_BYTE_POS] != ~0ull || err[ERR_MAXPASS_ROW] != ~0ull) {
+      const uint64_t r0 = waves[k].first, nr = waves[k].second - r0, base = offsets[r0];
+      std::vector<uint64_t> rel(nr + 1);
+      for (uint64_t i = 0; i <= nr; ++i) rel[i] = offsets[r0 + i] - base;
+      raise_device_errors(c, err, rel.data(), nr, r0, bytes + base, nullptr, nullptr);
+    }
+  };
+
+  try {
+    if (async) {
+      for (size_t k = 0; k < waves.size(); ++k) launch(k);
+      ck(cudaStreamSynchronize(c.d2h_stream), "encode");
+      for (size_t k = 0; k < waves.size(); ++k) raise_wave_errors(c.h_errs + k * ERR_N, k);
+      if (out_offsets[n] > out_capacity)
+        throw usage_error("output capacity " + std::to_string(out_capacity) + " is smaller than the " +
+                          std::to_string(out_offsets[n]) + " tokens produced");
+    } else {
+      size_t launched = 0;
+      uint64_t run = 0;
+      while (launched < waves.size() && launched < size_t(K - 1)) launch(launched++);
+      for (size_t k = 0; k < waves.size(); ++k) {
+        WaveSet& w = c.sets[k % K];
+        // Wave k's id copy goes out as soon as its size is known; the next
+        // wave's launch and the offsets rebase happen while it runs.
+        // Spin (not a blocking sync): the id copy should start the moment
+        // the wave's offsets land.
+        cudaError_t q;
+        while ((q = cudaEventQuery(w.off_done)) == cudaErrorNotReady) {
+        }
+        ck(q, "encode");
+        raise_wave_errors(w.h_err, k);
+        const uint64_t nr = w.r1 - w.r0, ntok = w.h_off[nr];
+        if (run + ntok > out_capacity)
+          throw usage_error("output capacity " + std::to_string(out_capacity) + " is smaller than the " +
+                            std::to_string(run + ntok) + " tokens produced");
+        tl_rec(k, 4, c.d2h_stream);
+        if (ntok)
+          ck(cudaMemcpyAsync(out_ids + run, w.out_ids.p, ntok * 4, cudaMemcpyDeviceToHost, c.d2h_stream),
+             "D2H ids");
+        ck(cudaEventRecord(w.d2h_done, c.d2h_stream), "event");
+        tl_rec(k, 5, c.d2h_stream);
+        if (launched < waves.size()) launch(launched++);
+        for (uint64_t i = 0; i <= nr; ++i) out_offsets[w.r0 + i] = run + w.h_off[i];
+        run += ntok;
+      }
+      ck(cudaStreamSynchronize(c.d2h_stream), "D2H ids");
+    }
     if (tl_on) {
-      std::fprintf(stderr, "[bbpe timeline] wave: h2d_start h2d_end comp_start comp_end d2h_start d2h_end (ms)\n");
+      std::fprintf(stderr, "[bbpe timeline] %s: h2d_start h2d_end comp_start comp_end d2h_start d2h_end (ms)\n",
+                   async ? "async" : "host-paced");
       for (size_t k = 0; k < waves.size(); ++k) {
         float v[6];
         for (int i = 0; i < 6; ++i) cudaEventElapsedTime(&v[i], tl0, tl[k][i]);
-        std::fprintf(stderr, "[bbpe timeline] %zu: %.3f %.3f %.3f %.3f %.3f %.3f\n", k, v[0], v[1], v[2], v[3],
-                     v[4], v[5]);
+        std::fprintf(stderr, "[bbpe timeline] %zu (%llu B): %.3f %.3f %.3f %.3f %.3f %.3f\n", k,
+                     (unsigned long long)(offsets[waves[k].second] - offsets[waves[k].first]), v[0], v[1], v[2],
+                     v[3], v[4], v[5]);
       }
       for (auto& a : tl)
         for (auto& e : a) cudaEventDestroy(e);
@@ -546,7 +666,8 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     }
   } catch (...) {
     cudaStreamSynchronize(c.h2d_stream);
-    cudaStreamSynchronize(c.stream);
+    for (WaveSet& w : c.sets)
+      if (w.stream) cudaStreamSynchronize(w.stream);
     cudaStreamSynchronize(c.off_stream);
     cudaStreamSynchronize(c.d2h_stream);
     throw;
@@ -772,15 +893,14 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (DevBuf* b : {&c->staging, &c->tile_count, &c->tile_lrec, &c->lrec, &c->tile_base, &c->long_idx, &c->tile_first, &c->status, &c->counters, &c->err, &c->lpo, &c->lpx,
-                      &c->lpy, &c->trace, &c->trace_count, &c->in_bytes, &c->in_offsets,
-                      &c->out_ids, &c->out_offsets})
-      b->release();
+    c->sc.release();
+    for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets}) b->release();
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     for (auto& set : c->ev_sets)
       for (auto e : set) cudaEventDestroy(e);
     for (WaveSet& w : c->sets) w.release();
+    if (c->h_errs) cudaFreeHost(c->h_errs);
     c->run_base.release();
     if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
     if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
@@ -834,11 +954,9 @@ int bbpe_encode(bbpe_ctx* c, const bbpe_table* t, const uint8_t* bytes, const ui
   auto t0 = std::chrono::steady_clock::now();
   if (!c || !t || !offsets || !out_offsets) throw bbpe::usage_error("null argument");
   validate_config(c->cfg);
-  {
-    bool bad = false;
-    for (size_t i = 0; i < n; ++i) bad |= offsets[i + 1] < offsets[i];
-    if (bad) throw bbpe::usage_error("offsets must be non-decreasing");
-  }
+  // Row offsets are checked on the device (k_tile_first, ERR_BAD_OFFSETS);
+  // the wave plan only needs the batch to be non-empty-or-ordered overall.
+  if (offsets[n] < offsets[0]) throw bbpe::usage_error("offsets must be non-decreasing");
   if (offsets[n] > offsets[0] && (!bytes || !out_ids)) throw bbpe::usage_error("null buffer");
   DeviceGuard g(c->device);
   maybe_build_memo(*c, *t);
@@ -866,7 +984,7 @@ int bbpe_encode_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
   maybe_build_memo(*c, *t);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
   if (sync) ck(cudaEventRecord(c->ev0, s), "event");
-  enqueue_encode(*c, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
+  enqueue_encode(*c, c->sc, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
   c->pending = true;
   c->pending_offsets = d_offsets;
   c->pending_stream = s;
@@ -971,28 +1089,28 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   EncodeArgs a{};
   a.n_rows = 1;
   a.total = n;
-  c->counters.ensure(CNT_N * 4);
-  c->err.ensure(ERR_N * 8);
-  c->lrec.ensure(sizeof(LongRec));
-  c->long_idx.ensure(4);
-  c->lpo.ensure((n + 1) * 4);
-  c->lpx.ensure(n * 8);
-  c->lpy.ensure(n * 8);
+  c->sc.counters.ensure(CNT_N * 4);
+  c->sc.err.ensure(ERR_N * 8);
+  c->sc.lrec.ensure(sizeof(LongRec));
+  c->sc.long_idx.ensure(4);
+  c->sc.lpo.ensure((n + 1) * 4);
+  c->sc.lpx.ensure(n * 8);
+  c->sc.lpy.ensure(n * 8);
   size_t tcap = trace ? trace_cap : 0;
-  c->trace.ensure(std::max<size_t>(tcap, 1) * 24);
-  c->trace_count.ensure(8);
-  a.counters = c->counters.as<uint32_t>();
-  a.err = c->err.as<uint64_t>();
-  a.lrec = c->lrec.as<LongRec>();
+  c->sc.trace.ensure(std::max<size_t>(tcap, 1) * 24);
+  c->sc.trace_count.ensure(8);
+  a.counters = c->sc.counters.as<uint32_t>();
+  a.err = c->sc.err.as<uint64_t>();
+  a.lrec = c->sc.lrec.as<LongRec>();
   a.lp_cap = 1;
-  a.long_idx = c->long_idx.as<uint32_t>();
+  a.long_idx = c->sc.long_idx.as<uint32_t>();
   a.long_cap = 1;
-  a.lpo = c->lpo.as<uint32_t>();
-  a.lpx = c->lpx.as<uint64_t>();
-  a.lpy = c->lpy.as<uint64_t>();
-  a.trace = c->trace.as<uint64_t>();
+  a.lpo = c->sc.lpo.as<uint32_t>();
+  a.lpx = c->sc.lpx.as<uint64_t>();
+  a.lpy = c->sc.lpy.as<uint64_t>();
+  a.trace = c->sc.trace.as<uint64_t>();
   a.trace_cap = tcap;
-  a.trace_count = c->trace_count.as<uint64_t>();
+  a.trace_count = c->sc.trace_count.as<uint64_t>();
   a.tokens_input = 1;
   a.engine = BBPE_ENGINE_BLOCK;
   a.max_passes = c->cfg.max_passes;

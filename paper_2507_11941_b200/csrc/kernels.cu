@@ -25,6 +25,7 @@
 //   k_gather      : decoupled look-back over tile groups -> CSR ids + row offsets
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -122,9 +123,16 @@ __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) 
 __global__ void k_tile_first(EncodeArgs a) {
   uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (s > a.n_rows) return;
-  const uint64_t o = a.offsets[s];
+  uint64_t o = a.offsets[s];
+  const uint64_t prev = s == 0 ? 0 : a.offsets[s - 1];
+  if (o < prev || o > a.total || (s == a.n_rows && o != a.total)) {
+    // Offsets must be non-decreasing (the host raises UsageError); clamp so
+    // that every kernel stays inside its buffers meanwhile.
+    atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_OFFSETS]), (unsigned long long)s);
+    o = min(max(o, prev), a.total);
+  }
   uint64_t hi = o / kTile;
-  uint64_t lo = (s == 0) ? 0 : a.offsets[s - 1] / kTile + 1;
+  uint64_t lo = (s == 0) ? 0 : min(prev, a.total) / kTile + 1;
   if (s == 0) hi = 0;  // offsets[0] == 0
   for (uint64_t t = lo; t <= hi && t < a.num_tiles; ++t) a.tile_first[t] = s;
   if (s == 0) a.tile_first[a.num_tiles] = a.n_rows + 1;
@@ -199,7 +207,7 @@ __device__ __noinline__ uint64_t long_piece_length(const uint64_t* offsets, uint
       const uint64_t mid = (lo + hi + 1) >> 1;
       if (offsets[mid] <= abs) lo = mid; else hi = mid - 1;
     }
-    row_end = offsets[lo + 1];
+    row_end = max(offsets[lo + 1], abs + kLmax + 1);  // (max: guards bad offsets)
   }
   row_end = __shfl_sync(kFull, row_end, 0);
   for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
@@ -296,6 +304,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   const bool async = a.bytes_aligned != 0;
   const bool chk = T.full_lut == 0;
 
+  // Tiles by ticket (in input order): the next ticket is taken one tile ahead.
   uint32_t tk = 0;
   if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
   uint64_t tile = __shfl_sync(kFull, tk, 0);
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   uint32_t mleft = 0;
 
   while (tile < a.num_tiles) {
-    // Prefetch: the next tile's window, the ticket after it, its row range.
+    // Prefetch: the next tile's window and row range, the ticket after it.
     if (async && nxt < a.num_tiles) issue_window(S, buf ^ 1, a, nxt, lane);
     cp_async_commit();
     if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
@@ -489,7 +498,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     // first piece (low 40 bits) and long pieces before it (above).
     for (uint64_t s = my_s, o = my_off;;) {
       if (!(s < s1 && s <= a.n_rows)) break;
-      const int r = int(o - b0);  // in [0, kTile]
+      const int r = int(min(max(o, b0), b0 + kTile) - b0);  // in [0, kTile] (clamped: bad offsets)
       const int w = r >> 5;
       const int kk = S.wpre[w] + __popc(S.bd[w] & ((1u << (r & 31)) - 1u));
       uint64_t lb = 0;
@@ -606,8 +615,9 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   __shared__ BlockScratch<NT> sc;
   __shared__ uint32_t s_idx;
-  for (int i = threadIdx.x; i < 256; i += NT) s_lut[i] = T.lut[i];
   const int tid = threadIdx.x;
+  if (blockIdx.x >= min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap)) return;  // nothing for this CTA
+  for (int i = threadIdx.x; i < 256; i += NT) s_lut[i] = T.lut[i];
   for (;;) {
     __syncthreads();
     if (tid == 0) s_idx = atomicAdd(&a.counters[CNT_LP_NEXT], 1u);
@@ -1134,6 +1144,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
     const uint64_t s0 = a.tile_first[t], s1 = a.tile_first[t + 1];
     const uint4* stage = reinterpret_cast<const uint4*>(a.staging + t * kStage);
     uint32_t* out = a.out_ids + tbase;
+    // The tile's row-start bits are consumed: leave them zero for the next encode.
+    if (a.rowbits && lane < kTile / 32) a.rowbits[t * (kTile / 32) + lane] = 0;
     const uint32_t nl = uint32_t(rec & 0xFFFFFF);
     const uint64_t lfirst = rec >> 24;
     const LongView LV{G, a.lrec + lfirst, nl};
@@ -1227,6 +1239,41 @@ void launch_rebase_input(uint64_t* d_off, uint64_t n, uint64_t base, cudaStream_
 void launch_advance_base(uint64_t* run_base, const uint64_t* wave_total, cudaStream_t stream) {
   k_advance_base<<<1, 1, 0, stream>>>(run_base, wave_total);
 }
+// k_copy_out: one wave's results -> the caller's pinned buffers through their
+// device mappings: row offsets (wave-relative + *run_base) and ids [0, n) to
+// dst[*run_base, ...), clamped to cap; 16-byte stores to host memory after an
+// aligning head, posted over PCIe. The waves' copy-outs run in order on one
+// stream; k_advance_base moves *run_base on after each.
+__global__ void k_copy_out(const uint32_t* __restrict__ src, uint32_t* dst, const uint64_t* __restrict__ d_off,
+                           uint64_t* dst_off, uint64_t nr, const uint64_t* run_base, uint64_t cap) {
+  const uint64_t rb = *run_base;
+  const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = tid; i <= nr; i += stride) dst_off[i] = rb + __ldcs(d_off + i);
+  const uint64_t o0 = rb, end = min(rb + d_off[nr], cap);
+  if (o0 >= end) return;
+  const uint64_t n = end - o0;
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(dst + o0) >> 2) & 3;
+  const uint64_t head = min(n, (4 - mis) & 3);
+  if (tid < head) dst[o0 + tid] = src[tid];
+  const uint64_t nv = (n - head) / 4;
+  uint4* dv = reinterpret_cast<uint4*>(dst + o0 + head);
+  for (uint64_t v = tid; v < nv; v += stride) {
+    const uint64_t i = head + 4 * v;
+    dv[v] = make_uint4(__ldcs(src + i), __ldcs(src + i + 1), __ldcs(src + i + 2), __ldcs(src + i + 3));
+  }
+  const uint64_t t0 = head + 4 * nv;
+  if (tid < n - t0) dst[o0 + t0 + tid] = src[t0 + tid];
+}
+
+void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t* d_wave_offsets,
+                     uint64_t* mapped_offsets, uint64_t nr, uint64_t* run_base, uint64_t cap, int sm_count,
+                     cudaStream_t stream) {
+  k_copy_out<<<unsigned(std::max(sm_count, 1)), 256, 0, stream>>>(d_ids, mapped_out, d_wave_offsets, mapped_offsets,
+                                                                   nr, run_base, cap);
+  k_advance_base<<<1, 1, 0, stream>>>(run_base, d_wave_offsets + nr);
+}
+
 void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_base, cudaStream_t stream) {
   if (n == 0) return;
   k_fill_offsets<<<unsigned((n + 255) / 256), 256, 0, stream>>>(d_out_off, n, run_base);

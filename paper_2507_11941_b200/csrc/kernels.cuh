@@ -28,7 +28,7 @@ constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // staging slot left empty by a mer
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
        CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_N = 8 };
 // Error slots (u64, initialised to ~0).
-enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_N = 4 };
+enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFSETS = 3, ERR_N = 4 };
 
 // Deferred pieces, found by k_pieces (or k_block_rows) and merged later:
 //  * long piece (> kLmax bytes, or a whole row under BBPE_ENGINE_BLOCK): a
@@ -111,6 +111,12 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
 void launch_rebase_input(uint64_t* d_off, uint64_t n, uint64_t base, cudaStream_t stream);
 void launch_advance_base(uint64_t* run_base, const uint64_t* wave_total, cudaStream_t stream);
 void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_base, cudaStream_t stream);
+// Copies one wave's results into the caller's device-mapped pinned buffers:
+// row offsets (wave-relative + *run_base) and ids at *run_base (clamped to
+// cap), then advances *run_base by the wave's token count.
+void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t* d_wave_offsets,
+                     uint64_t* mapped_offsets, uint64_t nr, uint64_t* run_base, uint64_t cap, int sm_count,
+                     cudaStream_t stream);
 // Long-piece kernel only (token input, used by bbpe_block_bpe).
 int launch_block_bpe(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p,
                      cudaStream_t stream);

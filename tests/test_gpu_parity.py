@@ -296,3 +296,92 @@ def test_large_vocab_cfg4_vs_oracle(which, engine, big_tables):
     wi, wo = orc.encode_packed(data, off, engine=1)
     ids, oo, _ = make_encoder(engine).encode_packed(table, data, off)
     assert np.array_equal(oo, wo) and np.array_equal(ids, wi)
+
+
+def _pinned(a):
+    torch = pytest.importorskip("torch")
+    t = torch.from_numpy(a).pin_memory()
+    return t, t.numpy()
+
+
+@pytest.mark.parametrize("wave_bytes", [0, 50_000, 1 << 20])
+def test_pinned_and_pageable_outputs_match(gpt2, wave_bytes):
+    """Pinned outputs take the device-driven copy-out path (k_copy_out into
+    the mapped buffer, no host round trip per wave); pageable outputs the
+    host-paced path. Both equal the single-wave result and the oracle's."""
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 6000, 256, seed=11)
+    ref_ids, ref_off, _ = bb.Encoder(0).encode_packed(gpt2, data, off)
+    e = bb.Encoder(0, wave_bytes=wave_bytes)
+    ids_a, off_a, st_a = e.encode_packed(gpt2, data, off)  # pageable (numpy) outputs
+    t_ids, h_ids = _pinned(np.zeros(data.size, np.uint32))
+    t_off, h_off = _pinned(np.zeros(off.size, np.uint64))
+    ids_b, off_b, st_b = e.encode_packed(gpt2, data, off, h_ids, h_off)
+    assert np.array_equal(off_a, ref_off) and np.array_equal(ids_a, ref_ids)
+    assert np.array_equal(off_b, ref_off) and np.array_equal(ids_b, ref_ids)
+    if wave_bytes:
+        assert st_b["waves"] > 1
+
+
+def test_ramped_waves_and_odd_alignment(gpt2, oracle_for):
+    """Ramped wave plan over rows of mixed length; the output buffer starts at
+    an odd u32 offset so k_copy_out's aligning head/tail paths run."""
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 3000, 2500)
+    data, off = synth.rows_lengths(gen, lens, seed=6)
+    want_ids, want_off = oracle_for("gpt2").encode_packed(data, off)
+    t_ids, h_ids = _pinned(np.zeros(data.size + 3, np.uint32))
+    t_off, h_off = _pinned(np.zeros(off.size, np.uint64))
+    e = bb.Encoder(0, wave_bytes=300_000)
+    ids, oo, st = e.encode_packed(gpt2, data, off, h_ids[1:], h_off)
+    assert st["waves"] > 4
+    assert np.array_equal(oo, want_off) and np.array_equal(ids, want_ids)
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_output_capacity_too_small(gpt2, pinned):
+    v = load_vectors("gpt2_text")
+    n_tok = int(v["out_offsets"][-1])
+    out = np.zeros(n_tok - 1, np.uint32)
+    oo = np.zeros(v["offsets"].size, np.uint64)
+    if pinned:
+        _t1, out = _pinned(out)
+        _t2, oo = _pinned(oo)
+    with pytest.raises(bb.UsageError, match="capacity"):
+        bb.Encoder(0).encode_packed(gpt2, v["data"], v["offsets"], out, oo)
+
+
+def test_decreasing_offsets_rejected(gpt2):
+    data = np.frombuffer(b"hello world, hello again", np.uint8).copy()
+    off = np.array([0, 5, 3, 24], np.uint64)
+    with pytest.raises(bb.UsageError, match="non-decreasing"):
+        bb.Encoder(0).encode_packed(gpt2, data, off)
+    torch = pytest.importorskip("torch")
+    d = torch.from_numpy(data).cuda()
+    o = torch.from_numpy(off.astype(np.int64)).cuda()
+    out = torch.empty(24, dtype=torch.int32, device="cuda")
+    oo = torch.empty(4, dtype=torch.int64, device="cuda")
+    with pytest.raises(bb.UsageError, match="non-decreasing"):
+        bb.Encoder(0).encode_device(gpt2, d.data_ptr(), o.data_ptr(), 3, 24, out.data_ptr(), oo.data_ptr(), sync=True)
+
+
+def test_device_api_unaligned_input(gpt2):
+    """Device input not 16-byte aligned: k_pieces loads its windows without
+    cp.async; results unchanged."""
+    torch = pytest.importorskip("torch")
+    v = load_vectors("gpt2_text")
+    total = int(v["offsets"][-1])
+    n = v["offsets"].size - 1
+    buf = torch.zeros(total + 16, dtype=torch.uint8, device="cuda")
+    buf[3:3 + total] = torch.from_numpy(v["data"]).cuda()
+    o = torch.from_numpy(v["offsets"].astype(np.int64)).cuda()
+    out = torch.empty(total, dtype=torch.int32, device="cuda")
+    oo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    bb.Encoder(0).encode_device(gpt2, buf.data_ptr() + 3, o.data_ptr(), n, total, out.data_ptr(), oo.data_ptr(),
+                                sync=True)
+    oo_h = oo.cpu().numpy().astype(np.uint64)
+    assert np.array_equal(oo_h, v["out_offsets"])
+    assert np.array_equal(out[: int(oo_h[-1])].cpu().numpy().astype(np.uint32), v["ids"])
