@@ -276,7 +276,7 @@ def main():
     # ---- the same, merge passes only (piece memo off), for reference ----
     merge_only = None
     if args.engine == "pieces" and not args.no_merge_only:
-        enc.set_config(piece_memo=False)
+        enc.set_config(piece_memo=False, dedup=False)
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
                 step()
@@ -297,7 +297,7 @@ def main():
         assert int(d_oo[-1].item()) == ntok
         merge_only = {"value": tokens_all / (mo_ms / 1e3), "unit": "tokens/s", "ms_per_step": mo_ms,
                       "kernel_ms": {k: v / max(kc, 1) for k, v in kt.items()}}
-        enc.set_config(piece_memo=True)
+        enc.set_config(piece_memo=True, dedup=True)
 
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}

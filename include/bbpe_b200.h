@@ -90,6 +90,11 @@ typedef struct bbpe_config {
                               encoding (exact; built from the table by this
                               engine on first use per device). 0: always run
                               the merge passes. Ignored by BBPE_ENGINE_BLOCK. */
+  int32_t no_dedup;        /* 0 (default): within one call, the merge passes run
+                              once per distinct merge piece of <= 15 bytes and
+                              repeats copy that result (exact: a piece's
+                              encoding depends on its bytes only). 1: every
+                              piece runs its own passes.                      */
 } bbpe_config;
 
 typedef struct bbpe_stats {

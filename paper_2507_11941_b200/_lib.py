@@ -25,6 +25,7 @@ class Config(C.Structure):
         ("engine", C.c_int32),
         ("wave_bytes", C.c_uint64),
         ("piece_memo", C.c_int32),
+        ("no_dedup", C.c_int32),
     ]
 
 

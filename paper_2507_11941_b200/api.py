@@ -368,8 +368,9 @@ class Encoder:
     """One encode context on one GPU (bbpe_ctx). Single-caller, like PhasePool."""
 
     def __init__(self, device: int = 0, config: Optional[BlockConfig] = None, engine: str = "pieces",
-                 wave_bytes: int = 0, piece_memo: bool = True):
+                 wave_bytes: int = 0, piece_memo: bool = True, dedup: bool = True):
         self.device = device
+        self.dedup = dedup
         self.config = config or BlockConfig()
         self.engine = engine
         self.wave_bytes = wave_bytes
@@ -382,10 +383,10 @@ class Encoder:
         if self.engine not in ENGINES:
             raise UsageError(f'unknown engine "{self.engine}"')
         return Config(self.config.block_size, self.config.max_passes or 0, ENGINES[self.engine], self.wave_bytes,
-                      1 if self.piece_memo else 0)
+                      1 if self.piece_memo else 0, 0 if self.dedup else 1)
 
     def set_config(self, config: BlockConfig = None, engine: str = None, wave_bytes: int = None,
-                   piece_memo: bool = None):
+                   piece_memo: bool = None, dedup: bool = None):
         if config is not None:
             self.config = config
         if engine is not None:
@@ -394,6 +395,8 @@ class Encoder:
             self.wave_bytes = wave_bytes
         if piece_memo is not None:
             self.piece_memo = piece_memo
+        if dedup is not None:
+            self.dedup = dedup
         _check(LIB.bbpe_ctx_set_config(self._h, C.byref(self._cfg())))
 
     def __del__(self):

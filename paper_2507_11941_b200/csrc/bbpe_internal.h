@@ -54,7 +54,7 @@ struct DevTable {
   uint32_t id_bits = 0;
   uint32_t rank_bits = 0;
   uint32_t n_merges = 0;
-  uint32_t key32 = 0;  // 1: 32-bit pair keys (ids < 2^16): slot = key32 << 32 | rank
+  uint32_t key32 = 0;  // 1: 32-bit pair keys (ids, ranks < 2^16): slot = key32 << 32 | rank << 16 | merged
   uint32_t full_lut = 0;  // 1: every byte value has a token (no invalid-byte checks)
 };
 

@@ -60,8 +60,9 @@ void ck(cudaError_t e, const char* what) {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
-  void ensure(size_t bytes) {
-    if (bytes <= cap && p) return;
+  // Returns true when the buffer was (re)allocated (contents undefined).
+  bool ensure(size_t bytes) {
+    if (bytes <= cap && p) return false;
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
@@ -69,6 +70,7 @@ struct DevBuf {
     want = want + want / 8;  // grow with slack so a sweep does not thrash
     ck(cudaMalloc(&p, want), "cudaMalloc (scratch)");
     cap = want;
+    return true;
   }
   void release() {
     if (p) cudaFree(p);
@@ -99,12 +101,16 @@ bool is_pinned(const void* p) {
 struct Scratch {
   DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
   DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
-  uint64_t rowbits_zeroed = 0;  // words known to be zero (k_pieces clears what it consumes)
+  DevBuf dkey, downer, owners, offs;
+  uint64_t rowbits_zeroed = 0;  // words known to be zero (k_gather clears what k_tile_first set)
+  bool ctrl_dirty = true;       // counters/status not known to be zero (k_gather resets them)  // words known to be zero (k_pieces clears what it consumes)
   void release() {
     for (DevBuf* b : {&tile_first, &status, &counters, &err, &lpo, &lpx, &lpy, &trace, &trace_count, &staging,
-                      &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &rowbits, &mrec})
+                      &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &rowbits, &mrec,
+                      &dkey, &downer, &owners, &offs})
       b->release();
     rowbits_zeroed = 0;
+    ctrl_dirty = true;
   }
 };
 
@@ -156,7 +162,7 @@ struct WaveSet {
 struct bbpe_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1};
+  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1, 0};
   bbpe::LaunchPlan plan;
   Scratch sc;  // device API / single-wave encodes (on `stream` or the caller's)
   DevBuf in_bytes, in_offsets, out_ids, out_offsets;
@@ -204,13 +210,21 @@ struct DeviceGuard {
 };
 
 // Sizes scratch and fills EncodeArgs for a device-resident batch.
+// Input offsets relative to `base` (pipelined waves) are rebased by
+// k_tile_first into scratch; the other kernels read the rebased copy.
 bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, const uint64_t* d_offsets,
                               uint64_t n, uint64_t total, uint32_t* d_out, uint64_t* d_out_off,
-                              cudaStream_t s, uint64_t* err = nullptr) {
+                              cudaStream_t s, uint64_t* err = nullptr, uint64_t base = 0) {
   using namespace bbpe;
   EncodeArgs a{};
   a.bytes = d_bytes;
   a.offsets = d_offsets;
+  if (base) {
+    sc.offs.ensure((n + 1) * 8);
+    a.offsets_raw = d_offsets;
+    a.offsets_base = base;
+    a.offsets = a.offsets_w = sc.offs.as<uint64_t>();
+  }
   a.n_rows = n;
   a.total = total;
   a.num_tiles = (total + kTile - 1) / kTile;
@@ -218,7 +232,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   a.out_offsets = d_out_off;
   a.num_groups = (a.num_tiles + kScanTilesPerCta - 1) / kScanTilesPerCta;
   sc.tile_first.ensure((a.num_tiles + 1) * 8);
-  sc.status.ensure(std::max<uint64_t>(a.num_groups, 1) * 8);
+  if (sc.status.ensure(std::max<uint64_t>(a.num_groups, 1) * 8)) sc.ctrl_dirty = true;
   sc.staging.ensure(std::max<uint64_t>(a.num_tiles, 1) * kStage * 4);
   sc.tile_count.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
   sc.tile_slots.ensure(std::max<uint64_t>(a.num_tiles, 1) * 4);
@@ -226,7 +240,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   sc.rowbits.ensure(rb_words * 4);
   sc.tile_lrec.ensure(std::max<uint64_t>(a.num_tiles, 1) * 8);
   sc.tile_base.ensure((a.num_tiles + 1) * 8);
-  sc.counters.ensure(CNT_N * 4);
+  if (sc.counters.ensure(CNT_N * 4)) sc.ctrl_dirty = true;
   sc.err.ensure(ERR_N * 8);
   const bool block = c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0;
   // Long records: every row (block engine) or, worst case, one per kLmax+1
@@ -236,8 +250,23 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   a.lp_cap = block ? n + 1 : total / (kLmax + 1) + 2;
   a.long_cap = a.lp_cap;
   a.mrec_cap = block ? 1 : total / 2 + total / 14 + uint64_t(std::max(c.plan.main_grid, 1)) * kWarpsPerCta * kMrecChunk;
-  sc.mrec.ensure(a.mrec_cap * 8);
-  a.mrec = sc.mrec.as<uint64_t>();
+  sc.mrec.ensure(a.mrec_cap * 16);
+  a.mrec = sc.mrec.as<ulonglong2>();
+  // Within-call dedupe of merge pieces (bbpe_config.no_dedup == 0): a table
+  // of ~total/128 slots (the distinct merge pieces of text are far fewer;
+  // a full neighbourhood just skips the dedupe for that piece).
+  if (!block && !c.cfg.no_dedup && total >= kDedupMinBytes) {
+    uint64_t slots = 4096;
+    while (slots < total / 128) slots <<= 1;
+    sc.dkey.ensure(slots * 16);
+    sc.downer.ensure(slots * 4);
+    a.dkey = sc.dkey.as<ulonglong2>();
+    a.downer = sc.downer.as<uint32_t>();
+    a.dmask = slots - 1;
+    sc.owners.ensure(a.mrec_cap * 4);
+    a.owners = sc.owners.as<uint32_t>();
+    ck(cudaMemsetAsync(a.dkey, 0, slots * 16, s), "memset dedupe keys");
+  }
   sc.lrec.ensure(a.lp_cap * sizeof(LongRec));
   sc.long_idx.ensure(a.long_cap * 4);
   a.long_idx = sc.long_idx.as<uint32_t>();
@@ -261,9 +290,13 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   a.lpy = sc.lpy.as<uint64_t>();
   a.engine = block ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES;
   a.max_passes = c.cfg.max_passes;
-  ck(cudaMemsetAsync(a.status, 0, std::max<uint64_t>(a.num_groups, 1) * 8, s), "memset status");
-  ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
-  if (sc.rowbits_zeroed < rb_words || c.cfg.engine == BBPE_ENGINE_BLOCK || c.cfg.max_passes > 0) {
+  // Counters and look-back status are left zero by k_gather; rowbits too.
+  if (sc.ctrl_dirty) {
+    ck(cudaMemsetAsync(a.status, 0, sc.status.cap, s), "memset status");
+    ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
+    sc.ctrl_dirty = false;
+  }
+  if (sc.rowbits_zeroed < rb_words) {
     ck(cudaMemsetAsync(a.rowbits, 0, sc.rowbits.cap, s), "memset rowbits");
     sc.rowbits_zeroed = sc.rowbits.cap / 4;
   }
@@ -281,7 +314,7 @@ void ensure_memo(bbpe_ctx& c, const bbpe_table& t);
 void enqueue_encode(bbpe_ctx& c, Scratch& sc, const bbpe_table& t, const uint8_t* d_bytes,
                     const uint64_t* d_offsets, uint64_t n, uint64_t total, uint32_t* d_out,
                     uint64_t* d_out_off, cudaStream_t s, bool allow_memo = true,
-                    uint64_t* err = nullptr, bool timed = true) {
+                    uint64_t* err = nullptr, bool timed = true, uint64_t base = 0) {
   if (total == 0) {
     ck(cudaMemsetAsync(d_out_off, 0, (n + 1) * 8, s), "memset out_offsets");
     sc.err.ensure(bbpe::ERR_N * 8);
@@ -295,7 +328,7 @@ void enqueue_encode(bbpe_ctx& c, Scratch& sc, const bbpe_table& t, const uint8_t
   // The memo itself is built at API entry (maybe_build_memo), never here:
   // building encodes through the ctx's own staging buffers.
   const bbpe::DevTable dt = bbpe::table_on_device(t, c.device);
-  bbpe::EncodeArgs a = prepare_args(c, sc, d_bytes, d_offsets, n, total, d_out, d_out_off, s, err);
+  bbpe::EncodeArgs a = prepare_args(c, sc, d_bytes, d_offsets, n, total, d_out, d_out_off, s, err, base);
   a.narrow = t.narrow ? 1 : 0;
   a.use_memo = memo && dt.memo ? 1 : 0;
   a.run_base = nullptr;
@@ -573,10 +606,9 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     if (w.used) ck(cudaStreamWaitEvent(w.stream, w.d2h_done, 0), "wait");
     w.used = true;
     tl_rec(k, 2, w.stream);
-    launch_rebase_input(w.in_offsets.as<uint64_t>(), nr + 1, base, w.stream);
     enqueue_encode(c, w.sc, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
                    w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), w.stream, true, w.err.as<uint64_t>(),
-                   /*timed=*/false);
+                   /*timed=*/false, base);
     ck(cudaEventRecord(w.comp_done, w.stream), "event");
     tl_rec(k, 3, w.stream);
     if (async) {
@@ -1122,6 +1154,7 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   ck(cudaMemcpyAsync(a.lrec, &lp, sizeof(lp), cudaMemcpyHostToDevice, c->stream), "H2D");
   ck(cudaMemcpyAsync(a.long_idx, &zero, 4, cudaMemcpyHostToDevice, c->stream), "H2D");
   ck(cudaMemcpyAsync(a.counters, counters, sizeof(counters), cudaMemcpyHostToDevice, c->stream), "H2D");
+  c->sc.ctrl_dirty = true;  // k_gather does not run here to leave the counters zero
   ck(cudaMemsetAsync(a.err, 0xFF, ERR_N * 8, c->stream), "memset");
   ck(cudaMemcpyAsync(a.lpx, x.data(), n * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
   c->launches += launch_block_bpe(a, dt, c->plan, c->stream);

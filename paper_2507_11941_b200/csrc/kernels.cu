@@ -50,7 +50,15 @@ __device__ __forceinline__ uint64_t dmix64(uint64_t h) {
   return h;
 }
 
-// Pair -> dense rank (kNoRank when absent). One 32-byte bucket per step.
+// Probe results ("rk"): for narrow tables (T.key32) rank << 16 | merged id,
+// for wide tables the dense rank (merged id = r2m[rank]). Both order like the
+// rank (ranks are unique), kNoRank when the pair is not in the table.
+__device__ __forceinline__ uint32_t rk_merged(const DevTable& T, uint32_t rk) {
+  return T.key32 ? (rk & 0xFFFFu) : __ldg(T.r2m + rk);
+}
+__device__ __forceinline__ uint32_t rk_rank(const DevTable& T, uint32_t rk) { return T.key32 ? rk >> 16 : rk; }
+
+// Pair -> rk (kNoRank when absent). One 32-byte bucket per step.
 __device__ __forceinline__ uint32_t probe32(const DevTable& T, uint32_t l, uint32_t r) {
   const uint32_t key = (l << 16) | r;
   uint64_t b = mix32(key) & T.bucket_mask;
@@ -123,8 +131,9 @@ __device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) 
 __global__ void k_tile_first(EncodeArgs a) {
   uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (s > a.n_rows) return;
-  uint64_t o = a.offsets[s];
-  const uint64_t prev = s == 0 ? 0 : a.offsets[s - 1];
+  const uint64_t* src = a.offsets_raw ? a.offsets_raw : a.offsets;
+  uint64_t o = src[s] - a.offsets_base;
+  const uint64_t prev = s == 0 ? 0 : src[s - 1] - a.offsets_base;
   if (o < prev || o > a.total || (s == a.n_rows && o != a.total)) {
     // Offsets must be non-decreasing (the host raises UsageError); clamp so
     // that every kernel stays inside its buffers meanwhile.
@@ -137,6 +146,7 @@ __global__ void k_tile_first(EncodeArgs a) {
   for (uint64_t t = lo; t <= hi && t < a.num_tiles; ++t) a.tile_first[t] = s;
   if (s == 0) a.tile_first[a.num_tiles] = a.n_rows + 1;
   if (a.rowbits && s < a.n_rows) atomicOr(&a.rowbits[o >> 5], 1u << (o & 31));
+  if (a.offsets_raw) a.offsets_w[s] = o;  // the rebased copy the other kernels read
 }
 
 // ---------------------------------------------------------------------------
@@ -274,6 +284,40 @@ __device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* w
   r1 = h.r1;
   nres = h.nres;
   return nres != 0;
+}
+
+// 128-bit compare-and-swap (sm_90+ atom.cas.b128); returns the old value.
+__device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulonglong2 val) {
+  ulonglong2 old;
+  asm volatile(
+      "{ .reg .b128 d, c, v; mov.b128 c, {%2, %3}; mov.b128 v, {%4, %5};\n"
+      "  atom.global.cas.b128 d, [%6], c, v; mov.b128 {%0, %1}, d; }\n"
+      : "=l"(old.x), "=l"(old.y)
+      : "l"(cmp.x), "l"(cmp.y), "l"(val.x), "l"(val.y), "l"(p)
+      : "memory");
+  return old;
+}
+
+// Within-call dedupe of merge pieces: finds or claims the slot of `key`.
+// Returns the slot (the caller owns it: its merge passes run), the slot with
+// bit 63 set (another piece with the same bytes owns it: copy its result),
+// or ~0 after 16 probes (no dedupe for this piece).
+__device__ __forceinline__ uint64_t dedup_claim(ulonglong2* dkey, uint64_t dmask, ulonglong2 key) {
+  uint64_t h = (key.x * 0x9E3779B97F4A7C15ull) ^ (key.y * 0xC2B2AE3D27D4EB4Full);
+  h ^= h >> 29;
+  h *= 0xBF58476D1CE4E5B9ull;
+  h ^= h >> 32;
+  uint64_t s = h & dmask;
+  for (int i = 0; i < 16; ++i) {
+    ulonglong2 cur = __ldcg(dkey + s);
+    if (cur.x == 0 && cur.y == 0) {
+      cur = cas128(dkey + s, make_ulonglong2(0, 0), key);
+      if (cur.x == 0 && cur.y == 0) return s;
+    }
+    if (cur.x == key.x && cur.y == key.y) return s | (1ull << 63);
+    s = (s + 1) & dmask;
+  }
+  return ~0ull;
 }
 
 #ifndef BBPE_PIECES_MINB
@@ -436,6 +480,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
           }
         }
       }
+      // The piece's first 8 bytes ride in its merge record (window byte q+16).
+      uint64_t b8 = 0;
+      if (merge) {
+        const int st = q + 16, wa = st >> 2;
+        const uint32_t sh = uint32_t(st & 3) * 8;
+        const uint32_t x0 = ww[wa], x1 = ww[wa + 1], x2 = ww[wa + 2];
+        b8 = uint64_t(__funnelshift_r(x0, x1, sh)) | (uint64_t(__funnelshift_r(x1, x2, sh)) << 32);
+      }
       const uint32_t inc = warp_incl_sum(c, lane);
       const uint32_t slot = run + inc - c;
       if (k < npieces) S.cnt[k] = static_cast<uint16_t>(slot);
@@ -448,15 +500,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         const uint32_t nm = __popc(mm);
         if (nm > mleft) {  // new chunk of merge records; the old chunk's tail becomes holes
           for (uint32_t i = lane; i < mleft; i += 32)
-            if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = ~0ull;
+            if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = make_ulonglong2(~0ull, 0);
           uint32_t c0 = 0;
           if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MREC], uint32_t(kMrecChunk));
           mbase = __shfl_sync(kFull, c0, 0);
           mleft = kMrecChunk;
         }
         if (merge) {
+          // The piece's first 8 bytes ride in the record (k_merge needs no
+          // dependent load for pieces of <= 8 bytes).
           const uint64_t at = mbase + __popc(mm & lanemask_lt(lane));
-          if (at < a.mrec_cap) a.mrec[at] = pack_mrec(b0 + q, slot, uint32_t(len));
+          if (at < a.mrec_cap) a.mrec[at] = make_ulonglong2(pack_mrec(b0 + q, slot, uint32_t(len)), b8);
         }
         mbase += nm;
         mleft -= nm;
@@ -515,7 +569,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   }
   cp_async_wait<0>();
   for (uint32_t i = lane; i < mleft; i += 32)
-    if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = ~0ull;
+    if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = make_ulonglong2(~0ull, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -690,7 +744,7 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
       uint32_t total_merges;
       const uint32_t before = block_excl_sum_u32<NT>(my_merges, sc, 1, &total_merges);
       // (4) compaction into Y (block_engine.hpp:166-182) with cached ranks.
-      const uint32_t M = T.r2m[m];
+      const uint32_t M = rk_merged(T, m);
       {
         uint32_t run = before;  // merges at pair positions q < i
         for (int32_t i = c0; i < c1; ++i) {
@@ -708,7 +762,7 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
       if (a.trace && tid == 0) {
         if (pass < a.trace_cap) {
           a.trace[3 * pass] = pass + 1;
-          a.trace[3 * pass + 1] = T.rank_orig[m];
+          a.trace[3 * pass + 1] = T.rank_orig[rk_rank(T, m)];
           a.trace[3 * pass + 2] = total_merges;
         }
       }
@@ -737,13 +791,6 @@ __global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
 }
 
 // ---------------------------------------------------------------------------
-// Marks in the per-lane working arrays of k_merge (16- or 32-bit).
-template <typename Tk>
-struct Marks {
-  static constexpr uint32_t kNone = Tk(~Tk(0));  // no rank / uncovered position
-};
-
-
 // Batched probe: issue the bucket loads, resolve later. K32: narrow tables
 // (ids < 2^16) with 32-bit keys, slot = key32 << 32 | rank.
 struct ProbeReq {
@@ -796,10 +843,6 @@ __device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTa
   return probe_overflow<K32>(T.slots, T.bucket_mask, T.rank_bits, q.key, probe_bucket<K32>(T, q.key));
 }
 
-template <typename Tk>
-__device__ __forceinline__ uint32_t tk_rank(uint32_t r) {
-  return r == kNoRank ? Marks<Tk>::kNone : r;
-}
 
 // ---------------------------------------------------------------------------
 // k_merge: the deferred 2..kLmax-byte pieces of every tile, lane per piece,
@@ -809,7 +852,7 @@ __device__ __forceinline__ uint32_t tk_rank(uint32_t r) {
 template <typename Tk>
 struct MergeSmem {
   Tk tok[kLmax][32];
-  Tk rnk[kLmax][32];       // rank of pair (i, i+1) once resolved
+  uint32_t rnk[kLmax][32];  // rk of pair (i, i+1) once resolved
   uint8_t pq[kLmax][32];   // pairs waiting for a probe (positions)
 };
 
@@ -826,10 +869,16 @@ struct MergeSmem {
 //           are exact: a pair's rank depends on its two tokens only) and
 //           give the next pass's minimum.
 // Lanes refill from the merge-record list as their pieces finish.
+#ifndef BBPE_MERGE_MINB
+#define BBPE_MERGE_MINB 3
+#endif
+#ifndef BBPE_MERGE_PROBES
+#define BBPE_MERGE_PROBES 3
+#endif
 template <typename Tk>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, DevTable T) {
-  constexpr bool K32 = sizeof(Tk) == 2;
-  constexpr uint32_t NONE = Marks<Tk>::kNone;
+__global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(EncodeArgs a, DevTable T) {
+  constexpr bool K32 = sizeof(Tk) == 2;  // narrow: 32-bit keys, merged id in the slot
+  constexpr uint32_t NONE = kNoRank;
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   MergeSmem<Tk>* s_m = reinterpret_cast<MergeSmem<Tk>*>(s_dyn);
@@ -837,37 +886,73 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, De
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   Tk(*tok)[32] = s_m[wid].tok;
-  Tk(*rnk)[32] = s_m[wid].rnk;
+  uint32_t(*rnk)[32] = s_m[wid].rnk;
   uint8_t(*pq)[32] = s_m[wid].pq;
-  const uint32_t nrec = min((uint64_t)a.counters[CNT_MREC], (uint64_t)a.mrec_cap);
+  // Records to merge: all of them, or (dedupe on) the owners k_dedup listed.
+  const bool listed = a.dmask != 0;
+  const uint32_t nrec = min((uint64_t)a.counters[listed ? CNT_OWNERS : CNT_MREC], (uint64_t)a.mrec_cap);
   const uint32_t* d2id = T.d2id;
+  // Records come 32 at a time: lane i holds record base + i of the current
+  // batch in registers and idle lanes take theirs by shuffle (no dependent
+  // global load on refill); the next batch is in flight meanwhile.
+  const ulonglong2 kHole = make_ulonglong2(~0ull, 0ull);
   uint32_t base = 0, next = 0, avail = 0;  // warp-uniform slice of record indices
+  uint32_t pbase = 0, pidx = 0, cidx = 0;  // record index held by this lane (prefetched / current)
+  ulonglong2 cur = kHole, pre = kHole;
+  auto fetch = [&]() {
+    uint32_t c0 = 0;
+    if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MERGE_TICKET], 32u);
+    pbase = __shfl_sync(kFull, c0, 0);
+    pidx = pbase + lane;
+    if (pidx < nrec) {
+      if (listed) pidx = __ldcs(a.owners + pidx);
+      pre = __ldcs(a.mrec + pidx);
+    } else {
+      pre = kHole;
+    }
+  };
+  fetch();
   bool exhausted = false;
   int n = 0;      // my piece's current length (0 = idle)
   int np = 0;     // pending probes
   uint32_t m = NONE;  // minimum over resolved ranks
   uint64_t rec = 0;
+  uint32_t ridx = 0;
   for (;;) {
     const bool idle = n == 0;
     const unsigned im = __ballot_sync(kFull, idle);
     if (im && next >= avail && !exhausted) {
-      uint32_t c0 = 0;
-      if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MERGE_TICKET], 32u);
-      base = __shfl_sync(kFull, c0, 0);
+      base = pbase;
+      cur = pre;
+      cidx = pidx;
       next = 0;
       avail = base < nrec ? min(32u, nrec - base) : 0u;
       exhausted = avail == 0;
+      if (!exhausted) fetch();
     }
     const uint32_t take = min(uint32_t(__popc(im)), avail - next);
     const uint32_t rank = __popc(im & lanemask_lt(lane));
-    if (idle && rank < take) {
-      rec = a.mrec[base + next + rank];
+    const bool takes = idle && rank < take;
+    const int src_lane = takes ? int(next + rank) : lane;
+    const uint64_t hdr = __shfl_sync(kFull, cur.x, src_lane);
+    const uint64_t b8 = __shfl_sync(kFull, cur.y, src_lane);
+    const uint32_t hidx = __shfl_sync(kFull, cidx, src_lane);
+    if (takes) {
+      rec = hdr;
+      ridx = hidx;
       if (rec != ~0ull) {
         n = int(rec & 63);
-        const uint8_t* src = a.bytes + (rec >> 16);
-        for (int i = 0; i < n; ++i) {
-          tok[i][lane] = Tk(s_lut[src[i]]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (i < n) tok[i][lane] = Tk(s_lut[(b8 >> (8 * i)) & 0xFF]);
           pq[i][lane] = static_cast<uint8_t>(i);
+        }
+        if (n > 8) {  // bytes past the record's 8 (rare)
+          const uint8_t* src = a.bytes + (rec >> 16);
+          for (int i = 8; i < n; ++i) {
+            tok[i][lane] = Tk(s_lut[__ldg(src + i)]);
+            pq[i][lane] = static_cast<uint8_t>(i);
+          }
         }
         np = n - 1;
         m = NONE;
@@ -880,20 +965,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, De
       continue;
     }
     if (!busy) continue;
-    // probe: pending pairs, four in flight.
-    for (int p = 0; p < np; p += 4) {
-      ProbeReq r[4];
-      int at[4];
+    // probe: pending pairs, BBPE_MERGE_PROBES in flight.
+    constexpr int PB = BBPE_MERGE_PROBES;
+    for (int p = 0; p < np; p += PB) {
+      ProbeReq r[PB];
+      int at[PB];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PB; ++u) {
         at[u] = p + u < np ? int(pq[p + u][lane]) : -1;
         if (at[u] >= 0) probe_issue<K32>(r[u], T, tok[at[u]][lane], tok[at[u] + 1][lane]);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < PB; ++u) {
         if (at[u] >= 0) {
-          const uint32_t rk = tk_rank<Tk>(probe_resolve<K32>(r[u], T));
-          rnk[at[u]][lane] = Tk(rk);
+          const uint32_t rk = probe_resolve<K32>(r[u], T);
+          rnk[at[u]][lane] = rk;
           m = min(m, rk);
         }
       }
@@ -910,11 +996,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, De
       }
       for (int i = n; i < len; ++i) dst[i] = kSentinel;
       if (len > n) atomicSub(&a.tile_count[start / kTile], uint32_t(len - n));
+      reinterpret_cast<uint64_t*>(a.mrec + ridx)[1] = uint64_t(n);  // count, for reference copies
       n = 0;
       continue;
     }
     // sweep at rank m.
-    const Tk M = Tk(__ldg(T.r2m + m));
+    const Tk M = Tk(K32 ? (m & 0xFFFFu) : __ldg(T.r2m + m));
     const uint32_t mm = m;
     int j = 0, i = 0;
     np = 0;
@@ -922,7 +1009,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, De
     uint32_t hold = NONE;  // rank of pair (j-1, j) if it survives
     bool prev_merged = false;
     while (i < n) {
-      const uint32_t ri = (i < n - 1) ? uint32_t(rnk[i][lane]) : NONE;
+      const uint32_t ri = (i < n - 1) ? rnk[i][lane] : NONE;
       if (ri == mm) {
         tok[j][lane] = M;
         if (j > 0 && !prev_merged) pq[np++][lane] = static_cast<uint8_t>(j - 1);
@@ -933,7 +1020,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, De
       } else {
         m = min(m, hold);  // pair (j-1, j) keeps its rank
         tok[j][lane] = tok[i][lane];
-        rnk[j][lane] = Tk(ri);
+        rnk[j][lane] = ri;
         hold = ri;  // rank of pair (j, j+1), kept unless the next output is a merge
         prev_merged = false;
         i += 1;
@@ -944,6 +1031,67 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 3) k_merge(EncodeArgs a, De
     n = j;
     // The last merged token has no right pair.
     if (np > 0 && int(pq[np - 1][lane]) >= n - 1) --np;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_dedup: thread per merge record. Pieces of <= kDedupMax bytes claim their
+// bytes' slot (dedup_claim); the first claimer of each distinct piece is its
+// owner and is listed for k_merge, the others become references (k_refs copies
+// the owner's tokens). Exact: a piece's encoding depends on its bytes only.
+// Longer pieces (and full neighbourhoods) are listed as owners of themselves.
+__global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
+  const uint64_t nrec = min((uint64_t)a.counters[CNT_MREC], a.mrec_cap);
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  const uint64_t i0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  for (uint64_t i = i0; i - lane < nrec; i += stride) {  // warp-uniform trip count
+    bool owner = false;
+    if (i < nrec) {
+      const ulonglong2 r = __ldcs(a.mrec + i);
+      if (r.x != ~0ull) {
+        const int len = int(r.x & 63);
+        uint64_t res = ~0ull;
+        if (len <= kDedupMax) {
+          const uint64_t k0 = len >= 8 ? r.y : (r.y & ((1ull << (8 * len)) - 1));
+          uint64_t k1 = 0;
+          const uint8_t* src = a.bytes + (r.x >> 16);
+          for (int j = 8; j < len; ++j) k1 |= uint64_t(__ldg(src + j)) << (8 * (j - 8));
+          res = dedup_claim(a.dkey, a.dmask, make_ulonglong2(k0, k1 | (uint64_t(len) << 56)));
+        }
+        if (res != ~0ull && (res >> 63)) {
+          a.mrec[i] = make_ulonglong2(r.x | kRefFlag, res & ~(1ull << 63));
+        } else {
+          owner = true;
+          if (res != ~0ull) a.downer[res] = uint32_t(i);
+        }
+      }
+    }
+    const unsigned om = __ballot_sync(kFull, owner);
+    uint32_t b = 0;
+    if (lane == 0 && om) b = atomicAdd(&a.counters[CNT_OWNERS], uint32_t(__popc(om)));
+    b = __shfl_sync(kFull, b, 0);
+    if (owner) a.owners[b + __popc(om & lanemask_lt(lane))] = uint32_t(i);
+  }
+}
+
+// k_refs: references (k_dedup) take their owner's tokens: thread per merge
+// record, copy from the owner's staging slots (k_merge left its count in the
+// record), kSentinel into the rest of the reserved slots, tile count adjusted.
+__global__ void __launch_bounds__(256) k_refs(EncodeArgs a) {
+  const uint64_t nrec = min((uint64_t)a.counters[CNT_MREC], a.mrec_cap);
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrec; i += stride) {
+    const ulonglong2 r = __ldcs(a.mrec + i);
+    if (r.x == ~0ull || !(r.x & kRefFlag)) continue;
+    const ulonglong2 o = __ldcg(a.mrec + __ldcg(a.downer + r.y));
+    const uint64_t start = (r.x & ~kRefFlag) >> 16, ostart = o.x >> 16;
+    const int len = int(r.x & 63), cnt = int(o.y);
+    const uint32_t* src = a.staging + (ostart / kTile) * kStage + ((o.x >> 6) & 1023);
+    uint32_t* dst = a.staging + (start / kTile) * kStage + ((r.x >> 6) & 1023);
+    for (int j = 0; j < cnt; ++j) dst[j] = __ldcg(src + j);
+    for (int j = cnt; j < len; ++j) dst[j] = kSentinel;
+    if (len > cnt) atomicSub(&a.tile_count[start / kTile], uint32_t(len - cnt));
   }
 }
 
@@ -1144,6 +1292,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
     const uint64_t s0 = a.tile_first[t], s1 = a.tile_first[t + 1];
     const uint4* stage = reinterpret_cast<const uint4*>(a.staging + t * kStage);
     uint32_t* out = a.out_ids + tbase;
+    // Leave the look-back status and the counters zero for the next encode.
+    if (t < a.num_groups && lane == 0) a.status[t] = 0;
+    if (t == 0 && lane < CNT_N) a.counters[lane] = 0;
     // The tile's row-start bits are consumed: leave them zero for the next encode.
     if (a.rowbits && lane < kTile / 32) a.rowbits[t * (kTile / 32) + lane] = 0;
     const uint32_t nl = uint32_t(rec & 0xFFFFFF);
@@ -1323,6 +1474,10 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     k_pieces<<<p.main_grid, kWarpsPerCta * 32, pieces_smem(), stream>>>(a, t);
     ++launched;
     if (ev) cudaEventRecord(ev[2], stream);
+    if (a.dmask) {  // timed together with k_merge
+      k_dedup<<<unsigned(p.sm_count * 8), 256, 0, stream>>>(a);
+      ++launched;
+    }
     if (a.narrow)
       k_merge<uint16_t><<<p.merge_grid, kWarpsPerCta * 32, sizeof(MergeSmem<uint16_t>) * kWarpsPerCta,
                           stream>>>(a, t);
@@ -1330,6 +1485,10 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
       k_merge<uint32_t><<<p.merge_grid_wide, kWarpsPerCta * 32, sizeof(MergeSmem<uint32_t>) * kWarpsPerCta,
                           stream>>>(a, t);
     ++launched;
+    if (a.dmask) {  // timed together with k_merge
+      k_refs<<<unsigned(p.sm_count * 4), 256, 0, stream>>>(a);
+      ++launched;
+    }
   }
   if (ev) cudaEventRecord(ev[3], stream);
   k_long_pieces<kLpThreads><<<p.lp_grid, kLpThreads, 0, stream>>>(a, t);

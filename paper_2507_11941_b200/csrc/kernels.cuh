@@ -23,10 +23,13 @@ constexpr int kWinVec = (kTile + 48) / 16;  // 16-byte chunks of a tile window: 
 constexpr int kRowWords = kTile / 32 + 4;   // row-start bit words copied per tile (whole 16-byte chunks)
 constexpr int kMrecChunk = 256;     // merge records a warp reserves at a time
 constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // staging slot left empty by a merge piece
+constexpr int kDedupMax = 15;       // longest merge piece deduplicated within a call
+constexpr uint64_t kDedupMinBytes = 64ull << 20;  // smaller batches: the dedupe pass costs more than it saves
+constexpr uint64_t kRefFlag = 1ull << 62;  // merge-record header: a reference (k_dedup)
 
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
-       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_N = 8 };
+       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_N = 8 };
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFSETS = 3, ERR_N = 4 };
 
@@ -35,10 +38,11 @@ enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFS
 //    LongRec, merged by k_long_pieces into lpo; takes no staging slots. The
 //    long records of one tile are contiguous and in piece order (k_gather
 //    interleaves their tokens with the tile's staging slots).
-//  * merge piece (2..kLmax bytes, not in the piece memo): a packed u64
-//    (start << 16 | spref << 6 | len) in `mrec`, merged by k_merge into the
-//    `len` staging slots reserved at `spref`; unused slots get kSentinel and
-//    the tile's token count drops by len - count. ~0 marks an unused record.
+//  * merge piece (2..kLmax bytes, not in the piece memo): a 16-byte record
+//    in `mrec`: {start << 16 | spref << 6 | len, the piece's first 8 bytes},
+//    merged by k_merge into the `len` staging slots reserved at `spref`;
+//    unused slots get kSentinel and the tile's token count drops by
+//    len - count. A header of ~0 marks an unused record.
 struct LongRec {
   uint64_t start;  // absolute byte position (token position for token input)
   uint64_t len;
@@ -53,6 +57,9 @@ __host__ __device__ inline uint64_t pack_mrec(uint64_t start, uint32_t spref, ui
 struct EncodeArgs {
   const uint8_t* bytes;
   const uint64_t* offsets;  // n_rows + 1, offsets[0] == 0
+  const uint64_t* offsets_raw;  // optional: offsets + offsets_base, rebased by k_tile_first into offsets_w
+  uint64_t* offsets_w;
+  uint64_t offsets_base;
   uint64_t n_rows;
   uint64_t total;           // offsets[n_rows]
   uint64_t num_tiles;
@@ -70,8 +77,18 @@ struct EncodeArgs {
   uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n long pieces, 0 when none
   uint32_t* rowbits;        // (num_tiles + 1) * (kTile/32) + kRowWords words: row-start bit per byte
   int bytes_aligned;        // bytes pointer is 16-byte aligned (cp.async window loads)
-  uint64_t* mrec;           // mrec_cap packed merge records (CNT_MREC allocated)
+  ulonglong2* mrec;         // mrec_cap merge records (CNT_MREC allocated); k_merge
+                            // leaves an owner's token count in .y
   uint64_t mrec_cap;
+  // Within-call dedupe of merge pieces of <= kDedupMax bytes (dmask 0: off),
+  // k_dedup: dkey[slot] = 16-byte key (15 zero-padded bytes, len in the top
+  // byte), claimed by 128-bit CAS. The claimer owns the slot (downer[slot] =
+  // its record, listed in `owners` for k_merge); a record whose bytes are
+  // already owned becomes a reference {hdr | kRefFlag, slot} for k_refs.
+  ulonglong2* dkey;
+  uint32_t* downer;
+  uint64_t dmask;
+  uint32_t* owners;         // mrec_cap: record indices k_merge processes (CNT_OWNERS used)
   LongRec* lrec;            // lp_cap records (CNT_LREC used)
   uint32_t* long_idx;       // indices of the long records (CNT_LONG used)
   uint64_t long_cap;

@@ -379,8 +379,10 @@ void build_device_layout(bbpe_table& t) {
     t.narrow = max_dense < 0xFFFDull && M < 0xFFFDull;
   }
 
-  // Bucketised open addressing, load <= 0.5. Narrow tables (ids < 2^16) use
-  // 32-bit keys: slot = key32 << 32 | rank, bucket = mix32(key32).
+  // Bucketised open addressing, load <= 0.5. Narrow tables (ids and ranks <
+  // 2^16) use 32-bit keys and carry the merged id in the slot:
+  // slot = key32 << 32 | rank << 16 | merged, bucket = mix32(key32), so one
+  // probe yields both (merge_table.hpp:142-145 Entry{rank, merged}).
   uint64_t buckets = 1;
   while (buckets * kBucketSlots < 2 * M + 8) buckets <<= 1;
   t.bucket_mask = buckets - 1;
@@ -389,7 +391,7 @@ void build_device_layout(bbpe_table& t) {
     uint64_t slot, bk;
     if (t.narrow) {
       const uint32_t key = (t.dense(t.m_left[i]) << 16) | t.dense(t.m_right[i]);
-      slot = (uint64_t(key) << 32) | i;
+      slot = (uint64_t(key) << 32) | (uint64_t(i) << 16) | t.dense(t.m_merged[i]);
       bk = mix32(key) & t.bucket_mask;
     } else {
       const uint64_t key = (uint64_t(t.dense(t.m_left[i])) << t.id_bits) | t.dense(t.m_right[i]);

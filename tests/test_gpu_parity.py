@@ -385,3 +385,22 @@ def test_device_api_unaligned_input(gpt2):
     oo_h = oo.cpu().numpy().astype(np.uint64)
     assert np.array_equal(oo_h, v["out_offsets"])
     assert np.array_equal(out[: int(oo_h[-1])].cpu().numpy().astype(np.uint32), v["ids"])
+
+
+@pytest.mark.parametrize("memo", [True, False])
+def test_dedupe_is_results_neutral(gpt2, oracle_for, memo):
+    """Within-call dedupe of merge pieces (default) vs every piece merged on
+    its own: identical ids/offsets, and equal to the oracle. Text with heavy
+    repetition (numbers, capitalised words) and random bytes."""
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 4000, 256, seed=21)
+    rng = np.random.default_rng(22)
+    rnd = rng.integers(0, 256, 200_000).astype(np.uint8)
+    roff = np.arange(0, 200_001, 1000, dtype=np.uint64)
+    for d, o in ((data, off), (rnd, roff)):
+        a = bb.Encoder(0, piece_memo=memo, dedup=True).encode_packed(gpt2, d, o)
+        b = bb.Encoder(0, piece_memo=memo, dedup=False).encode_packed(gpt2, d, o)
+        want_ids, want_off = oracle_for("gpt2").encode_packed(d, o)
+        assert np.array_equal(a[1], want_off) and np.array_equal(a[0], want_ids)
+        assert np.array_equal(b[1], want_off) and np.array_equal(b[0], want_ids)
