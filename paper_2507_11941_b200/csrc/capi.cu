@@ -101,13 +101,13 @@ bool is_pinned(const void* p) {
 struct Scratch {
   DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
   DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
-  DevBuf dkey, downer, owners, offs;
+  DevBuf dkey, dres, owners, offs;
   uint64_t rowbits_zeroed = 0;  // words known to be zero (k_gather clears what k_tile_first set)
   bool ctrl_dirty = true;       // counters/status not known to be zero (k_gather resets them)  // words known to be zero (k_pieces clears what it consumes)
   void release() {
     for (DevBuf* b : {&tile_first, &status, &counters, &err, &lpo, &lpx, &lpy, &trace, &trace_count, &staging,
                       &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &rowbits, &mrec,
-                      &dkey, &downer, &owners, &offs})
+                      &dkey, &dres, &owners, &offs})
       b->release();
     rowbits_zeroed = 0;
     ctrl_dirty = true;
@@ -259,12 +259,12 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
     uint64_t slots = 4096;
     while (slots < total / 128) slots <<= 1;
     sc.dkey.ensure(slots * 16);
-    sc.downer.ensure(slots * 4);
+    sc.dres.ensure(slots * 8);
     a.dkey = sc.dkey.as<ulonglong2>();
-    a.downer = sc.downer.as<uint32_t>();
+    a.dres = sc.dres.as<uint64_t>();
     a.dmask = slots - 1;
-    sc.owners.ensure(a.mrec_cap * 4);
-    a.owners = sc.owners.as<uint32_t>();
+    sc.owners.ensure(a.mrec_cap * 8);
+    a.owners = sc.owners.as<uint64_t>();
     ck(cudaMemsetAsync(a.dkey, 0, slots * 16, s), "memset dedupe keys");
   }
   sc.lrec.ensure(a.lp_cap * sizeof(LongRec));

@@ -898,14 +898,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
   const ulonglong2 kHole = make_ulonglong2(~0ull, 0ull);
   uint32_t base = 0, next = 0, avail = 0;  // warp-uniform slice of record indices
   uint32_t pbase = 0, pidx = 0, cidx = 0;  // record index held by this lane (prefetched / current)
+  uint32_t pslot = 0, cslot = 0;           // its dedupe slot + 1 (0: none)
   ulonglong2 cur = kHole, pre = kHole;
   auto fetch = [&]() {
     uint32_t c0 = 0;
     if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MERGE_TICKET], 32u);
     pbase = __shfl_sync(kFull, c0, 0);
     pidx = pbase + lane;
+    pslot = 0;
     if (pidx < nrec) {
-      if (listed) pidx = __ldcs(a.owners + pidx);
+      if (listed) {
+        const uint64_t o = __ldcs(a.owners + pidx);
+        pidx = uint32_t(o);
+        pslot = uint32_t(o >> 32);
+      }
       pre = __ldcs(a.mrec + pidx);
     } else {
       pre = kHole;
@@ -917,7 +923,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
   int np = 0;     // pending probes
   uint32_t m = NONE;  // minimum over resolved ranks
   uint64_t rec = 0;
-  uint32_t ridx = 0;
+  uint32_t ridx = 0, rslot = 0;
   for (;;) {
     const bool idle = n == 0;
     const unsigned im = __ballot_sync(kFull, idle);
@@ -925,6 +931,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
       base = pbase;
       cur = pre;
       cidx = pidx;
+      cslot = pslot;
       next = 0;
       avail = base < nrec ? min(32u, nrec - base) : 0u;
       exhausted = avail == 0;
@@ -937,9 +944,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
     const uint64_t hdr = __shfl_sync(kFull, cur.x, src_lane);
     const uint64_t b8 = __shfl_sync(kFull, cur.y, src_lane);
     const uint32_t hidx = __shfl_sync(kFull, cidx, src_lane);
+    const uint32_t hslot = __shfl_sync(kFull, cslot, src_lane);
     if (takes) {
       rec = hdr;
       ridx = hidx;
+      rslot = hslot;
       if (rec != ~0ull) {
         n = int(rec & 63);
 #pragma unroll
@@ -996,7 +1005,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
       }
       for (int i = n; i < len; ++i) dst[i] = kSentinel;
       if (len > n) atomicSub(&a.tile_count[start / kTile], uint32_t(len - n));
-      reinterpret_cast<uint64_t*>(a.mrec + ridx)[1] = uint64_t(n);  // count, for reference copies
+      if (rslot) {  // owner of a dedupe slot: where its tokens are, for the references
+        const uint64_t at = (start / kTile) * kStage + ((rec >> 6) & 1023);
+        a.dres[rslot - 1] = at | (uint64_t(n) << 48);
+      }
       n = 0;
       continue;
     }
@@ -1047,6 +1059,7 @@ __global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
   const uint64_t i0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   for (uint64_t i = i0; i - lane < nrec; i += stride) {  // warp-uniform trip count
     bool owner = false;
+    uint64_t oslot = 0;
     if (i < nrec) {
       const ulonglong2 r = __ldcs(a.mrec + i);
       if (r.x != ~0ull) {
@@ -1063,7 +1076,7 @@ __global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
           a.mrec[i] = make_ulonglong2(r.x | kRefFlag, res & ~(1ull << 63));
         } else {
           owner = true;
-          if (res != ~0ull) a.downer[res] = uint32_t(i);
+          oslot = res == ~0ull ? 0 : res + 1;
         }
       }
     }
@@ -1071,7 +1084,7 @@ __global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
     uint32_t b = 0;
     if (lane == 0 && om) b = atomicAdd(&a.counters[CNT_OWNERS], uint32_t(__popc(om)));
     b = __shfl_sync(kFull, b, 0);
-    if (owner) a.owners[b + __popc(om & lanemask_lt(lane))] = uint32_t(i);
+    if (owner) a.owners[b + __popc(om & lanemask_lt(lane))] = i | (oslot << 32);
   }
 }
 
@@ -1084,13 +1097,18 @@ __global__ void __launch_bounds__(256) k_refs(EncodeArgs a) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrec; i += stride) {
     const ulonglong2 r = __ldcs(a.mrec + i);
     if (r.x == ~0ull || !(r.x & kRefFlag)) continue;
-    const ulonglong2 o = __ldcg(a.mrec + __ldcg(a.downer + r.y));
-    const uint64_t start = (r.x & ~kRefFlag) >> 16, ostart = o.x >> 16;
-    const int len = int(r.x & 63), cnt = int(o.y);
-    const uint32_t* src = a.staging + (ostart / kTile) * kStage + ((o.x >> 6) & 1023);
+    const uint64_t d = __ldcg(a.dres + r.y);  // owner's staging index | count << 48
+    const uint64_t start = (r.x & ~kRefFlag) >> 16;
+    const int len = int(r.x & 63), cnt = int(d >> 48);
+    const uint32_t* src = a.staging + (d & ((1ull << 48) - 1));
     uint32_t* dst = a.staging + (start / kTile) * kStage + ((r.x >> 6) & 1023);
-    for (int j = 0; j < cnt; ++j) dst[j] = __ldcg(src + j);
-    for (int j = cnt; j < len; ++j) dst[j] = kSentinel;
+    uint32_t v[kDedupMax];
+#pragma unroll
+    for (int j = 0; j < kDedupMax; ++j)
+      if (j < cnt) v[j] = __ldcg(src + j);  // all loads in flight together
+#pragma unroll
+    for (int j = 0; j < kDedupMax; ++j)
+      if (j < len) dst[j] = j < cnt ? v[j] : kSentinel;
     if (len > cnt) atomicSub(&a.tile_count[start / kTile], uint32_t(len - cnt));
   }
 }
@@ -1275,7 +1293,10 @@ __device__ __forceinline__ uint32_t compact_at(const GatherSmem& G, uint32_t slo
   return G.pre[slot >> 2] + __popc(G.msk[slot >> 2] & ((1u << (slot & 3)) - 1u));
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevTable T) {
+#ifndef BBPE_GATHER_MINB
+#define BBPE_GATHER_MINB 4
+#endif
+__global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   __shared__ GatherSmem s_g[kWarpsPerCta];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
@@ -1285,13 +1306,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
   const uint32_t* d2id = T.d2id;
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
   const uint64_t rb = a.run_base ? *a.run_base : 0;
-  for (uint64_t t = blockIdx.x * uint64_t(kWarpsPerCta) + (threadIdx.x >> 5); t < a.num_tiles; t += nwarps) {
-    const uint64_t tbase = __ldcg(a.tile_base + t);
-    const uint64_t rec = __ldcg(a.tile_lrec + t);
-    const uint32_t nslots = __ldcg(a.tile_slots + t);
-    const uint64_t s0 = a.tile_first[t], s1 = a.tile_first[t + 1];
+  // Tile metadata is prefetched one tile ahead; a tile's staged slots and row
+  // offsets are all loaded before any is used (one round trip, not one per
+  // 128-slot chunk).
+  uint64_t t = blockIdx.x * uint64_t(kWarpsPerCta) + (threadIdx.x >> 5);
+  uint64_t m_tb = 0, m_rec = 0, m_s0 = 0, m_s1 = 0;
+  uint32_t m_ns = 0;
+  auto meta = [&](uint64_t u) {
+    if (u < a.num_tiles) {
+      m_tb = __ldcg(a.tile_base + u);
+      m_rec = __ldcg(a.tile_lrec + u);
+      m_ns = __ldcg(a.tile_slots + u);
+      m_s0 = a.tile_first[u];
+      m_s1 = a.tile_first[u + 1];
+    }
+  };
+  meta(t);
+  for (; t < a.num_tiles; t += nwarps) {
+    const uint64_t tbase = m_tb, rec = m_rec, s0 = m_s0, s1 = m_s1;
+    const uint32_t nslots = m_ns;
+    meta(t + nwarps);
     const uint4* stage = reinterpret_cast<const uint4*>(a.staging + t * kStage);
     uint32_t* out = a.out_ids + tbase;
+    constexpr int kVecPerLane = (kStageVec + 31) / 32;
+    const uint32_t nvec = (nslots + 3) / 4;
+    uint4 xs[kVecPerLane];
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      const uint32_t v = 32 * j + lane;
+      xs[j] = v < nvec ? __ldcs(stage + v) : make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+    }
+    uint64_t roff = 0;
+    if (s0 + lane < s1 && s0 + lane <= a.n_rows) roff = __ldcg(a.out_offsets + s0 + lane);
     // Leave the look-back status and the counters zero for the next encode.
     if (t < a.num_groups && lane == 0) a.status[t] = 0;
     if (t == 0 && lane < CNT_N) a.counters[lane] = 0;
@@ -1309,13 +1355,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
       __syncwarp();
     }
     // Staged slots, 4 per lane per step: compaction by warp scan.
-    const uint32_t nvec = (nslots + 3) / 4;
     uint32_t run = 0;
-    for (uint32_t v0 = 0; v0 < nvec; v0 += 32) {
-      const uint32_t v = v0 + lane;
-      uint4 x = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
-      if (v < nvec) x = __ldcs(stage + v);
-      const uint32_t e[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int j = 0; j < kVecPerLane; ++j) {
+      if (32u * j >= nvec) break;
+      const uint32_t v = 32 * j + lane;
+      const uint32_t e[4] = {xs[j].x, xs[j].y, xs[j].z, xs[j].w};
       uint32_t m = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -1359,7 +1404,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_gather(EncodeArgs a, DevT
     // Row offsets: compacted staging slots before the row plus the tokens of
     // the first (v >> 40) long pieces of the tile.
     for (uint64_t s = s0 + lane; s < s1 && s <= a.n_rows; s += 32) {
-      const uint64_t v = __ldcg(a.out_offsets + s);
+      const uint64_t v = s == s0 + lane ? roff : __ldcg(a.out_offsets + s);
       const uint32_t lb = uint32_t(v >> 40);
       uint64_t lsum = 0;
       for (uint32_t li = 0; li < lb; ++li) lsum += LV.cnt(li);
@@ -1486,7 +1531,7 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
                           stream>>>(a, t);
     ++launched;
     if (a.dmask) {  // timed together with k_merge
-      k_refs<<<unsigned(p.sm_count * 4), 256, 0, stream>>>(a);
+      k_refs<<<unsigned(p.sm_count * 8), 256, 0, stream>>>(a);
       ++launched;
     }
   }

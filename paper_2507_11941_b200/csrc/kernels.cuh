@@ -86,9 +86,9 @@ struct EncodeArgs {
   // its record, listed in `owners` for k_merge); a record whose bytes are
   // already owned becomes a reference {hdr | kRefFlag, slot} for k_refs.
   ulonglong2* dkey;
-  uint32_t* downer;
+  uint64_t* dres;           // per slot, set by the owner in k_merge: staging index | count << 48
   uint64_t dmask;
-  uint32_t* owners;         // mrec_cap: record indices k_merge processes (CNT_OWNERS used)
+  uint64_t* owners;         // mrec_cap: record index | (slot + 1) << 32 for k_merge (CNT_OWNERS used)
   LongRec* lrec;            // lp_cap records (CNT_LREC used)
   uint32_t* long_idx;       // indices of the long records (CNT_LONG used)
   uint64_t long_cap;
