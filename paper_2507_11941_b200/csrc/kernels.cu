@@ -348,25 +348,31 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   const bool async = a.bytes_aligned != 0;
   const bool chk = T.full_lut == 0;
 
-  // Tiles by ticket (in input order): the next ticket is taken one tile ahead.
+  // Tiles by ticket, kTilesPerTicket consecutive tiles per ticket (in input
+  // order); the next ticket is taken a whole group ahead.
+  // (one tile per ticket when there are few tiles per warp: keep every warp busy)
+  const uint64_t G = a.num_tiles >= uint64_t(gridDim.x) * kWarpsPerCta * 16 ? kTilesPerTicket : 1;
   uint32_t tk = 0;
   if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
-  uint64_t tile = __shfl_sync(kFull, tk, 0);
+  uint64_t tile = uint64_t(__shfl_sync(kFull, tk, 0)) * G;
   if (tile >= a.num_tiles) return;
   if (async) issue_window(S, 0, a, tile, lane);
   cp_async_commit();
   if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
-  uint64_t nxt = __shfl_sync(kFull, tk, 0);
+  uint64_t nxt = tile + 1;
+  if (G == 1) {
+    nxt = __shfl_sync(kFull, tk, 0);
+    if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
+  }
   uint64_t f = lane < 2 ? a.tile_first[tile + lane] : 0;
   int buf = 0;
   uint64_t mbase = 0;
   uint32_t mleft = 0;
 
   while (tile < a.num_tiles) {
-    // Prefetch: the next tile's window and row range, the ticket after it.
+    // Prefetch: the next tile's window and row range.
     if (async && nxt < a.num_tiles) issue_window(S, buf ^ 1, a, nxt, lane);
     cp_async_commit();
-    if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
     const uint64_t nf = (lane < 2 && nxt < a.num_tiles) ? a.tile_first[nxt + lane] : 0;
     if (async) {
       cp_async_wait<1>();
@@ -563,7 +569,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     }
     __syncwarp();
     tile = nxt;
-    nxt = __shfl_sync(kFull, tk, 0);
+    if (G > 1 && (nxt + 1) % G) {
+      nxt = nxt + 1;
+    } else {  // next group: the ticket taken a group ago, and the one after it
+      nxt = uint64_t(__shfl_sync(kFull, tk, 0)) * G;
+      if (lane == 0) tk = atomicAdd(&a.counters[CNT_TILE_TICKET], 1u);
+    }
     f = nf;
     buf ^= 1;
   }

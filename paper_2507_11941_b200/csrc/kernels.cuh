@@ -18,6 +18,7 @@ constexpr int kWin = kTile + kLmax + 1;  // window positions [0, kWin) after b0
 constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece tokens)
 constexpr int kScanTilesPerCta = 4096;  // k_tile_scan: 512 threads x 8 tiles
 constexpr int kWarpsPerCta = 8;
+constexpr int kTilesPerTicket = 4;  // k_pieces: consecutive tiles per ticket
 constexpr int kLpThreads = 512;     // CTA size of the long-piece (block engine) kernel
 constexpr int kWinVec = (kTile + 48) / 16;  // 16-byte chunks of a tile window: bytes [b0-16, b0+kTile+32)
 constexpr int kRowWords = kTile / 32 + 4;   // row-start bit words copied per tile (whole 16-byte chunks)
