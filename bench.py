@@ -299,6 +299,24 @@ def main():
                       "kernel_ms": {k: v / max(kc, 1) for k, v in kt.items()}}
         enc.set_config(piece_memo=True, dedup=True)
 
+    # ---- device decode of the step's output, round-trip checked ----
+    decode = None
+    if args.engine == "pieces":
+        d_back = torch.empty(max(total, 1), dtype=torch.uint8, device="cuda")
+        d_boff = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        dec_args = (table, d_ids.data_ptr(), d_oo.data_ptr(), n, ntok, d_back.data_ptr(), total, d_boff.data_ptr())
+        enc.decode_device(*dec_args)
+        assert torch.equal(d_back[:total], d_data), "device decode did not invert the encode"
+        times = []
+        for _ in range(max(3, args.steps // 2)):
+            t0 = time.perf_counter()
+            enc.decode_device(*dec_args)
+            times.append(time.perf_counter() - t0)
+        d_ms = float(np.median(times)) * 1e3
+        decode = {"ms_per_step": d_ms, "output_GBps": total / (d_ms / 1e3) / 1e9,
+                  "tokens_per_s": ntok / (d_ms / 1e3), "timing": "wall clock of the synchronous call",
+                  "round_trip": "bit-exact"}
+
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
     dom = max(k_ms, key=k_ms.get)
@@ -363,6 +381,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "merge_only": merge_only,
+            "decode": decode,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

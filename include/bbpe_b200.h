@@ -151,6 +151,21 @@ uint32_t bbpe_table_rank_of(const bbpe_table* t, uint32_t left, uint32_t right,
 int bbpe_decode(const bbpe_table* t, const uint32_t* ids, size_t n, uint8_t* out, size_t cap,
                 size_t* len);
 
+/* ---- device batch decode (decode merge_table.hpp:565-579,
+ * decode_batch batch.hpp:128-154): CSR token ids -> CSR bytes.
+ * ids[tok_offsets[r]..tok_offsets[r+1]) of row r decode to
+ * out_bytes[out_byte_offsets[r]..out_byte_offsets[r+1]). At most cap bytes
+ * are written; *total receives the full length (check it against cap).
+ * Unknown id -> BBPE_DECODE, "row r: unknown token id X at index i".
+ * Specials are not table tokens: decode rows containing them on the host. */
+int bbpe_decode_batch(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* ids, const uint64_t* tok_offsets,
+                      size_t n_rows, uint8_t* out_bytes, uint64_t cap, uint64_t* out_byte_offsets,
+                      uint64_t* total);
+/* The same on device buffers (n_ids = tok_offsets[n_rows] - tok_offsets[0]); synchronous. */
+int bbpe_decode_device(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* d_ids, const uint64_t* d_tok_offsets,
+                       size_t n_rows, uint64_t n_ids, uint8_t* d_out_bytes, uint64_t cap,
+                       uint64_t* d_out_byte_offsets, uint64_t* total);
+
 /* ---- per-device encode contexts ---- */
 int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out);
 int bbpe_ctx_destroy(bbpe_ctx* ctx);

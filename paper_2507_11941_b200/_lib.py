@@ -75,6 +75,9 @@ SIGNATURES = {
     "bbpe_table_byte_token": (C.c_uint32, [C.c_void_p, C.c_uint8]),
     "bbpe_table_rank_of": (C.c_uint32, [C.c_void_p, C.c_uint32, C.c_uint32, u32p]),
     "bbpe_decode": (C.c_int, [C.c_void_p, u32p, C.c_size_t, u8p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "bbpe_decode_batch": (C.c_int, [C.c_void_p, C.c_void_p, u32p, u64p, C.c_size_t, u8p, C.c_uint64, u64p, u64p]),
+    "bbpe_decode_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64,
+                                     C.c_void_p, C.c_uint64, C.c_void_p, u64p]),
     "bbpe_ctx_create": (C.c_int, [C.c_int, C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "bbpe_ctx_destroy": (C.c_int, [C.c_void_p]),
     "bbpe_ctx_set_config": (C.c_int, [C.c_void_p, C.POINTER(Config)]),

@@ -234,6 +234,13 @@ class MergeTable:
     def bytes_of(self, tid: int) -> Optional[bytes]:
         return self.token_bytes().get(tid)
 
+    def max_token_bytes(self) -> int:
+        """Length of the longest token (bounds a decode's output)."""
+        if getattr(self, "_max_tok", None) is None:
+            _, off, _, _ = self.export()
+            self._max_tok = int((off[1:] - off[:-1]).max()) if off.size > 1 else 1
+        return self._max_tok
+
 
 def load_merge_table_files(vocab_path: str, merges_path: Optional[str], fmt: Union[str, int] = "gpt2") -> MergeTable:
     return MergeTable.load_files(vocab_path, merges_path, fmt)
@@ -459,6 +466,34 @@ class Encoder:
 
     def sync(self):
         _check(LIB.bbpe_ctx_sync(self._h))
+
+    def decode_packed(self, table: MergeTable, ids: np.ndarray, offsets: np.ndarray,
+                      out: Optional[np.ndarray] = None, out_offsets: Optional[np.ndarray] = None):
+        """Device batch decode (decode / decode_batch, merge_table.hpp:565-579,
+        batch.hpp:128-154): CSR ids -> (bytes u8, byte offsets u64[n+1])."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        n = offsets.size - 1
+        if out is None:
+            # Upper bound: the longest token times the number of ids.
+            out = np.empty(max(int(offsets[-1] - offsets[0]) * table.max_token_bytes(), 1), dtype=np.uint8)
+        if out_offsets is None:
+            out_offsets = np.empty(n + 1, dtype=np.uint64)
+        total = C.c_uint64()
+        _check(LIB.bbpe_decode_batch(self._h, table.handle, _p(ids, C.c_uint32) if ids.size else None,
+                                     _p(offsets, C.c_uint64), n, _p(out, C.c_uint8), out.size,
+                                     _p(out_offsets, C.c_uint64), C.byref(total)))
+        if total.value > out.size:
+            raise UsageError(f"decode output capacity {out.size} is smaller than the {total.value} bytes produced")
+        return out[: total.value], out_offsets
+
+    def decode_device(self, table: MergeTable, d_ids, d_offsets, n_rows: int, n_ids: int, d_out, cap: int,
+                      d_out_offsets) -> int:
+        """Device pointers: CSR ids -> CSR bytes on device; returns the byte total."""
+        total = C.c_uint64()
+        _check(LIB.bbpe_decode_device(self._h, table.handle, C.c_void_p(d_ids), C.c_void_p(d_offsets), n_rows,
+                                      n_ids, C.c_void_p(d_out), cap, C.c_void_p(d_out_offsets), C.byref(total)))
+        return total.value
 
     def block_bpe(self, table: MergeTable, tokens: Sequence[int], trace: bool = False):
         """block_engine.hpp:268-310 on explicit ids. Returns ids, or (ids, trace)

@@ -96,6 +96,10 @@ struct DeviceReplica {
   void* base = nullptr;  // one cudaMalloc holding every array
   void* memo = nullptr;  // memo slots (separate allocation)
   int memo_state = 0;    // 0 not built, 1 building, 2 built (or not applicable)
+  // Decode table (decode.cu), built on first device decode: dec_n u64
+  // entries (byte start << 24 | length, ~0 = no token) then the token bytes.
+  void* dec = nullptr;
+  uint64_t dec_n = 0;
 };
 
 }  // namespace bbpe

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "bbpe_internal.h"
+#include "decode.cuh"
 #include "kernels.cuh"
 
 namespace bbpe {
@@ -186,6 +187,8 @@ struct bbpe_ctx {
   WaveSet sets[kSets];
   uint64_t* h_errs = nullptr;  // pinned: error slots of every wave of the last host encode
   size_t h_errs_cap = 0;
+  // Device decode scratch and host-API staging.
+  DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff;
   DevBuf run_base;
 };
 
@@ -900,6 +903,139 @@ int bbpe_decode(const bbpe_table* t, const uint32_t* ids, size_t n, uint8_t* out
   return BBPE_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Device decode table of `t` on the ctx's device (built once, like the memo).
+const bbpe::DeviceReplica& decode_table(bbpe_ctx& c, const bbpe_table& t) {
+  using namespace bbpe;
+  table_on_device(t, c.device);
+  DeviceReplica& rep = replica_of(t, c.device);
+  std::lock_guard<std::mutex> lock(const_cast<bbpe_table&>(t).mu);
+  if (rep.dec) return rep;
+  const uint64_t dec_n = uint64_t(t.max_id) + 1;
+  if (dec_n > (1ull << 26)) throw usage_error("token ids too sparse for the device decode table");
+  std::vector<uint64_t> ent(dec_n, ~0ull);
+  for (size_t i = 0; i < t.ids.size(); ++i)
+    ent[t.ids[i]] = (t.tok_off[i] << 24) | (t.tok_off[i + 1] - t.tok_off[i]);
+  const size_t nb = t.tok_bytes.size();
+  void* p = nullptr;
+  ck(cudaMalloc(&p, dec_n * 8 + std::max<size_t>(nb, 1)), "cudaMalloc (decode table)");
+  ck(cudaMemcpy(p, ent.data(), dec_n * 8, cudaMemcpyHostToDevice), "decode table upload");
+  if (nb) ck(cudaMemcpy(static_cast<char*>(p) + dec_n * 8, t.tok_bytes.data(), nb, cudaMemcpyHostToDevice),
+             "decode table upload");
+  rep.dec = p;
+  rep.dec_n = dec_n;
+  return rep;
+}
+
+// Decodes device CSR ids into device CSR bytes on c.stream (synchronous);
+// raises the reference's DecodeError for the first unknown id.
+uint64_t decode_on_device(bbpe_ctx& c, const bbpe_table& t, const uint32_t* d_ids, const uint64_t* d_toff,
+                          uint64_t n_rows, uint64_t n_ids, uint8_t* d_out, uint64_t cap, uint64_t* d_ooff,
+                          const uint64_t* h_toff) {
+  using namespace bbpe;
+  const DeviceReplica& rep = decode_table(c, t);
+  DecodeArgs a{};
+  a.ids = d_ids;
+  a.tok_off = d_toff;
+  a.n_rows = n_rows;
+  a.n_ids = n_ids;
+  a.dec = static_cast<const uint64_t*>(rep.dec);
+  a.dec_n = rep.dec_n;
+  a.dec_bytes = static_cast<const uint8_t*>(rep.dec) + rep.dec_n * 8;
+  a.n_blocks = (n_ids + 255) / 256;
+  c.dec_pos.ensure(std::max<uint64_t>(n_ids, 1) * 8);
+  c.dec_sums.ensure((a.n_blocks + 1) * 8);
+  c.dec_err.ensure(8);
+  a.pos = c.dec_pos.as<uint64_t>();
+  a.block_sums = c.dec_sums.as<uint64_t>();
+  a.err = c.dec_err.as<uint64_t>();
+  a.out = d_out;
+  a.cap = cap;
+  a.out_off = d_ooff;
+  ck(cudaMemsetAsync(a.err, 0xFF, 8, c.stream), "memset");
+  launch_decode(a, c.stream);
+  c.launches += n_ids ? 4 : 1;
+  ck(cudaGetLastError(), "decode launch");
+  uint64_t res[2];
+  ck(cudaMemcpyAsync(&res[0], a.err, 8, cudaMemcpyDeviceToHost, c.stream), "D2H");
+  ck(cudaMemcpyAsync(&res[1], a.block_sums + a.n_blocks, 8, cudaMemcpyDeviceToHost, c.stream), "D2H");
+  ck(cudaStreamSynchronize(c.stream), "decode");
+  if (res[0] != ~0ull) {
+    std::vector<uint64_t> tmp;
+    if (!h_toff) {
+      tmp.resize(n_rows + 1);
+      ck(cudaMemcpy(tmp.data(), d_toff, (n_rows + 1) * 8, cudaMemcpyDeviceToHost), "D2H");
+      h_toff = tmp.data();
+    }
+    const uint64_t base = h_toff[0], i = res[0];
+    uint64_t lo = 0, hi = n_rows ? n_rows - 1 : 0;  // max r with h_toff[r] - base <= i
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) / 2;
+      if (h_toff[mid] - base <= i) lo = mid; else hi = mid - 1;
+    }
+    uint32_t id = 0;
+    ck(cudaMemcpy(&id, d_ids + i, 4, cudaMemcpyDeviceToHost), "D2H");
+    throw Error(BBPE_DECODE, "row " + std::to_string(lo) + ": unknown token id " + std::to_string(id) +
+                                 " at index " + std::to_string(i - (h_toff[lo] - base)));
+  }
+  return res[1];
+}
+
+}  // namespace
+
+extern "C" {
+
+int bbpe_decode_device(bbpe_ctx* c, const bbpe_table* t, const uint32_t* d_ids, const uint64_t* d_tok_offsets,
+                       size_t n_rows, uint64_t n_ids, uint8_t* d_out_bytes, uint64_t cap,
+                       uint64_t* d_out_byte_offsets, uint64_t* total) {
+  BBPE_TRY
+  if (!c || !t || !d_tok_offsets || !d_out_byte_offsets) throw bbpe::usage_error("null argument");
+  if (n_ids && (!d_ids || (cap && !d_out_bytes))) throw bbpe::usage_error("null buffer");
+  DeviceGuard g(c->device);
+  const uint64_t tot = decode_on_device(*c, *t, d_ids, d_tok_offsets, n_rows, n_ids, d_out_bytes, cap,
+                                        d_out_byte_offsets, nullptr);
+  if (total) *total = tot;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_decode_batch(bbpe_ctx* c, const bbpe_table* t, const uint32_t* ids, const uint64_t* tok_offsets,
+                      size_t n_rows, uint8_t* out_bytes, uint64_t cap, uint64_t* out_byte_offsets,
+                      uint64_t* total) {
+  BBPE_TRY
+  if (!c || !t || !tok_offsets || !out_byte_offsets) throw bbpe::usage_error("null argument");
+  const uint64_t base = tok_offsets[0], n_ids = tok_offsets[n_rows] - base;
+  if (tok_offsets[n_rows] < base) throw bbpe::usage_error("offsets must be non-decreasing");
+  if (n_ids && !ids) throw bbpe::usage_error("null buffer");
+  for (size_t r = 0; r < n_rows; ++r)
+    if (tok_offsets[r + 1] < tok_offsets[r]) throw bbpe::usage_error("offsets must be non-decreasing");
+  DeviceGuard g(c->device);
+  c->dec_ids.ensure(std::max<uint64_t>(n_ids, 1) * 4);
+  c->dec_toff.ensure((n_rows + 1) * 8);
+  c->dec_ooff.ensure((n_rows + 1) * 8);
+  if (n_ids)
+    ck(cudaMemcpyAsync(c->dec_ids.p, ids + base, n_ids * 4, cudaMemcpyHostToDevice, c->stream), "H2D ids");
+  ck(cudaMemcpyAsync(c->dec_toff.p, tok_offsets, (n_rows + 1) * 8, cudaMemcpyHostToDevice, c->stream),
+     "H2D offsets");
+  // Output bytes: the exact size after a first pass would cost a round trip;
+  // size the device buffer by the caller's capacity instead.
+  c->dec_out.ensure(std::max<uint64_t>(cap, 1));
+  const uint64_t tot = decode_on_device(*c, *t, c->dec_ids.as<uint32_t>(), c->dec_toff.as<uint64_t>(), n_rows,
+                                        n_ids, c->dec_out.as<uint8_t>(), cap, c->dec_ooff.as<uint64_t>(),
+                                        tok_offsets);
+  const uint64_t ncopy = std::min(tot, cap);
+  if (ncopy) ck(cudaMemcpyAsync(out_bytes, c->dec_out.p, ncopy, cudaMemcpyDeviceToHost, c->stream), "D2H bytes");
+  ck(cudaMemcpyAsync(out_byte_offsets, c->dec_ooff.p, (n_rows + 1) * 8, cudaMemcpyDeviceToHost, c->stream),
+     "D2H offsets");
+  ck(cudaStreamSynchronize(c->stream), "decode");
+  if (total) *total = tot;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
 int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out) {
   BBPE_TRY
   if (!out) throw bbpe::usage_error("out is null");
@@ -926,7 +1062,9 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->sc.release();
-    for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets}) b->release();
+    for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_sums,
+                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff})
+      b->release();
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     for (auto& set : c->ev_sets)

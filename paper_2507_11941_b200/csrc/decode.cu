@@ -1,0 +1,131 @@
+// decode.cu -- batch decode on the device: CSR token ids ->
+// CSR bytes, the inverse of the encode path. Semantics of
+// decode (merge_table.hpp:565-579: concatenate each id's bytes, DecodeError
+// "unknown token id X at index i") and decode_batch (batch.hpp:128-154: per
+// row, error prefixed "row r: ").
+//
+// Device table: dec[id] = byte start << 24 | byte length (~0: no such token),
+// dense over ids 0..max_id, and the token bytes; built once per device.
+// Kernels: k_dec_len (token lengths, block-local exclusive scan, first bad
+// token), k_dec_scan (block totals -> block bases, one CTA), k_dec_copy
+// (bytes gathered to their output position), k_dec_rows (row byte offsets).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "decode.cuh"
+
+namespace bbpe {
+namespace {
+
+constexpr int kDecThreads = 256;
+
+__global__ void __launch_bounds__(kDecThreads) k_dec_len(DecodeArgs a) {
+  __shared__ uint64_t s_warp[kDecThreads / 32];
+  const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t len = 0;
+  if (i < a.n_ids) {
+    const uint32_t id = a.ids[i];
+    const uint64_t e = id < a.dec_n ? __ldg(a.dec + id) : ~0ull;
+    if (e == ~0ull) {
+      atomicMin(reinterpret_cast<unsigned long long*>(a.err), (unsigned long long)i);
+    } else {
+      len = e & 0xFFFFFF;
+    }
+  }
+  uint64_t inc = len;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t x = lane < kDecThreads / 32 ? s_warp[lane] : 0;
+    uint64_t xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, xi, d);
+      if (lane >= d) xi += u;
+    }
+    if (lane < kDecThreads / 32) s_warp[lane] = xi - x;
+    if (lane == 31) a.block_sums[blockIdx.x] = xi;
+  }
+  __syncthreads();
+  if (i < a.n_ids) a.pos[i] = s_warp[wid] + inc - len;
+}
+
+// One CTA: exclusive scan of the block totals in place, total at [n_blocks].
+__global__ void __launch_bounds__(1024) k_dec_scan(uint64_t* sums, uint64_t n_blocks) {
+  __shared__ uint64_t s_warp[32];
+  __shared__ uint64_t s_carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint64_t b0 = 0; b0 < n_blocks; b0 += 1024) {
+    const uint64_t b = b0 + threadIdx.x;
+    const uint64_t v = b < n_blocks ? sums[b] : 0;
+    uint64_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const uint64_t x = s_warp[lane];
+      uint64_t xi = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, xi, d);
+        if (lane >= d) xi += u;
+      }
+      s_warp[lane] = xi - x;
+    }
+    __syncthreads();
+    const uint64_t carry = s_carry;
+    if (b < n_blocks) sums[b] = carry + s_warp[wid] + inc - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = carry + s_warp[wid] + inc;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[n_blocks] = s_carry;
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_dec_copy(DecodeArgs a) {
+  const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
+  if (i >= a.n_ids) return;
+  const uint32_t id = a.ids[i];
+  const uint64_t e = id < a.dec_n ? __ldg(a.dec + id) : ~0ull;
+  if (e == ~0ull) return;
+  const uint64_t pos = a.block_sums[blockIdx.x] + a.pos[i];
+  const uint64_t len = e & 0xFFFFFF;
+  const uint8_t* src = a.dec_bytes + (e >> 24);
+  for (uint64_t k = 0; k < len && pos + k < a.cap; ++k) a.out[pos + k] = __ldg(src + k);
+}
+
+__global__ void k_dec_rows(DecodeArgs a) {
+  const uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (r > a.n_rows) return;
+  const uint64_t t = a.tok_off[r] - a.tok_off[0];
+  const uint64_t b = t / kDecThreads;
+  a.out_off[r] = t >= a.n_ids ? a.block_sums[a.n_blocks] : a.block_sums[b] + a.pos[t];
+}
+
+}  // namespace
+
+void launch_decode(const DecodeArgs& a, cudaStream_t s) {
+  if (a.n_ids) {
+    k_dec_len<<<unsigned(a.n_blocks), kDecThreads, 0, s>>>(a);
+    k_dec_scan<<<1, 1024, 0, s>>>(a.block_sums, a.n_blocks);
+    k_dec_copy<<<unsigned(a.n_blocks), kDecThreads, 0, s>>>(a);
+  } else {
+    cudaMemsetAsync(a.block_sums, 0, 8, s);
+  }
+  k_dec_rows<<<unsigned((a.n_rows + 1 + 255) / 256), 256, 0, s>>>(a);
+}
+
+}  // namespace bbpe

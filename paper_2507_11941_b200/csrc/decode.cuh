@@ -1,0 +1,29 @@
+// decode.cuh -- device batch decode (decode.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bbpe {
+
+struct DecodeArgs {
+  const uint32_t* ids;       // n_ids token ids
+  const uint64_t* tok_off;   // n_rows + 1 row offsets into ids (relative to tok_off[0])
+  uint64_t n_rows;
+  uint64_t n_ids;
+  const uint64_t* dec;       // dec_n entries: byte start << 24 | length, ~0 = unknown id
+  uint64_t dec_n;
+  const uint8_t* dec_bytes;
+  uint64_t* pos;             // n_ids: byte offset of each token within its block of 256
+  uint64_t* block_sums;      // n_blocks + 1: block byte totals -> exclusive bases, total last
+  uint64_t n_blocks;
+  uint8_t* out;              // cap bytes
+  uint64_t cap;
+  uint64_t* out_off;         // n_rows + 1 row byte offsets
+  uint64_t* err;             // min index of an unknown id (~0 = none)
+};
+
+void launch_decode(const DecodeArgs& a, cudaStream_t s);
+
+}  // namespace bbpe

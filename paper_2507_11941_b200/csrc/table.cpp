@@ -518,6 +518,7 @@ void release_replicas(bbpe_table& t) {
     cudaSetDevice(dev);
     cudaFree(rep.base);
     if (rep.memo) cudaFree(rep.memo);
+    if (rep.dec) cudaFree(rep.dec);
   }
   cudaSetDevice(prev);
   t.replicas.clear();

@@ -404,3 +404,51 @@ def test_dedupe_is_results_neutral(gpt2, oracle_for, memo):
         want_ids, want_off = oracle_for("gpt2").encode_packed(d, o)
         assert np.array_equal(a[1], want_off) and np.array_equal(a[0], want_ids)
         assert np.array_equal(b[1], want_off) and np.array_equal(b[0], want_ids)
+
+
+def test_device_decode_round_trip(gpt2):
+    """Device decode inverts the device encode: lossless
+    round trip (acceptance_test.cpp:111-129) on Zipf text, random bytes and
+    empty rows; row byte offsets equal the input offsets."""
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 3000, 256, seed=31)
+    rng = np.random.default_rng(32)
+    rnd = rng.integers(0, 256, 100_000).astype(np.uint8)
+    roff = np.sort(np.concatenate([[0, 100_000], rng.integers(0, 100_000, 500)])).astype(np.uint64)
+    enc = bb.Encoder(0)
+    for d, o in ((data, off), (rnd, roff)):
+        ids, oo, _ = enc.encode_packed(gpt2, d, o)
+        b, bo = enc.decode_packed(gpt2, ids, oo)
+        assert np.array_equal(bo, o - o[0])
+        assert np.array_equal(b, d)
+
+
+def test_device_decode_matches_host_decode_and_errors(gpt2):
+    v = load_vectors("gpt2_text")
+    enc = bb.Encoder(0)
+    b, bo = enc.decode_packed(gpt2, v["ids"], v["out_offsets"])
+    for r in range(0, v["out_offsets"].size - 1, 7):
+        ids = v["ids"][int(v["out_offsets"][r]):int(v["out_offsets"][r + 1])]
+        assert bytes(b[int(bo[r]):int(bo[r + 1])]) == bb.decode(gpt2, bb.SpecialTokenSet(), ids)
+    # Unknown id: DecodeError naming the row and the index in the row (decode_batch).
+    ids = np.array([31373, 995, 13, 99999999, 5], np.uint32)
+    off = np.array([0, 2, 5], np.uint64)
+    with pytest.raises(bb.DecodeError, match=r"row 1: unknown token id 99999999 at index 1"):
+        enc.decode_packed(gpt2, ids, off)
+
+
+def test_device_decode_device_api(gpt2):
+    torch = pytest.importorskip("torch")
+    v = load_vectors("gpt2_random")
+    ids = torch.from_numpy(v["ids"].astype(np.int32)).cuda()
+    off = torch.from_numpy(v["out_offsets"].astype(np.int64)).cuda()
+    n = v["out_offsets"].size - 1
+    cap = int(v["offsets"][-1])
+    out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    oo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    tot = bb.Encoder(0).decode_device(gpt2, ids.data_ptr(), off.data_ptr(), n, int(v["ids"].size), out.data_ptr(),
+                                      cap, oo.data_ptr())
+    assert tot == cap
+    assert np.array_equal(out.cpu().numpy(), v["data"])
+    assert np.array_equal(oo.cpu().numpy().astype(np.uint64), v["offsets"])
