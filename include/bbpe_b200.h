@@ -166,6 +166,17 @@ int bbpe_decode_device(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* d_ids
                        size_t n_rows, uint64_t n_ids, uint8_t* d_out_bytes, uint64_t cap,
                        uint64_t* d_out_byte_offsets, uint64_t* total);
 
+/* ---- encode_batch's padded BatchEncoding on the device (
+ * batch.hpp:64-126) from device CSR ids: row r = [bos] + ids + [eos],
+ * right-truncated to max_len, pad_id elsewhere, u32 lengths, u8 mask.
+ * bos_id / eos_id = 0xFFFFFFFF: not added. Both calls are synchronous. ---- */
+/* Widest row (ids + add_bos + add_eos): the max_len encode_batch uses without limits. */
+int bbpe_batch_widest_device(bbpe_ctx* ctx, const uint64_t* d_tok_offsets, size_t n_rows, int add_bos,
+                             int add_eos, uint64_t* widest);
+int bbpe_pad_device(bbpe_ctx* ctx, const uint32_t* d_ids, const uint64_t* d_tok_offsets, size_t n_rows,
+                    uint32_t pad_id, uint32_t bos_id, uint32_t eos_id, uint64_t max_len, uint32_t* d_out_ids,
+                    uint32_t* d_lengths, uint8_t* d_mask, uint64_t* truncated_rows);
+
 /* ---- per-device encode contexts ---- */
 int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out);
 int bbpe_ctx_destroy(bbpe_ctx* ctx);

@@ -640,11 +640,67 @@ def encode_batch_csr(inputs: Sequence[Union[bytes, str]], table: MergeTable, spe
     return (np.concatenate(out) if out else np.zeros(0, np.uint32)), np.cumsum(lens).astype(np.uint64)
 
 
+def _encode_batch_device(rows: List[bytes], table: MergeTable, specials: SpecialTokenSet, config: BlockConfig,
+                         pad_id: int, add_bos: bool, add_eos: bool, enc: "Encoder",
+                         limits: Optional[BatchLimits]) -> BatchEncoding:
+    """Device epilogue: CSR encode, widest row and padding all
+    on the GPU (bbpe_encode_device, bbpe_batch_widest_device, bbpe_pad_device);
+    one copy of the padded batch back."""
+    import torch
+    dev = torch.device("cuda", enc.device)
+    data, offsets = pack_rows(rows)
+    n, total = len(rows), int(offsets[-1])
+    d_data = torch.from_numpy(data if data.flags.writeable else data.copy()).to(dev)
+    d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
+    d_ids = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    d_oo = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    enc.encode_device(table, d_data.data_ptr(), d_off.data_ptr(), n, total, d_ids.data_ptr(), d_oo.data_ptr(),
+                      sync=True)
+    widest = C.c_uint64()
+    _check(LIB.bbpe_batch_widest_device(enc.handle, C.c_void_p(d_oo.data_ptr()), n, int(add_bos), int(add_eos),
+                                        C.byref(widest)))
+    out = BatchEncoding(batch_size=n, pad_id=pad_id)
+    out.max_len = int(limits.max_len) if limits is not None and limits.max_len is not None else widest.value
+    L = out.max_len
+    t_ids = torch.empty(max(n * L, 1), dtype=torch.int32, device=dev)
+    t_mask = torch.empty(max(n * L, 1), dtype=torch.uint8, device=dev)
+    t_len = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    tr = C.c_uint64()
+    nid = 0xFFFFFFFF
+    _check(LIB.bbpe_pad_device(enc.handle, C.c_void_p(d_ids.data_ptr()), C.c_void_p(d_oo.data_ptr()), n, pad_id,
+                               specials.bos_id() if add_bos else nid, specials.eos_id() if add_eos else nid, L,
+                               C.c_void_p(t_ids.data_ptr()), C.c_void_p(t_len.data_ptr()),
+                               C.c_void_p(t_mask.data_ptr()), C.byref(tr)))
+    out.ids = t_ids[: n * L].cpu().numpy().view(np.uint32).copy()
+    out.mask = t_mask[: n * L].cpu().numpy().copy()
+    out.lengths = t_len[:n].cpu().numpy().view(np.uint32).copy()
+    out.truncated_rows = int(tr.value)
+    return out
+
+
 def encode_batch(inputs: Sequence[Union[bytes, str]], table: MergeTable, specials: SpecialTokenSet,
                  config: BlockConfig, pad_id: int, add_bos: bool = False, add_eos: bool = False,
-                 encoder: Optional[Encoder] = None, limits: Optional[BatchLimits] = None) -> BatchEncoding:
+                 encoder: Optional[Encoder] = None, limits: Optional[BatchLimits] = None,
+                 device_epilogue: Optional[bool] = None) -> BatchEncoding:
     """batch.hpp:64-126: rows encoded on the GPU, padded to max_len (or the fixed
-    limits.max_len with right truncation), u8 mask."""
+    limits.max_len with right truncation), u8 mask. With an empty special-token
+    set the padding runs on the device too (device_epilogue, default); with
+    specials the literal segments are re-stitched and padded on the host."""
+    config.validate()
+    if add_bos and specials.bos_id() is None:
+        raise UsageError("add_bos requires a bos entry in the special token set")
+    if add_eos and specials.eos_id() is None:
+        raise UsageError("add_eos requires an eos entry in the special token set")
+    # Special tokens are matched in the input text (split_specials), which
+    # happens on the host; without any, the whole batch stays on the device.
+    if device_epilogue is None:
+        device_epilogue = True
+    if device_epilogue and specials.empty():
+        enc = encoder or default_encoder()
+        if enc.config.block_size != config.block_size or enc.config.max_passes != config.max_passes:
+            enc.set_config(config=config)
+        rows = [r.encode() if isinstance(r, str) else bytes(r) for r in inputs]
+        return _encode_batch_device(rows, table, specials, config, pad_id, add_bos, add_eos, enc, limits)
     ids, off = encode_batch_csr(inputs, table, specials, config, add_bos, add_eos, encoder)
     n = len(inputs)
     lengths = (off[1:] - off[:-1]).astype(np.int64)

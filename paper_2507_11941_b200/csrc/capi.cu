@@ -22,6 +22,7 @@
 
 #include "bbpe_internal.h"
 #include "decode.cuh"
+#include "epilogue.cuh"
 #include "kernels.cuh"
 
 namespace bbpe {
@@ -189,6 +190,7 @@ struct bbpe_ctx {
   size_t h_errs_cap = 0;
   // Device decode scratch and host-API staging.
   DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff;
+  DevBuf pad_scalar;  // epilogue: widest row / truncated count
   DevBuf run_base;
 };
 
@@ -1036,6 +1038,52 @@ int bbpe_decode_batch(bbpe_ctx* c, const bbpe_table* t, const uint32_t* ids, con
   BBPE_CATCH
 }
 
+int bbpe_batch_widest_device(bbpe_ctx* c, const uint64_t* d_tok_offsets, size_t n_rows, int add_bos,
+                             int add_eos, uint64_t* widest) {
+  BBPE_TRY
+  if (!c || !d_tok_offsets || !widest) throw bbpe::usage_error("null argument");
+  DeviceGuard g(c->device);
+  c->pad_scalar.ensure(8);
+  bbpe::launch_row_max(d_tok_offsets, n_rows, uint32_t((add_bos ? 1 : 0) + (add_eos ? 1 : 0)),
+                       c->pad_scalar.as<unsigned long long>(), c->stream);
+  c->launches += n_rows ? 1 : 0;
+  ck(cudaMemcpyAsync(widest, c->pad_scalar.p, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "widest");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_pad_device(bbpe_ctx* c, const uint32_t* d_ids, const uint64_t* d_tok_offsets, size_t n_rows,
+                    uint32_t pad_id, uint32_t bos_id, uint32_t eos_id, uint64_t max_len, uint32_t* d_out_ids,
+                    uint32_t* d_lengths, uint8_t* d_mask, uint64_t* truncated_rows) {
+  BBPE_TRY
+  if (!c || !d_tok_offsets) throw bbpe::usage_error("null argument");
+  if (n_rows && (!d_lengths || (max_len && (!d_out_ids || !d_mask)))) throw bbpe::usage_error("null buffer");
+  DeviceGuard g(c->device);
+  ensure_plan(*c);
+  c->pad_scalar.ensure(8);
+  bbpe::PadArgs a{};
+  a.ids = d_ids;
+  a.off = d_tok_offsets;
+  a.n_rows = n_rows;
+  a.pad = pad_id;
+  a.bos = bos_id;
+  a.eos = eos_id;
+  a.max_len = max_len;
+  a.out_ids = d_out_ids;
+  a.lengths = d_lengths;
+  a.out_mask = d_mask;
+  a.truncated = c->pad_scalar.as<unsigned long long>();
+  bbpe::launch_pad(a, c->plan.sm_count, c->stream);
+  c->launches += n_rows ? (max_len ? 2 : 1) : 0;
+  uint64_t tr = 0;
+  ck(cudaMemcpyAsync(&tr, c->pad_scalar.p, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "pad");
+  if (truncated_rows) *truncated_rows = tr;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
 int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out) {
   BBPE_TRY
   if (!out) throw bbpe::usage_error("out is null");
@@ -1063,7 +1111,7 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaStreamSynchronize(c->stream);
     c->sc.release();
     for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_sums,
-                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff})
+                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar})
       b->release();
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);

@@ -452,3 +452,56 @@ def test_device_decode_device_api(gpt2):
     assert tot == cap
     assert np.array_equal(out.cpu().numpy(), v["data"])
     assert np.array_equal(oo.cpu().numpy().astype(np.uint64), v["offsets"])
+
+
+@pytest.mark.parametrize("max_len", [None, 0, 1, 17, 64])
+def test_device_epilogue_matches_host_padding(gpt2, max_len):
+    """encode_batch's padded BatchEncoding built on the device
+    equals the host padding of the same CSR (batch.hpp:98-125): widest or
+    fixed max_len with right truncation, pad ids, lengths, mask, truncated
+    row count; empty rows included."""
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    rng = np.random.default_rng(41)
+    lens = rng.integers(0, 400, 700)
+    lens[::50] = 0
+    data, off = synth.rows_lengths(gen, lens, seed=42)
+    rows = [bytes(data[int(off[i]):int(off[i + 1])]) for i in range(lens.size)]
+    cfg = bb.BlockConfig(256, None)
+    none = bb.SpecialTokenSet()
+    lim = bb.BatchLimits(max_len) if max_len is not None else None
+    d = bb.encode_batch(rows, gpt2, none, cfg, 7, limits=lim, device_epilogue=True)
+    h = bb.encode_batch(rows, gpt2, none, cfg, 7, limits=lim, device_epilogue=False)
+    assert d.max_len == h.max_len and d.truncated_rows == h.truncated_rows
+    assert np.array_equal(d.lengths, h.lengths)
+    assert np.array_equal(d.ids, h.ids) and np.array_equal(d.mask, h.mask)
+
+
+def test_pad_device_bos_eos(gpt2):
+    """bbpe_pad_device with BOS/EOS ids: [bos] + ids + [eos], truncation may
+    cut the EOS (batch.hpp:76-79, 100-104)."""
+    torch = pytest.importorskip("torch")
+    import ctypes as C
+    from paper_2507_11941_b200._lib import LIB
+    ids = np.arange(1, 11, dtype=np.uint32)
+    off = np.array([0, 3, 3, 10], np.uint64)
+    d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    enc = bb.Encoder(0)
+    w = C.c_uint64()
+    assert LIB.bbpe_batch_widest_device(enc.handle, C.c_void_p(d_off.data_ptr()), 3, 1, 1, C.byref(w)) == 0
+    assert w.value == 9
+    for L in (9, 5):
+        o = torch.empty(3 * L, dtype=torch.int32, device="cuda")
+        m = torch.empty(3 * L, dtype=torch.uint8, device="cuda")
+        ln = torch.empty(3, dtype=torch.int32, device="cuda")
+        tr = C.c_uint64()
+        assert LIB.bbpe_pad_device(enc.handle, C.c_void_p(d_ids.data_ptr()), C.c_void_p(d_off.data_ptr()), 3, 0,
+                                   100, 200, L, C.c_void_p(o.data_ptr()), C.c_void_p(ln.data_ptr()),
+                                   C.c_void_p(m.data_ptr()), C.byref(tr)) == 0
+        want = [[100, 1, 2, 3, 200], [100, 200], [100, 4, 5, 6, 7, 8, 9, 10, 200]]
+        want = [r[:L] + [0] * (L - len(r[:L])) for r in want]
+        assert o.cpu().numpy().reshape(3, L).tolist() == want
+        assert ln.cpu().numpy().tolist() == [min(5, L), 2, min(9, L)]
+        assert tr.value == (1 if L == 5 else 0)
+        assert m.cpu().numpy().reshape(3, L).sum(1).tolist() == [min(5, L), 2, min(9, L)]
