@@ -759,7 +759,7 @@ void ensure_memo(bbpe_ctx& c, const bbpe_table& t) {
     encode_wave(c, t, blob.data(), offs.data(), 0, cand.size(), ids.data(), 0, ids.size(), oo.data(),
                 nullptr, /*allow_memo=*/false);
     uint64_t cap = 16;
-    while (cap < cand.size() * 5 / 2) cap <<= 1;
+    while (cap < cand.size() * 8) cap <<= 1;  // load <= 1/8: a lookup resolves at its first slot
     mask = cap - 1;
     slots.assign(cap, MemoEntry{});
     for (size_t j = 0; j < cand.size(); ++j) {
