@@ -336,7 +336,6 @@ void enqueue_encode(bbpe_ctx& c, Scratch& sc, const bbpe_table& t, const uint8_t
   bbpe::EncodeArgs a = prepare_args(c, sc, d_bytes, d_offsets, n, total, d_out, d_out_off, s, err, base);
   a.narrow = t.narrow ? 1 : 0;
   a.use_memo = memo && dt.memo ? 1 : 0;
-  a.run_base = nullptr;
   // Per-kernel timing events (BBPE_NO_KERNEL_TIMING=1 disables them, e.g.
   // for stream capture into a CUDA graph).
   static const bool no_timing = std::getenv("BBPE_NO_KERNEL_TIMING") != nullptr;

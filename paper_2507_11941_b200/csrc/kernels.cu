@@ -16,13 +16,17 @@
 // merged by one lane each; longer pieces (and, with BBPE_ENGINE_BLOCK, whole
 // rows) by one CTA each with the reference's phase structure.
 //
-// Kernels (one stream, no host sync in between):
-//   k_tile_first  : row index of the first row starting at or after each tile
-//   k_pieces      : warp-per-tile piece split + lane-per-piece pass loops ->
-//                   tokens staged per tile (no ordering wait)
+// Kernels (one stream, no host sync in between; DESIGN.md §3):
+//   k_tile_first  : first row of each tile, row-start bitmap, offsets check/rebase
+//   k_pieces      : warp per tile: boundaries, piece list, single bytes and
+//                   piece-memo hits staged; merge / long records for the rest
+//   k_dedup       : (large batches) one owner per distinct merge piece
+//   k_merge       : lane-per-piece pass loops over the merge records (owners)
+//   k_refs        : (large batches) references copy their owner's tokens
 //   k_long_pieces : CTA-per-piece pass loop over the long pieces k_pieces found
 //                   (the paper's block engine; every row under BBPE_ENGINE_BLOCK)
-//   k_gather      : decoupled look-back over tile groups -> CSR ids + row offsets
+//   k_tile_scan   : tile token counts -> tile bases (decoupled look-back)
+//   k_gather      : staging compaction -> CSR ids + row offsets
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1316,7 +1320,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
   GatherSmem& G = s_g[threadIdx.x >> 5];
   const uint32_t* d2id = T.d2id;
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
-  const uint64_t rb = a.run_base ? *a.run_base : 0;
   // Tile metadata is prefetched one tile ahead; a tile's staged slots and row
   // offsets are all loaded before any is used (one round trip, not one per
   // 128-slot chunk).
@@ -1419,33 +1422,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
       const uint32_t lb = uint32_t(v >> 40);
       uint64_t lsum = 0;
       for (uint32_t li = 0; li < lb; ++li) lsum += LV.cnt(li);
-      a.out_offsets[s] = rb + tbase + compact_at(G, uint32_t(v & ((1ull << 40) - 1)), nslots, run) + lsum;
+      a.out_offsets[s] = tbase + compact_at(G, uint32_t(v & ((1ull << 40) - 1)), nslots, run) + lsum;
     }
     __syncwarp();
   }
 }
 
-__global__ void k_rebase_input(uint64_t* off, uint64_t n, uint64_t base) {
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i < n) off[i] -= base;
-}
 __global__ void k_advance_base(uint64_t* run_base, const uint64_t* wave_total) {
   *run_base += *wave_total;
 }
-__global__ void k_fill_offsets(uint64_t* out, uint64_t n, const uint64_t* run_base) {
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (i < n) out[i] = run_base ? *run_base : 0;
-}
-
 }  // namespace
 
-void launch_rebase_input(uint64_t* d_off, uint64_t n, uint64_t base, cudaStream_t stream) {
-  if (base == 0 || n == 0) return;
-  k_rebase_input<<<unsigned((n + 255) / 256), 256, 0, stream>>>(d_off, n, base);
-}
-void launch_advance_base(uint64_t* run_base, const uint64_t* wave_total, cudaStream_t stream) {
-  k_advance_base<<<1, 1, 0, stream>>>(run_base, wave_total);
-}
 // k_copy_out: one wave's results -> the caller's pinned buffers through their
 // device mappings: row offsets (wave-relative + *run_base) and ids [0, n) to
 // dst[*run_base, ...), clamped to cap; 16-byte stores to host memory after an
@@ -1479,11 +1466,6 @@ void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t
   k_copy_out<<<unsigned(std::max(sm_count, 1)), 256, 0, stream>>>(d_ids, mapped_out, d_wave_offsets, mapped_offsets,
                                                                    nr, run_base, cap);
   k_advance_base<<<1, 1, 0, stream>>>(run_base, d_wave_offsets + nr);
-}
-
-void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_base, cudaStream_t stream) {
-  if (n == 0) return;
-  k_fill_offsets<<<unsigned((n + 255) / 256), 256, 0, stream>>>(d_out_off, n, run_base);
 }
 
 size_t pieces_smem() { return sizeof(PieceSmem) * kWarpsPerCta; }

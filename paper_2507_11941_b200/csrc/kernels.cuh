@@ -71,7 +71,6 @@ struct EncodeArgs {
   uint64_t* status;         // look-back words of k_tile_scan's CTAs
   uint64_t num_groups;      // k_tile_scan CTAs
   uint64_t* tile_base;      // num_tiles + 1: first output token of each tile
-  const uint64_t* run_base; // optional: added to every row offset (pipelined waves)
   uint32_t* staging;        // num_tiles * kStage: each tile's short-piece tokens, in order
   uint32_t* tile_count;     // num_tiles: tokens produced by the tile (final after k_merge/k_long_pieces)
   uint32_t* tile_slots;     // num_tiles: staging slots the tile used (incl. reserved)
@@ -124,11 +123,6 @@ LaunchPlan plan_launch(int device);
 // ev (optional): BBPE_N_KERNELS + 1 events, before the first and after each kernel.
 int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, cudaStream_t stream,
                   cudaEvent_t* ev = nullptr);
-// Pipelined-wave helpers: subtract `base` from n input offsets; advance the
-// running output base by the wave's token total; fill n offsets with the base.
-void launch_rebase_input(uint64_t* d_off, uint64_t n, uint64_t base, cudaStream_t stream);
-void launch_advance_base(uint64_t* run_base, const uint64_t* wave_total, cudaStream_t stream);
-void launch_fill_offsets(uint64_t* d_out_off, uint64_t n, const uint64_t* run_base, cudaStream_t stream);
 // Copies one wave's results into the caller's device-mapped pinned buffers:
 // row offsets (wave-relative + *run_base) and ids at *run_base (clamped to
 // cap), then advances *run_base by the wave's token count.
