@@ -264,7 +264,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
     uint64_t slots = 4096;
     while (slots < total / 128) slots <<= 1;
     sc.dkey.ensure(slots * 16);
-    sc.dres.ensure(slots * 8);
+    sc.dres.ensure(slots * 32);
     a.dkey = sc.dkey.as<ulonglong2>();
     a.dres = sc.dres.as<uint64_t>();
     a.dmask = slots - 1;

@@ -526,8 +526,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         mleft -= nm;
       }
       const unsigned lm = __ballot_sync(kFull, lg);
-      if (lg) S.lk[nlong + __popc(lm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-      nlong += __popc(lm);
+      if (lm) {  // (rare)
+        if (lg) S.lk[nlong + __popc(lm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
+        nlong += __popc(lm);
+      }
       run += __shfl_sync(kFull, inc, 31);
     }
     if (lane == 0) S.cnt[npieces] = static_cast<uint16_t>(run);
@@ -1020,9 +1022,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
       }
       for (int i = n; i < len; ++i) dst[i] = kSentinel;
       if (len > n) atomicSub(&a.tile_count[start / kTile], uint32_t(len - n));
-      if (rslot) {  // owner of a dedupe slot: where its tokens are, for the references
+      if (rslot) {  // owner of a dedupe slot: its result for the references (DedupRes)
         const uint64_t at = (start / kTile) * kStage + ((rec >> 6) & 1023);
-        a.dres[rslot - 1] = at | (uint64_t(n) << 48);
+        uint32_t v[kInlineRes];
+#pragma unroll
+        for (int i = 0; i < kInlineRes; ++i) {
+          const uint32_t t = i < n ? uint32_t(tok[i][lane]) : 0u;
+          v[i] = d2id && i < n ? __ldg(d2id + t) : t;
+        }
+        ulonglong2* e = reinterpret_cast<ulonglong2*>(a.dres + 4 * uint64_t(rslot - 1));
+        e[0] = make_ulonglong2(at | (uint64_t(n) << 48), uint64_t(v[0]) | (uint64_t(v[1]) << 32));
+        e[1] = make_ulonglong2(uint64_t(v[2]) | (uint64_t(v[3]) << 32), uint64_t(v[4]) | (uint64_t(v[5]) << 32));
       }
       n = 0;
       continue;
@@ -1107,24 +1117,55 @@ __global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
 // record, copy from the owner's staging slots (k_merge left its count in the
 // record), kSentinel into the rest of the reserved slots, tile count adjusted.
 __global__ void __launch_bounds__(256) k_refs(EncodeArgs a) {
+  // Warp per 32 records: each lane loads one record and its owner's result,
+  // then the records are written out by half-warps, lane j writing slot j
+  // (coalesced stores into the reference's contiguous slots).
+  static_assert(kDedupMax < 16, "a half-warp covers a reference's slots");
   const uint64_t nrec = min((uint64_t)a.counters[CNT_MREC], a.mrec_cap);
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < nrec; i += stride) {
-    const ulonglong2 r = __ldcs(a.mrec + i);
-    if (r.x == ~0ull || !(r.x & kRefFlag)) continue;
-    const uint64_t d = __ldcg(a.dres + r.y);  // owner's staging index | count << 48
-    const uint64_t start = (r.x & ~kRefFlag) >> 16;
-    const int len = int(r.x & 63), cnt = int(d >> 48);
-    const uint32_t* src = a.staging + (d & ((1ull << 48) - 1));
-    uint32_t* dst = a.staging + (start / kTile) * kStage + ((r.x >> 6) & 1023);
-    uint32_t v[kDedupMax];
-#pragma unroll
-    for (int j = 0; j < kDedupMax; ++j)
-      if (j < cnt) v[j] = __ldcg(src + j);  // all loads in flight together
-#pragma unroll
-    for (int j = 0; j < kDedupMax; ++j)
-      if (j < len) dst[j] = j < cnt ? v[j] : kSentinel;
-    if (len > cnt) atomicSub(&a.tile_count[start / kTile], uint32_t(len - cnt));
+  const int lane = threadIdx.x & 31, h = lane >> 4, j = lane & 15;
+  const uint64_t wstride = uint64_t(gridDim.x) * (blockDim.x / 32) * 32;
+  for (uint64_t w0 = (blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5)) * 32; w0 < nrec; w0 += wstride) {
+    const uint64_t i = w0 + lane;
+    bool ref = false;
+    uint64_t hdr = 0;
+    ulonglong2 d0 = make_ulonglong2(0, 0), d1 = make_ulonglong2(0, 0);
+    if (i < nrec) {
+      const ulonglong2 r = __ldcs(a.mrec + i);
+      ref = r.x != ~0ull && (r.x & kRefFlag);
+      if (ref) {
+        hdr = r.x & ~kRefFlag;
+        const ulonglong2* de = reinterpret_cast<const ulonglong2*>(a.dres + 4 * r.y);
+        d0 = __ldcg(de);
+        d1 = __ldcg(de + 1);
+      }
+    }
+    const unsigned rm = __ballot_sync(kFull, ref);
+    for (int it = 0; it < 16; ++it) {
+      if (!((rm >> (2 * it)) & 3u)) continue;  // warp-uniform
+      const int src = 2 * it + h;
+      const uint64_t rh = __shfl_sync(kFull, hdr, src);
+      const uint64_t e0 = __shfl_sync(kFull, d0.x, src);
+      const uint64_t t01 = __shfl_sync(kFull, d0.y, src);
+      const uint64_t t23 = __shfl_sync(kFull, d1.x, src);
+      const uint64_t t45 = __shfl_sync(kFull, d1.y, src);
+      if (!((rm >> src) & 1u)) continue;
+      const int len = int(rh & 63), cnt = int(e0 >> 48);
+      const uint64_t start = rh >> 16;
+      uint32_t* dst = a.staging + (start / kTile) * kStage + ((rh >> 6) & 1023);
+      if (j < len) {
+        uint32_t v = kSentinel;
+        if (j < cnt) {
+          if (cnt <= kInlineRes) {
+            const uint64_t pair = j < 2 ? t01 : (j < 4 ? t23 : t45);
+            v = uint32_t(pair >> (32 * (j & 1)));
+          } else {
+            v = __ldcg(a.staging + (e0 & ((1ull << 48) - 1)) + j);
+          }
+        }
+        dst[j] = v;
+      }
+      if (j == 0 && len > cnt) atomicSub(&a.tile_count[start / kTile], uint32_t(len - cnt));
+    }
   }
 }
 

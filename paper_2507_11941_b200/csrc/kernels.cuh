@@ -27,6 +27,10 @@ constexpr uint32_t kSentinel = 0xFFFFFFFFu;  // staging slot left empty by a mer
 constexpr int kDedupMax = 15;       // longest merge piece deduplicated within a call
 constexpr uint64_t kDedupMinBytes = 64ull << 20;  // smaller batches: the dedupe pass costs more than it saves
 constexpr uint64_t kRefFlag = 1ull << 62;  // merge-record header: a reference (k_dedup)
+// DedupRes (32 bytes per dedupe slot): {staging index | count << 48, then up
+// to kInlineRes result tokens (original ids, u32)}; references copy inline
+// results without touching the owner's staging.
+constexpr int kInlineRes = 6;
 
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
@@ -86,7 +90,7 @@ struct EncodeArgs {
   // its record, listed in `owners` for k_merge); a record whose bytes are
   // already owned becomes a reference {hdr | kRefFlag, slot} for k_refs.
   ulonglong2* dkey;
-  uint64_t* dres;           // per slot, set by the owner in k_merge: staging index | count << 48
+  uint64_t* dres;           // 4 u64 per slot, set by the owner in k_merge (DedupRes)
   uint64_t dmask;
   uint64_t* owners;         // mrec_cap: record index | (slot + 1) << 32 for k_merge (CNT_OWNERS used)
   LongRec* lrec;            // lp_cap records (CNT_LREC used)
