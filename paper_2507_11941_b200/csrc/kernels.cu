@@ -240,15 +240,17 @@ __device__ __noinline__ uint64_t long_piece_length(const uint64_t* offsets, uint
 __device__ __forceinline__ int memo_match(const ulonglong2 lo, const ulonglong2 hi, const uint32_t* w,
                                           int len, uint32_t& r0, uint32_t& r1, uint32_t& nres) {
   const uint32_t meta = uint32_t(hi.x >> 32), elen = meta & 0xFF;
-  if (elen == 0) return 0;  // empty slot: miss
-  if (elen == uint32_t(len) && lo.x == (uint64_t(w[1]) << 32 | w[0]) && lo.y == (uint64_t(w[3]) << 32 | w[2]) &&
-      uint32_t(hi.x) == w[4]) {
+  // Branch-free compare: with a short-circuit the compiler sinks the load of
+  // `lo` behind the length test, i.e. a second dependent L2 round trip.
+  const bool hit = (elen == uint32_t(len)) & (lo.x == (uint64_t(w[1]) << 32 | w[0])) &
+                   (lo.y == (uint64_t(w[3]) << 32 | w[2])) & (uint32_t(hi.x) == w[4]);
+  if (hit) {
     nres = (meta >> 8) & 0xFF;
     r0 = uint32_t(hi.y);
     r1 = uint32_t(hi.y >> 32);
-    return 1;  // hit
+    return 1;
   }
-  return -1;  // occupied by another piece: keep probing
+  return elen == 0 ? 0 : -1;  // empty slot: miss; occupied by another piece: keep probing
 }
 
 // Everything by value: a pointer would force the caller's key into local memory.
@@ -847,16 +849,22 @@ __device__ __noinline__ uint32_t probe_overflow(const uint64_t* slots, uint64_t 
 
 template <bool K32>
 __device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTable& T) {
+  // Branch-free over the bucket (both halves of the 32-byte load are used
+  // unconditionally, so the compiler cannot sink one behind the other): a key
+  // occupies at most one slot and slots fill left to right, so the result is
+  // the matching slot, else no rank if the bucket has an empty slot, else the
+  // next bucket (rare at load <= 0.5).
   const uint64_t s[4] = {q.s01.x, q.s01.y, q.s23.x, q.s23.y};
+  uint32_t res = kNoRank;
+  bool any_empty = false;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (s[j] == kEmptySlot) return kNoRank;
-    if (K32) {
-      if (uint32_t(s[j] >> 32) == uint32_t(q.key)) return uint32_t(s[j]);
-    } else {
-      if ((s[j] >> T.rank_bits) == q.key) return static_cast<uint32_t>(s[j] & ((1ull << T.rank_bits) - 1));
-    }
+  for (int j = 3; j >= 0; --j) {
+    const bool hit = K32 ? (uint32_t(s[j] >> 32) == uint32_t(q.key)) : ((s[j] >> T.rank_bits) == q.key);
+    const uint32_t v = K32 ? uint32_t(s[j]) : static_cast<uint32_t>(s[j] & ((1ull << T.rank_bits) - 1));
+    res = hit ? v : res;
+    any_empty |= s[j] == kEmptySlot;
   }
+  if (res != kNoRank || any_empty) return res;
   return probe_overflow<K32>(T.slots, T.bucket_mask, T.rank_bits, q.key, probe_bucket<K32>(T, q.key));
 }
 
