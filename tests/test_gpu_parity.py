@@ -505,3 +505,37 @@ def test_pad_device_bos_eos(gpt2):
         assert ln.cpu().numpy().tolist() == [min(5, L), 2, min(9, L)]
         assert tr.value == (1 if L == 5 else 0)
         assert m.cpu().numpy().reshape(3, L).sum(1).tolist() == [min(5, L), 2, min(9, L)]
+
+
+@pytest.mark.parametrize("cfg", [3, 5])
+def test_full_size_long_row_configs(gpt2, cfg):
+    """BASELINE configs 3 (16,384 rows of 8-64 KiB, 604 MB) and 5 (log-uniform
+    128 B-64 KiB, 1 GB here): full-size encode through the pipelined host API,
+    device-resident encode agrees, device decode round trip is lossless, and
+    sampled long rows equal the oracle (heap engine = block engine on GPT-2)."""
+    torch = pytest.importorskip("torch")
+    from oracle.oracle import CRestatement
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off, _ = synth.config_rows(gen, cfg, scale=1.0 if cfg == 3 else 1 / 16)
+    e = bb.Encoder(0)
+    ids, oo, st = e.encode_packed(gpt2, data, off)
+    assert st["waves"] > 1
+    n, total = off.size - 1, int(off[-1])
+    d_data = torch.from_numpy(data).cuda()
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    d_ids = torch.empty(total, dtype=torch.int32, device="cuda")
+    d_oo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    e.encode_device(gpt2, d_data.data_ptr(), d_off.data_ptr(), n, total, d_ids.data_ptr(), d_oo.data_ptr(), sync=True)
+    assert np.array_equal(d_oo.cpu().numpy().view(np.uint64), oo)
+    assert torch.equal(d_ids[: int(oo[-1])].cpu(), torch.from_numpy(ids.view(np.int32)))
+    back = torch.empty(total, dtype=torch.uint8, device="cuda")
+    boff = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    assert e.decode_device(gpt2, d_ids.data_ptr(), d_oo.data_ptr(), n, int(oo[-1]), back.data_ptr(), total,
+                           boff.data_ptr()) == total
+    assert torch.equal(back, d_data) and torch.equal(boff, d_off)
+    _, _, _, m4 = gpt2.export()
+    orc = CRestatement(m4, [gpt2.byte_token(b) for b in range(256)])
+    for r in np.random.default_rng(cfg).integers(0, n, 12):
+        s = data[int(off[r]):int(off[r + 1])].tobytes()
+        assert ids[int(oo[r]):int(oo[r + 1])].tolist() == orc.heap_bpe(orc.initial(s))
