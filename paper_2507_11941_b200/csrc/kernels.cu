@@ -1330,11 +1330,11 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(EncodeArgs a) {
 // tile's long pieces (rare) at their slot positions, and resolves the row
 // offsets written by k_pieces. The compacted prefix of every 4-slot group is
 // kept in shared memory for the row offsets.
-constexpr int kStageVec = kStage / 4;
+constexpr int kStageIt = (kStage + 31) / 32;  // 32-slot steps per tile
 constexpr int kLongCache = kTile / (kLmax + 1) + 2;  // long pieces of a k_pieces tile
 struct GatherSmem {
-  uint16_t pre[kStageVec + 1];  // valid slots before 4-slot group v
-  uint8_t msk[kStageVec + 1];   // valid-slot mask of group v
+  uint16_t pre[kStageIt + 1];   // valid slots before 32-slot step j
+  uint32_t bal[kStageIt + 1];   // valid-slot ballot of step j
   uint32_t lsp[kLongCache];     // long pieces: slot position
   uint32_t lcnt[kLongCache];    // long pieces: token count
 };
@@ -1349,12 +1349,11 @@ struct LongView {
     return n <= kLongCache ? G.lcnt[i] : __ldcg(&r[i].count);
   }
 };
-static_assert(kStage % 4 == 0, "staging groups");
 
 __device__ __forceinline__ uint32_t compact_at(const GatherSmem& G, uint32_t slot, uint32_t nslots,
                                                uint32_t total) {
   if (slot >= nslots) return total;
-  return G.pre[slot >> 2] + __popc(G.msk[slot >> 2] & ((1u << (slot & 3)) - 1u));
+  return G.pre[slot >> 5] + __popc(G.bal[slot >> 5] & ((1u << (slot & 31)) - 1u));
 }
 
 #ifndef BBPE_GATHER_MINB
@@ -1389,15 +1388,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
     const uint64_t tbase = m_tb, rec = m_rec, s0 = m_s0, s1 = m_s1;
     const uint32_t nslots = m_ns;
     meta(t + nwarps);
-    const uint4* stage = reinterpret_cast<const uint4*>(a.staging + t * kStage);
+    const uint32_t* stage = a.staging + t * kStage;
     uint32_t* out = a.out_ids + tbase;
-    constexpr int kVecPerLane = (kStageVec + 31) / 32;
-    const uint32_t nvec = (nslots + 3) / 4;
-    uint4 xs[kVecPerLane];
+    uint32_t xs[kStageIt];
 #pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
+    for (int j = 0; j < kStageIt; ++j) {
       const uint32_t v = 32 * j + lane;
-      xs[j] = v < nvec ? __ldcs(stage + v) : make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+      xs[j] = v < nslots ? __ldcs(stage + v) : kSentinel;
     }
     uint64_t roff = 0;
     if (s0 + lane < s1 && s0 + lane <= a.n_rows) roff = __ldcg(a.out_offsets + s0 + lane);
@@ -1417,37 +1414,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
       }
       __syncwarp();
     }
-    // Staged slots, 4 per lane per step: compaction by warp scan.
+    // Staged slots, one per lane per step: compaction by ballot.
     uint32_t run = 0;
 #pragma unroll
-    for (int j = 0; j < kVecPerLane; ++j) {
-      if (32u * j >= nvec) break;
-      const uint32_t v = 32 * j + lane;
-      const uint32_t e[4] = {xs[j].x, xs[j].y, xs[j].z, xs[j].w};
-      uint32_t m = 0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (e[i] != kSentinel && 4 * v + i < nslots) m |= 1u << i;
-      const uint32_t c = __popc(m);
-      const uint32_t inc = warp_incl_sum(c, lane);
-      uint32_t pos = run + inc - c;
-      if (v < nvec) {
-        G.pre[v] = static_cast<uint16_t>(pos);
-        G.msk[v] = static_cast<uint8_t>(m);
+    for (int j = 0; j < kStageIt; ++j) {
+      if (32u * j >= nslots) break;
+      const bool valid = xs[j] != kSentinel;
+      const uint32_t bal = __ballot_sync(kFull, valid);
+      if (lane == 0) {
+        G.pre[j] = static_cast<uint16_t>(run);
+        G.bal[j] = bal;
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (m & (1u << i)) {
-          uint32_t o = pos;
-          if (nl) {  // tokens after the long pieces that precede this slot
-            const uint32_t slot = 4 * v + i;
-            for (uint32_t li = 0; li < nl && LV.sp(li) <= slot; ++li) o += LV.cnt(li);
-          }
-          __stcs(out + o, e[i]);
-          ++pos;
+      if (valid) {
+        uint32_t o = run + __popc(bal & lanemask_lt(lane));
+        if (nl) {  // tokens after the long pieces that precede this slot
+          const uint32_t slot = 32 * j + lane;
+          for (uint32_t li = 0; li < nl && LV.sp(li) <= slot; ++li) o += LV.cnt(li);
         }
+        __stcs(out + o, xs[j]);
       }
-      run += __shfl_sync(kFull, inc, 31);
+      run += __popc(bal);
     }
     __syncwarp();
     if (nl) {  // long pieces' tokens (rare path)
