@@ -466,71 +466,89 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     }
     __syncwarp();
 
-    // (3) Resolve 32 pieces per round.
+    // (3) Resolve 64 pieces per round: lane l takes the adjacent pieces
+    // k0 + 2l and k0 + 2l + 1 (two memo lookups in flight per lane, one slot
+    // scan per 64 pieces).
+    constexpr int PPL = 2;
     uint32_t* stage = a.staging + tile * kStage;
     uint32_t run = 0, nlong = 0;
-    for (int k0 = 0; k0 < npieces; k0 += 32) {
-      const int k = k0 + lane;
-      int len = 0, q = 0;
-      uint32_t c = 0, r0 = 0, r1 = 0;
-      bool merge = false, lg = false;
-      if (k < npieces) {
-        q = S.plist[k];
-        len = S.plist[k + 1] - q;
-        if (len > kLmax) {
-          lg = true;  // long: k_long_pieces, no staging slots
-        } else if (len == 1) {
-          c = 1;
-          r0 = s_lo[wb[q + 16]];
-        } else {
-          uint32_t nres = 0;
-          if (a.use_memo && len <= kMemoMaxLen && memo_lookup(T, ww, q + 16, len, r0, r1, nres)) {
-            c = nres;
+    for (int k0 = 0; k0 < npieces; k0 += 32 * PPL) {
+      int len[PPL], q[PPL];
+      uint32_t c[PPL], r0[PPL], r1[PPL];
+      bool merge[PPL], lg[PPL];
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) {
+        const int k = k0 + PPL * lane + u;
+        len[u] = 0;
+        q[u] = 0;
+        c[u] = r0[u] = r1[u] = 0;
+        merge[u] = lg[u] = false;
+        if (k < npieces) {
+          q[u] = S.plist[k];
+          len[u] = S.plist[k + 1] - q[u];
+          if (len[u] > kLmax) {
+            lg[u] = true;  // long: k_long_pieces, no staging slots
+          } else if (len[u] == 1) {
+            c[u] = 1;
+            r0[u] = s_lo[wb[q[u] + 16]];
           } else {
-            merge = true;  // k_merge fills the `len` reserved slots
-            c = uint32_t(len);
+            uint32_t nres = 0;
+            if (a.use_memo && len[u] <= kMemoMaxLen && memo_lookup(T, ww, q[u] + 16, len[u], r0[u], r1[u], nres)) {
+              c[u] = nres;
+            } else {
+              merge[u] = true;  // k_merge fills the `len` reserved slots
+              c[u] = uint32_t(len[u]);
+            }
           }
         }
       }
-      // The piece's first 8 bytes ride in its merge record (window byte q+16).
-      uint64_t b8 = 0;
-      if (merge) {
-        const int st = q + 16, wa = st >> 2;
-        const uint32_t sh = uint32_t(st & 3) * 8;
-        const uint32_t x0 = ww[wa], x1 = ww[wa + 1], x2 = ww[wa + 2];
-        b8 = uint64_t(__funnelshift_r(x0, x1, sh)) | (uint64_t(__funnelshift_r(x1, x2, sh)) << 32);
+      const uint32_t cl = c[0] + c[1];
+      const uint32_t inc = warp_incl_sum(cl, lane);
+      uint32_t slot[PPL];
+      slot[0] = run + inc - cl;
+      slot[1] = slot[0] + c[0];
+      const unsigned mm0 = __ballot_sync(kFull, merge[0]), mm1 = __ballot_sync(kFull, merge[1]);
+      const unsigned lm0 = __ballot_sync(kFull, lg[0]), lm1 = __ballot_sync(kFull, lg[1]);
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) {
+        const int k = k0 + PPL * lane + u;
+        if (k < npieces) S.cnt[k] = static_cast<uint16_t>(slot[u]);
+        if (!merge[u] && c[u]) {
+          stage[slot[u]] = r0[u];
+          if (c[u] > 1) stage[slot[u] + 1] = r1[u];
+        }
       }
-      const uint32_t inc = warp_incl_sum(c, lane);
-      const uint32_t slot = run + inc - c;
-      if (k < npieces) S.cnt[k] = static_cast<uint16_t>(slot);
-      if (!merge && c) {
-        stage[slot] = r0;
-        if (c > 1) stage[slot + 1] = r1;
-      }
-      const unsigned mm = __ballot_sync(kFull, merge);
-      if (mm) {
-        const uint32_t nm = __popc(mm);
+      if (mm0 | mm1) {
+        const uint32_t n0 = __popc(mm0), nm = n0 + __popc(mm1);
         if (nm > mleft) {  // new chunk of merge records; the old chunk's tail becomes holes
           for (uint32_t i = lane; i < mleft; i += 32)
             if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = make_ulonglong2(~0ull, 0);
-          uint32_t c0 = 0;
-          if (lane == 0) c0 = atomicAdd(&a.counters[CNT_MREC], uint32_t(kMrecChunk));
-          mbase = __shfl_sync(kFull, c0, 0);
+          uint32_t cc = 0;
+          if (lane == 0) cc = atomicAdd(&a.counters[CNT_MREC], uint32_t(kMrecChunk));
+          mbase = __shfl_sync(kFull, cc, 0);
           mleft = kMrecChunk;
         }
-        if (merge) {
-          // The piece's first 8 bytes ride in the record (k_merge needs no
-          // dependent load for pieces of <= 8 bytes).
-          const uint64_t at = mbase + __popc(mm & lanemask_lt(lane));
-          if (at < a.mrec_cap) a.mrec[at] = make_ulonglong2(pack_mrec(b0 + q, slot, uint32_t(len)), b8);
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          if (merge[u]) {
+            // The piece's first 8 bytes ride in its record (k_merge needs no
+            // dependent load for pieces of <= 8 bytes); window byte q+16.
+            const int st = q[u] + 16, wa = st >> 2;
+            const uint32_t sh = uint32_t(st & 3) * 8;
+            const uint32_t x0 = ww[wa], x1 = ww[wa + 1], x2 = ww[wa + 2];
+            const uint64_t b8 = uint64_t(__funnelshift_r(x0, x1, sh)) | (uint64_t(__funnelshift_r(x1, x2, sh)) << 32);
+            const uint64_t at = mbase + (u ? n0 : 0) + __popc((u ? mm1 : mm0) & lanemask_lt(lane));
+            if (at < a.mrec_cap) a.mrec[at] = make_ulonglong2(pack_mrec(b0 + q[u], slot[u], uint32_t(len[u])), b8);
+          }
         }
         mbase += nm;
         mleft -= nm;
       }
-      const unsigned lm = __ballot_sync(kFull, lg);
-      if (lm) {  // (rare)
-        if (lg) S.lk[nlong + __popc(lm & lanemask_lt(lane))] = static_cast<uint16_t>(k);
-        nlong += __popc(lm);
+      if (lm0 | lm1) {  // (rare) long pieces, listed in piece order
+        const uint32_t before = nlong + __popc(lm0 & lanemask_lt(lane)) + __popc(lm1 & lanemask_lt(lane));
+        if (lg[0]) S.lk[before] = static_cast<uint16_t>(k0 + PPL * lane);
+        if (lg[1]) S.lk[before + (lg[0] ? 1 : 0)] = static_cast<uint16_t>(k0 + PPL * lane + 1);
+        nlong += __popc(lm0) + __popc(lm1);
       }
       run += __shfl_sync(kFull, inc, 31);
     }
