@@ -329,6 +329,9 @@ __device__ __forceinline__ uint64_t dedup_claim(ulonglong2* dkey, uint64_t dmask
 #ifndef BBPE_PIECES_MINB
 #define BBPE_PIECES_MINB 4
 #endif
+#ifndef BBPE_PIECES_PER_LANE
+#define BBPE_PIECES_PER_LANE 2
+#endif
 // k_pieces: warp per 512-byte tile, persistent over tiles by ticket, the next
 // tile's window and row bits in flight (cp.async) while the current one is
 // processed.
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     // (3) Resolve 64 pieces per round: lane l takes the adjacent pieces
     // k0 + 2l and k0 + 2l + 1 (two memo lookups in flight per lane, one slot
     // scan per 64 pieces).
-    constexpr int PPL = 2;
+    constexpr int PPL = BBPE_PIECES_PER_LANE;
     uint32_t* stage = a.staging + tile * kStage;
     uint32_t run = 0, nlong = 0;
     for (int k0 = 0; k0 < npieces; k0 += 32 * PPL) {
@@ -502,13 +505,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
           }
         }
       }
-      const uint32_t cl = c[0] + c[1];
+      uint32_t cl = 0;
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) cl += c[u];
       const uint32_t inc = warp_incl_sum(cl, lane);
       uint32_t slot[PPL];
-      slot[0] = run + inc - cl;
-      slot[1] = slot[0] + c[0];
-      const unsigned mm0 = __ballot_sync(kFull, merge[0]), mm1 = __ballot_sync(kFull, merge[1]);
-      const unsigned lm0 = __ballot_sync(kFull, lg[0]), lm1 = __ballot_sync(kFull, lg[1]);
+      unsigned mmu[PPL], lmu[PPL], mm_any = 0, lm_any = 0;
+#pragma unroll
+      for (int u = 0; u < PPL; ++u) {
+        slot[u] = (u ? slot[u - 1] + c[u - 1] : run + inc - cl);
+        mmu[u] = __ballot_sync(kFull, merge[u]);
+        lmu[u] = __ballot_sync(kFull, lg[u]);
+        mm_any |= mmu[u];
+        lm_any |= lmu[u];
+      }
 #pragma unroll
       for (int u = 0; u < PPL; ++u) {
         const int k = k0 + PPL * lane + u;
@@ -518,8 +528,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
           if (c[u] > 1) stage[slot[u] + 1] = r1[u];
         }
       }
-      if (mm0 | mm1) {
-        const uint32_t n0 = __popc(mm0), nm = n0 + __popc(mm1);
+      if (mm_any) {
+        uint32_t nm = 0;
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) nm += __popc(mmu[u]);
         if (nm > mleft) {  // new chunk of merge records; the old chunk's tail becomes holes
           for (uint32_t i = lane; i < mleft; i += 32)
             if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = make_ulonglong2(~0ull, 0);
@@ -528,6 +540,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
           mbase = __shfl_sync(kFull, cc, 0);
           mleft = kMrecChunk;
         }
+        uint32_t before_u = 0;  // merges of the earlier piece positions, all lanes
 #pragma unroll
         for (int u = 0; u < PPL; ++u) {
           if (merge[u]) {
@@ -537,18 +550,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
             const uint32_t sh = uint32_t(st & 3) * 8;
             const uint32_t x0 = ww[wa], x1 = ww[wa + 1], x2 = ww[wa + 2];
             const uint64_t b8 = uint64_t(__funnelshift_r(x0, x1, sh)) | (uint64_t(__funnelshift_r(x1, x2, sh)) << 32);
-            const uint64_t at = mbase + (u ? n0 : 0) + __popc((u ? mm1 : mm0) & lanemask_lt(lane));
+            const uint64_t at = mbase + before_u + __popc(mmu[u] & lanemask_lt(lane));
             if (at < a.mrec_cap) a.mrec[at] = make_ulonglong2(pack_mrec(b0 + q[u], slot[u], uint32_t(len[u])), b8);
           }
+          before_u += __popc(mmu[u]);
         }
         mbase += nm;
         mleft -= nm;
       }
-      if (lm0 | lm1) {  // (rare) long pieces, listed in piece order
-        const uint32_t before = nlong + __popc(lm0 & lanemask_lt(lane)) + __popc(lm1 & lanemask_lt(lane));
-        if (lg[0]) S.lk[before] = static_cast<uint16_t>(k0 + PPL * lane);
-        if (lg[1]) S.lk[before + (lg[0] ? 1 : 0)] = static_cast<uint16_t>(k0 + PPL * lane + 1);
-        nlong += __popc(lm0) + __popc(lm1);
+      if (lm_any) {  // (rare) long pieces, listed in piece order
+        uint32_t before = nlong;
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) before += __popc(lmu[u] & lanemask_lt(lane));
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) {
+          if (lg[u]) S.lk[before++] = static_cast<uint16_t>(k0 + PPL * lane + u);
+          nlong += __popc(lmu[u]);
+        }
       }
       run += __shfl_sync(kFull, inc, 31);
     }
