@@ -6,6 +6,7 @@ usage: python profiles/summarize.py <report.ncu-rep> <out-prefix> [kernels.cu]
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -61,8 +62,8 @@ with open(out + ".txt", "w") as f:
     cs = ncu("--page", "source", "--csv", "--print-source=cuda,sass")
     tmp = out + ".source.csv.tmp"
     open(tmp, "w").write(cs)
-    r = subprocess.run([sys.executable, "profiles/ncu_lines.py", tmp, "25"], capture_output=True, text=True)
-    f.write(r.stdout)
-    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, os.path.join(here, "ncu_lines.py"), tmp, "25"], capture_output=True, text=True)
+    f.write(r.stdout or r.stderr)
     os.remove(tmp)
 print(open(out + ".txt").read())
