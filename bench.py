@@ -65,6 +65,7 @@ class ClockSampler:
             pynvml.nvmlInit()
             self._nv = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))  # ~50 ms: once
         except Exception:
             self._nv = None
             self.source = "nvidia-smi"
@@ -83,8 +84,7 @@ class ClockSampler:
             try:
                 if self._nv:
                     nv, h = self._nv, self._h
-                    self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
-                                         float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                    self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), self._max,
                                          int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
                 else:
                     self.samples.append(self._sample_smi())
