@@ -456,9 +456,43 @@ inline std::string decode(const MergeTable& table, const SpecialTokenSet& specia
   return out;
 }
 
+// decode_batch (batch.hpp:128-154). With an Encoder, rows without special
+// ids (or with skip_specials) decode on its GPU (bbpe_decode_batch, SURVEY
+// §8f(2)); the result and the row-tagged DecodeError are the same.
 inline std::vector<std::string> decode_batch(const BatchEncoding& enc, const MergeTable& table,
-                                             const SpecialTokenSet& specials, bool skip_specials) {
+                                             const SpecialTokenSet& specials, bool skip_specials,
+                                             Encoder* gpu = nullptr) {
   std::vector<std::string> out(enc.batch_size);
+  if (gpu) {
+    std::vector<std::uint32_t> ids;
+    std::vector<std::uint64_t> off{0};
+    bool host_only = false;
+    for (std::size_t r = 0; r < enc.batch_size && !host_only; ++r) {
+      for (TokenId id : enc.row(r)) {
+        if (specials.contains_id(id)) {
+          if (skip_specials) continue;
+          host_only = true;  // special bytes are not table tokens
+          break;
+        }
+        ids.push_back(id);
+      }
+      off.push_back(ids.size());
+    }
+    if (!host_only) {
+      // First call sizes the output (cap 0), second fills it.
+      std::vector<std::uint8_t> bytes;
+      std::vector<std::uint64_t> boff(enc.batch_size + 1);
+      std::uint64_t total = 0;
+      detail::check(bbpe_decode_batch(gpu->handle(), table.handle(), ids.data(), off.data(), enc.batch_size,
+                                      nullptr, 0, boff.data(), &total));
+      bytes.resize(std::max<std::uint64_t>(total, 1));
+      detail::check(bbpe_decode_batch(gpu->handle(), table.handle(), ids.data(), off.data(), enc.batch_size,
+                                      bytes.data(), total, boff.data(), &total));
+      for (std::size_t r = 0; r < enc.batch_size; ++r)
+        out[r].assign(reinterpret_cast<const char*>(bytes.data()) + boff[r], boff[r + 1] - boff[r]);
+      return out;
+    }
+  }
   for (std::size_t r = 0; r < enc.batch_size; ++r) {
     TokenSeq ids = enc.row(r);
     if (skip_specials) {

@@ -60,6 +60,10 @@ int main(int argc, char** argv) {
   EXPECT((bb::encode_single("hi<|endoftext|>", gpt2, sp, cfg) == bb::TokenSeq{5303, 50256}));
   auto e5 = bb::encode_batch({"hello world", "...."}, gpt2, sp, cfg, 50256, true, true);
   EXPECT((bb::decode_batch(e5, gpt2, sp, true) == std::vector<std::string>{"hello world", "...."}));
+  bb::Encoder gpu0(0);  // decode_batch on the device
+  EXPECT((bb::decode_batch(e5, gpt2, sp, true, &gpu0) == std::vector<std::string>{"hello world", "...."}));
+  auto e6 = bb::encode_batch({"hello world", "", "....", "\xff" "ab"}, gpt2, none, cfg, 0, false, false, &gpu0);
+  EXPECT((bb::decode_batch(e6, gpt2, none, false, &gpu0) == bb::decode_batch(e6, gpt2, none, false)));
 
   // block_bpe with a PassTrace: 64 x "ab" collapses in 7 passes (test_block_engine.cpp:165-185)
   std::vector<std::pair<bb::TokenId, std::string>> dt{{0, "a"}, {1, "b"}, {3, "ab"}};
