@@ -122,6 +122,7 @@ struct WaveSet {
   DevBuf in_bytes, in_offsets, out_ids, out_offsets, err;
   Scratch sc;
   cudaStream_t stream = nullptr;
+  cudaGraphExec_t exec = nullptr;  // the wave's kernels as a CUDA graph (updated per wave)
   uint64_t* h_off = nullptr;  // pinned: the wave's CSR offsets
   uint64_t* h_rel = nullptr;  // pinned: the wave's input offsets, rebased
   uint64_t* h_err = nullptr;  // pinned: error slots
@@ -147,6 +148,8 @@ struct WaveSet {
   void release() {
     for (DevBuf* b : {&in_bytes, &in_offsets, &out_ids, &out_offsets, &err}) b->release();
     sc.release();
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
     if (stream) cudaStreamDestroy(stream);
     stream = nullptr;
     if (h_off) cudaFreeHost(h_off);
@@ -590,6 +593,19 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     ck(cudaStreamWaitEvent(c.h2d_stream, tl0, 0), "wait");
   }
 
+  static const bool use_graphs = [] {
+    const char* v = std::getenv("BBPE_WAVE_GRAPHS");
+    return !(v && std::string(v) == "0");
+  }();
+  if (use_graphs) {  // size every set's scratch for the largest wave before any capture
+    table_on_device(t, c.device);
+    ensure_plan(c);
+    for (WaveSet& w : c.sets)
+      prepare_args(c, w.sc, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), max_rows,
+                   std::max<uint64_t>(max_bytes, 1), w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), w.stream,
+                   w.err.as<uint64_t>(), 1);
+  }
+
   auto launch = [&](size_t k) {
     WaveSet& w = c.sets[k % K];
     // Input buffers are free once the wave K back has been encoded.
@@ -610,9 +626,40 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
     if (w.used) ck(cudaStreamWaitEvent(w.stream, w.d2h_done, 0), "wait");
     w.used = true;
     tl_rec(k, 2, w.stream);
-    enqueue_encode(c, w.sc, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
-                   w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), w.stream, true, w.err.as<uint64_t>(),
-                   /*timed=*/false, base);
+    if (use_graphs) {
+      // One graph launch per wave instead of ~12 commands: under saturated
+      // PCIe every command the GPU front end fetches costs tens of us. The
+      // set's executable graph is updated in place (launches in flight keep
+      // their parameters); scratch was sized for the largest wave up front,
+      // so nothing allocates during capture.
+      cudaGraph_t g = nullptr;
+      ck(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+      try {
+        enqueue_encode(c, w.sc, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
+                       w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), w.stream, true, w.err.as<uint64_t>(),
+                       /*timed=*/false, base);
+      } catch (...) {
+        cudaStreamEndCapture(w.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      ck(cudaStreamEndCapture(w.stream, &g), "end capture");
+      if (w.exec) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(w.exec, g, &info) != cudaSuccess) {
+          cudaGetLastError();
+          cudaGraphExecDestroy(w.exec);
+          w.exec = nullptr;
+        }
+      }
+      if (!w.exec) ck(cudaGraphInstantiate(&w.exec, g, 0), "graph instantiate");
+      cudaGraphDestroy(g);
+      ck(cudaGraphLaunch(w.exec, w.stream), "graph launch");
+    } else {
+      enqueue_encode(c, w.sc, t, w.in_bytes.as<uint8_t>(), w.in_offsets.as<uint64_t>(), nr, tot,
+                     w.out_ids.as<uint32_t>(), w.out_offsets.as<uint64_t>(), w.stream, true, w.err.as<uint64_t>(),
+                     /*timed=*/false, base);
+    }
     ck(cudaEventRecord(w.comp_done, w.stream), "event");
     tl_rec(k, 3, w.stream);
     if (async) {
