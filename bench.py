@@ -335,6 +335,49 @@ def main():
                   "tokens_per_s": ntok / (d_ms / 1e3), "timing": "wall clock of the synchronous call",
                   "round_trip": "bit-exact"}
 
+    # ---- device padded BatchEncoding of the step's output ----
+    epilogue = None
+    if args.engine == "pieces":
+        import ctypes as C
+        from paper_2507_11941_b200._lib import LIB
+        w = C.c_uint64()
+        assert LIB.bbpe_batch_widest_device(enc.handle, C.c_void_p(d_oo.data_ptr()), n, 0, 0, C.byref(w)) == 0
+        L = int(w.value)
+        p_ids = torch.empty(max(n * L, 1), dtype=torch.int32, device="cuda")
+        p_mask = torch.empty(max(n * L, 1), dtype=torch.uint8, device="cuda")
+        p_len = torch.empty(max(n, 1), dtype=torch.int32, device="cuda")
+        tr = C.c_uint64()
+
+        def pad():
+            assert LIB.bbpe_pad_device(enc.handle, C.c_void_p(d_ids.data_ptr()), C.c_void_p(d_oo.data_ptr()), n, 0,
+                                       0xFFFFFFFF, 0xFFFFFFFF, L, C.c_void_p(p_ids.data_ptr()),
+                                       C.c_void_p(p_len.data_ptr()), C.c_void_p(p_mask.data_ptr()), C.byref(tr)) == 0
+        pad()
+        assert int(p_len.sum().item()) == ntok
+        times = []
+        for _ in range(max(3, args.steps // 2)):
+            t0 = time.perf_counter()
+            pad()
+            times.append(time.perf_counter() - t0)
+        p_ms = float(np.median(times)) * 1e3
+        epilogue = {"ms_per_step": p_ms, "max_len": L, "output_GBps": n * L * 5 / (p_ms / 1e3) / 1e9,
+                    "timing": "wall clock of the synchronous call (widest row not included)"}
+
+    # ---- JSON-lines text of the step's output on the device ----
+    jsonl = None
+    if args.engine == "pieces":
+        cap = enc.jsonl_device(d_ids.data_ptr(), d_oo.data_ptr(), n, ntok, 0, 0)
+        j_out = torch.empty(max(cap, 1), dtype=torch.uint8, device="cuda")
+        times = []
+        for _ in range(max(3, args.steps // 2)):
+            t0 = time.perf_counter()
+            assert enc.jsonl_device(d_ids.data_ptr(), d_oo.data_ptr(), n, ntok, j_out.data_ptr(), cap) == cap
+            times.append(time.perf_counter() - t0)
+        j_ms = float(np.median(times)) * 1e3
+        jsonl = {"ms_per_step": j_ms, "text_bytes": cap, "output_GBps": cap / (j_ms / 1e3) / 1e9,
+                 "timing": "wall clock of the synchronous call"}
+        del j_out
+
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
     dom = max(k_ms, key=k_ms.get)
@@ -400,6 +443,8 @@ def main():
             "e2e": e2e,
             "merge_only": merge_only,
             "decode": decode,
+            "epilogue": epilogue,
+            "jsonl": jsonl,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -166,6 +166,13 @@ int bbpe_decode_device(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* d_ids
                        size_t n_rows, uint64_t n_ids, uint8_t* d_out_bytes, uint64_t cap,
                        uint64_t* d_out_byte_offsets, uint64_t* total);
 
+/* ---- JSON-lines text of a device CSR batch (
+ * write_batch_jsonl, batch.hpp:157-166): {"ids":[...],"len":n}\n per row,
+ * byte-identical to the compact nlohmann dump. Writes at most cap bytes;
+ * *total receives the full text length. Synchronous. ---- */
+int bbpe_jsonl_device(bbpe_ctx* ctx, const uint32_t* d_ids, const uint64_t* d_tok_offsets, size_t n_rows,
+                      uint64_t n_ids, uint8_t* d_out, uint64_t cap, uint64_t* total);
+
 /* ---- encode_batch's padded BatchEncoding on the device (
  * batch.hpp:64-126) from device CSR ids: row r = [bos] + ids + [eos],
  * right-truncated to max_len, pad_id elsewhere, u32 lengths, u8 mask.

@@ -487,6 +487,14 @@ class Encoder:
             raise UsageError(f"decode output capacity {out.size} is smaller than the {total.value} bytes produced")
         return out[: total.value], out_offsets
 
+    def jsonl_device(self, d_ids, d_offsets, n_rows: int, n_ids: int, d_out, cap: int) -> int:
+        """JSON-lines text of a device CSR batch (write_batch_jsonl, batch.hpp:157-166)
+        into d_out (at most cap bytes); returns the full text length."""
+        total = C.c_uint64()
+        _check(LIB.bbpe_jsonl_device(self._h, C.c_void_p(d_ids), C.c_void_p(d_offsets), n_rows, n_ids,
+                                     C.c_void_p(d_out), cap, C.byref(total)))
+        return total.value
+
     def decode_device(self, table: MergeTable, d_ids, d_offsets, n_rows: int, n_ids: int, d_out, cap: int,
                       d_out_offsets) -> int:
         """Device pointers: CSR ids -> CSR bytes on device; returns the byte total."""

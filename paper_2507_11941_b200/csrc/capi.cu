@@ -1084,6 +1084,42 @@ int bbpe_decode_batch(bbpe_ctx* c, const bbpe_table* t, const uint32_t* ids, con
   BBPE_CATCH
 }
 
+int bbpe_jsonl_device(bbpe_ctx* c, const uint32_t* d_ids, const uint64_t* d_tok_offsets, size_t n_rows,
+                      uint64_t n_ids, uint8_t* d_out, uint64_t cap, uint64_t* total) {
+  BBPE_TRY
+  if (!c || !d_tok_offsets || !total) throw bbpe::usage_error("null argument");
+  if ((n_ids && !d_ids) || (cap && !d_out)) throw bbpe::usage_error("null buffer");
+  DeviceGuard g(c->device);
+  ensure_plan(*c);
+  bbpe::JsonArgs a{};
+  a.ids = d_ids;
+  a.tok_off = d_tok_offsets;
+  a.n_rows = n_rows;
+  a.n_ids = n_ids;
+  a.n_tok_blocks = (n_ids + 255) / 256;
+  a.n_row_blocks = (n_rows + 255) / 256;
+  c->dec_pos.ensure(std::max<uint64_t>(n_ids, 1) * 8);
+  c->dec_sums.ensure((a.n_tok_blocks + 1) * 8);
+  c->dec_toff.ensure(std::max<uint64_t>(n_rows, 1) * 8);
+  c->dec_ooff.ensure((a.n_row_blocks + 1) * 8);
+  a.tok_pos = c->dec_pos.as<uint64_t>();
+  a.tok_sums = c->dec_sums.as<uint64_t>();
+  a.row_pos = c->dec_toff.as<uint64_t>();
+  a.row_sums = c->dec_ooff.as<uint64_t>();
+  a.out = d_out;
+  a.cap = cap;
+  bbpe::launch_jsonl(a, c->plan.sm_count, c->stream);
+  c->launches += (n_ids ? 2 : 0) + (n_rows ? 3 : 0);
+  ck(cudaGetLastError(), "jsonl launch");
+  uint64_t t[2];
+  ck(cudaMemcpyAsync(&t[0], a.tok_sums + a.n_tok_blocks, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(&t[1], a.row_sums + a.n_row_blocks, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "jsonl");
+  *total = t[0] + t[1];
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
 int bbpe_batch_widest_device(bbpe_ctx* c, const uint64_t* d_tok_offsets, size_t n_rows, int add_bos,
                              int add_eos, uint64_t* widest) {
   BBPE_TRY

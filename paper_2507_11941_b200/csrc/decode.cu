@@ -1,5 +1,6 @@
 // decode.cu -- batch decode on the device: CSR token ids ->
-// CSR bytes, the inverse of the encode path. Semantics of
+// CSR bytes, the inverse of the encode path; and the JSON-lines text of a
+// batch (write_batch_jsonl). Semantics of
 // decode (merge_table.hpp:565-579: concatenate each id's bytes, DecodeError
 // "unknown token id X at index i") and decode_batch (batch.hpp:128-154: per
 // row, error prefixed "row r: ").
@@ -115,7 +116,124 @@ __global__ void k_dec_rows(DecodeArgs a) {
   a.out_off[r] = t >= a.n_ids ? a.block_sums[a.n_blocks] : a.block_sums[b] + a.pos[t];
 }
 
+// ---- JSON-lines text (write_batch_jsonl, batch.hpp:157-166): per row
+// {"ids":[i0,i1,...],"len":n}\n, the compact nlohmann dump. Token i takes
+// digits(id) + 1 characters (its comma, or the row's closing bracket is
+// accounted in the row frame); row r's frame is 18 + digits(n) - (n > 0).
+__device__ __forceinline__ uint32_t ndigits(uint64_t v) {
+  uint32_t d = 1;
+  while (v >= 10) {
+    v /= 10;
+    ++d;
+  }
+  return d;
+}
+
+__device__ __forceinline__ void put_digits(uint8_t* out, uint64_t pos, uint64_t cap, uint64_t v, uint32_t d) {
+  for (int k = int(d) - 1; k >= 0; --k) {
+    if (pos + k < cap) out[pos + k] = uint8_t('0' + v % 10);
+    v /= 10;
+  }
+}
+
+__device__ __forceinline__ void put_str(uint8_t* out, uint64_t pos, uint64_t cap, const char* s, int n) {
+  for (int k = 0; k < n; ++k)
+    if (pos + k < cap) out[pos + k] = uint8_t(s[k]);
+}
+
+// Block-local exclusive scan of v over kDecThreads threads; block total to sums[block].
+__device__ __forceinline__ uint64_t block_excl(uint64_t v, uint64_t* sums) {
+  __shared__ uint64_t s_warp[kDecThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += u;
+  }
+  if (lane == 31) s_warp[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const uint64_t x = lane < kDecThreads / 32 ? s_warp[lane] : 0;
+    uint64_t xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, xi, d);
+      if (lane >= d) xi += u;
+    }
+    if (lane < kDecThreads / 32) s_warp[lane] = xi - x;
+    if (lane == 31) sums[blockIdx.x] = xi;
+  }
+  __syncthreads();
+  return s_warp[wid] + inc - v;
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_json_tok(JsonArgs a) {
+  const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
+  const uint64_t v = i < a.n_ids ? ndigits(a.ids[i]) + 1 : 0;
+  const uint64_t e = block_excl(v, a.tok_sums);
+  if (i < a.n_ids) a.tok_pos[i] = e;
+}
+
+__global__ void __launch_bounds__(kDecThreads) k_json_row(JsonArgs a) {
+  const uint64_t r = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
+  uint64_t v = 0;
+  if (r < a.n_rows) {
+    const uint64_t len = a.tok_off[r + 1] - a.tok_off[r];
+    v = 18 + ndigits(len) - (len > 0 ? 1 : 0);
+  }
+  const uint64_t e = block_excl(v, a.row_sums);
+  if (r < a.n_rows) a.row_pos[r] = e;
+}
+
+__device__ __forceinline__ uint64_t tok_text_pos(const JsonArgs& a, uint64_t i) {  // exclusive, i <= n_ids
+  return i >= a.n_ids ? a.tok_sums[a.n_tok_blocks] : a.tok_sums[i / kDecThreads] + a.tok_pos[i];
+}
+
+// Warp per row: lane per token; lane 0 writes the frame.
+__global__ void k_json_write(JsonArgs a) {
+  const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x / 32);
+  const int lane = threadIdx.x & 31;
+  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); r < a.n_rows; r += nw) {
+    const uint64_t t0 = a.tok_off[r] - a.tok_off[0], t1 = a.tok_off[r + 1] - a.tok_off[0];
+    const uint64_t len = t1 - t0;
+    const uint64_t p0 = tok_text_pos(a, t0);
+    const uint64_t start = a.row_sums[r / kDecThreads] + a.row_pos[r] + p0;
+    for (uint64_t i = t0 + lane; i < t1; i += 32) {
+      const uint32_t id = a.ids[i];
+      const uint32_t d = ndigits(id);
+      const uint64_t pos = start + 8 + (tok_text_pos(a, i) - p0);
+      put_digits(a.out, pos, a.cap, id, d);
+      if (i + 1 < t1 && pos + d < a.cap) a.out[pos + d] = ',';
+    }
+    if (lane == 0) {
+      put_str(a.out, start, a.cap, "{\"ids\":[", 8);
+      const uint64_t q = start + 8 + (tok_text_pos(a, t1) - p0) - (len > 0 ? 1 : 0);
+      put_str(a.out, q, a.cap, "],\"len\":", 8);
+      const uint32_t d = ndigits(len);
+      put_digits(a.out, q + 8, a.cap, len, d);
+      put_str(a.out, q + 8 + d, a.cap, "}\n", 2);
+    }
+  }
+}
+
 }  // namespace
+
+void launch_jsonl(const JsonArgs& a, int sm_count, cudaStream_t s) {
+  if (a.n_ids) {
+    k_json_tok<<<unsigned(a.n_tok_blocks), kDecThreads, 0, s>>>(a);
+    k_dec_scan<<<1, 1024, 0, s>>>(a.tok_sums, a.n_tok_blocks);
+  } else {
+    cudaMemsetAsync(a.tok_sums, 0, 8, s);
+  }
+  if (a.n_rows) {
+    k_json_row<<<unsigned(a.n_row_blocks), kDecThreads, 0, s>>>(a);
+    k_dec_scan<<<1, 1024, 0, s>>>(a.row_sums, a.n_row_blocks);
+    k_json_write<<<unsigned(sm_count * 8), 256, 0, s>>>(a);
+  } else {
+    cudaMemsetAsync(a.row_sums, 0, 8, s);
+  }
+}
 
 void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   if (a.n_ids) {

@@ -26,4 +26,22 @@ struct DecodeArgs {
 
 void launch_decode(const DecodeArgs& a, cudaStream_t s);
 
+struct JsonArgs {
+  const uint32_t* ids;
+  const uint64_t* tok_off;   // n_rows + 1 (relative to tok_off[0])
+  uint64_t n_rows;
+  uint64_t n_ids;
+  uint64_t* tok_pos;         // n_ids: text offset of each token within its block
+  uint64_t* tok_sums;        // n_tok_blocks + 1
+  uint64_t n_tok_blocks;
+  uint64_t* row_pos;         // n_rows: frame offset of each row within its block
+  uint64_t* row_sums;        // n_row_blocks + 1
+  uint64_t n_row_blocks;
+  uint8_t* out;
+  uint64_t cap;
+};
+
+// JSON-lines text of a CSR batch; total length = tok_sums[n_tok_blocks] + row_sums[n_row_blocks].
+void launch_jsonl(const JsonArgs& a, int sm_count, cudaStream_t s);
+
 }  // namespace bbpe

@@ -539,3 +539,37 @@ def test_full_size_long_row_configs(gpt2, cfg):
     for r in np.random.default_rng(cfg).integers(0, n, 12):
         s = data[int(off[r]):int(off[r + 1])].tobytes()
         assert ids[int(oo[r]):int(oo[r + 1])].tolist() == orc.heap_bpe(orc.initial(s))
+
+
+def test_device_jsonl_matches_reference_format(gpt2):
+    """JSON-lines text on the device is byte-identical to
+    write_batch_jsonl (batch.hpp:157-166: compact {"ids":[...],"len":n} per
+    row, as the host mirror writes it), including empty rows; a capacity
+    shorter than the text reports the full length."""
+    torch = pytest.importorskip("torch")
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    rng = np.random.default_rng(51)
+    lens = rng.integers(0, 300, 900)
+    lens[::37] = 0
+    data, off = synth.rows_lengths(gen, lens, seed=52)
+    enc = bb.Encoder(0)
+    ids, oo, _ = enc.encode_packed(gpt2, data, off)
+    be = bb.BatchEncoding(batch_size=lens.size, pad_id=0)
+    L = int(np.diff(oo.astype(np.int64)).max())
+    be.max_len = L
+    be.ids = np.zeros(lens.size * L, np.uint32)
+    be.mask = np.zeros(lens.size * L, np.uint8)
+    be.lengths = np.diff(oo.astype(np.int64)).astype(np.uint32)
+    for r in range(lens.size):
+        row = ids[int(oo[r]):int(oo[r + 1])]
+        be.ids[r * L: r * L + row.size] = row
+        be.mask[r * L: r * L + row.size] = 1
+    want = bb.write_batch_jsonl(be).encode()
+    d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+    d_oo = torch.from_numpy(oo.view(np.int64)).cuda()
+    out = torch.empty(len(want) + 64, dtype=torch.uint8, device="cuda")
+    n = enc.jsonl_device(d_ids.data_ptr(), d_oo.data_ptr(), lens.size, ids.size, out.data_ptr(), out.numel())
+    assert n == len(want)
+    assert bytes(out[:n].cpu().numpy()) == want
+    assert enc.jsonl_device(d_ids.data_ptr(), d_oo.data_ptr(), lens.size, ids.size, out.data_ptr(), 10) == len(want)
