@@ -958,7 +958,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
   // global load on refill); the next batch is in flight meanwhile.
   const ulonglong2 kHole = make_ulonglong2(~0ull, 0ull);
   uint32_t base = 0, next = 0, avail = 0;  // warp-uniform slice of record indices
-  uint32_t pbase = 0, pidx = 0, cidx = 0;  // record index held by this lane (prefetched / current)
+  uint32_t pbase = 0, pidx = 0;  // record index held by this lane (prefetched batch)
   uint32_t pslot = 0, cslot = 0;           // its dedupe slot + 1 (0: none)
   ulonglong2 cur = kHole, pre = kHole;
   auto fetch = [&]() {
@@ -984,14 +984,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
   int np = 0;     // pending probes
   uint32_t m = NONE;  // minimum over resolved ranks
   uint64_t rec = 0;
-  uint32_t ridx = 0, rslot = 0;
+  uint32_t rslot = 0;
   for (;;) {
     const bool idle = n == 0;
     const unsigned im = __ballot_sync(kFull, idle);
     if (im && next >= avail && !exhausted) {
       base = pbase;
       cur = pre;
-      cidx = pidx;
       cslot = pslot;
       next = 0;
       avail = base < nrec ? min(32u, nrec - base) : 0u;
@@ -1004,11 +1003,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
     const int src_lane = takes ? int(next + rank) : lane;
     const uint64_t hdr = __shfl_sync(kFull, cur.x, src_lane);
     const uint64_t b8 = __shfl_sync(kFull, cur.y, src_lane);
-    const uint32_t hidx = __shfl_sync(kFull, cidx, src_lane);
     const uint32_t hslot = __shfl_sync(kFull, cslot, src_lane);
     if (takes) {
       rec = hdr;
-      ridx = hidx;
       rslot = hslot;
       if (rec != ~0ull) {
         n = int(rec & 63);
