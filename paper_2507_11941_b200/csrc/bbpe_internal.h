@@ -70,6 +70,7 @@ __host__ __device__ inline uint32_t mix32(uint32_t h) {
 
 // 32-byte memo entry: piece bytes (zero padded), length, 1-2 result tokens
 // (original ids: memo results are final output). len == 0 marks an empty slot.
+// Single bytes are entries too (one lookup path for every short piece).
 constexpr int kMemoMaxLen = 20;
 struct MemoEntry {
   uint32_t w[5];
@@ -81,10 +82,12 @@ struct MemoEntry {
 static_assert(sizeof(MemoEntry) == 32, "memo entry is one sector");
 
 // Hash of a piece given as 5 little-endian words (bytes past len are zero):
-// one xor-multiply per word, then a murmur-style finaliser.
+// the length and the first 12 bytes (99.5% of pieces are shorter; longer ones
+// sharing a 12-byte prefix and a length just probe on), one xor-multiply per
+// word, then a murmur-style finaliser. Lookups compare all 20 bytes.
 __host__ __device__ inline uint32_t memo_hash(const uint32_t* w, uint32_t len) {
   uint32_t h = len * 0x9E3779B9u;
-  for (int i = 0; i < 5; ++i) h = (h ^ w[i]) * 0x85EBCA6Bu;
+  for (int i = 0; i < 3; ++i) h = (h ^ w[i]) * 0x85EBCA6Bu;
   h ^= h >> 15;
   h *= 0xC2B2AE35u;
   h ^= h >> 13;

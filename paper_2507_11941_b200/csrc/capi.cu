@@ -799,15 +799,27 @@ void ensure_memo(bbpe_ctx& c, const bbpe_table& t) {
   }
   std::vector<MemoEntry> slots;
   uint64_t mask = 0;
-  if (!cand.empty()) {
-    std::vector<uint32_t> ids(blob.size());
-    std::vector<uint64_t> oo(cand.size() + 1);
-    encode_wave(c, t, blob.data(), offs.data(), 0, cand.size(), ids.data(), 0, ids.size(), oo.data(),
-                nullptr, /*allow_memo=*/false);
+  {
+    std::vector<uint32_t> ids(std::max<size_t>(blob.size(), 1));
+    std::vector<uint64_t> oo(cand.size() + 1, 0);
+    if (!cand.empty())
+      encode_wave(c, t, blob.data(), offs.data(), 0, cand.size(), ids.data(), 0, ids.size(), oo.data(),
+                  nullptr, /*allow_memo=*/false);
     uint64_t cap = 16;
-    while (cap < cand.size() * 8) cap <<= 1;  // load <= 1/8: a lookup resolves at its first slot
+    while (cap < (cand.size() + 256) * 8) cap <<= 1;  // load <= 1/8: a lookup resolves at its first slot
     mask = cap - 1;
     slots.assign(cap, MemoEntry{});
+    for (int byte = 0; byte < 256; ++byte) {  // single bytes: their byte token
+      if (t.byte_tokens[byte] == kInvalidToken) continue;
+      MemoEntry m{};
+      m.w[0] = uint32_t(byte);
+      m.len = 1;
+      m.nres = 1;
+      m.res[0] = t.byte_tokens[byte];
+      uint64_t b = memo_hash(m.w, m.len) & mask;
+      while (slots[b].len != 0) b = (b + 1) & mask;
+      slots[b] = m;
+    }
     for (size_t j = 0; j < cand.size(); ++j) {
       const uint64_t nres = oo[j + 1] - oo[j];
       if (nres < 1 || nres > 2) continue;

@@ -270,17 +270,27 @@ __device__ __noinline__ MemoHit memo_overflow(const MemoEntry* memo, uint64_t ma
   }
 }
 
-__device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* ww, int start, int len,
-                                            uint32_t& r0, uint32_t& r1, uint32_t& nres) {
+// Byte masks of the 5 key words for each piece length (shared memory,
+// s_mask[8 * len + i]), built once per CTA.
+__device__ __forceinline__ void build_mask_table(uint32_t* s_mask) {
+  for (int i = threadIdx.x; i < (kMemoMaxLen + 1) * 8; i += blockDim.x) {
+    const int len = i >> 3, wi = i & 7;
+    const int nb = len - 4 * wi;
+    s_mask[i] = wi >= 5 ? 0u : (nb >= 4 ? ~0u : (nb <= 0 ? 0u : (1u << (8 * nb)) - 1u));
+  }
+}
+
+__device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* ww, const uint32_t* s_mask,
+                                            int start, int len, uint32_t& r0, uint32_t& r1, uint32_t& nres) {
   const int a = start >> 2;
   const uint32_t sh = uint32_t(start & 3) * 8;
-  const int base = 32 - 8 * len;  // mask shift of word i: base + 32 i (clamped to [0, 32])
+  const uint4 m03 = *reinterpret_cast<const uint4*>(s_mask + 8 * len);
+  const uint32_t mk[5] = {m03.x, m03.y, m03.z, m03.w, s_mask[8 * len + 4]};
   uint32_t x[6], w[5];
 #pragma unroll
   for (int i = 0; i < 6; ++i) x[i] = ww[a + i];
 #pragma unroll
-  for (int i = 0; i < 5; ++i)
-    w[i] = __funnelshift_r(x[i], x[i + 1], sh) & __funnelshift_rc(~0u, 0u, uint32_t(max(0, base + 32 * i)));
+  for (int i = 0; i < 5; ++i) w[i] = __funnelshift_r(x[i], x[i + 1], sh) & mk[i];
   const uint64_t b = memo_hash(w, uint32_t(len)) & T.memo_mask;
   const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.memo + b);
   const int m = memo_match(__ldg(p), __ldg(p + 1), w, len, r0, r1, nres);
@@ -348,9 +358,11 @@ __device__ __forceinline__ uint64_t dedup_claim(ulonglong2* dkey, uint64_t dmask
 __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_jt[2048];
   __shared__ uint32_t s_lo[256];
+  __shared__ __align__(16) uint32_t s_mask[(kMemoMaxLen + 1) * 8];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_jt[i] = T.junction_t[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lo[i] = T.lut_out[i];
+  build_mask_table(s_mask);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   PieceSmem& S = reinterpret_cast<PieceSmem*>(s_dyn)[wid];
@@ -451,17 +463,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     if (lane == 0) S.bd[kTile / 32] = 0;
     __syncwarp();
 
-    // (2) Piece list.
+    // (2) Piece list: two lanes per boundary word (16 positions each).
+    static_assert(kTile / 32 * 2 == 32, "two lanes per boundary word");
     int npieces;
     {
-      const uint32_t m = lane < kTile / 32 ? S.bd[lane] : 0u;
+      const uint32_t m = (S.bd[lane >> 1] >> (16 * (lane & 1))) & 0xFFFFu;
       const uint32_t c = __popc(m);
       const uint32_t inc = warp_incl_sum(c, lane);
-      if (lane <= kTile / 32) S.wpre[lane] = static_cast<uint16_t>(inc - c);
+      const uint32_t tot = __shfl_sync(kFull, inc, 31);
+      if ((lane & 1) == 0) S.wpre[lane >> 1] = static_cast<uint16_t>(inc - c);
+      if (lane == 0) S.wpre[kTile / 32] = static_cast<uint16_t>(tot);
       int pos = int(inc - c);
       uint32_t mm = m;
       while (mm) {
-        S.plist[pos++] = static_cast<uint16_t>(32 * lane + __ffs(mm) - 1);
+        S.plist[pos++] = static_cast<uint16_t>(16 * lane + __ffs(mm) - 1);
         mm &= mm - 1;
       }
       npieces = int(__shfl_sync(kFull, inc, 31));
@@ -491,12 +506,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
           len[u] = S.plist[k + 1] - q[u];
           if (len[u] > kLmax) {
             lg[u] = true;  // long: k_long_pieces, no staging slots
-          } else if (len[u] == 1) {
+          } else if (len[u] == 1 && !a.use_memo) {  // (with the memo, single bytes are entries)
             c[u] = 1;
             r0[u] = s_lo[wb[q[u] + 16]];
           } else {
             uint32_t nres = 0;
-            if (a.use_memo && len[u] <= kMemoMaxLen && memo_lookup(T, ww, q[u] + 16, len[u], r0[u], r1[u], nres)) {
+            if (a.use_memo && len[u] <= kMemoMaxLen &&
+                memo_lookup(T, ww, s_mask, q[u] + 16, len[u], r0[u], r1[u], nres)) {
               c[u] = nres;
             } else {
               merge[u] = true;  // k_merge fills the `len` reserved slots
