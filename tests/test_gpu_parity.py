@@ -573,3 +573,33 @@ def test_device_jsonl_matches_reference_format(gpt2):
     assert n == len(want)
     assert bytes(out[:n].cpu().numpy()) == want
     assert enc.jsonl_device(d_ids.data_ptr(), d_oo.data_ptr(), lens.size, ids.size, out.data_ptr(), 10) == len(want)
+
+
+def test_device_outputs_on_empty_and_degenerate_batches(gpt2):
+    """Decode / JSONL / padding of empty batches, all-empty rows, a single
+    empty row, and an unknown id in an otherwise empty batch."""
+    torch = pytest.importorskip("torch")
+    import ctypes as C
+    from paper_2507_11941_b200._lib import LIB
+    enc = bb.Encoder(0)
+    for n in (0, 1, 5):
+        off = np.zeros(n + 1, np.uint64)
+        b, bo = enc.decode_packed(gpt2, np.zeros(0, np.uint32), off)
+        assert b.size == 0 and np.array_equal(bo, off)
+        d_ids = torch.zeros(1, dtype=torch.int32, device="cuda")
+        d_off = torch.from_numpy(off.view(np.int64)).cuda()
+        out = torch.empty(128, dtype=torch.uint8, device="cuda")
+        t = enc.jsonl_device(d_ids.data_ptr(), d_off.data_ptr(), n, 0, out.data_ptr(), 128)
+        assert t <= 128 and bytes(out[:t].cpu().numpy()) == b'{"ids":[],"len":0}\n' * n
+        w = C.c_uint64()
+        assert LIB.bbpe_batch_widest_device(enc.handle, C.c_void_p(d_off.data_ptr()), n, 0, 0, C.byref(w)) == 0
+        assert w.value == 0
+        ln = torch.full((max(n, 1),), 7, dtype=torch.int32, device="cuda")
+        tr = C.c_uint64(9)
+        assert LIB.bbpe_pad_device(enc.handle, C.c_void_p(d_ids.data_ptr()), C.c_void_p(d_off.data_ptr()), n, 0,
+                                   0xFFFFFFFF, 0xFFFFFFFF, 0, None, C.c_void_p(ln.data_ptr()), None, C.byref(tr)) == 0
+        assert tr.value == 0 and (n == 0 or ln[:n].cpu().tolist() == [0] * n)
+    with pytest.raises(bb.DecodeError, match="row 2: unknown token id 60000 at index 0"):
+        enc.decode_packed(gpt2, np.array([60000], np.uint32), np.array([0, 0, 0, 1], np.uint64))
+    rows = bb.encode_batch([], gpt2, bb.SpecialTokenSet(), bb.BlockConfig(256, None), 0)
+    assert rows.batch_size == 0 and rows.max_len == 0
