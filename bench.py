@@ -14,12 +14,17 @@ value     device-resident throughput (tokens/s over all ranks): bytes + offsets
           max over ranks. Inputs (256 MiB) exceed the 126 MB L2.
 e2e       same metric through the public host API (bbpe_encode) from pinned
           host memory: H2D of the bytes+offsets, encode, D2H of ids+offsets,
-          every step.
-roofline  k_encode (the dominant kernel): algorithmic bytes per launch =
+          every step (pipelined waves).
+roofline  k_pieces (the dominant kernel): algorithmic bytes per launch =
           input bytes + 4 x tokens + 16 x rows / its average
-          CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+          CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs; traffic =
+          DRAM bytes of one launch from profiles/r1_k_pieces_cfg<N>.json.
 cpu_baseline  the unmodified reference encode_batch (oracle/_ref, block engine,
-          PhasePool over all host cores) on a bounded sample of the same rows.
+          PhasePool over all host cores) on a bounded sample of the same rows;
+          heap_engine: the reference's heap_bpe over PhasePool::run_items.
+decode / epilogue / jsonl  the §8f device paths on the step's output: decode
+          back to bytes (round trip checked), padded BatchEncoding, JSON-lines.
+merge_only  memo and dedupe off: every piece through the merge passes.
 """
 import argparse
 import json
@@ -212,10 +217,26 @@ def cpu_baseline(table, data, offsets, seconds):
     t0 = time.perf_counter()
     ids, oo = ref.encode_batch(data, offsets[: n + 1], workers=cores)
     dt = time.perf_counter() - t0
-    return {"value": int(oo[-1]) / dt, "unit": "tokens/s", "cores": cores, "kind": "reference",
-            "sample": f"first {n} of {n_all} rows ({int(offsets[n])} B), reference encode_batch "
-                      f"(block engine, PhasePool({cores}))",
-            "input_GBps": int(offsets[n]) / dt / 1e9}
+    out = {"value": int(oo[-1]) / dt, "unit": "tokens/s", "cores": cores, "kind": "reference",
+           "sample": f"first {n} of {n_all} rows ({int(offsets[n])} B), reference encode_batch "
+                     f"(block engine, PhasePool({cores}))",
+           "input_GBps": int(offsets[n]) / dt / 1e9}
+    # The reference's fastest CPU engine too: heap_bpe per row
+    # over PhasePool::run_items -- equal results on these rank-consistent tables.
+    m = min(n_all, 4096)
+    ref.encode_heap(data, offsets[: m + 1], workers=cores)
+    t0 = time.perf_counter()
+    ref.encode_heap(data, offsets[: m + 1], workers=cores)
+    dt = time.perf_counter() - t0
+    m = int(min(n_all, max(m, m * seconds / 2 / max(dt, 1e-3))))
+    t0 = time.perf_counter()
+    _, ho = ref.encode_heap(data, offsets[: m + 1], workers=cores)
+    dt = time.perf_counter() - t0
+    out["heap_engine"] = {"value": int(ho[-1]) / dt, "unit": "tokens/s", "cores": cores,
+                          "sample": f"first {m} of {n_all} rows ({int(offsets[m])} B), reference heap_bpe "
+                                    f"over PhasePool::run_items({cores})",
+                          "input_GBps": int(offsets[m]) / dt / 1e9}
+    return out
 
 
 def main():
