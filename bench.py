@@ -399,6 +399,30 @@ def main():
                  "timing": "wall clock of the synchronous call"}
         del j_out
 
+    # ---- gpt2 split pattern mode (encode_reference pattern mode) ----
+    pattern = None
+    if args.engine == "pieces":
+        enc.set_config(pattern="gpt2")
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                step()
+        enc.sync()
+        enc.kernel_times(reset=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+        enc.sync()
+        torch.cuda.synchronize()
+        pt_ms = e0.elapsed_time(e1) / args.steps
+        kt, kc = enc.kernel_times(reset=True)
+        pattern = {"value": int(d_oo[-1].item()) / (pt_ms / 1e3), "unit": "tokens/s", "ms_per_step": pt_ms,
+                   "kernel_ms": {k: v / max(kc, 1) for k, v in kt.items()},
+                   "note": "k_tile_first includes the gpt2 splitter (thread per row)"}
+        enc.set_config(pattern=None)
+
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
     dom = max(k_ms, key=k_ms.get)
@@ -466,6 +490,7 @@ def main():
             "decode": decode,
             "epilogue": epilogue,
             "jsonl": jsonl,
+            "pattern_mode": pattern,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

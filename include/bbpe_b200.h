@@ -95,6 +95,13 @@ typedef struct bbpe_config {
                               repeats copy that result (exact: a piece's
                               encoding depends on its bytes only). 1: every
                               piece runs its own passes.                      */
+  int32_t pattern;         /* 0 (default): byte-level, merges across the whole row
+                              (the block engine, encode_batch). 1: the gpt2 split
+                              pattern (pattern_pretokenize, pretokenize.hpp:79-
+                              258) on the device first, merges within each chunk
+                              -- encode_reference's pattern mode (ref_engines.hpp
+                              :119-146). Needs the pieces engine and a
+                              rank-consistent table (heap == block there).    */
 } bbpe_config;
 
 typedef struct bbpe_stats {

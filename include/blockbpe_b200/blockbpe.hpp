@@ -269,7 +269,7 @@ class Encoder {
   explicit Encoder(int device = 0, BlockConfig cfg = {}, bool piece_memo = true) {
     cfg.validate();
     bbpe_config c{cfg.block_size, cfg.max_passes ? static_cast<std::int64_t>(*cfg.max_passes) : 0,
-                  BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0, 0};
+                  BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0, 0, 0};
     bbpe_ctx* h = nullptr;
     detail::check(bbpe_ctx_create(device, &c, &h));
     h_.reset(h);
@@ -278,7 +278,7 @@ class Encoder {
   void configure(const BlockConfig& cfg, bool block_engine = false, bool piece_memo = true) {
     cfg.validate();
     bbpe_config c{cfg.block_size, cfg.max_passes ? static_cast<std::int64_t>(*cfg.max_passes) : 0,
-                  block_engine ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0, 0};
+                  block_engine ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0, 0, 0};
     detail::check(bbpe_ctx_set_config(h_.get(), &c));
   }
   // Packed rows -> CSR.

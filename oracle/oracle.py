@@ -163,6 +163,11 @@ class Reference:
                                          u32p, u64p, C.c_uint64, C.c_size_t, C.c_int64]
         lib.ref_encode_heap.restype = C.c_int64
         lib.ref_encode_heap.argtypes = [C.c_void_p, u8p, u64p, C.c_size_t, C.c_uint, u32p, u64p, C.c_uint64]
+        lib.ref_encode_pattern.restype = C.c_int64
+        lib.ref_encode_pattern.argtypes = [C.c_void_p, u8p, u64p, C.c_size_t, C.c_uint, C.c_char_p, u32p, u64p,
+                                           C.c_uint64]
+        lib.ref_pretokenize.restype = C.c_int64
+        lib.ref_pretokenize.argtypes = [u8p, C.c_size_t, C.c_char_p, u64p, C.c_size_t]
         lib.ref_block_bpe_trace.restype = C.c_int64
         lib.ref_block_bpe_trace.argtypes = [C.c_void_p, u32p, C.c_size_t, C.c_uint32, C.c_int64, u32p, u64p,
                                             C.c_size_t, C.POINTER(C.c_size_t)]
@@ -235,6 +240,31 @@ class Reference:
         if k < 0:
             raise RuntimeError(-k, self.lib.ref_last_error().decode())
         return ids[:k], oo
+
+    def encode_pattern(self, data, offsets, pattern: str = "gpt2", workers: int = 1):
+        """encode_reference in pattern mode (ref_engines.hpp:119-146), heap engine."""
+        data = np.ascontiguousarray(data, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        cap = max(int(offsets[-1]), 1)
+        ids = np.zeros(cap, np.uint32)
+        oo = np.zeros(n + 1, np.uint64)
+        k = self.lib.ref_encode_pattern(self.h, _p(data, C.c_uint8) if data.size else None,
+                                        _p(offsets, C.c_uint64), n, workers, pattern.encode(), _p(ids, C.c_uint32),
+                                        _p(oo, C.c_uint64), cap)
+        if k < 0:
+            raise RuntimeError(-k, self.lib.ref_last_error().decode())
+        return ids[:k], oo
+
+    def pretokenize(self, s: bytes, pattern: str = "gpt2") -> List[int]:
+        """Chunk start offsets of pattern_pretokenize (pretokenize.hpp:252-258)."""
+        buf = np.frombuffer(s, np.uint8) if s else np.zeros(1, np.uint8)
+        starts = np.zeros(max(len(s), 1), np.uint64)
+        k = self.lib.ref_pretokenize(_p(buf, C.c_uint8), len(s), pattern.encode(), _p(starts, C.c_uint64),
+                                     starts.size)
+        if k < 0:
+            raise RuntimeError(-k, self.lib.ref_last_error().decode())
+        return starts[:k].tolist()
 
     def encode_heap(self, data, offsets, workers: int = 1):
         data = np.ascontiguousarray(data, np.uint8)

@@ -13,6 +13,8 @@
 //                            (ref_engines.hpp:46-103, thread_pool.hpp:95-101)
 //   ref_block_bpe_trace   -> blockbpe::block_bpe with a PassTrace (block_engine.hpp:268-310)
 //   ref_naive_bpe         -> blockbpe::naive_bpe (ref_engines.hpp:22-40)
+//   ref_encode_pattern    -> encode_reference, pattern mode (ref_engines.hpp:119-146)
+//   ref_pretokenize       -> pattern_pretokenize (pretokenize.hpp:252-258)
 // The batch outputs are returned as CSR (ids + u64 offsets), the layout the
 // B200 path produces; padding is stripped using BatchEncoding::lengths.
 
@@ -223,6 +225,59 @@ std::int64_t ref_encode_heap(void* h, const std::uint8_t* bytes, const std::uint
       out_offsets[r + 1] = pos;
     }
     return static_cast<std::int64_t>(pos);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -err_code(e);
+  }
+}
+
+// encode_reference in pattern mode (ref_engines.hpp:119-146: pattern_pretokenize
+// chunks, heap_bpe within each chunk), rows fanned over PhasePool::run_items.
+std::int64_t ref_encode_pattern(void* h, const std::uint8_t* bytes, const std::uint64_t* offsets,
+                                std::size_t n, unsigned workers, const char* pattern, std::uint32_t* out_ids,
+                                std::uint64_t* out_offsets, std::uint64_t capacity) {
+  try {
+    auto* t = static_cast<RefTable*>(h);
+    PhasePool pool(workers);
+    std::vector<TokenSeq> rows(n);
+    const PreSpec pre = PreSpec::with_pattern(pattern);
+    auto row = [&](std::size_t r) {
+      std::string_view s(reinterpret_cast<const char*>(bytes) + offsets[r], offsets[r + 1] - offsets[r]);
+      rows[r] = encode_reference(s, t->table, t->specials, pre, RefEngine::heap);
+    };
+    if (pool.worker_count() >= 2)
+      pool.run_items(n, row);
+    else
+      for (std::size_t r = 0; r < n; ++r) row(r);
+    std::uint64_t pos = 0;
+    out_offsets[0] = 0;
+    for (std::size_t r = 0; r < n; ++r) {
+      if (pos + rows[r].size() > capacity) throw UsageError("output capacity exceeded");
+      std::memcpy(out_ids + pos, rows[r].data(), rows[r].size() * 4);
+      pos += rows[r].size();
+      out_offsets[r + 1] = pos;
+    }
+    return static_cast<std::int64_t>(pos);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -err_code(e);
+  }
+}
+
+// pattern_pretokenize (pretokenize.hpp:252-258) of one string: chunk start
+// offsets into starts[], returns the chunk count (or -code).
+std::int64_t ref_pretokenize(const std::uint8_t* bytes, std::size_t len, const char* pattern,
+                             std::uint64_t* starts, std::size_t cap) {
+  try {
+    std::string_view s(reinterpret_cast<const char*>(bytes), len);
+    std::uint64_t pos = 0;
+    std::size_t k = 0;
+    for (const std::string& chunk : pattern_pretokenize(s, pattern)) {
+      if (k < cap) starts[k] = pos;
+      ++k;
+      pos += chunk.size();
+    }
+    return static_cast<std::int64_t>(k);
   } catch (const std::exception& e) {
     g_err = e.what();
     return -err_code(e);

@@ -26,6 +26,7 @@ class Config(C.Structure):
         ("wave_bytes", C.c_uint64),
         ("piece_memo", C.c_int32),
         ("no_dedup", C.c_int32),
+        ("pattern", C.c_int32),
     ]
 
 

@@ -371,13 +371,27 @@ def pack_rows(rows: Sequence[Union[bytes, str]]) -> Tuple[np.ndarray, np.ndarray
 ENGINES = {"pieces": 0, "block": 1}
 
 
+GPT2_PATTERN = r"""'s|'t|'re|'ve|'m|'ll|'d| ?\p{L}+| ?\p{N}+| ?[^\s\p{L}\p{N}]+|\s+(?!\S)|\s+"""
+
+
+def _pattern_code(pattern: Optional[str]) -> int:
+    """None: byte-level (encode_batch); "gpt2" or the published gpt2 pattern
+    (pretokenize.hpp:86-87): the device splitter."""
+    if pattern is None:
+        return 0
+    if pattern in ("gpt2", GPT2_PATTERN):
+        return 1
+    raise UsageError(f'only the gpt2 split pattern runs on the device, got "{pattern}"')
+
+
 class Encoder:
     """One encode context on one GPU (bbpe_ctx). Single-caller, like PhasePool."""
 
     def __init__(self, device: int = 0, config: Optional[BlockConfig] = None, engine: str = "pieces",
-                 wave_bytes: int = 0, piece_memo: bool = True, dedup: bool = True):
+                 wave_bytes: int = 0, piece_memo: bool = True, dedup: bool = True, pattern: Optional[str] = None):
         self.device = device
         self.dedup = dedup
+        self.pattern = pattern
         self.config = config or BlockConfig()
         self.engine = engine
         self.wave_bytes = wave_bytes
@@ -390,10 +404,10 @@ class Encoder:
         if self.engine not in ENGINES:
             raise UsageError(f'unknown engine "{self.engine}"')
         return Config(self.config.block_size, self.config.max_passes or 0, ENGINES[self.engine], self.wave_bytes,
-                      1 if self.piece_memo else 0, 0 if self.dedup else 1)
+                      1 if self.piece_memo else 0, 0 if self.dedup else 1, _pattern_code(self.pattern))
 
     def set_config(self, config: BlockConfig = None, engine: str = None, wave_bytes: int = None,
-                   piece_memo: bool = None, dedup: bool = None):
+                   piece_memo: bool = None, dedup: bool = None, pattern: Optional[str] = "unchanged"):
         if config is not None:
             self.config = config
         if engine is not None:
@@ -404,6 +418,8 @@ class Encoder:
             self.piece_memo = piece_memo
         if dedup is not None:
             self.dedup = dedup
+        if pattern != "unchanged":
+            self.pattern = pattern
         _check(LIB.bbpe_ctx_set_config(self._h, C.byref(self._cfg())))
 
     def __del__(self):

@@ -167,7 +167,7 @@ struct WaveSet {
 struct bbpe_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1, 0};
+  bbpe_config cfg{256, 0, BBPE_ENGINE_PIECES, 0, 1, 0, 0};
   bbpe::LaunchPlan plan;
   Scratch sc;  // device API / single-wave encodes (on `stream` or the caller's)
   DevBuf in_bytes, in_offsets, out_ids, out_offsets;
@@ -206,6 +206,11 @@ void validate_config(const bbpe_config& c) {
                             std::to_string(c.block_size));
   if (c.engine != BBPE_ENGINE_PIECES && c.engine != BBPE_ENGINE_BLOCK)
     throw bbpe::usage_error("unknown engine " + std::to_string(c.engine));
+  if (c.pattern != 0 && c.pattern != 1)
+    throw bbpe::usage_error("unknown split pattern " + std::to_string(c.pattern) +
+                            " (0 byte-level, 1 gpt2; other regexes run on the host reference only)");
+  if (c.pattern && (c.engine != BBPE_ENGINE_PIECES || c.max_passes > 0))
+    throw bbpe::usage_error("the gpt2 split pattern needs the pieces engine without a pass cap");
 }
 
 struct DeviceGuard {
@@ -298,6 +303,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   a.lpy = sc.lpy.as<uint64_t>();
   a.engine = block ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES;
   a.max_passes = c.cfg.max_passes;
+  a.pattern = c.cfg.pattern;
   // Counters and look-back status are left zero by k_gather; rowbits too.
   if (sc.ctrl_dirty) {
     ck(cudaMemsetAsync(a.status, 0, sc.status.cap, s), "memset status");
@@ -331,6 +337,9 @@ void enqueue_encode(bbpe_ctx& c, Scratch& sc, const bbpe_table& t, const uint8_t
   }
   bbpe::table_on_device(t, c.device);
   ensure_plan(c);
+  if (c.cfg.pattern && !t.rank_consistent)
+    throw bbpe::usage_error("the gpt2 split pattern needs a rank-consistent merge table (the reference's pattern "
+                            "mode runs heap_bpe, which equals the block engine only on such tables)");
   const bool memo = allow_memo && c.cfg.piece_memo && c.cfg.engine == BBPE_ENGINE_PIECES &&
                     c.cfg.max_passes <= 0;
   // The memo itself is built at API entry (maybe_build_memo), never here:
@@ -802,9 +811,20 @@ void ensure_memo(bbpe_ctx& c, const bbpe_table& t) {
   {
     std::vector<uint32_t> ids(std::max<size_t>(blob.size(), 1));
     std::vector<uint64_t> oo(cand.size() + 1, 0);
-    if (!cand.empty())
-      encode_wave(c, t, blob.data(), offs.data(), 0, cand.size(), ids.data(), 0, ids.size(), oo.data(),
-                  nullptr, /*allow_memo=*/false);
+    if (!cand.empty()) {
+      // The memo holds each string's own (byte-level) encoding whatever the
+      // ctx's split pattern: entries are only used for pieces inside one chunk.
+      const int32_t pattern = c.cfg.pattern;
+      c.cfg.pattern = 0;
+      try {
+        encode_wave(c, t, blob.data(), offs.data(), 0, cand.size(), ids.data(), 0, ids.size(), oo.data(),
+                    nullptr, /*allow_memo=*/false);
+      } catch (...) {
+        c.cfg.pattern = pattern;
+        throw;
+      }
+      c.cfg.pattern = pattern;
+    }
     uint64_t cap = 16;
     while (cap < (cand.size() + 256) * 8) cap <<= 1;  // load <= 1/8: a lookup resolves at its first slot
     mask = cap - 1;

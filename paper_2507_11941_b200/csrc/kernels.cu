@@ -33,6 +33,7 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "pretok.cuh"
 
 namespace bbpe {
 namespace {
@@ -1586,6 +1587,10 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     unsigned blocks = unsigned((a.n_rows + 1 + threads - 1) / threads);
     k_tile_first<<<blocks, threads, 0, stream>>>(a);
     ++launched;
+    if (a.pattern && a.engine != BBPE_ENGINE_BLOCK) {  // (timed with k_tile_first)
+      launch_pretok_gpt2(a.bytes, a.offsets, a.n_rows, a.rowbits, p.sm_count, stream);
+      ++launched;
+    }
   }
   if (ev) cudaEventRecord(ev[1], stream);
   if (a.engine == BBPE_ENGINE_BLOCK) {

@@ -109,6 +109,7 @@ struct EncodeArgs {
   int narrow;               // 1: 16-bit working arrays (ids < 0xFFFE, merges < 0xFFFE)
   int use_memo;             // 1: look whole pieces up in the table's piece memo first
   int tokens_input;         // 1: lpx already holds initial tokens (bbpe_block_bpe)
+  int pattern;              // 1: gpt2 split pattern chunk starts are piece boundaries (pretok.cu)
   int64_t max_passes;       // <= 0: none
 };
 

@@ -603,3 +603,49 @@ def test_device_outputs_on_empty_and_degenerate_batches(gpt2):
         enc.decode_packed(gpt2, np.array([60000], np.uint32), np.array([0, 0, 0, 1], np.uint64))
     rows = bb.encode_batch([], gpt2, bb.SpecialTokenSet(), bb.BlockConfig(256, None), 0)
     assert rows.batch_size == 0 and rows.max_len == 0
+
+
+PATTERN_CASES = [
+    b"Hello world's test", b"it's we're they've I'm you'll he'd 'S 'tis", b"  leading and trailing  ",
+    b"a\n\nb\n \nc\t\t x", b"x" * 40 + b"   " + b"1234567890" * 5, b"emoji \xf0\x9f\x98\x80 ok",
+    "café naïve Ångström".encode(), "αβγ абв 中文 가나".encode(),
+    "١٢ ²³  thin　ideo".encode(), b"\xaa\xb5\xba\x80\xff\xfe broken utf8 \xe2\x82",
+    b"...!!!???", b"'", b" ", b"'ll", b"", b"don't stop-believin' 2023/24 $5.00",
+]
+
+
+@pytest.mark.parametrize("engine", ["pieces", "nomemo"])
+def test_gpt2_pattern_mode_vs_reference(gpt2, engine):
+    """encode_reference's pattern mode (ref_engines.hpp:119-146) with the gpt2
+    splitter on the device: identical ids to the reference
+    (oracle/_ref: pattern_pretokenize + heap_bpe) on contractions, whitespace
+    runs and backoff, unicode letters/numbers/spaces, broken UTF-8, and Zipf
+    text; the chunk starts equal the reference splitter's."""
+    from oracle.oracle import Reference
+    from paper_2507_11941_b200 import synth
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ids_, off_, blob_, m4_ = gpt2.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 2000, 256, seed=61)
+    rows = PATTERN_CASES + [bytes(data[int(off[i]):int(off[i + 1])]) for i in range(off.size - 1)]
+    d, o = bb.pack_rows(rows)
+    want_ids, want_off = ref.encode_pattern(d, o, "gpt2", workers=8)
+    enc = bb.Encoder(0, pattern="gpt2", piece_memo=(engine == "pieces"))
+    ids, oo, _ = enc.encode_packed(gpt2, d, o)
+    assert np.array_equal(oo, want_off)
+    assert np.array_equal(ids, want_ids)
+    # Byte-level and pattern mode differ somewhere on this input (the split is real).
+    b_ids, b_oo, _ = bb.Encoder(0).encode_packed(gpt2, d, o)
+    assert not np.array_equal(b_oo, oo) or not np.array_equal(b_ids, ids)
+
+
+def test_gpt2_pattern_mode_rules(gpt2):
+    with pytest.raises(bb.UsageError, match="only the gpt2 split pattern"):
+        bb.Encoder(0, pattern=r"\w+")
+    with pytest.raises(bb.UsageError, match="pieces engine"):
+        bb.Encoder(0, pattern="gpt2", engine="block")
+    enc = bb.Encoder(0, pattern=bb.api.GPT2_PATTERN)
+    ids, oo, _ = enc.encode_packed(gpt2, *bb.pack_rows([b"hello world"]))
+    assert ids.tolist() == [31373, 995]
