@@ -103,15 +103,17 @@ bool is_pinned(const void* p) {
 struct Scratch {
   DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
   DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
-  DevBuf dkey, dres, owners, offs;
+  DevBuf dkey, dres, owners, offs, chunkbits;
   uint64_t rowbits_zeroed = 0;  // words known to be zero (k_gather clears what k_tile_first set)
+  uint64_t chunkbits_zeroed = 0;  // the same for the pattern splitter's chunk bits
   bool ctrl_dirty = true;       // counters/status not known to be zero (k_gather resets them)  // words known to be zero (k_pieces clears what it consumes)
   void release() {
     for (DevBuf* b : {&tile_first, &status, &counters, &err, &lpo, &lpx, &lpy, &trace, &trace_count, &staging,
                       &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &rowbits, &mrec,
-                      &dkey, &dres, &owners, &offs})
+                      &dkey, &dres, &owners, &offs, &chunkbits})
       b->release();
     rowbits_zeroed = 0;
+    chunkbits_zeroed = 0;
     ctrl_dirty = true;
   }
 };
@@ -309,6 +311,14 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
     ck(cudaMemsetAsync(a.status, 0, sc.status.cap, s), "memset status");
     ck(cudaMemsetAsync(a.counters, 0, CNT_N * 4, s), "memset counters");
     sc.ctrl_dirty = false;
+  }
+  if (c.cfg.pattern && !block) {
+    sc.chunkbits.ensure(rb_words * 4);
+    a.chunkbits = sc.chunkbits.as<uint32_t>();
+    if (sc.chunkbits_zeroed < rb_words) {
+      ck(cudaMemsetAsync(a.chunkbits, 0, sc.chunkbits.cap, s), "memset chunkbits");
+      sc.chunkbits_zeroed = sc.chunkbits.cap / 4;
+    }
   }
   if (sc.rowbits_zeroed < rb_words) {
     ck(cudaMemsetAsync(a.rowbits, 0, sc.rowbits.cap, s), "memset rowbits");

@@ -177,6 +177,7 @@ __device__ __forceinline__ bool is_junction_t(const uint32_t* jt, uint32_t a, ui
 struct PieceSmem {
   uint4 win[2][kWinVec];          // bytes [b0-16, b0+kTile+32): position q at byte q+16
   uint32_t rb[2][kRowWords];      // row-start bits of positions [0, 32*kRowWords)
+  uint32_t cb[2][kRowWords];      // pattern mode: chunk-start bits, same positions
   uint32_t bd[kTile / 32 + 1];    // piece-start bits of positions [0, min(kTile, limit)); [16] = 0
   uint16_t wpre[kTile / 32 + 1];  // pieces starting in words < w
   uint16_t plist[kTile + 1];      // piece starts in order, then the end of the last piece
@@ -197,24 +198,33 @@ __device__ __forceinline__ void issue_window(PieceSmem& S, int buf, const Encode
   }
   if (lane < kRowWords / 4)
     cp_async16(&S.rb[buf][4 * lane], a.rowbits + tile * (kTile / 32) + 4 * lane, 16);
+  else if (a.chunkbits && lane < kRowWords / 2)
+    cp_async16(&S.cb[buf][4 * (lane - kRowWords / 4)], a.chunkbits + tile * (kTile / 32) + 4 * (lane - kRowWords / 4),
+               16);
 }
 
 // Window load without cp.async (input pointer not 16-byte aligned): plain
 // byte loads into the same layout.
 __device__ __noinline__ void load_window_slow(PieceSmem& S, int buf, const uint8_t* bytes, uint64_t total,
-                                              const uint32_t* rowbits, uint64_t tile, int lane) {
+                                              const uint32_t* rowbits, const uint32_t* chunkbits, uint64_t tile,
+                                              int lane) {
   const int64_t g0 = int64_t(tile) * kTile - 16;
   uint8_t* w = reinterpret_cast<uint8_t*>(S.win[buf]);
   for (int i = lane; i < kWinVec * 16; i += 32) {
     const int64_t pos = g0 + i;
     w[i] = (pos >= 0 && pos < int64_t(total)) ? bytes[pos] : 0;
   }
-  for (int i = lane; i < kRowWords; i += 32) S.rb[buf][i] = rowbits[tile * (kTile / 32) + i];
+  for (int i = lane; i < kRowWords; i += 32) {
+    S.rb[buf][i] = rowbits[tile * (kTile / 32) + i];
+    if (chunkbits) S.cb[buf][i] = chunkbits[tile * (kTile / 32) + i];
+  }
 }
 
 // Length of a long piece starting at abs (warp-cooperative, rare path).
+// In pattern mode a piece also ends at a chunk start (chunkbits).
 __device__ __noinline__ uint64_t long_piece_length(const uint64_t* offsets, uint64_t n_rows, const uint8_t* bytes,
-                                                   const uint32_t* jt, uint64_t abs, int lane) {
+                                                   const uint32_t* jt, const uint32_t* chunkbits, uint64_t abs,
+                                                   int lane) {
   uint64_t row_end = 0;
   if (lane == 0) {
     uint64_t lo = 0, hi = n_rows;  // max s with offsets[s] <= abs
@@ -227,7 +237,8 @@ __device__ __noinline__ uint64_t long_piece_length(const uint64_t* offsets, uint
   row_end = __shfl_sync(kFull, row_end, 0);
   for (uint64_t x = abs + kLmax + 1; x < row_end; x += 32) {
     const uint64_t y = x + lane;
-    const bool bnd = y < row_end && !is_junction_t(jt, bytes[y - 1], bytes[y]);
+    const bool bnd =
+        y < row_end && (!is_junction_t(jt, bytes[y - 1], bytes[y]) || (chunkbits && ((chunkbits[y >> 5] >> (y & 31)) & 1u)));
     const unsigned bm = __ballot_sync(kFull, bnd);
     if (bm) return x + __ffs(bm) - 1 - abs;
   }
@@ -399,7 +410,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     if (async) {
       cp_async_wait<1>();
     } else {
-      load_window_slow(S, buf, a.bytes, a.total, a.rowbits, tile, lane);
+      load_window_slow(S, buf, a.bytes, a.total, a.rowbits, a.chunkbits, tile, lane);
     }
     __syncwarp();
 
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
       }
       const uint32_t other = __shfl_down_sync(kFull, m, 1);
       if ((lane & 1) == 0) {
-        uint32_t wbits = m | (other << 16) | S.rb[buf][lane >> 1];
+        uint32_t wbits = m | (other << 16) | S.rb[buf][lane >> 1] | (a.chunkbits ? S.cb[buf][lane >> 1] : 0u);
         const int64_t q0 = 16 * lane;  // word (lane/2) covers [q0, q0 + 32)
         if (q0 + 32 > limit) wbits &= limit <= q0 ? 0u : ((1u << (limit - q0)) - 1u);
         S.bd[lane >> 1] = wbits;
@@ -456,7 +467,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     {
       const int p = kTile + lane;
       const uint32_t pa = wb[p + 15], pc = wb[p + 16];
-      const bool cut = p >= limit || ((S.rb[buf][p >> 5] >> (p & 31)) & 1u) || !is_junction_t(s_jt, pa, pc);
+      const bool cut = p >= limit || (((S.rb[buf][p >> 5] | (a.chunkbits ? S.cb[buf][p >> 5] : 0u)) >> (p & 31)) & 1u) ||
+                       !is_junction_t(s_jt, pa, pc);
       const unsigned cm = __ballot_sync(kFull, cut);
       last_end = cm ? kTile + __ffs(cm) - 1 : kTile + 32;
       if (limit < kTile) last_end = int(limit);
@@ -603,7 +615,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
       for (uint32_t i = 0; i < nlong; ++i) {
         const int k = S.lk[i];
         const uint64_t abs = b0 + S.plist[k];
-        const uint64_t len = long_piece_length(a.offsets, a.n_rows, a.bytes, s_jt, abs, lane);
+        const uint64_t len = long_piece_length(a.offsets, a.n_rows, a.bytes, s_jt, a.chunkbits, abs, lane);
         if (lane == 0) {
           if (lfirst + i < a.lp_cap) a.lrec[lfirst + i] = LongRec{abs, len, 0, S.cnt[k], 0u};
           if (x0 + i < a.long_cap) a.long_idx[x0 + i] = uint32_t(lfirst + i);
@@ -1453,6 +1465,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
     if (t == 0 && lane < CNT_N) a.counters[lane] = 0;
     // The tile's row-start bits are consumed: leave them zero for the next encode.
     if (a.rowbits && lane < kTile / 32) a.rowbits[t * (kTile / 32) + lane] = 0;
+    if (a.chunkbits && lane < kTile / 32) a.chunkbits[t * (kTile / 32) + lane] = 0;
     const uint32_t nl = uint32_t(rec & 0xFFFFFF);
     const uint64_t lfirst = rec >> 24;
     const LongView LV{G, a.lrec + lfirst, nl};
@@ -1588,7 +1601,7 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     k_tile_first<<<blocks, threads, 0, stream>>>(a);
     ++launched;
     if (a.pattern && a.engine != BBPE_ENGINE_BLOCK) {  // (timed with k_tile_first)
-      launch_pretok_gpt2(a.bytes, a.offsets, a.n_rows, a.rowbits, p.sm_count, stream);
+      launch_pretok_gpt2(a.bytes, a.offsets, a.tile_first, a.n_rows, a.total, a.rowbits, a.chunkbits, p.sm_count, stream);
       ++launched;
     }
   }

@@ -80,6 +80,7 @@ struct EncodeArgs {
   uint32_t* tile_slots;     // num_tiles: staging slots the tile used (incl. reserved)
   uint64_t* tile_lrec;      // num_tiles: (first LongRec << 24) | n long pieces, 0 when none
   uint32_t* rowbits;        // (num_tiles + 1) * (kTile/32) + kRowWords words: row-start bit per byte
+  uint32_t* chunkbits;      // same layout, pattern mode only (else null): split-pattern chunk starts
   int bytes_aligned;        // bytes pointer is 16-byte aligned (cp.async window loads)
   ulonglong2* mrec;         // mrec_cap merge records (CNT_MREC allocated); k_merge
                             // leaves an owner's token count in .y

@@ -649,3 +649,26 @@ def test_gpt2_pattern_mode_rules(gpt2):
     enc = bb.Encoder(0, pattern=bb.api.GPT2_PATTERN)
     ids, oo, _ = enc.encode_packed(gpt2, *bb.pack_rows([b"hello world"]))
     assert ids.tolist() == [31373, 995]
+
+
+def test_gpt2_pattern_mode_long_rows_and_newline_runs(gpt2):
+    """The span-parallel splitter restarts after newlines: long rows with and
+    without newlines, newline runs, CR/LF, and rows of one character class,
+    against the reference splitter (chunk starts) and pattern encode."""
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ids_, off_, blob_, m4_ = gpt2.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    rng = np.random.default_rng(71)
+    alphabet = list(b"ab cd\n\n\r\t'sll.,!0123 ") + ["é".encode(), "αβ".encode(), b"\xe3\x80\x80", b"\xc2\xa0"]
+    rows = []
+    for _ in range(60):
+        n = int(rng.integers(0, 3000))
+        rows.append(b"".join(alphabet[i] if isinstance(alphabet[i], bytes) else bytes([alphabet[i]])
+                             for i in rng.integers(0, len(alphabet), n)))
+    rows += [b"word " * 2000, b"\n" * 500 + b"x", b"x\n" * 700, b"a" * 5000, b" \n \n  \n\t\n" * 90]
+    d, o = bb.pack_rows(rows)
+    want_ids, want_off = ref.encode_pattern(d, o, "gpt2", workers=8)
+    ids, oo, _ = bb.Encoder(0, pattern="gpt2").encode_packed(gpt2, d, o)
+    assert np.array_equal(oo, want_off) and np.array_equal(ids, want_ids)
