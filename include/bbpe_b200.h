@@ -191,6 +191,28 @@ int bbpe_pad_device(bbpe_ctx* ctx, const uint32_t* d_ids, const uint64_t* d_tok_
                     uint32_t pad_id, uint32_t bos_id, uint32_t eos_id, uint64_t max_len, uint32_t* d_out_ids,
                     uint32_t* d_lengths, uint8_t* d_mask, uint64_t* truncated_rows);
 
+/* ---- special tokens on the device ----
+ * bbpe_ctx_set_specials replaces the ctx's special-token set (SpecialTokenSet,
+ * merge_table.hpp:309-369): n byte strings blob[offsets[i], offsets[i+1]) with
+ * ids[i]; empty or duplicate strings are BBPE_USAGE; n = 0 clears the set.
+ * bbpe_encode_batch_device then produces encode_batch's rows (batch.hpp:64-126,
+ * unpadded) as CSR: each row split at the specials (split_specials,
+ * pretokenize.hpp:32-57: greedy, longest special first), literal segments
+ * BPE-encoded, special ids passed through, bos_id / eos_id added unless
+ * 0xFFFFFFFF. All buffers are device buffers; out_capacity ids are available
+ * at d_out_ids (BBPE_USAGE if the rows need more); *n_out_ids receives the
+ * total. Errors carry the input row ("row r: "). Synchronous. */
+int bbpe_ctx_set_specials(bbpe_ctx* ctx, size_t n, const uint8_t* blob, const uint64_t* offsets,
+                          const uint32_t* ids);
+int bbpe_encode_batch_device(bbpe_ctx* ctx, const bbpe_table* t, const uint8_t* d_bytes,
+                             const uint64_t* d_offsets, size_t n_rows, uint64_t total_bytes, uint32_t bos_id,
+                             uint32_t eos_id, uint32_t* d_out_ids, uint64_t out_capacity,
+                             uint64_t* d_out_offsets, uint64_t* n_out_ids);
+/* The same on host buffers (offsets[0] may be non-zero; out_offsets start at 0). */
+int bbpe_encode_batch(bbpe_ctx* ctx, const bbpe_table* t, const uint8_t* bytes, const uint64_t* offsets,
+                      size_t n_rows, uint32_t bos_id, uint32_t eos_id, uint32_t* out_ids, uint64_t out_capacity,
+                      uint64_t* out_offsets, uint64_t* n_out_ids);
+
 /* ---- per-device encode contexts ---- */
 int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out);
 int bbpe_ctx_destroy(bbpe_ctx* ctx);

@@ -291,6 +291,31 @@ class Encoder {
                               offsets.data(), n, ids.data(), ids.size(), out_offsets.data(), nullptr));
     ids.resize(out_offsets[n]);
   }
+  // encode_batch's rows as CSR: split at `specials` on the device, BOS/EOS
+  // added (bbpe_ctx_set_specials + bbpe_encode_batch).
+  void encode_rows_csr(const MergeTable& t, const SpecialTokenSet& specials, bool add_bos, bool add_eos,
+                       const std::string& bytes, const std::vector<std::uint64_t>& offsets, std::vector<TokenId>& ids,
+                       std::vector<std::uint64_t>& out_offsets) {
+    std::string blob;
+    std::vector<std::uint64_t> so{0};
+    std::vector<std::uint32_t> sid;
+    for (const auto& [b, id] : specials.entries()) {
+      blob += b;
+      so.push_back(blob.size());
+      sid.push_back(id);
+    }
+    detail::check(bbpe_ctx_set_specials(h_.get(), sid.size(), reinterpret_cast<const std::uint8_t*>(blob.data()),
+                                        so.data(), sid.data()));
+    const std::size_t n = offsets.size() - 1;
+    ids.resize(offsets.back() - offsets.front() + 2 * n + 1);
+    out_offsets.resize(n + 1);
+    std::uint64_t k = 0;
+    detail::check(bbpe_encode_batch(h_.get(), t.handle(), reinterpret_cast<const std::uint8_t*>(bytes.data()),
+                                    offsets.data(), n, add_bos ? *specials.bos_id() : 0xFFFFFFFFu,
+                                    add_eos ? *specials.eos_id() : 0xFFFFFFFFu, ids.data(), ids.size(),
+                                    out_offsets.data(), &k));
+    ids.resize(k);
+  }
 
  private:
   struct Del {
@@ -323,8 +348,8 @@ struct BatchLimits {
   std::optional<std::uint32_t> max_len;
 };
 
-// batch.hpp:64-126 -- specials split on the host, literal segments merged on
-// the GPU, rows assembled with BOS/EOS, padding, mask and truncation.
+// batch.hpp:64-126 -- specials split, literal segments merged and BOS/EOS
+// added on the GPU; padding, mask and truncation assembled here.
 inline BatchEncoding encode_batch(const std::vector<std::string>& inputs, const MergeTable& table,
                                   const SpecialTokenSet& specials, const BlockConfig& config,
                                   TokenId pad_id, bool add_bos, bool add_eos, Encoder* encoder = nullptr,
@@ -334,61 +359,18 @@ inline BatchEncoding encode_batch(const std::vector<std::string>& inputs, const 
   if (add_eos && !specials.eos_id()) throw UsageError("add_eos requires an eos entry in the special token set");
   Encoder& enc = encoder ? *encoder : default_encoder();
   enc.configure(config);
-  // Device rows: literal segments (one per input when there are no specials).
+  // Rows split at the specials, encoded, BOS/EOS added -- all on the device.
   std::string blob;
   std::vector<std::uint64_t> offs{0};
-  std::vector<std::size_t> seg_row;
-  struct Item {
-    bool special;
-    TokenId id;
-    std::size_t seg;
-  };
-  std::vector<std::vector<Item>> plan(inputs.size());
-  for (std::size_t r = 0; r < inputs.size(); ++r) {
-    if (specials.empty()) {
-      plan[r].push_back({false, 0, seg_row.size()});
-      blob += inputs[r];
-      offs.push_back(blob.size());
-      seg_row.push_back(r);
-      continue;
-    }
-    for (auto& s : split_specials(inputs[r], specials)) {
-      if (s.kind == Segment::Kind::special) {
-        plan[r].push_back({true, *s.special_id, 0});
-      } else {
-        plan[r].push_back({false, 0, seg_row.size()});
-        blob += s.bytes;
-        offs.push_back(blob.size());
-        seg_row.push_back(r);
-      }
-    }
+  for (const std::string& in : inputs) {
+    blob += in;
+    offs.push_back(blob.size());
   }
   std::vector<TokenId> ids;
   std::vector<std::uint64_t> oo;
-  try {
-    enc.encode_csr(table, blob, offs, ids, oo);
-  } catch (const Error& e) {
-    // Row tags from the device refer to segments; report the input row.
-    std::string m = e.what();
-    if (m.rfind("row ", 0) == 0) {
-      const std::size_t colon = m.find(':');
-      const std::size_t seg = std::stoull(m.substr(4, colon - 4));
-      m = "row " + std::to_string(seg_row.at(seg)) + m.substr(colon);
-    }
-    if (dynamic_cast<const IntegrityError*>(&e)) throw IntegrityError(m);
-    if (dynamic_cast<const UsageError*>(&e)) throw UsageError(m);
-    throw Error(m);
-  }
+  enc.encode_rows_csr(table, specials, add_bos, add_eos, blob, offs, ids, oo);
   std::vector<TokenSeq> rows(inputs.size());
-  for (std::size_t r = 0; r < inputs.size(); ++r) {
-    TokenSeq& row = rows[r];
-    if (add_bos) row.push_back(*specials.bos_id());
-    for (const Item& it : plan[r]) {
-      if (it.special) row.push_back(it.id);
-      else row.insert(row.end(), ids.begin() + oo[it.seg], ids.begin() + oo[it.seg + 1]);
-    }
-    if (add_eos) row.push_back(*specials.eos_id());
-  }
+  for (std::size_t r = 0; r < inputs.size(); ++r) rows[r].assign(ids.begin() + oo[r], ids.begin() + oo[r + 1]);
   BatchEncoding out;
   out.batch_size = inputs.size();
   out.pad_id = pad_id;

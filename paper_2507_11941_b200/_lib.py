@@ -84,6 +84,11 @@ SIGNATURES = {
     "bbpe_batch_widest_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int, u64p]),
     "bbpe_pad_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint32,
                                   C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
+    "bbpe_ctx_set_specials": (C.c_int, [C.c_void_p, C.c_size_t, u8p, u64p, u32p]),
+    "bbpe_encode_batch_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64,
+                                           C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, u64p]),
+    "bbpe_encode_batch": (C.c_int, [C.c_void_p, C.c_void_p, u8p, u64p, C.c_size_t, C.c_uint32, C.c_uint32, u32p,
+                                    C.c_uint64, u64p, u64p]),
     "bbpe_ctx_create": (C.c_int, [C.c_int, C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "bbpe_ctx_destroy": (C.c_int, [C.c_void_p]),
     "bbpe_ctx_set_config": (C.c_int, [C.c_void_p, C.POINTER(Config)]),

@@ -397,6 +397,7 @@ class Encoder:
         self.wave_bytes = wave_bytes
         self.piece_memo = piece_memo
         self._h = C.c_void_p()
+        self._sp_key = ()
         _check(LIB.bbpe_ctx_create(device, C.byref(self._cfg()), C.byref(self._h)))
 
     def _cfg(self) -> Config:
@@ -482,6 +483,50 @@ class Encoder:
 
     def sync(self):
         _check(LIB.bbpe_ctx_sync(self._h))
+
+    def set_specials(self, specials: Optional["SpecialTokenSet"]):
+        """The device copy of a special-token set (bbpe_ctx_set_specials); None clears it."""
+        ents = specials.entries() if specials is not None else []
+        key = tuple(ents)
+        if key == self._sp_key:
+            return
+        blob = np.frombuffer(b"".join(b for b, _ in ents) or b"\0", dtype=np.uint8)
+        offs = np.zeros(len(ents) + 1, np.uint64)
+        offs[1:] = np.cumsum([len(b) for b, _ in ents], dtype=np.uint64)
+        ids = np.array([i for _, i in ents] or [0], np.uint32)
+        _check(LIB.bbpe_ctx_set_specials(self._h, len(ents), _p(blob, C.c_uint8), _p(offs, C.c_uint64),
+                                         _p(ids, C.c_uint32)))
+        self._sp_key = key
+
+    def encode_batch_packed(self, table: MergeTable, data: np.ndarray, offsets: np.ndarray,
+                            bos_id: Optional[int] = None, eos_id: Optional[int] = None):
+        """Host buffers through bbpe_encode_batch (what the C++ drop-in calls):
+        encode_batch's rows as CSR (ids u32, offsets u64[n+1])."""
+        data = np.ascontiguousarray(data, dtype=np.uint8)
+        offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
+        n = offsets.size - 1
+        ids = np.empty(max(int(offsets[-1] - offsets[0]) + 2 * n + 1, 1), np.uint32)
+        oo = np.empty(n + 1, np.uint64)
+        k = C.c_uint64()
+        none = 0xFFFFFFFF
+        _check(LIB.bbpe_encode_batch(self._h, table.handle, _p(data, C.c_uint8) if data.size else None,
+                                     _p(offsets, C.c_uint64), n, none if bos_id is None else bos_id,
+                                     none if eos_id is None else eos_id, _p(ids, C.c_uint32), ids.size,
+                                     _p(oo, C.c_uint64), C.byref(k)))
+        return ids[: k.value], oo
+
+    def encode_batch_device(self, table: MergeTable, d_bytes, d_offsets, n: int, total: int, d_out_ids, cap: int,
+                            d_out_offsets, bos_id: Optional[int] = None, eos_id: Optional[int] = None) -> int:
+        """encode_batch's rows as device CSR (bbpe_encode_batch_device): split at
+        this encoder's special tokens (set_specials), literal segments encoded,
+        special ids passed through, BOS/EOS added. Returns the id count."""
+        nout = C.c_uint64()
+        none = 0xFFFFFFFF
+        _check(LIB.bbpe_encode_batch_device(self._h, table.handle, C.c_void_p(d_bytes), C.c_void_p(d_offsets), n,
+                                            total, none if bos_id is None else bos_id,
+                                            none if eos_id is None else eos_id, C.c_void_p(d_out_ids), cap,
+                                            C.c_void_p(d_out_offsets), C.byref(nout)))
+        return nout.value
 
     def decode_packed(self, table: MergeTable, ids: np.ndarray, offsets: np.ndarray,
                       out: Optional[np.ndarray] = None, out_offsets: Optional[np.ndarray] = None):
@@ -606,10 +651,32 @@ def _remap_row_error(e: Error, seg_row: Sequence[int]):
     raise type(e)(f"row {r}: {str(e)[m.end():]}") from None
 
 
+def _encode_rows_device(rows: List[bytes], table: MergeTable, specials: SpecialTokenSet, add_bos: bool,
+                        add_eos: bool, enc: "Encoder"):
+    """Rows -> device CSR of encode_batch's rows (specials split on the device,
+    bbpe_encode_batch_device). Returns (d_ids, d_offsets, n_ids) torch tensors."""
+    import torch
+    dev = torch.device("cuda", enc.device)
+    data, offsets = pack_rows(rows)
+    n, total = len(rows), int(offsets[-1])
+    enc.set_specials(specials)
+    d_data = torch.from_numpy(data if data.flags.writeable else data.copy()).to(dev)
+    d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
+    cap = max(total + 2 * n, 1)  # literal tokens + specials <= bytes, plus BOS/EOS
+    d_ids = torch.empty(cap, dtype=torch.int32, device=dev)
+    d_oo = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    nout = enc.encode_batch_device(table, d_data.data_ptr(), d_off.data_ptr(), n, total, d_ids.data_ptr(), cap,
+                                   d_oo.data_ptr(), specials.bos_id() if add_bos else None,
+                                   specials.eos_id() if add_eos else None)
+    return d_ids, d_oo, nout
+
+
 def encode_batch_csr(inputs: Sequence[Union[bytes, str]], table: MergeTable, specials: SpecialTokenSet,
                      config: BlockConfig, add_bos: bool = False, add_eos: bool = False,
-                     encoder: Optional[Encoder] = None) -> Tuple[np.ndarray, np.ndarray]:
-    """encode_batch's per-row results as CSR (ids, offsets) -- no padding."""
+                     encoder: Optional[Encoder] = None, device_split: bool = True) -> Tuple[np.ndarray, np.ndarray]:
+    """encode_batch's per-row results as CSR (ids, offsets) -- no padding.
+    Specials are split on the device (device_split, default) or, for A/B
+    checks, on the host with the literal segments encoded on the device."""
     config.validate()
     if add_bos and specials.bos_id() is None:
         raise UsageError("add_bos requires a bos entry in the special token set")
@@ -621,11 +688,11 @@ def encode_batch_csr(inputs: Sequence[Union[bytes, str]], table: MergeTable, spe
     rows = [r.encode() if isinstance(r, str) else bytes(r) for r in inputs]
     if specials.empty() and not add_bos and not add_eos:
         data, offsets = pack_rows(rows)
-        try:
-            ids, off, _ = enc.encode_packed(table, data, offsets)
-        except Error as e:
-            raise
+        ids, off, _ = enc.encode_packed(table, data, offsets)
         return ids, off
+    if device_split:
+        d_ids, d_oo, nout = _encode_rows_device(rows, table, specials, add_bos, add_eos, enc)
+        return d_ids[:nout].cpu().numpy().view(np.uint32).copy(), d_oo.cpu().numpy().view(np.uint64).copy()
     # Specials / BOS / EOS: literal segments become device rows, re-stitched here.
     seg_rows: List[bytes] = []
     seg_row: List[int] = []
@@ -667,22 +734,15 @@ def encode_batch_csr(inputs: Sequence[Union[bytes, str]], table: MergeTable, spe
 def _encode_batch_device(rows: List[bytes], table: MergeTable, specials: SpecialTokenSet, config: BlockConfig,
                          pad_id: int, add_bos: bool, add_eos: bool, enc: "Encoder",
                          limits: Optional[BatchLimits]) -> BatchEncoding:
-    """Device epilogue: CSR encode, widest row and padding all
-    on the GPU (bbpe_encode_device, bbpe_batch_widest_device, bbpe_pad_device);
-    one copy of the padded batch back."""
+    """Device epilogue: specials split, CSR encode, BOS/EOS,
+    widest row and padding all on the GPU (bbpe_encode_batch_device,
+    bbpe_batch_widest_device, bbpe_pad_device); one copy of the padded batch back."""
     import torch
     dev = torch.device("cuda", enc.device)
-    data, offsets = pack_rows(rows)
-    n, total = len(rows), int(offsets[-1])
-    d_data = torch.from_numpy(data if data.flags.writeable else data.copy()).to(dev)
-    d_off = torch.from_numpy(offsets.view(np.int64)).to(dev)
-    d_ids = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
-    d_oo = torch.empty(n + 1, dtype=torch.int64, device=dev)
-    enc.encode_device(table, d_data.data_ptr(), d_off.data_ptr(), n, total, d_ids.data_ptr(), d_oo.data_ptr(),
-                      sync=True)
+    n = len(rows)
+    d_ids, d_oo, _ = _encode_rows_device(rows, table, specials, add_bos, add_eos, enc)
     widest = C.c_uint64()
-    _check(LIB.bbpe_batch_widest_device(enc.handle, C.c_void_p(d_oo.data_ptr()), n, int(add_bos), int(add_eos),
-                                        C.byref(widest)))
+    _check(LIB.bbpe_batch_widest_device(enc.handle, C.c_void_p(d_oo.data_ptr()), n, 0, 0, C.byref(widest)))
     out = BatchEncoding(batch_size=n, pad_id=pad_id)
     out.max_len = int(limits.max_len) if limits is not None and limits.max_len is not None else widest.value
     L = out.max_len
@@ -692,7 +752,7 @@ def _encode_batch_device(rows: List[bytes], table: MergeTable, specials: Special
     tr = C.c_uint64()
     nid = 0xFFFFFFFF
     _check(LIB.bbpe_pad_device(enc.handle, C.c_void_p(d_ids.data_ptr()), C.c_void_p(d_oo.data_ptr()), n, pad_id,
-                               specials.bos_id() if add_bos else nid, specials.eos_id() if add_eos else nid, L,
+                               nid, nid, L,
                                C.c_void_p(t_ids.data_ptr()), C.c_void_p(t_len.data_ptr()),
                                C.c_void_p(t_mask.data_ptr()), C.byref(tr)))
     out.ids = t_ids[: n * L].cpu().numpy().view(np.uint32).copy()
@@ -709,23 +769,22 @@ def encode_batch(inputs: Sequence[Union[bytes, str]], table: MergeTable, special
     """batch.hpp:64-126: rows encoded on the GPU, padded to max_len (or the fixed
     limits.max_len with right truncation), u8 mask. With an empty special-token
     set the padding runs on the device too (device_epilogue, default); with
-    specials the literal segments are re-stitched and padded on the host."""
+    specials as well: the rows are split at special tokens on the device
+    (device_epilogue=False: host split and padding, for A/B checks)."""
     config.validate()
     if add_bos and specials.bos_id() is None:
         raise UsageError("add_bos requires a bos entry in the special token set")
     if add_eos and specials.eos_id() is None:
         raise UsageError("add_eos requires an eos entry in the special token set")
-    # Special tokens are matched in the input text (split_specials), which
-    # happens on the host; without any, the whole batch stays on the device.
     if device_epilogue is None:
         device_epilogue = True
-    if device_epilogue and specials.empty():
+    if device_epilogue:
         enc = encoder or default_encoder()
         if enc.config.block_size != config.block_size or enc.config.max_passes != config.max_passes:
             enc.set_config(config=config)
         rows = [r.encode() if isinstance(r, str) else bytes(r) for r in inputs]
         return _encode_batch_device(rows, table, specials, config, pad_id, add_bos, add_eos, enc, limits)
-    ids, off = encode_batch_csr(inputs, table, specials, config, add_bos, add_eos, encoder)
+    ids, off = encode_batch_csr(inputs, table, specials, config, add_bos, add_eos, encoder, device_split=False)
     n = len(inputs)
     lengths = (off[1:] - off[:-1]).astype(np.int64)
     out = BatchEncoding(batch_size=n, pad_id=pad_id)

@@ -24,6 +24,7 @@
 #include "decode.cuh"
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include "specials.cuh"
 
 namespace bbpe {
 bbpe_table* table_load_files(const char* vocab, const char* merges, int format);
@@ -197,6 +198,11 @@ struct bbpe_ctx {
   DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff;
   DevBuf pad_scalar;  // epilogue: widest row / truncated count
   DevBuf run_base;
+  // Special-token set (bbpe_ctx_set_specials), longest first, and the scratch
+  // of bbpe_encode_batch_device.
+  uint32_t sp_n = 0;
+  DevBuf sp_blob, sp_off, sp_id, sp_first;
+  DevBuf sp_cand, sp_cnt, sp_lit, sp_sums, sp_segoff, sp_segsrc, sp_ids, sp_compact, sp_segtok, sp_segtokoff;
 };
 
 namespace {
@@ -1208,6 +1214,213 @@ int bbpe_pad_device(bbpe_ctx* c, const uint32_t* d_ids, const uint64_t* d_tok_of
   BBPE_CATCH
 }
 
+int bbpe_ctx_set_specials(bbpe_ctx* c, size_t n, const uint8_t* blob, const uint64_t* offsets,
+                          const uint32_t* ids) {
+  BBPE_TRY
+  if (!c) throw bbpe::usage_error("null ctx");
+  if (n && (!blob || !offsets || !ids)) throw bbpe::usage_error("null argument");
+  // SpecialTokenSet::add (merge_table.hpp:311-319): non-empty, unique, kept
+  // longest first (a new entry goes after every entry at least as long).
+  struct Ent {
+    std::string b;
+    uint32_t id;
+  };
+  std::vector<Ent> es;
+  for (size_t i = 0; i < n; ++i) {
+    if (offsets[i + 1] < offsets[i]) throw bbpe::usage_error("special offsets must be non-decreasing");
+    std::string b(reinterpret_cast<const char*>(blob + offsets[i]), offsets[i + 1] - offsets[i]);
+    if (b.empty()) throw bbpe::usage_error("special token byte string may not be empty");
+    for (const Ent& e : es)
+      if (e.b == b) throw bbpe::usage_error("duplicate special token \"" + b + "\"");
+    auto it = es.begin();
+    while (it != es.end() && it->b.size() >= b.size()) ++it;
+    es.insert(it, Ent{std::move(b), ids[i]});
+  }
+  std::vector<uint8_t> hb;
+  std::vector<uint32_t> ho{0}, hi, hf(8, 0);
+  for (const Ent& e : es) {
+    hb.insert(hb.end(), e.b.begin(), e.b.end());
+    if (hb.size() > 0xFFFFFFFFull) throw bbpe::usage_error("special tokens too long");
+    ho.push_back(uint32_t(hb.size()));
+    hi.push_back(e.id);
+    const uint8_t f = uint8_t(e.b[0]);
+    hf[f >> 5] |= 1u << (f & 31);
+  }
+  DeviceGuard g(c->device);
+  c->sp_n = 0;
+  if (es.empty()) return BBPE_OK;
+  c->sp_blob.ensure(hb.size());
+  c->sp_off.ensure(ho.size() * 4);
+  c->sp_id.ensure(hi.size() * 4);
+  c->sp_first.ensure(32);
+  ck(cudaMemcpy(c->sp_blob.p, hb.data(), hb.size(), cudaMemcpyHostToDevice), "specials upload");
+  ck(cudaMemcpy(c->sp_off.p, ho.data(), ho.size() * 4, cudaMemcpyHostToDevice), "specials upload");
+  ck(cudaMemcpy(c->sp_id.p, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice), "specials upload");
+  ck(cudaMemcpy(c->sp_first.p, hf.data(), 32, cudaMemcpyHostToDevice), "specials upload");
+  c->sp_n = uint32_t(es.size());
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+namespace {
+
+// bbpe_encode_batch_device's body; returns the id total.
+uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
+                                const uint64_t* d_offsets, size_t n, uint64_t total_bytes, uint32_t bos_id,
+                                uint32_t eos_id, uint32_t* d_out_ids, uint64_t out_capacity,
+                                uint64_t* d_out_offsets) {
+  validate_config(c->cfg);
+  DeviceGuard g(c->device);
+  ensure_plan(*c);
+  maybe_build_memo(*c, *t);
+  cudaStream_t s = c->stream;
+  const uint32_t none = 0xFFFFFFFFu;
+  const int add_bos = bos_id != none, add_eos = eos_id != none;
+  const int sm = c->plan.sm_count;
+  auto read_u64 = [&](const void* p) {
+    uint64_t v = 0;
+    ck(cudaMemcpyAsync(&v, p, 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "specials");
+    return v;
+  };
+  // (1) split at special tokens: per-row match counts and literal bytes, scanned.
+  c->sp_cnt.ensure((n + 1) * 8);
+  c->sp_sums.ensure(bbpe::scan_sums_len(n) * 8);
+  uint64_t* match_base = c->sp_cnt.as<uint64_t>();
+  uint64_t M = 0;
+  bbpe::SpecArgs sp{c->sp_blob.as<uint8_t>(), c->sp_off.as<uint32_t>(), c->sp_id.as<uint32_t>(),
+                    c->sp_first.as<uint32_t>(), c->sp_n};
+  if (c->sp_n && total_bytes) {
+    c->sp_cand.ensure((total_bytes + 31) / 32 * 4);
+    c->sp_lit.ensure((n + 1) * 8);
+    bbpe::launch_sp_candidates(d_bytes, total_bytes, sp, c->sp_cand.as<uint32_t>(), sm, s);
+    bbpe::launch_sp_rows(d_bytes, d_offsets, n, sp, c->sp_cand.as<uint32_t>(), match_base,
+                         c->sp_lit.as<uint64_t>(), s);
+    bbpe::launch_scan_u64(match_base, n, c->sp_sums.as<uint64_t>(), s);
+    c->launches += 2 + (n ? 3 : 0);
+    M = read_u64(match_base + n);
+  } else {
+    ck(cudaMemsetAsync(match_base, 0, (n + 1) * 8, s), "memset");
+  }
+  if (M == 0 && !add_bos && !add_eos && out_capacity >= total_bytes) {  // plain CSR encode
+    enqueue_encode(*c, c->sc, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
+    ck(cudaStreamSynchronize(s), "encode");
+    check_device_errors(*c, nullptr, n, 0, nullptr, d_offsets, d_bytes);
+    return read_u64(d_out_offsets + n);
+  }
+  // (2) literal segments: r + match_base[r] + j, j = 0..matches(r), compacted.
+  const uint8_t* seg_bytes = d_bytes;
+  const uint64_t* seg_offsets = d_offsets;
+  uint64_t n_seg = n, seg_total = total_bytes;
+  if (M) {
+    bbpe::launch_scan_u64(c->sp_lit.as<uint64_t>(), n, c->sp_sums.as<uint64_t>(), s);
+    seg_total = read_u64(c->sp_lit.as<uint64_t>() + n);
+    n_seg = n + M;
+    c->sp_segoff.ensure((n_seg + 1) * 8);
+    c->sp_segsrc.ensure(n_seg * 8);
+    c->sp_ids.ensure(M * 4);
+    c->sp_compact.ensure(seg_total + 16);
+    bbpe::launch_sp_emit(d_bytes, d_offsets, n, sp, c->sp_cand.as<uint32_t>(), match_base,
+                         c->sp_lit.as<uint64_t>(), c->sp_segoff.as<uint64_t>(), c->sp_segsrc.as<uint64_t>(),
+                         c->sp_ids.as<uint32_t>(), s);
+    bbpe::launch_sp_copy(d_bytes, n_seg, c->sp_segoff.as<uint64_t>(), c->sp_segsrc.as<uint64_t>(),
+                         c->sp_compact.as<uint8_t>(), sm, s);
+    c->launches += 5;
+    seg_bytes = c->sp_compact.as<uint8_t>();
+    seg_offsets = c->sp_segoff.as<uint64_t>();
+  }
+  // (3) encode the literal segments as rows.
+  c->sp_segtok.ensure(std::max<uint64_t>(seg_total, 1) * 4);
+  c->sp_segtokoff.ensure((n_seg + 1) * 8);
+  enqueue_encode(*c, c->sc, *t, seg_bytes, seg_offsets, n_seg, seg_total, c->sp_segtok.as<uint32_t>(),
+                 c->sp_segtokoff.as<uint64_t>(), s);
+  ck(cudaStreamSynchronize(s), "encode");
+  try {
+    check_device_errors(*c, nullptr, n_seg, 0, nullptr, seg_offsets, seg_bytes);
+  } catch (const bbpe::Error& e) {
+    // "row <segment>: ..." -> the input row holding that segment.
+    const std::string m = e.what();
+    if (!M || m.compare(0, 4, "row ") != 0) throw;
+    const size_t colon = m.find(':');
+    const uint64_t seg = std::stoull(m.substr(4, colon - 4));
+    std::vector<uint64_t> mb(n + 1);
+    ck(cudaMemcpy(mb.data(), match_base, (n + 1) * 8, cudaMemcpyDeviceToHost), "D2H");
+    uint64_t lo = 0, hi = n - 1;  // max r with r + mb[r] <= seg
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) / 2;
+      if (mid + mb[mid] <= seg) lo = mid; else hi = mid - 1;
+    }
+    throw bbpe::Error(e.code, "row " + std::to_string(lo) + m.substr(colon));
+  }
+  // (4) stitch: BOS, segment tokens, special ids, EOS.
+  bbpe::launch_sp_lengths(n, match_base, c->sp_segtokoff.as<uint64_t>(), add_bos, add_eos, d_out_offsets, s);
+  bbpe::launch_scan_u64(d_out_offsets, n, c->sp_sums.as<uint64_t>(), s);
+  const uint64_t out_total = read_u64(d_out_offsets + n);
+  if (out_total > out_capacity)
+    throw bbpe::usage_error("output capacity " + std::to_string(out_capacity) + " < " +
+                            std::to_string(out_total) + " ids");
+  if (out_total && !d_out_ids) throw bbpe::usage_error("null output ids");
+  bbpe::launch_sp_stitch(n, match_base, c->sp_segtokoff.as<uint64_t>(), c->sp_segtok.as<uint32_t>(),
+                         c->sp_ids.as<uint32_t>(), d_out_offsets, bos_id, eos_id, d_out_ids, sm, s);
+  c->launches += n ? 5 : 1;
+  ck(cudaStreamSynchronize(s), "stitch");
+  return out_total;
+}
+
+}  // namespace
+
+int bbpe_encode_batch_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
+                             const uint64_t* d_offsets, size_t n, uint64_t total_bytes, uint32_t bos_id,
+                             uint32_t eos_id, uint32_t* d_out_ids, uint64_t out_capacity, uint64_t* d_out_offsets,
+                             uint64_t* n_out_ids) {
+  BBPE_TRY
+  if (!c || !t || !d_offsets || !d_out_offsets) throw bbpe::usage_error("null argument");
+  if (total_bytes && !d_bytes) throw bbpe::usage_error("null bytes");
+  const uint64_t k = encode_batch_on_device(c, t, d_bytes, d_offsets, n, total_bytes, bos_id, eos_id, d_out_ids,
+                                            out_capacity, d_out_offsets);
+  if (n_out_ids) *n_out_ids = k;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_encode_batch(bbpe_ctx* c, const bbpe_table* t, const uint8_t* bytes, const uint64_t* offsets, size_t n,
+                      uint32_t bos_id, uint32_t eos_id, uint32_t* out_ids, uint64_t out_capacity,
+                      uint64_t* out_offsets, uint64_t* n_out_ids) {
+  BBPE_TRY
+  if (!c || !t || !offsets || !out_offsets) throw bbpe::usage_error("null argument");
+  const uint64_t base = offsets[0], total = offsets[n] - base;
+  if (total && !bytes) throw bbpe::usage_error("null bytes");
+  for (size_t i = 0; i < n; ++i)
+    if (offsets[i + 1] < offsets[i]) throw bbpe::usage_error("offsets must be non-decreasing");
+  DeviceGuard g(c->device);
+  validate_config(c->cfg);
+  ensure_plan(*c);
+  maybe_build_memo(*c, *t);  // first: the memo build encodes through in_bytes / out_ids
+  std::vector<uint64_t> rel(n + 1);
+  for (size_t i = 0; i <= n; ++i) rel[i] = offsets[i] - base;
+  const uint64_t cap = total + 2 * uint64_t(n) + 1;  // literal tokens + specials <= bytes, plus BOS/EOS
+  c->in_bytes.ensure(std::max<uint64_t>(total, 1) + 16);
+  c->in_offsets.ensure((n + 1) * 8);
+  c->out_ids.ensure(cap * 4);
+  c->out_offsets.ensure((n + 1) * 8);
+  if (total)
+    ck(cudaMemcpyAsync(c->in_bytes.p, bytes + base, total, cudaMemcpyHostToDevice, c->stream), "H2D bytes");
+  ck(cudaMemcpyAsync(c->in_offsets.p, rel.data(), (n + 1) * 8, cudaMemcpyHostToDevice, c->stream), "H2D offsets");
+  const uint64_t k = encode_batch_on_device(c, t, c->in_bytes.as<uint8_t>(), c->in_offsets.as<uint64_t>(), n, total,
+                                            bos_id, eos_id, c->out_ids.as<uint32_t>(), cap,
+                                            c->out_offsets.as<uint64_t>());
+  if (k > out_capacity)
+    throw bbpe::usage_error("output capacity " + std::to_string(out_capacity) + " < " + std::to_string(k) +
+                            " ids");
+  if (k && !out_ids) throw bbpe::usage_error("null output ids");
+  if (k) ck(cudaMemcpyAsync(out_ids, c->out_ids.p, k * 4, cudaMemcpyDeviceToHost, c->stream), "D2H ids");
+  ck(cudaMemcpyAsync(out_offsets, c->out_offsets.p, (n + 1) * 8, cudaMemcpyDeviceToHost, c->stream), "D2H offsets");
+  ck(cudaStreamSynchronize(c->stream), "D2H");
+  if (n_out_ids) *n_out_ids = k;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
 int bbpe_ctx_create(int device, const bbpe_config* cfg, bbpe_ctx** out) {
   BBPE_TRY
   if (!out) throw bbpe::usage_error("out is null");
@@ -1235,7 +1448,10 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaStreamSynchronize(c->stream);
     c->sc.release();
     for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_sums,
-                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar})
+                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar,
+                      &c->sp_blob, &c->sp_off, &c->sp_id, &c->sp_first, &c->sp_cand, &c->sp_cnt, &c->sp_lit,
+                      &c->sp_sums, &c->sp_segoff, &c->sp_segsrc, &c->sp_ids, &c->sp_compact, &c->sp_segtok,
+                      &c->sp_segtokoff})
       b->release();
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);

@@ -62,6 +62,21 @@ int main(int argc, char** argv) {
   EXPECT((bb::decode_batch(e5, gpt2, sp, true) == std::vector<std::string>{"hello world", "...."}));
   bb::Encoder gpu0(0);  // decode_batch on the device
   EXPECT((bb::decode_batch(e5, gpt2, sp, true, &gpu0) == std::vector<std::string>{"hello world", "...."}));
+  // Specials split on the device: greedy, longest first,
+  // special bytes never encoded, errors name the input row.
+  bb::SpecialTokenSet sx;
+  sx.add("x", 900);
+  sx.add("xab", 901);
+  auto e7 = bb::encode_batch({"abx", "xab", "x", "abxxab"}, toy, sx, cfg, 99, false, false, &gpu0);
+  EXPECT((e7.row(0) == bb::TokenSeq{3, 900} && e7.row(1) == bb::TokenSeq{901} && e7.row(2) == bb::TokenSeq{900}));
+  EXPECT((e7.row(3) == bb::TokenSeq{3, 900, 901}));
+  threw = false;
+  try {
+    bb::encode_batch({"abx", "xab", "xay", "ab"}, toy, sx, cfg, 99, false, false, &gpu0);
+  } catch (const bb::IntegrityError& e) {
+    threw = std::string(e.what()).rfind("row 2: ", 0) == 0;
+  }
+  EXPECT(threw);
   auto e6 = bb::encode_batch({"hello world", "", "....", "\xff" "ab"}, gpt2, none, cfg, 0, false, false, &gpu0);
   EXPECT((bb::decode_batch(e6, gpt2, none, false, &gpu0) == bb::decode_batch(e6, gpt2, none, false)));
 

@@ -672,3 +672,115 @@ def test_gpt2_pattern_mode_long_rows_and_newline_runs(gpt2):
     want_ids, want_off = ref.encode_pattern(d, o, "gpt2", workers=8)
     ids, oo, _ = bb.Encoder(0, pattern="gpt2").encode_packed(gpt2, d, o)
     assert np.array_equal(oo, want_off) and np.array_equal(ids, want_ids)
+
+
+SPECIALS = [(b"<|endoftext|>", 50256), (b"<|pad|>", 50300), (b"<|a|>", 60001), (b"<|a|>x", 60002),
+            (b"\n\n", 60003), ("é".encode(), 60004), (b"zz", 60005)]
+SPECIAL_CASES = [b"", b"<|endoftext|>", b"hi<|endoftext|>there", b"<|a|>x<|a|><|a|>xx", b"zzzzz", b"a\n\n\nb",
+                 b"<|endofte", b"xt|>", b"<|endof", b"text|>", "café é\n\n".encode(), b"<|pad|><|pad|>",
+                 b"plain text without any", b"<|a|", b"zz"]
+
+
+def _special_rows(gpt2):
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    rng = np.random.default_rng(83)
+    data, off = synth.rows_fixed(gen, 1500, 256, seed=84)
+    rows = list(SPECIAL_CASES)
+    for i in range(off.size - 1):
+        r = bytes(data[int(off[i]):int(off[i + 1])])
+        for _ in range(int(rng.integers(0, 4))):  # sprinkle specials in
+            p = int(rng.integers(0, len(r) + 1))
+            r = r[:p] + SPECIALS[int(rng.integers(0, len(SPECIALS)))][0] + r[p:]
+        rows.append(r)
+    long = b"".join(rows[15:60])  # long rows: many specials, incl. the common "\n\n"
+    rows += [long * 3, b"\n\n" * 3000 + b"x", long]
+    return rows
+
+
+@pytest.mark.parametrize("bos_eos", [(False, False), (True, False), (False, True), (True, True)])
+def test_device_specials_vs_reference(gpt2, bos_eos):
+    """encode_batch with special tokens: the device split
+    (bbpe_encode_batch_device: greedy longest-first split_specials,
+    pretokenize.hpp:32-57, literal segments encoded, ids passed through,
+    BOS/EOS) equals the compiled reference's encode_batch row for row, and
+    the host split of the same rows."""
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    add_bos, add_eos = bos_eos
+    ids_, off_, blob_, m4_ = gpt2.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    sp = bb.SpecialTokenSet()
+    for b, i in SPECIALS:
+        ref.add_special(b, i)
+        sp.add(b, i)
+    ref.add_special(b"<|endoftext|>", 50256, 1)
+    ref.add_special(b"<|pad|>", 50300, 2)
+    sp.set_bos("<|endoftext|>")
+    sp.set_eos("<|pad|>")
+    rows = _special_rows(gpt2)
+    d, o = bb.pack_rows(rows)
+    want_ids, want_off = ref.encode_batch(d, o, workers=8, add_bos=add_bos, add_eos=add_eos)
+    cfg = bb.BlockConfig(256, None)
+    ids, oo = bb.encode_batch_csr(rows, gpt2, sp, cfg, add_bos, add_eos)
+    assert np.array_equal(oo, want_off)
+    assert np.array_equal(ids, want_ids)
+    h_ids, h_oo = bb.encode_batch_csr(rows, gpt2, sp, cfg, add_bos, add_eos, device_split=False)
+    assert np.array_equal(h_oo, oo) and np.array_equal(h_ids, ids)
+    # The padded BatchEncoding from the device equals the host assembly.
+    dv = bb.encode_batch(rows[:300], gpt2, sp, cfg, 7, add_bos, add_eos, device_epilogue=True)
+    hv = bb.encode_batch(rows[:300], gpt2, sp, cfg, 7, add_bos, add_eos, device_epilogue=False)
+    assert dv.max_len == hv.max_len and np.array_equal(dv.ids, hv.ids) and np.array_equal(dv.mask, hv.mask)
+    assert np.array_equal(dv.lengths, hv.lengths)
+
+
+def test_device_specials_errors_and_rules(gpt2, tables):
+    """Special bytes are never BPE-encoded (a special may hold a byte with no
+    token); an invalid byte in a literal segment names the INPUT row; the set
+    rejects empty and duplicate strings (SpecialTokenSet::add)."""
+    toy = tables["toy"]
+    cfg = bb.BlockConfig(256, None)
+    sp = bb.SpecialTokenSet()
+    sp.add("x", 900)
+    ids, oo = bb.encode_batch_csr([b"abx", b"xab", b"x"], toy, sp, cfg)
+    plain = bb.Encoder(0).encode_rows(toy, [b"ab"])[0]
+    assert [ids[int(oo[i]):int(oo[i + 1])].tolist() for i in range(3)] == [plain + [900], [900] + plain, [900]]
+    with pytest.raises(bb.IntegrityError, match=r"^row 2: .*byte value 121"):
+        bb.encode_batch_csr([b"abx", b"xab", b"xay", b"ab"], toy, sp, cfg)
+
+    class Raw:
+        def __init__(self, e):
+            self.e = e
+
+        def entries(self):
+            return self.e
+
+    # Host entry (bbpe_encode_batch) as the FIRST call of a fresh ctx: the
+    # lazy memo build must not clobber the staged input.
+    fresh = bb.Encoder(0)
+    d0, o0 = bb.pack_rows([b"abc", b"ab", b"cab"])
+    ids0, oo0 = fresh.encode_batch_packed(toy, d0, o0)
+    assert [ids0[int(oo0[i]):int(oo0[i + 1])].tolist() for i in range(3)] == [[4], [3], [2, 3]]
+    fresh.set_specials(sp)
+    ids0, oo0 = fresh.encode_batch_packed(toy, *bb.pack_rows([b"abx", b"xabc"]), bos_id=900, eos_id=900)
+    assert ids0.tolist() == [900, 3, 900, 900, 900, 900, 4, 900] and oo0.tolist() == [0, 4, 8]
+    enc = bb.Encoder(0)
+    with pytest.raises(bb.UsageError, match="duplicate special"):
+        enc.set_specials(Raw([(b"ab", 1), (b"ab", 2)]))
+    with pytest.raises(bb.UsageError, match="may not be empty"):
+        enc.set_specials(Raw([(b"", 1)]))
+    # Longest first whatever the insertion order; n = 0 clears.
+    enc.set_specials(Raw([(b"a", 1), (b"abc", 3), (b"ab", 2)]))
+    import torch
+    d = torch.tensor(list(b"abcabxa"), dtype=torch.uint8, device="cuda")
+    o = torch.tensor([0, 7], dtype=torch.int64, device="cuda")
+    out = torch.empty(16, dtype=torch.int32, device="cuda")
+    oo = torch.empty(2, dtype=torch.int64, device="cuda")
+    n = enc.encode_batch_device(gpt2, d.data_ptr(), o.data_ptr(), 1, 7, out.data_ptr(), 16, oo.data_ptr())
+    assert n == 4 and out[:4].tolist() == [3, 2, gpt2.byte_token(ord("x")), 1] and oo.tolist() == [0, 4]
+    with pytest.raises(bb.UsageError, match="output capacity"):
+        enc.encode_batch_device(gpt2, d.data_ptr(), o.data_ptr(), 1, 7, out.data_ptr(), 3, oo.data_ptr())
+    enc.set_specials(None)
+    n = enc.encode_batch_device(gpt2, d.data_ptr(), o.data_ptr(), 1, 7, out.data_ptr(), 16, oo.data_ptr())
+    assert out[:n].tolist() == bb.Encoder(0).encode_rows(gpt2, [b"abcabxa"])[0]
