@@ -8,7 +8,7 @@ from .api import (  # noqa: F401
     BatchEncoding, BatchLimits, BlockConfig, ContractViolation, DecodeError, Encoder, Error,
     IntegrityError, MaxPassesError, MergeTable, ParseError, Segment, SpecialTokenSet, UsageError,
     block_bpe, bytes_to_initial_tokens, coarsening_factor, decode, decode_batch, default_encoder,
-    encode_batch, encode_batch_csr, encode_sharded, encode_single, load_merge_table_files, pack_rows,
+    encode_batch, encode_batch_csr, encode_sharded, gather_csr, encode_single, load_merge_table_files, pack_rows,
     parse_vocab_format, partition, read_batch_binary, read_jsonl_token_seqs, split_specials,
     validate_specials, write_batch_binary, write_batch_jsonl,
 )

@@ -484,6 +484,30 @@ class Encoder:
     def sync(self):
         _check(LIB.bbpe_ctx_sync(self._h))
 
+    def encode_tensors(self, table: MergeTable, data, offsets):
+        """Zero-copy hand-off: device tensors in, device tensors
+        out -- uint8 bytes and int64 row offsets on this encoder's GPU -> (ids
+        int32, offsets int64), CSR, on the same GPU, ordered on torch's current
+        stream. Export with torch.utils.dlpack.to_dlpack for other frameworks."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if data.device != dev or offsets.device != dev:
+            raise UsageError(f"encode_tensors needs tensors on {dev}")
+        if data.dtype != torch.uint8 or offsets.dtype != torch.int64:
+            raise UsageError("encode_tensors takes uint8 bytes and int64 offsets")
+        data, offsets = data.contiguous(), offsets.contiguous()
+        n = offsets.numel() - 1
+        if n < 0:
+            raise UsageError("offsets need n + 1 entries")
+        first, total = (int(v) for v in offsets[[0, -1]].tolist())
+        if first:
+            data, offsets, total = data[first:], offsets - first, total - first
+        ids = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        oo = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        self.encode_device(table, data.data_ptr(), offsets.data_ptr(), n, total, ids.data_ptr(), oo.data_ptr(),
+                           stream=torch.cuda.current_stream(dev).cuda_stream)
+        return ids[: int(oo[-1].item())], oo
+
     def set_specials(self, specials: Optional["SpecialTokenSet"]):
         """The device copy of a special-token set (bbpe_ctx_set_specials); None clears it."""
         ents = specials.entries() if specials is not None else []
@@ -601,6 +625,44 @@ def partition(offsets: np.ndarray, parts: int) -> np.ndarray:
     b = np.zeros(parts + 1, np.uint64)
     _check(LIB.bbpe_partition(_p(offsets, C.c_uint64), offsets.size - 1, parts, _p(b, C.c_uint64)))
     return b
+
+
+def gather_csr(ids, offsets, dst: int = 0, group=None):
+    """Per-rank CSR (ids int32 [k], offsets int64 [n+1] from 0) gathered to
+    rank `dst` as one CSR in rank order, offsets rebased: the optional
+    gather-to-one-GPU epilogue of a sharded encode. Sizes
+    are all-gathered, then ids and offsets go point to point (NCCL send/recv
+    over NVLink on GPUs, gloo on CPU). Returns (ids, offsets) on dst, None
+    elsewhere. Not on the encode path: shards never exchange data to encode."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    k, n = ids.numel(), offsets.numel() - 1
+    sz = torch.tensor([k, n], dtype=torch.int64, device=offsets.device)
+    sizes = [torch.empty_like(sz) for _ in range(world)]
+    dist.all_gather(sizes, sz, group=group)
+    sizes = [tuple(int(v) for v in t.tolist()) for t in sizes]
+    if rank != dst:
+        if k:
+            dist.send(ids.contiguous(), dst, group=group)
+        dist.send(offsets.contiguous(), dst, group=group)
+        return None
+    out_ids = torch.empty(sum(x[0] for x in sizes), dtype=ids.dtype, device=ids.device)
+    out_off = torch.empty(sum(x[1] for x in sizes) + 1, dtype=offsets.dtype, device=offsets.device)
+    tb = rb = 0
+    for r, (kr, nr) in enumerate(sizes):
+        if r == dst:
+            out_ids[tb:tb + kr] = ids
+            o = offsets
+        else:
+            if kr:
+                dist.recv(out_ids[tb:tb + kr], r, group=group)
+            o = torch.empty(nr + 1, dtype=offsets.dtype, device=offsets.device)
+            dist.recv(o, r, group=group)
+        out_off[rb:rb + nr + 1] = o + tb
+        tb += kr
+        rb += nr
+    return out_ids, out_off
 
 
 def encode_sharded(encoders: Sequence[Encoder], table: MergeTable, data: np.ndarray, offsets: np.ndarray):

@@ -784,3 +784,28 @@ def test_device_specials_errors_and_rules(gpt2, tables):
     enc.set_specials(None)
     n = enc.encode_batch_device(gpt2, d.data_ptr(), o.data_ptr(), 1, 7, out.data_ptr(), 16, oo.data_ptr())
     assert out[:n].tolist() == bb.Encoder(0).encode_rows(gpt2, [b"abcabxa"])[0]
+
+
+def test_encode_tensors_zero_copy(gpt2):
+    """Zero-copy CSR hand-off: torch device tensors in and out,
+    DLPack export shares the memory; a row window (offsets[0] != 0) works."""
+    import torch
+    from torch.utils.dlpack import from_dlpack, to_dlpack
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 3000, 200, seed=91)
+    enc = bb.Encoder(0)
+    want_ids, want_off, _ = enc.encode_packed(gpt2, data, off)
+    d = torch.from_numpy(data.copy()).cuda()
+    o = torch.from_numpy(off.view(np.int64).copy()).cuda()
+    ids, oo = enc.encode_tensors(gpt2, d, o)
+    assert ids.is_cuda and ids.dtype == torch.int32 and oo.dtype == torch.int64
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), want_ids)
+    assert np.array_equal(oo.cpu().numpy().view(np.uint64), want_off)
+    assert from_dlpack(to_dlpack(ids)).data_ptr() == ids.data_ptr()
+    sub_ids, sub_oo = enc.encode_tensors(gpt2, d, o[100:201])
+    a, b = int(want_off[100]), int(want_off[200])
+    assert np.array_equal(sub_ids.cpu().numpy().view(np.uint32), want_ids[a:b])
+    assert np.array_equal(sub_oo.cpu().numpy(), (want_off[100:201] - want_off[100]).astype(np.int64))
+    with pytest.raises(bb.UsageError):
+        enc.encode_tensors(gpt2, d.cpu(), o)

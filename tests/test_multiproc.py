@@ -59,3 +59,38 @@ def test_partition_shards_cover_rows():
     assert b[0] == 0 and b[-1] == 1000
     sizes = np.diff(b.astype(np.int64))
     assert sizes.max() - sizes.min() <= 1
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import paper_2507_11941_b200 as bb
+    # rank r holds rows of lengths r+1, r+2, ... (rank 1's shard has an empty row)
+    rng = np.random.default_rng(rank)
+    lens = [0, 3, 5] if rank == 1 else [2, 4]
+    ids = torch.tensor(rng.integers(0, 50000, sum(lens)), dtype=torch.int32)
+    off = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int64)
+    got = bb.gather_csr(ids, off, dst=0)
+    q.put((rank, None if got is None else (got[0].tolist(), got[1].tolist()), ids.tolist(), off.tolist()))
+    dist.destroy_process_group()
+
+
+def test_gather_csr_two_ranks_gloo():
+    """The optional gather-to-one-GPU epilogue (bb.gather_csr): rank order,
+    rebased offsets, empty rows kept; nothing on the non-destination rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted((q.get(timeout=240) for _ in procs), key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, got, ids0, off0), (_, none, ids1, off1) = res
+    assert none is None
+    assert got[0] == ids0 + ids1
+    assert got[1] == off0 + [o + len(ids0) for o in off1[1:]]
