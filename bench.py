@@ -446,11 +446,11 @@ def main():
         h_oo = torch.empty(n + 1, dtype=torch.int64).pin_memory()
         hd, ho = h_data.numpy(), h_off.numpy().view(np.uint64)
         hi, hoo = h_ids.numpy().view(np.uint32), h_oo.numpy().view(np.uint64)
-        for _ in range(2):
+        for _ in range(max(5, args.warmup)):
             enc.encode_packed(table, hd, ho, hi, hoo)
         barrier(world)
         times = []
-        for _ in range(max(3, args.steps // 2)):
+        for _ in range(max(10, args.steps)):
             t0 = time.perf_counter()
             enc.encode_packed(table, hd, ho, hi, hoo)
             times.append(time.perf_counter() - t0)
