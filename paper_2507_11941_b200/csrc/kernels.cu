@@ -170,7 +170,7 @@ __device__ __forceinline__ void cp_async_wait() {
 // Junction test on the transposed bitmap: bit (c << 8 | a) for the bigram (a, c).
 __device__ __forceinline__ bool is_junction_t(const uint32_t* jt, uint32_t a, uint32_t c) {
   const uint32_t bit = (c << 8) | a;
-  return (jt[bit >> 5] >> (bit & 31)) & 1u;
+  return (jt[((bit >> 5) ^ bit) & 0x7FF] >> (bit & 31)) & 1u;  // swizzled words (table.cpp)
 }
 
 // Per-warp shared state of k_pieces (double-buffered input window).
@@ -283,12 +283,13 @@ __device__ __noinline__ MemoHit memo_overflow(const MemoEntry* memo, uint64_t ma
 }
 
 // Byte masks of the 5 key words for each piece length (shared memory,
-// s_mask[8 * len + i]), built once per CTA.
+// s_mask[32 * i + len]: lanes reading word i for any mix of lengths hit
+// distinct banks or broadcast), built once per CTA.
 __device__ __forceinline__ void build_mask_table(uint32_t* s_mask) {
-  for (int i = threadIdx.x; i < (kMemoMaxLen + 1) * 8; i += blockDim.x) {
-    const int len = i >> 3, wi = i & 7;
+  for (int k = threadIdx.x; k < 5 * 32; k += blockDim.x) {
+    const int len = k & 31, wi = k >> 5;
     const int nb = len - 4 * wi;
-    s_mask[i] = wi >= 5 ? 0u : (nb >= 4 ? ~0u : (nb <= 0 ? 0u : (1u << (8 * nb)) - 1u));
+    s_mask[k] = nb >= 4 ? ~0u : (nb <= 0 ? 0u : (1u << (8 * nb)) - 1u);
   }
 }
 
@@ -296,8 +297,7 @@ __device__ __forceinline__ bool memo_lookup(const DevTable& T, const uint32_t* w
                                             int start, int len, uint32_t& r0, uint32_t& r1, uint32_t& nres) {
   const int a = start >> 2;
   const uint32_t sh = uint32_t(start & 3) * 8;
-  const uint4 m03 = *reinterpret_cast<const uint4*>(s_mask + 8 * len);
-  const uint32_t mk[5] = {m03.x, m03.y, m03.z, m03.w, s_mask[8 * len + 4]};
+  const uint32_t mk[5] = {s_mask[len], s_mask[32 + len], s_mask[64 + len], s_mask[96 + len], s_mask[128 + len]};
   uint32_t x[6], w[5];
 #pragma unroll
   for (int i = 0; i < 6; ++i) x[i] = ww[a + i];
@@ -370,7 +370,8 @@ __device__ __forceinline__ uint64_t dedup_claim(ulonglong2* dkey, uint64_t dmask
 __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_jt[2048];
   __shared__ uint32_t s_lo[256];
-  __shared__ __align__(16) uint32_t s_mask[(kMemoMaxLen + 1) * 8];
+  static_assert(kMemoMaxLen < 32, "mask table columns");
+  __shared__ __align__(16) uint32_t s_mask[5 * 32];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) s_jt[i] = T.junction_t[i];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lo[i] = T.lut_out[i];
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         const uint32_t lo = y[r >> 2];
         const uint32_t hi = ((r & 3) == 3) ? y[(r >> 2) + 1] : lo;
         const uint32_t v = __byte_perm(lo, hi, uint32_t((r & 3) | (((r & 3) + 1) << 4)));
-        const uint32_t wd = s_jt[(v >> 5) & 0x7FF];
+        const uint32_t wd = s_jt[((v >> 5) ^ v) & 0x7FF];
         jm |= (__funnelshift_r(wd, wd, v) & 1u) << j;
       }
       uint32_t m = (~jm) & 0xFFFFu;  // not a junction: boundary

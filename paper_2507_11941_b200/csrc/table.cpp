@@ -472,8 +472,11 @@ const DevTable& table_on_device(const bbpe_table& tc, int device) {
     uint32_t* jt = reinterpret_cast<uint32_t*>(host.data() + o_junct);
     for (uint32_t bit = 0; bit < 65536; ++bit)
       if ((t.junction[bit >> 5] >> (bit & 31)) & 1u) {
+        // Transposed pair v = right << 8 | left, word ((v >> 5) ^ v) & 0x7FF, bit
+        // v & 31: a bijection whose bank bits mix the left byte's low bits
+        // (the unswizzled word put ASCII text on ~12 of 32 banks).
         const uint32_t tb = ((bit & 0xFF) << 8) | (bit >> 8);
-        jt[tb >> 5] |= 1u << (tb & 31);
+        jt[((tb >> 5) ^ tb) & 0x7FF] |= 1u << (tb & 31);
       }
     uint32_t* lo = reinterpret_cast<uint32_t*>(host.data() + o_lutout);
     for (int b = 0; b < 256; ++b) lo[b] = t.byte_tokens[b];
