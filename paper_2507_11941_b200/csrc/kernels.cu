@@ -1602,7 +1602,8 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     k_tile_first<<<blocks, threads, 0, stream>>>(a);
     ++launched;
     if (a.pattern && a.engine != BBPE_ENGINE_BLOCK) {  // (timed with k_tile_first)
-      launch_pretok_gpt2(a.bytes, a.offsets, a.tile_first, a.n_rows, a.total, a.rowbits, a.chunkbits, p.sm_count, stream);
+      launch_pretok_gpt2(a.bytes, a.offsets, a.tile_first, a.n_rows, a.total, a.rowbits, a.chunkbits,
+                         a.counters + CNT_PRETOK, p.sm_count, stream);
       ++launched;
     }
   }

@@ -34,7 +34,7 @@ constexpr int kInlineRes = 6;
 
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
-       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_N = 8 };
+       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_PRETOK = 8, CNT_N = 9 };
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFSETS = 3, ERR_N = 4 };
 

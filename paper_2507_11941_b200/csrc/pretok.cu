@@ -81,9 +81,28 @@ __device__ __forceinline__ bool in_ranges(uint32_t cp, const uint32_t (&r)[N][2]
   return false;
 }
 
+__host__ __device__ constexpr int ascii_class(uint32_t c) {
+  return ((c >= 'A' && c <= 'Z') || (c >= 'a' && c <= 'z')) ? kLetter
+         : (c >= '0' && c <= '9')                            ? kNumber
+         : (c == ' ' || (c >= 0x09 && c <= 0x0d))            ? kSpace
+                                                             : kOther;
+}
+
+// The ASCII classes in shared memory (accessors carry the pointer): one load
+// instead of compare chains, and no divergent branch per character.
+__device__ __forceinline__ void build_ascii_classes(uint8_t* cls) {
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) cls[i] = uint8_t(ascii_class(i));
+  __syncthreads();
+}
+
 // classify (pretokenize.hpp:157-165) with is_letter / is_number / is_space (133-149).
 template <typename Txt>
 __device__ __forceinline__ int classify(const Txt& s, uint64_t n, uint64_t pos, uint64_t& adv) {
+  const uint32_t b0 = s[pos];
+  if (b0 < 0x80) {
+    adv = 1;
+    return s.cls[b0];
+  }
   uint64_t next = pos;
   const uint32_t cp = next_utf8(s, n, next);
   adv = next - pos;
@@ -112,7 +131,7 @@ __device__ __forceinline__ uint64_t run_of(const Txt& s, uint64_t n, int want, u
 
 // gpt2_chunk_end (pretokenize.hpp:168-219): end of the match starting at pos.
 template <typename Txt>
-__device__ uint64_t gpt2_chunk_end(const Txt& s, uint64_t n, uint64_t pos) {
+__device__ __forceinline__ uint64_t gpt2_chunk_end(const Txt& s, uint64_t n, uint64_t pos) {
   uint64_t adv0;
   const int c0 = classify(s, n, pos, adv0);
   // 's|'t|'re|'ve|'m|'ll|'d (case-sensitive)
@@ -155,18 +174,55 @@ __device__ uint64_t gpt2_chunk_end(const Txt& s, uint64_t n, uint64_t pos) {
 // Short rows (<= kShortRow bytes): thread per row, the reference scan as is.
 constexpr uint64_t kShortRow = 4096;
 
-struct Plain {
+// A 16-byte register window over 16-aligned global bytes: a sequential scan
+// loads memory once per 16 bytes instead of once per byte (the row scan was
+// load-latency bound). The last partial block is read bytewise (no read past
+// `total`).
+struct RegWin {
   const uint8_t* g;
-  __device__ __forceinline__ uint8_t operator[](uint64_t p) const { return g[p]; }
+  const uint8_t* cls;  // ascii_class table (shared memory)
+  uint64_t total;
+  mutable uint64_t base;
+  mutable uint4 v;
+  __device__ __forceinline__ uint8_t operator[](uint64_t p) const {
+    const uint64_t b = p & ~15ull;
+    if (b != base) {
+      base = b;
+      if (b + 16 <= total) {
+        v = __ldg(reinterpret_cast<const uint4*>(g + b));
+      } else {
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (uint64_t i = b; i < total; ++i) w[(i - b) >> 2] |= uint32_t(g[i]) << (8 * ((i - b) & 3));
+        v = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    const uint32_t k = uint32_t(p) & 15;
+    const uint32_t x = (k & 8) ? ((k & 4) ? v.w : v.z) : ((k & 4) ? v.y : v.x);
+    return uint8_t(x >> (8 * (k & 3)));
+  }
 };
 
-__global__ void __launch_bounds__(256) k_pretok_rows(const uint8_t* bytes, const uint64_t* offsets, uint64_t n_rows,
-                                                     uint32_t* chunkbits) {
+struct Plain;
+template <typename Txt>
+__device__ __forceinline__ Txt make_txt(const uint8_t* bytes, const uint8_t* cls, uint64_t total);
+template <>
+__device__ __forceinline__ RegWin make_txt<RegWin>(const uint8_t* bytes, const uint8_t* cls, uint64_t total) {
+  return RegWin{bytes, cls, total, ~0ull, make_uint4(0, 0, 0, 0)};
+}
+
+template <typename Txt>
+__global__ void __launch_bounds__(256) k_pretok_rows(const uint8_t* bytes, uint64_t total, const uint64_t* offsets,
+                                                     uint64_t n_rows, uint32_t* chunkbits, uint32_t* long_flag) {
+  __shared__ uint8_t s_cls[128];
+  build_ascii_classes(s_cls);
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  const Plain txt{bytes};
+  const Txt txt = make_txt<Txt>(bytes, s_cls, total);
   for (uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; r < n_rows; r += stride) {
     const uint64_t rs = offsets[r], re = offsets[r + 1];
-    if (re - rs > kShortRow || re == rs) continue;  // long rows: k_pretok_gpt2
+    if (re - rs > kShortRow) {  // long rows: k_pretok_gpt2
+      *long_flag = 1;
+      continue;
+    }
     uint64_t word = ~0ull;
     uint32_t bits = 0;
     for (uint64_t pos = rs; pos < re;) {
@@ -182,11 +238,9 @@ __global__ void __launch_bounds__(256) k_pretok_rows(const uint8_t* bytes, const
   }
 }
 
-// Long rows: warp per 512-byte tile, lane per 16-byte span. The tile's bytes (with 16
-// bytes before and kAhead after) and its row-start bits sit in shared memory
-// (coalesced loads); scans that run further read global memory. A restart
-// point is a position where the reference's left-to-right scan always starts
-// a chunk, whatever came before:
+// Long rows (> kShortRow bytes): thread per kSpan-byte span. A restart point
+// is a position where the reference's left-to-right scan always starts a
+// chunk, whatever came before:
 //  * a row start;
 //  * p with ' ' at p after an ASCII non-whitespace character at p-1: the
 //    chunk holding p-1 is a letter/number/other run or a contraction, none of
@@ -196,37 +250,29 @@ __global__ void __launch_bounds__(256) k_pretok_rows(const uint8_t* bytes, const
 //    leading space.
 // Both need p-1 to start a character under the reference's lenient UTF-8
 // decoding (next_utf8 decides a length from the lead byte alone): no byte
-// >= 0xC0 in p-4..p-2 within the row. A lane scans chunks from the first
-// restart point in its span until it reaches a restart point at or past the
-// span end (the next owner's first one); spans without one are covered by an
-// earlier lane. Chunk starts go to `chunkbits` (row starts stay read-only).
-constexpr int kAhead = 128;
-constexpr int kPreBytes = 16 + kTile + kAhead + 16;  // [b0 - 16, b0 + kTile + kAhead + 16)
-constexpr int kPreWords = (kTile + kAhead) / 32 + 2;  // row / chunk bits of [b0 - 32, b0 + kTile + kAhead + 32)
+// >= 0xC0 in p-4..p-2 within the row. A thread scans chunks from the first
+// restart point of a long row in its span until it reaches a restart point
+// at or past the span end (the next span's first one); spans without one are
+// covered by an earlier thread. Chunk starts go to `chunkbits` (row starts
+// stay read-only).
+constexpr uint64_t kSpan = 1024;
 
-struct __align__(16) PreSmem {
-  uint8_t w[kPreBytes];
-  uint32_t rb[kPreWords];
-  uint32_t cb[kPreWords];
-};
-
-// Byte view: shared-memory window, global memory outside it.
-struct Text {
-  const uint8_t* w;  // window byte 0 = position lo
+// Plain byte loads (unaligned input).
+struct Plain {
   const uint8_t* g;
-  uint64_t lo, hi;
-  __device__ __forceinline__ uint8_t operator[](uint64_t p) const { return p - lo < hi - lo ? w[p - lo] : g[p]; }
+  const uint8_t* cls;  // ascii_class table (shared memory)
+  __device__ __forceinline__ uint8_t operator[](uint64_t p) const { return g[p]; }
 };
-struct Bits {
-  const uint32_t* w;  // window word 0 = word wlo
+
+template <>
+__device__ __forceinline__ Plain make_txt<Plain>(const uint8_t* bytes, const uint8_t* cls, uint64_t) {
+  return Plain{bytes, cls};
+}
+
+struct Bits {  // row-start bitmap
   const uint32_t* g;
-  uint64_t wlo, whi;
-  __device__ __forceinline__ bool operator()(uint64_t p) const {
-    const uint64_t x = p >> 5;
-    const uint32_t v = x - wlo < whi - wlo ? w[x - wlo] : g[x];
-    return (v >> (p & 31)) & 1u;
-  }
-  __device__ __forceinline__ uint32_t word(uint64_t x) const { return x - wlo < whi - wlo ? w[x - wlo] : g[x]; }
+  __device__ __forceinline__ bool operator()(uint64_t p) const { return (g[p >> 5] >> (p & 31)) & 1u; }
+  __device__ __forceinline__ uint32_t word(uint64_t x) const { return g[x]; }
 };
 
 // min(next row start after p, p + lim, total): scans at most lim / 32 + 1 words.
@@ -256,10 +302,10 @@ struct Rows {
     }
     return lo;
   }
-  __device__ __forceinline__ uint64_t end_of(uint64_t p) const { return off[upper(p)]; }
 };
 
-__device__ __forceinline__ bool is_restart(const Text& s, const Bits& row, uint64_t total, uint64_t p) {
+template <typename Txt>
+__device__ __forceinline__ bool is_restart(const Txt& s, const Bits& row, uint64_t total, uint64_t p) {
   if (p >= total) return false;
   if (row(p)) return true;
   if (p == 0) return true;
@@ -275,81 +321,77 @@ __device__ __forceinline__ bool is_restart(const Text& s, const Bits& row, uint6
   return classify(s, row_end_near(row, total, p, 8), p, adv) != kSpace;  // reads < 8 bytes ahead
 }
 
-__global__ void __launch_bounds__(256) k_pretok_gpt2(const uint8_t* bytes, uint64_t total, uint64_t num_tiles,
-                                                     const uint32_t* rowbits, Rows rows, uint32_t* chunkbits) {
-  __shared__ PreSmem sm[8];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  PreSmem& S = sm[wid];
-  const uint64_t nw = uint64_t(gridDim.x) * 8;
-  for (uint64_t tile = blockIdx.x * uint64_t(8) + wid; tile < num_tiles; tile += nw) {
-    const uint64_t b0 = tile * kTile;
-    const uint64_t lo = b0 >= 16 ? b0 - 16 : 0;
-    const uint64_t hi = min(total, b0 + kTile + kAhead + 16);
-    constexpr int kVec = kPreBytes / 16;  // 42 16-byte chunks
-    static_assert(kPreBytes % 16 == 0 && kVec <= 64, "window chunks");
-    if ((reinterpret_cast<uintptr_t>(bytes) & 15) == 0 && b0 >= 16 && hi - lo == uint64_t(kPreBytes)) {
-      // Interior tile, aligned input: two 16-byte loads per lane, both in flight.
-      const uint4* src = reinterpret_cast<const uint4*>(bytes + lo);
-      uint4 v0 = __ldg(src + lane), v1 = make_uint4(0, 0, 0, 0);
-      if (lane + 32 < kVec) v1 = __ldg(src + lane + 32);
-      reinterpret_cast<uint4*>(S.w)[lane] = v0;
-      if (lane + 32 < kVec) reinterpret_cast<uint4*>(S.w)[lane + 32] = v1;
-    } else {
-      for (uint64_t i = lane; i < hi - lo; i += 32) S.w[i] = bytes[lo + i];
-    }
-    const uint64_t wlo = b0 / 32 >= 1 ? b0 / 32 - 1 : 0;
-    const uint64_t whi = min((total + 31) / 32 + 1, wlo + kPreWords);
-    for (uint64_t i = lane; i < whi - wlo; i += 32) {
-      S.rb[i] = rowbits[wlo + i];
-      S.cb[i] = 0;
-    }
-    __syncwarp();
-    const Text txt{S.w, bytes, lo, hi};
-    const Bits row{S.rb, rowbits, wlo, whi};
-    const uint64_t sb = b0 + 16 * lane, se = min(total, sb + 16);
-    uint64_t pos = se;
-    if (sb < se) {  // spans of short rows belong to k_pretok_rows
-      const uint64_t u = rows.upper(sb);
-      if (rows.off[u] - rows.off[u - 1] <= kShortRow) pos = se + 1;  // skip
-    }
-    if (pos == se)
-      for (uint64_t p = sb; p < se; ++p)
-        if (is_restart(txt, row, total, p)) {
-          pos = p;
-          break;
-        }
-    if (pos < se) {
-      uint64_t re = rows.end_of(pos);
-      for (;;) {
-        if (pos >= re) {
-          if (re >= total) break;
-          pos = re;  // the next row's start is a restart point
-          re = rows.end_of(pos);
-          if (pos >= se) break;
-        }
-        if (pos >= se && is_restart(txt, row, total, pos)) break;  // the next owner's
-        const uint64_t x = pos >> 5;
-        if (x - wlo < whi - wlo) atomicOr(&S.cb[x - wlo], 1u << (pos & 31));
-        else atomicOr(&chunkbits[x], 1u << (pos & 31));
-        pos = gpt2_chunk_end(txt, re, pos);
+// Row [rs, re) of a restart point p, skipping short rows: returns false when
+// no long row has a restart point in [p, se).
+template <typename Txt>
+__device__ __forceinline__ bool first_long_restart(const Txt& txt, const Bits& row, const Rows& rows,
+                                                   uint64_t total, uint64_t short_row, uint64_t se, uint64_t& pos,
+                                                   uint64_t& re) {
+  for (;;) {
+    uint64_t p = pos;
+    while (p < se && !is_restart(txt, row, total, p)) ++p;
+    if (p >= se) return false;
+    const uint64_t u = rows.upper(p);
+    re = rows.off[u];
+    pos = p;
+    if (re - rows.off[u - 1] > short_row) return true;
+    pos = re;  // a short row (k_pretok_rows): its end is the next restart point
+  }
+}
+
+template <typename Txt>
+__global__ void __launch_bounds__(256) k_pretok_spans(const uint8_t* bytes, uint64_t total, const uint32_t* rowbits,
+                                                      Rows rows, uint32_t* chunkbits, uint64_t short_row,
+                                                      const uint32_t* long_flag) {
+  if (short_row && *reinterpret_cast<const volatile uint32_t*>(long_flag) == 0) return;  // no long row
+  __shared__ uint8_t s_cls[128];
+  build_ascii_classes(s_cls);
+  const Txt txt = make_txt<Txt>(bytes, s_cls, total);
+  const Bits row{rowbits};
+  const uint64_t spans = (total + kSpan - 1) / kSpan, stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t sp = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; sp < spans; sp += stride) {
+    const uint64_t se = min(total, (sp + 1) * kSpan);
+    uint64_t pos = sp * kSpan, re = 0;
+    if (!first_long_restart(txt, row, rows, total, short_row, se, pos, re)) continue;
+    uint64_t word = ~0ull;
+    uint32_t bits = 0;
+    for (;;) {
+      if (pos >= re) {  // the next row's start is a restart point
+        if (re >= total || re >= se) break;
+        pos = re;
+        if (!first_long_restart(txt, row, rows, total, short_row, se, pos, re)) break;
       }
+      if (pos >= se && is_restart(txt, row, total, pos)) break;  // the next span's
+      if ((pos >> 5) != word) {
+        if (bits) atomicOr(&chunkbits[word], bits);
+        word = pos >> 5;
+        bits = 0;
+      }
+      bits |= 1u << (pos & 31);
+      pos = gpt2_chunk_end(txt, re, pos);
     }
-    __syncwarp();
-    for (uint64_t i = lane; i < whi - wlo; i += 32)
-      if (S.cb[i]) atomicOr(&chunkbits[wlo + i], S.cb[i]);
-    __syncwarp();
+    if (bits) atomicOr(&chunkbits[word], bits);
   }
 }
 
 }  // namespace
 
 void launch_pretok_gpt2(const uint8_t* d_bytes, const uint64_t* d_offsets, const uint64_t* d_tile_first,
-                        uint64_t n_rows, uint64_t total, const uint32_t* d_rowbits, uint32_t* d_chunkbits, int sm_count, cudaStream_t s) {
+                        uint64_t n_rows, uint64_t total, const uint32_t* d_rowbits, uint32_t* d_chunkbits,
+                        uint32_t* d_long_flag, int sm_count, cudaStream_t s) {
   const uint64_t tiles = (total + kTile - 1) / kTile;
   if (!tiles) return;
-  k_pretok_rows<<<unsigned(sm_count * 8), 256, 0, s>>>(d_bytes, d_offsets, n_rows, d_chunkbits);
   const Rows rows{d_offsets, d_tile_first, n_rows, tiles};
-  k_pretok_gpt2<<<unsigned(sm_count * 4), 256, 0, s>>>(d_bytes, total, tiles, d_rowbits, rows, d_chunkbits);
+  const unsigned grid = unsigned(sm_count * 8);
+  if ((reinterpret_cast<uintptr_t>(d_bytes) & 15) == 0) {  // 16-byte register windows
+    k_pretok_rows<RegWin><<<grid, 256, 0, s>>>(d_bytes, total, d_offsets, n_rows, d_chunkbits, d_long_flag);
+    k_pretok_spans<RegWin><<<grid, 256, 0, s>>>(d_bytes, total, d_rowbits, rows, d_chunkbits, kShortRow,
+                                                d_long_flag);
+  } else {
+    k_pretok_rows<Plain><<<grid, 256, 0, s>>>(d_bytes, total, d_offsets, n_rows, d_chunkbits, d_long_flag);
+    k_pretok_spans<Plain><<<grid, 256, 0, s>>>(d_bytes, total, d_rowbits, rows, d_chunkbits, kShortRow,
+                                               d_long_flag);
+  }
 }
 
 }  // namespace bbpe

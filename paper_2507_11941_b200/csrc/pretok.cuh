@@ -12,7 +12,7 @@ namespace bbpe {
 // (k_tile_first), read-only here.
 // Rows of <= 4 KiB: thread per row; longer rows: warp per tile, lane per span.
 void launch_pretok_gpt2(const uint8_t* d_bytes, const uint64_t* d_offsets, const uint64_t* d_tile_first,
-                        uint64_t n_rows, uint64_t total,
-                        const uint32_t* d_rowbits, uint32_t* d_chunkbits, int sm_count, cudaStream_t s);
+                        uint64_t n_rows, uint64_t total, const uint32_t* d_rowbits, uint32_t* d_chunkbits,
+                        uint32_t* d_long_flag /* zero on entry; k_gather resets it */, int sm_count, cudaStream_t s);
 
 }  // namespace bbpe

@@ -668,10 +668,37 @@ def test_gpt2_pattern_mode_long_rows_and_newline_runs(gpt2):
         rows.append(b"".join(alphabet[i] if isinstance(alphabet[i], bytes) else bytes([alphabet[i]])
                              for i in rng.integers(0, len(alphabet), n)))
     rows += [b"word " * 2000, b"\n" * 500 + b"x", b"x\n" * 700, b"a" * 5000, b" \n \n  \n\t\n" * 90]
+    # Short and long rows (threshold 4 KiB) interleaved so long rows start at
+    # arbitrary offsets inside the splitter's 1 KiB spans.
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    tdata, toff = synth.rows_fixed(gen, 40, 9000, seed=72)
+    for i in range(40):
+        n = int(rng.integers(1000, 9000))
+        if i % 2:
+            rows.append(bytes(tdata[int(toff[i]):int(toff[i]) + n]))
+        else:
+            rows.append(b"".join(alphabet[j] if isinstance(alphabet[j], bytes) else bytes([alphabet[j]])
+                                 for j in rng.integers(0, len(alphabet), n // 2)))
     d, o = bb.pack_rows(rows)
     want_ids, want_off = ref.encode_pattern(d, o, "gpt2", workers=8)
     ids, oo, _ = bb.Encoder(0, pattern="gpt2").encode_packed(gpt2, d, o)
     assert np.array_equal(oo, want_off) and np.array_equal(ids, want_ids)
+    # Device API on an unaligned byte pointer (the splitter's row kernel needs
+    # 16-byte alignment; unaligned input takes the tile kernel for every row).
+    import torch
+    enc = bb.Encoder(0, pattern="gpt2")
+    for shift in (0, 3):
+        buf = torch.zeros(d.size + 16, dtype=torch.uint8, device="cuda")
+        buf[shift:shift + d.size] = torch.from_numpy(d.copy()).cuda()
+        d_off = torch.from_numpy(o.view(np.int64).copy()).cuda()
+        d_ids = torch.empty(d.size, dtype=torch.int32, device="cuda")
+        d_oo = torch.empty(o.size, dtype=torch.int64, device="cuda")
+        enc.encode_device(gpt2, buf.data_ptr() + shift, d_off.data_ptr(), o.size - 1, d.size, d_ids.data_ptr(),
+                          d_oo.data_ptr())
+        k = int(d_oo[-1].item())
+        assert np.array_equal(d_oo.cpu().numpy().view(np.uint64), want_off)
+        assert np.array_equal(d_ids[:k].cpu().numpy().view(np.uint32), want_ids)
 
 
 SPECIALS = [(b"<|endoftext|>", 50256), (b"<|pad|>", 50300), (b"<|a|>", 60001), (b"<|a|>x", 60002),
