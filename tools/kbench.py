@@ -10,14 +10,15 @@ import paper_2507_11941_b200 as bb
 from paper_2507_11941_b200 import synth
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 memo = (sys.argv[2] != "nomemo") if len(sys.argv) > 2 else True
-pattern = sys.argv[3] if len(sys.argv) > 3 else None
+pattern = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "none" else None
+dedup = (sys.argv[4] != "nodedup") if len(sys.argv) > 4 else True
 t = bb.load_merge_table_files(os.path.join(ROOT, "tests/golden/gpt2.bbpt"), None, "binary")
 if cfg == 4:
     t, _ = synth.extend_table(t, 200000)
 gen = synth.TextGen(synth.word_list(t))
 data, off, desc = synth.config_rows(gen, cfg, scale=1 / 16 if cfg == 5 else 1.0, seed=cfg * 1000)
 n, total = off.size - 1, int(off[-1])
-enc = bb.Encoder(device=0, piece_memo=memo, pattern=pattern)
+enc = bb.Encoder(device=0, piece_memo=memo, pattern=pattern, dedup=dedup)
 enc.prepare(t)
 s = torch.cuda.Stream()
 d_data = torch.from_numpy(data).cuda()
