@@ -2,9 +2,11 @@
 """PCIe bound of the e2e pipeline: the same H2D (bytes + offsets) and D2H
 (ids + offsets) volumes as cfg2, in 16 MiB waves, H2D and D2H on two streams
 (D2H of wave k after H2D of wave k), no kernels."""
+import sys
 import time
 import torch
-IN, OUT, W = 276824072, 275898992, 16 << 20
+# argv[1]: output bytes per output id (4 = u32 ids, 2 = u16 transport)
+IN, OUT, W = 276824072, 275898992 * int(sys.argv[1] if len(sys.argv) > 1 else 4) // 4, 16 << 20
 h_in = torch.empty(IN, dtype=torch.uint8).pin_memory()
 h_out = torch.empty(OUT, dtype=torch.uint8).pin_memory()
 d_in = torch.empty(IN, dtype=torch.uint8, device="cuda")
