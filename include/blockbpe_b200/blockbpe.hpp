@@ -24,6 +24,7 @@
 #include <memory>
 #include <optional>
 #include <stdexcept>
+#include <ostream>
 #include <string>
 #include <string_view>
 #include <utility>
@@ -397,6 +398,56 @@ inline BatchEncoding encode_batch(const std::vector<std::string>& inputs, const 
     }
   }
   return out;
+}
+
+// validate_specials (merge_table.hpp:374-385): a special id may not be a
+// base byte token nor the merged result of any pair.
+inline void validate_specials(const MergeTable& table, const SpecialTokenSet& specials) {
+  for (const auto& [b, id] : specials.entries()) {
+    (void)b;
+    auto tb = table.bytes_of(id);
+    if (tb && tb->size() == 1 && table.byte_token(static_cast<unsigned char>((*tb)[0])) == id)
+      throw IntegrityError("special id " + std::to_string(id) + " is a base byte token");
+  }
+  std::uint64_t nt = 0, nb = 0, nm = 0;
+  detail::check(bbpe_table_export(table.handle(), nullptr, nullptr, nullptr, &nt, &nb, nullptr, &nm));
+  std::vector<std::uint32_t> ids(nt), m4(4 * nm + 4);
+  std::vector<std::uint64_t> off(nt + 1);
+  std::vector<std::uint8_t> blob(nb + 1);
+  detail::check(bbpe_table_export(table.handle(), ids.data(), off.data(), blob.data(), &nt, &nb, m4.data(), &nm));
+  for (std::uint64_t k = 0; k < nm; ++k)
+    if (specials.contains_id(m4[4 * k + 3]))
+      throw IntegrityError("special id " + std::to_string(m4[4 * k + 3]) + " collides with a merge-derived token");
+}
+
+// write_batch_jsonl (batch.hpp:157-166): {"ids":[...],"len":n} per row, the
+// compact nlohmann dump byte for byte.
+inline void write_batch_jsonl(std::ostream& os, const BatchEncoding& e) {
+  std::string line;
+  for (std::size_t r = 0; r < e.batch_size; ++r) {
+    line.assign("{\"ids\":[");
+    for (std::uint32_t c = 0; c < e.lengths[r]; ++c) {
+      if (c) line.push_back(',');
+      line += std::to_string(e.ids[r * e.max_len + c]);
+    }
+    line += "],\"len\":" + std::to_string(e.lengths[r]) + "}\n";
+    os.write(line.data(), static_cast<std::streamsize>(line.size()));
+  }
+}
+
+// write_batch_binary (batch.hpp:205-213): "BBPE", u32 batch, max_len, pad_id,
+// row-major u32 ids, little-endian.
+inline void write_batch_binary(std::ostream& os, const BatchEncoding& e) {
+  auto put = [&](std::uint32_t v) {
+    const unsigned char b[4] = {static_cast<unsigned char>(v), static_cast<unsigned char>(v >> 8),
+                                static_cast<unsigned char>(v >> 16), static_cast<unsigned char>(v >> 24)};
+    os.write(reinterpret_cast<const char*>(b), 4);
+  };
+  os.write("BBPE", 4);
+  put(static_cast<std::uint32_t>(e.batch_size));
+  put(static_cast<std::uint32_t>(e.max_len));
+  put(e.pad_id);
+  for (TokenId id : e.ids) put(id);
 }
 
 inline TokenSeq encode_single(std::string_view input, const MergeTable& table, const SpecialTokenSet& specials,

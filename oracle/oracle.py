@@ -163,6 +163,9 @@ class Reference:
                                          u32p, u64p, C.c_uint64, C.c_size_t, C.c_int64]
         lib.ref_encode_heap.restype = C.c_int64
         lib.ref_encode_heap.argtypes = [C.c_void_p, u8p, u64p, C.c_size_t, C.c_uint, u32p, u64p, C.c_uint64]
+        lib.ref_write_batch.restype = C.c_int64
+        lib.ref_write_batch.argtypes = [C.c_void_p, u8p, u64p, C.c_size_t, C.c_uint, C.c_int, C.c_int, C.c_uint32,
+                                        C.c_int, u8p, C.c_uint64]
         lib.ref_encode_pattern.restype = C.c_int64
         lib.ref_encode_pattern.argtypes = [C.c_void_p, u8p, u64p, C.c_size_t, C.c_uint, C.c_char_p, u32p, u64p,
                                            C.c_uint64]
@@ -240,6 +243,23 @@ class Reference:
         if k < 0:
             raise RuntimeError(-k, self.lib.ref_last_error().decode())
         return ids[:k], oo
+
+    def write_batch(self, data, offsets, pad_id: int, binary: bool, workers: int = 1, add_bos=False,
+                    add_eos=False) -> bytes:
+        """The reference CLI's tokenize output (blockbpe_cli.cpp:73-127): encode_batch
+        with pad_id, then write_batch_jsonl / write_batch_binary (batch.hpp:157-213)."""
+        data = np.ascontiguousarray(data, np.uint8)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        n = offsets.size - 1
+        lib = self.lib
+        k = lib.ref_write_batch(self.h, _p(data, C.c_uint8) if data.size else None, _p(offsets, C.c_uint64), n,
+                                workers, int(add_bos), int(add_eos), pad_id, int(binary), None, 0)
+        if k < 0:
+            raise RuntimeError(-k, lib.ref_last_error().decode())
+        out = np.zeros(max(k, 1), np.uint8)
+        lib.ref_write_batch(self.h, _p(data, C.c_uint8) if data.size else None, _p(offsets, C.c_uint64), n,
+                            workers, int(add_bos), int(add_eos), pad_id, int(binary), _p(out, C.c_uint8), k)
+        return out[:k].tobytes()
 
     def encode_pattern(self, data, offsets, pattern: str = "gpt2", workers: int = 1):
         """encode_reference in pattern mode (ref_engines.hpp:119-146), heap engine."""

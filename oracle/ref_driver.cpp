@@ -23,6 +23,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -187,6 +188,33 @@ std::int64_t ref_encode_batch(void* h, const std::uint8_t* bytes, const std::uin
       }
     }
     return static_cast<std::int64_t>(pos);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -err_code(e);
+  }
+}
+
+// The reference CLI's `tokenize` with the block engine (blockbpe_cli.cpp:73-127):
+// encode_batch with pad_id, then write_batch_jsonl (binary == 0) or
+// write_batch_binary; the bytes to out (at most cap). Returns the full length,
+// or -(status) on error.
+std::int64_t ref_write_batch(void* h, const std::uint8_t* bytes, const std::uint64_t* offsets, std::size_t n,
+                             unsigned workers, int add_bos, int add_eos, std::uint32_t pad_id, int binary,
+                             std::uint8_t* out, std::uint64_t cap) {
+  try {
+    auto* t = static_cast<RefTable*>(h);
+    PhasePool pool(workers);
+    std::vector<std::string> rows(n);
+    for (std::size_t i = 0; i < n; ++i)
+      rows[i].assign(reinterpret_cast<const char*>(bytes) + offsets[i], offsets[i + 1] - offsets[i]);
+    const BatchEncoding enc =
+        encode_batch(rows, t->table, t->specials, BlockConfig{256, std::nullopt}, pad_id, add_bos, add_eos, &pool);
+    std::ostringstream os;
+    if (binary) write_batch_binary(os, enc);
+    else write_batch_jsonl(os, enc);
+    const std::string b = os.str();
+    if (out) std::memcpy(out, b.data(), std::min<std::uint64_t>(cap, b.size()));
+    return static_cast<std::int64_t>(b.size());
   } catch (const std::exception& e) {
     g_err = e.what();
     return -err_code(e);
