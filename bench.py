@@ -420,7 +420,7 @@ def main():
         kt, kc = enc.kernel_times(reset=True)
         pattern = {"value": int(d_oo[-1].item()) / (pt_ms / 1e3), "unit": "tokens/s", "ms_per_step": pt_ms,
                    "kernel_ms": {k: v / max(kc, 1) for k, v in kt.items()},
-                   "note": "k_tile_first includes the gpt2 splitter (k_pretok_rows + k_pretok_gpt2)"}
+                   "note": "k_tile_first includes the gpt2 splitter (k_pretok_rows + k_pretok_spans)"}
         enc.set_config(pattern=None)
 
     # ---- roofline of the dominant kernel ----

@@ -274,13 +274,24 @@ class Encoder {
     bbpe_ctx* h = nullptr;
     detail::check(bbpe_ctx_create(device, &c, &h));
     h_.reset(h);
+    cfg_ = c;
   }
   bbpe_ctx* handle() const { return h_.get(); }
   void configure(const BlockConfig& cfg, bool block_engine = false, bool piece_memo = true) {
     cfg.validate();
     bbpe_config c{cfg.block_size, cfg.max_passes ? static_cast<std::int64_t>(*cfg.max_passes) : 0,
-                  block_engine ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0, 0, 0};
+                  block_engine ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES, 0, piece_memo ? 1 : 0, 0, pattern_};
     detail::check(bbpe_ctx_set_config(h_.get(), &c));
+    cfg_ = c;
+  }
+  // Split pattern of later encodes: "gpt2" (the reference's built-in gpt2
+  // matcher, pattern_pretokenize) or "" (byte-level, encode_batch).
+  void set_split_pattern(std::string_view name) {
+    if (name != "" && name != "gpt2")
+      throw UsageError("only the gpt2 split pattern runs on the device, got \"" + std::string(name) + "\"");
+    pattern_ = name == "gpt2" ? 1 : 0;
+    cfg_.pattern = pattern_;
+    detail::check(bbpe_ctx_set_config(h_.get(), &cfg_));
   }
   // Packed rows -> CSR.
   void encode_csr(const MergeTable& t, const std::string& bytes, const std::vector<std::uint64_t>& offsets,
@@ -323,6 +334,8 @@ class Encoder {
     void operator()(bbpe_ctx* c) const { bbpe_ctx_destroy(c); }
   };
   std::unique_ptr<bbpe_ctx, Del> h_;
+  bbpe_config cfg_{};
+  int pattern_ = 0;
 };
 
 inline Encoder& default_encoder() {

@@ -92,3 +92,40 @@ def test_cli_errors_are_row_tagged(tmp_path):
     r = run("tokenize", "--vocab", str(vocab), "--format", "json", str(src))
     assert r.returncode == 2, r.stderr.decode()
     assert b"row 2" in r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("as_json", [False, True])
+def test_cli_compare_matches_reference(tmp_path, gpt2, as_json):
+    """`compare --pattern gpt2` (both encodes on the GPU: byte-level rows vs the
+    gpt2 split-pattern mode) prints the reference's divergence report
+    (eval.hpp:147-273, oracle/_ref/ref_compare) byte for byte."""
+    import paper_2507_11941_b200 as bb
+    from paper_2507_11941_b200 import synth
+    ref_bin = os.path.join(ROOT, "oracle", "_ref", "ref_compare")
+    if not os.path.exists(ref_bin):
+        pytest.skip("oracle/_ref not built")
+    build_cli()
+    ids_, off_, blob_, m4_ = gpt2.export()
+    canon = {"tokens": [[int(i), [int(b) for b in blob_[int(off_[k]):int(off_[k + 1])]]] for k, i in enumerate(ids_)],
+             "merges": np.asarray(m4_).reshape(-1, 4).astype(np.int64).tolist()}
+    vocab = tmp_path / "gpt2_canonical.json"
+    vocab.write_text(json.dumps(canon))
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 200, 160, seed=99)
+    rows = [bytes(data[int(off[i]):int(off[i + 1])]).replace(b"\n", b" ") for i in range(200)]
+    rows += [b"", b"hello!!! world", b"it's 12345 and 678", b"don't   stop\t now", "café ünïcode 中文".encode(),
+             b"...???!!!", b"a'll b're c've", b"\xff\xfe broken", b"   ", b"x" * 300,
+             # NBSP runs: GPT-2's byte-level merges and its split pattern disagree here
+             b"\xc2\xa0\xc2\xa0x", b"x\xc2\xa0\xc2\xa0\xc2\xa0y", b"\xc2\xa0\xc2\xa0z"]
+    src = tmp_path / "in.txt"
+    src.write_bytes(b"\n".join(rows) + b"\n")
+    flag = ["--json"] if as_json else []
+    r = run("compare", "--vocab", os.path.join(GOLDEN, "gpt2.bbpt"), "--format", "binary", "--pattern", "gpt2",
+            *flag, str(src))
+    assert r.returncode == 0, r.stderr.decode()
+    want = subprocess.run([ref_bin, str(vocab), "gpt2", "1" if as_json else "0", str(src)], capture_output=True,
+                          timeout=600)
+    assert want.returncode == 0, want.stderr.decode()
+    assert r.stdout == want.stdout
+    assert (b'"divergent": true' if as_json else b"DIVERGE [") in r.stdout  # items that differ are reported

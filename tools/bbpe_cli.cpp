@@ -1,20 +1,28 @@
-// bbpe_cli -- the reference CLI's `tokenize` subcommand (tools/blockbpe_cli.cpp:
-// run_tokenize 73-127, options 219-230) on the B200 encoder, through the
-// drop-in header. Same options, output formats and exit codes (0 success,
-// 1 usage error, 2 integrity/parse error); the engine is `cuda` (the reference's
-// parse_engine must keep rejecting "gpu", test_bench.cpp:176).
+// bbpe_cli -- the reference CLI's `tokenize` and `compare` subcommands
+// (tools/blockbpe_cli.cpp: run_tokenize 73-127, run_compare 133-149, options
+// 219-250) on the B200 encoder, through the drop-in header. Same options,
+// output formats and exit codes (0 success, 1 usage error, 2 integrity/parse
+// error); the engine is `cuda` (the reference's parse_engine must keep
+// rejecting "gpu", test_bench.cpp:176). `compare` runs both sides on the GPU:
+// byte-level rows (the block engine's output) against the gpt2 split-pattern
+// encode (encode_reference's pattern mode), the report as eval.hpp:147-273.
 //
 //   bbpe_cli tokenize --vocab V [--merges M] [--format gpt2|json|binary]
 //            [--specials S.json] [--bos-token T] [--eos-token T] [--engine cuda]
 //            [--block-size N] [--bos] [--eos] [--out jsonl|bin] [--output F]
 //            [--pad-id N] [--workers N] [--device N] input
+//   bbpe_cli compare --vocab V ... --pattern gpt2 [--block-size N] [--json]
+//            [--output F] [--device N] input
 #include <blockbpe_b200/blockbpe.hpp>
 
 #include <nlohmann/json.hpp>
 
+#include <algorithm>
 #include <cstdio>
 #include <fstream>
+#include <iomanip>
 #include <iostream>
+#include <numeric>
 #include <optional>
 #include <string>
 #include <vector>
@@ -63,13 +71,16 @@ std::vector<std::string> read_lines(const std::string& path) {
 const char* kUsage =
     "usage: bbpe_cli tokenize --vocab V [--merges M] [--format gpt2|json|binary] [--specials S]\n"
     "                [--bos-token T] [--eos-token T] [--engine cuda] [--block-size N] [--bos] [--eos]\n"
-    "                [--out jsonl|bin] [--output F] [--pad-id N] [--workers N] [--device N] input\n";
+    "                [--out jsonl|bin] [--output F] [--pad-id N] [--workers N] [--device N] input\n"
+    "       bbpe_cli compare --vocab V [vocab options] --pattern gpt2 [--block-size N] [--json]\n"
+    "                [--output F] [--device N] input\n";
 
 struct Args {
+  std::string cmd;
   std::string vocab, merges, format = "gpt2", specials, bos_token, eos_token, engine = "cuda";
-  std::string out = "jsonl", output, input;
+  std::string out = "jsonl", output, input, pattern;
   std::uint32_t block_size = 256;
-  bool bos = false, eos = false;
+  bool bos = false, eos = false, json = false;
   std::optional<bb::TokenId> pad_id;
   int device = 0;
 };
@@ -86,8 +97,10 @@ std::uint64_t to_u64(const std::string& opt, const std::string& v) {
 }
 
 Args parse(int argc, char** argv) {
-  if (argc < 2 || std::string(argv[1]) != "tokenize") throw bb::UsageError("expected the tokenize subcommand");
+  if (argc < 2 || (std::string(argv[1]) != "tokenize" && std::string(argv[1]) != "compare"))
+    throw bb::UsageError("expected the tokenize or compare subcommand");
   Args a;
+  a.cmd = argv[1];
   for (int i = 2; i < argc; ++i) {
     const std::string k = argv[i];
     auto val = [&]() -> std::string {
@@ -109,27 +122,170 @@ Args parse(int argc, char** argv) {
     else if (k == "--pad-id") a.pad_id = static_cast<bb::TokenId>(to_u64(k, val()));
     else if (k == "--workers") (void)to_u64(k, val());  // host threads: not used by the device path
     else if (k == "--device") a.device = static_cast<int>(to_u64(k, val()));
+    else if (k == "--pattern" && a.cmd == "compare") a.pattern = val();
+    else if (k == "--json" && a.cmd == "compare") a.json = true;
     else if (!k.empty() && k[0] == '-') throw bb::UsageError("unknown option " + k);
     else if (a.input.empty()) a.input = k;
     else throw bb::UsageError("unexpected argument " + k);
   }
   if (a.vocab.empty()) throw bb::UsageError("--vocab is required");
   if (a.input.empty()) throw bb::UsageError("the input file is required");
+  if (a.cmd == "compare" && a.pattern.empty()) throw bb::UsageError("--pattern is required");
+  if (a.cmd == "compare" && a.pattern != "gpt2")
+    throw bb::UsageError("only the gpt2 split pattern runs on the device, got \"" + a.pattern + "\"");
   if (a.engine != "cuda") throw bb::UsageError("unknown engine \"" + a.engine + "\" (expected cuda)");
   if (a.out != "jsonl" && a.out != "bin")
     throw bb::UsageError("unknown output format \"" + a.out + "\" (expected jsonl|bin)");
   return a;
 }
 
-int run_tokenize(const Args& a) {
+bb::MergeTable load_table(const Args& a) {
   const bb::VocabFormat fmt = bb::parse_vocab_format(a.format);
   if (fmt == bb::VocabFormat::gpt2 && a.merges.empty()) throw bb::UsageError("--merges is required for gpt2 format");
-  const bb::MergeTable table = bb::load_merge_table_files(a.vocab, a.merges, fmt);
+  return bb::load_merge_table_files(a.vocab, a.merges, fmt);
+}
+
+bb::SpecialTokenSet load_specials_arg(const Args& a, const bb::MergeTable& table) {
   bb::SpecialTokenSet specials;
   if (!a.specials.empty()) specials = load_specials_file(a.specials);
   if (!a.bos_token.empty()) specials.set_bos(a.bos_token);
   if (!a.eos_token.empty()) specials.set_eos(a.eos_token);
   bb::validate_specials(table, specials);
+  return specials;
+}
+
+std::ostream& open_output(std::ofstream& file, const std::string& path) {
+  if (path.empty()) return std::cout;
+  file.open(path, std::ios::binary);
+  if (!file) throw bb::UsageError("cannot open output file " + path);
+  return file;
+}
+
+// ---- compare: the divergence report (eval.hpp:147-273) ----
+
+// levenshtein (eval.hpp:20-41): edits between token sequences, two rolling rows.
+std::uint32_t levenshtein(const bb::TokenSeq& a, const bb::TokenSeq& b) {
+  const bb::TokenSeq& lo = a.size() >= b.size() ? a : b;
+  const bb::TokenSeq& sh = a.size() >= b.size() ? b : a;
+  if (sh.empty()) return static_cast<std::uint32_t>(lo.size());
+  std::vector<std::uint32_t> prev(sh.size() + 1), cur(sh.size() + 1);
+  std::iota(prev.begin(), prev.end(), 0u);
+  for (std::size_t i = 1; i <= lo.size(); ++i) {
+    cur[0] = static_cast<std::uint32_t>(i);
+    for (std::size_t j = 1; j <= sh.size(); ++j)
+      cur[j] = std::min({prev[j] + 1, cur[j - 1] + 1, prev[j - 1] + (lo[i - 1] == sh[j - 1] ? 0u : 1u)});
+    std::swap(prev, cur);
+  }
+  return prev[sh.size()];
+}
+
+// categorize_input (eval.hpp:91-113): >= 2 equal punctuation bytes in a row,
+// else >= 4 ASCII digits in a row, else other.
+const char* category_of(const std::string& in) {
+  auto punct = [](unsigned char b) {
+    return (b >= 33 && b <= 47) || (b >= 58 && b <= 64) || (b >= 91 && b <= 96) || (b >= 123 && b <= 126);
+  };
+  std::size_t pr = 0, dr = 0;
+  unsigned char prev = 0;
+  for (std::size_t i = 0; i < in.size(); ++i) {
+    const unsigned char b = static_cast<unsigned char>(in[i]);
+    pr = (punct(b) && i > 0 && b == prev) ? pr + 1 : (punct(b) ? 1 : 0);
+    if (pr >= 2) return "punct_run";
+    dr = (b >= '0' && b <= '9') ? dr + 1 : 0;
+    if (dr >= 4) return "digit_run";
+    prev = b;
+  }
+  return "other";
+}
+
+// escape_bytes (eval.hpp:193-206): non-printables and '\\' as \xHH.
+std::string escape_bytes(const std::string& in) {
+  static const char* hex = "0123456789abcdef";
+  std::string out;
+  for (unsigned char b : in) {
+    if (b >= 32 && b < 127 && b != '\\') {
+      out.push_back(static_cast<char>(b));
+    } else {
+      out += "\\x";
+      out.push_back(hex[b >> 4]);
+      out.push_back(hex[b & 0xf]);
+    }
+  }
+  return out;
+}
+
+int run_compare(const Args& a) {
+  const bb::MergeTable table = load_table(a);
+  const bb::SpecialTokenSet specials = load_specials_arg(a, table);
+  const std::vector<std::string> inputs = read_lines(a.input);
+  const bb::BlockConfig config{a.block_size, std::nullopt};
+  config.validate();
+  bb::Encoder enc(a.device, config);
+  const bb::BatchEncoding blk = bb::encode_batch(inputs, table, specials, config, 0, false, false, &enc);
+  // The reference side: the gpt2 split pattern on the device.
+  enc.set_split_pattern("gpt2");
+  const bb::BatchEncoding pat = bb::encode_batch(inputs, table, specials, config, 0, false, false, &enc);
+  struct Stats {
+    std::size_t total = 0, divergent = 0;
+  } st[3];
+  const char* names[3] = {"punct_run", "digit_run", "other"};
+  nlohmann::json items = nlohmann::json::array();
+  std::size_t ndiv = 0;
+  double sum = 0.0;
+  std::vector<double> sims(inputs.size());
+  std::vector<int> cats(inputs.size());
+  std::vector<bool> div(inputs.size());
+  for (std::size_t i = 0; i < inputs.size(); ++i) {
+    const bb::TokenSeq b = blk.row(i), r = pat.row(i);
+    div[i] = b != r;
+    sims[i] = 1.0 - static_cast<double>(levenshtein(r, b)) / static_cast<double>(std::max<std::size_t>(inputs[i].size(), 1));
+    const std::string c = category_of(inputs[i]);
+    cats[i] = c == "punct_run" ? 0 : (c == "digit_run" ? 1 : 2);
+    ++st[cats[i]].total;
+    if (div[i]) {
+      ++st[cats[i]].divergent;
+      ++ndiv;
+    }
+    sum += sims[i];
+    if (a.json)
+      items.push_back({{"input", escape_bytes(inputs[i])}, {"block_tokens", b}, {"reference_tokens", r},
+                       {"divergent", bool(div[i])}, {"item_sim", sims[i]}, {"category", names[cats[i]]}});
+  }
+  const double agg = inputs.empty() ? 1.0 : sum / static_cast<double>(inputs.size());
+  std::ofstream file;
+  std::ostream& os = open_output(file, a.output);
+  if (a.json) {  // to_json(DivergenceReport) (eval.hpp:219-237), dump(2)
+    auto js = [&](int k) { return nlohmann::json{{"total", st[k].total}, {"divergent", st[k].divergent}}; };
+    const nlohmann::json doc = {{"count", inputs.size()},
+                                {"divergent_count", ndiv},
+                                {"aggregate_sim", agg},
+                                {"by_category", {{"punct_run", js(0)}, {"digit_run", js(1)}, {"other", js(2)}}},
+                                {"items", items}};
+    os << doc.dump(2) << '\n';
+    return 0;
+  }
+  // write_text(DivergenceReport) (eval.hpp:251-273)
+  os << "items: " << inputs.size() << "  divergent: " << ndiv << "  aggregate_sim: " << std::setprecision(6)
+     << std::fixed << agg << "\n";
+  for (int k = 0; k < 3; ++k)
+    os << "  " << std::setw(10) << std::left << names[k] << std::right << " total " << std::setw(6) << st[k].total
+       << "  divergent " << std::setw(6) << st[k].divergent << "\n";
+  for (std::size_t i = 0; i < inputs.size(); ++i) {
+    if (!div[i]) continue;
+    const bb::TokenSeq b = blk.row(i), r = pat.row(i);
+    os << "  DIVERGE [" << names[cats[i]] << "] \"" << escape_bytes(inputs[i]) << "\" sim=" << sims[i]
+       << "\n    block: [";
+    for (std::size_t j = 0; j < b.size(); ++j) os << (j ? ", " : "") << b[j];
+    os << "]\n    ref:   [";
+    for (std::size_t j = 0; j < r.size(); ++j) os << (j ? ", " : "") << r[j];
+    os << "]\n";
+  }
+  return 0;
+}
+
+int run_tokenize(const Args& a) {
+  const bb::MergeTable table = load_table(a);
+  const bb::SpecialTokenSet specials = load_specials_arg(a, table);
   const bb::BlockConfig config{a.block_size, std::nullopt};
   config.validate();
   const bb::TokenId pad = a.pad_id.value_or(specials.eos_id().value_or(0));
@@ -137,15 +293,10 @@ int run_tokenize(const Args& a) {
   bb::Encoder enc(a.device, config);
   const bb::BatchEncoding e = bb::encode_batch(inputs, table, specials, config, pad, a.bos, a.eos, &enc);
   std::ofstream file;
-  std::ostream* os = &std::cout;
-  if (!a.output.empty()) {
-    file.open(a.output, std::ios::binary);
-    if (!file) throw bb::UsageError("cannot open output file " + a.output);
-    os = &file;
-  }
-  if (a.out == "jsonl") bb::write_batch_jsonl(*os, e);
-  else bb::write_batch_binary(*os, e);
-  os->flush();
+  std::ostream& os = open_output(file, a.output);
+  if (a.out == "jsonl") bb::write_batch_jsonl(os, e);
+  else bb::write_batch_binary(os, e);
+  os.flush();
   return 0;
 }
 
@@ -157,7 +308,8 @@ int main(int argc, char** argv) {
     return 0;
   }
   try {
-    return run_tokenize(parse(argc, argv));
+    const Args a = parse(argc, argv);
+    return a.cmd == "compare" ? run_compare(a) : run_tokenize(a);
   } catch (const bb::UsageError& e) {
     std::cerr << "error: " << e.what() << '\n' << kUsage;
     return 1;
