@@ -426,7 +426,9 @@ def main():
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
     dom = max(k_ms, key=k_ms.get)
-    alg_bytes = total + 4 * ntok + 16 * n
+    # Per launch: a device batch above 2 GiB runs as several chunk launches.
+    per_step = max(kcalls, 1) / max(args.steps, 1)
+    alg_bytes = (total + 4 * ntok + 16 * n) / per_step
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms["k_pieces"] / 1e3) / 1e9
     # DRAM traffic of the same kernel on the same command, from the committed

@@ -1531,6 +1531,64 @@ int bbpe_encode(bbpe_ctx* c, const bbpe_table* t, const uint8_t* bytes, const ui
   BBPE_CATCH
 }
 
+namespace {
+
+// Device batches above kDeviceChunk input bytes run as row-range chunks (the
+// scratch of one launch is sized for adversarial input, ~38 B per input
+// byte): chunk ids land at d_out_ids + the running token base, the chunk's
+// offsets are moved onto it by k_add_u64; one sync per chunk. Chunk starts
+// prefer 16-byte aligned rows (k_pieces' asynchronous window loads).
+constexpr uint64_t kDeviceChunk = 2ull << 30;
+
+double encode_device_chunked(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                             uint64_t n, uint64_t total, uint32_t* d_out_ids, uint64_t* d_out_offsets,
+                             cudaStream_t s) {
+  std::vector<uint64_t> off(n + 1);
+  ck(cudaMemcpyAsync(off.data(), d_offsets, (n + 1) * 8, cudaMemcpyDeviceToHost, s), "D2H offsets");
+  ck(cudaStreamSynchronize(s), "D2H offsets");
+  if (off[0] != 0 || off[n] != total) throw bbpe::usage_error("offsets must start at 0 and end at total_bytes");
+  for (uint64_t i = 0; i < n; ++i)
+    if (off[i + 1] < off[i]) throw bbpe::usage_error("offsets must be non-decreasing");
+  ensure_plan(c);
+  float ms_total = 0;
+  uint64_t r0 = 0, tok = 0;
+  while (r0 < n) {
+    uint64_t r1 = uint64_t(std::upper_bound(off.begin() + r0 + 1, off.end(), off[r0] + kDeviceChunk) - off.begin()) - 1;
+    if (r1 <= r0) r1 = r0 + 1;  // one row above the chunk size: alone
+    if (r1 < n) {
+      for (uint64_t k = r1, lim = r1 > r0 + 4096 ? r1 - 4096 : r0 + 1; k >= lim && k > r0; --k)
+        if (((reinterpret_cast<uintptr_t>(d_bytes) + off[k]) & 15) == 0) {
+          r1 = k;
+          break;
+        }
+    }
+    const uint64_t nr = r1 - r0, base = off[r0], tot = off[r1] - base;
+    ck(cudaEventRecord(c.ev0, s), "event");
+    enqueue_encode(c, c.sc, t, d_bytes + base, d_offsets + r0, nr, tot, d_out_ids + tok, d_out_offsets + r0, s,
+                   true, nullptr, true, base);
+    uint64_t ntok = 0;
+    ck(cudaMemcpyAsync(&ntok, d_out_offsets + r1, 8, cudaMemcpyDeviceToHost, s), "D2H count");
+    ck(cudaEventRecord(c.ev1, s), "event");
+    ck(cudaStreamSynchronize(s), "encode");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c.ev0, c.ev1);
+    ms_total += ms;
+    std::vector<uint64_t> rel(nr + 1);
+    for (uint64_t i = 0; i <= nr; ++i) rel[i] = off[r0 + i] - base;
+    uint64_t err[bbpe::ERR_N];
+    ck(cudaMemcpy(err, c.sc.err.p, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
+    raise_device_errors(c, err, rel.data(), nr, r0, nullptr, nullptr, d_bytes + base);
+    bbpe::launch_add_u64(d_out_offsets + r0, nr + 1, tok, c.plan.sm_count, s);
+    ++c.launches;
+    tok += ntok;
+    r0 = r1;
+  }
+  ck(cudaStreamSynchronize(s), "encode");
+  return ms_total;
+}
+
+}  // namespace
+
 int bbpe_encode_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
                        const uint64_t* d_offsets, size_t n, uint64_t total_bytes,
                        uint32_t* d_out_ids, uint64_t* d_out_offsets, void* stream, int sync,
@@ -1541,6 +1599,16 @@ int bbpe_encode_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
   DeviceGuard g(c->device);
   maybe_build_memo(*c, *t);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+  if (total_bytes > kDeviceChunk) {  // scratch for one launch is ~38 B per input byte
+    const double ms = encode_device_chunked(*c, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
+    if (st) {
+      *st = bbpe_stats{};
+      st->n_rows = n;
+      st->input_bytes = total_bytes;
+      st->device_ms = ms;
+    }
+    return BBPE_OK;
+  }
   if (sync) ck(cudaEventRecord(c->ev0, s), "event");
   enqueue_encode(*c, c->sc, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
   c->pending = true;

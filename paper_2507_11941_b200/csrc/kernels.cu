@@ -1559,6 +1559,15 @@ __global__ void k_copy_out(const uint32_t* __restrict__ src, uint32_t* dst, cons
   if (tid < n - t0) dst[o0 + t0 + tid] = src[t0 + tid];
 }
 
+__global__ void k_add_u64(uint64_t* p, uint64_t n, uint64_t v) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    p[i] += v;
+}
+
+void launch_add_u64(uint64_t* d_p, uint64_t n, uint64_t v, int sm_count, cudaStream_t stream) {
+  if (n && v) k_add_u64<<<unsigned(std::max(sm_count, 1) * 2), 256, 0, stream>>>(d_p, n, v);
+}
+
 void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t* d_wave_offsets,
                      uint64_t* mapped_offsets, uint64_t nr, uint64_t* run_base, uint64_t cap, int sm_count,
                      cudaStream_t stream) {

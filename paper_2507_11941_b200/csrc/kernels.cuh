@@ -132,6 +132,8 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
 // Copies one wave's results into the caller's device-mapped pinned buffers:
 // row offsets (wave-relative + *run_base) and ids at *run_base (clamped to
 // cap), then advances *run_base by the wave's token count.
+// p[i] += v for i < n (chunked device encodes: a chunk's offsets onto the running base).
+void launch_add_u64(uint64_t* d_p, uint64_t n, uint64_t v, int sm_count, cudaStream_t stream);
 void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t* d_wave_offsets,
                      uint64_t* mapped_offsets, uint64_t nr, uint64_t* run_base, uint64_t cap, int sm_count,
                      cudaStream_t stream);

@@ -836,3 +836,32 @@ def test_encode_tensors_zero_copy(gpt2):
     assert np.array_equal(sub_oo.cpu().numpy(), (want_off[100:201] - want_off[100]).astype(np.int64))
     with pytest.raises(bb.UsageError):
         enc.encode_tensors(gpt2, d.cpu(), o)
+
+
+def test_device_call_over_4_gib(gpt2):
+    """One device-API call over 4 GiB of input (20 x the cfg2 batch, 5.4 GB):
+    no 32-bit tile / slot / record index overflows -- the ids and offsets are
+    exactly the single batch's, repeated (rows are independent)."""
+    import torch
+    from paper_2507_11941_b200 import synth
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off, _ = synth.config_rows(gen, 2)
+    e = bb.Encoder(0)
+    ids1, oo1, _ = e.encode_packed(gpt2, data, off)
+    R, n, B, T = 20, off.size - 1, int(off[-1]), int(oo1[-1])
+    assert R * B > (1 << 32)
+    d1 = torch.from_numpy(data).cuda()
+    d = d1.repeat(R)
+    o1 = torch.from_numpy(off.view(np.int64)).cuda()
+    o = torch.cat([o1[:-1] + k * B for k in range(R)] + [torch.tensor([R * B], device="cuda")])
+    del d1
+    ids = torch.empty(R * B, dtype=torch.int32, device="cuda")
+    oo = torch.empty(R * n + 1, dtype=torch.int64, device="cuda")
+    e.encode_device(gpt2, d.data_ptr(), o.data_ptr(), R * n, R * B, ids.data_ptr(), oo.data_ptr())
+    del d
+    assert int(oo[-1].item()) == R * T
+    want_ids = torch.from_numpy(ids1.view(np.int32)).cuda()
+    want_oo = torch.from_numpy(oo1.view(np.int64)).cuda()
+    for k in range(R):
+        assert torch.equal(ids[k * T:(k + 1) * T], want_ids)
+        assert torch.equal(oo[k * n:(k + 1) * n + 1] - k * T, want_oo)
