@@ -1264,6 +1264,23 @@ int bbpe_ctx_set_specials(bbpe_ctx* c, size_t n, const uint8_t* blob, const uint
 
 namespace {
 
+constexpr uint64_t kDeviceChunk = 2ull << 30;  // larger device batches run in chunks
+double encode_device_chunked(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                             uint64_t n, uint64_t total, uint32_t* d_out_ids, uint64_t* d_out_offsets,
+                             cudaStream_t s);
+
+// Synchronous device encode with the reference's errors; chunked above kDeviceChunk.
+void encode_device_sync(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes, const uint64_t* d_offsets,
+                        uint64_t n, uint64_t total, uint32_t* d_out, uint64_t* d_out_off, cudaStream_t s) {
+  if (total > kDeviceChunk) {
+    encode_device_chunked(c, t, d_bytes, d_offsets, n, total, d_out, d_out_off, s);
+    return;
+  }
+  enqueue_encode(c, c.sc, t, d_bytes, d_offsets, n, total, d_out, d_out_off, s);
+  ck(cudaStreamSynchronize(s), "encode");
+  check_device_errors(c, nullptr, n, 0, nullptr, d_offsets, d_bytes);
+}
+
 // bbpe_encode_batch_device's body; returns the id total.
 uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t* d_bytes,
                                 const uint64_t* d_offsets, size_t n, uint64_t total_bytes, uint32_t bos_id,
@@ -1303,9 +1320,7 @@ uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t*
     ck(cudaMemsetAsync(match_base, 0, (n + 1) * 8, s), "memset");
   }
   if (M == 0 && !add_bos && !add_eos && out_capacity >= total_bytes) {  // plain CSR encode
-    enqueue_encode(*c, c->sc, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
-    ck(cudaStreamSynchronize(s), "encode");
-    check_device_errors(*c, nullptr, n, 0, nullptr, d_offsets, d_bytes);
+    encode_device_sync(*c, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
     return read_u64(d_out_offsets + n);
   }
   // (2) literal segments: r + match_base[r] + j, j = 0..matches(r), compacted.
@@ -1332,11 +1347,9 @@ uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t*
   // (3) encode the literal segments as rows.
   c->sp_segtok.ensure(std::max<uint64_t>(seg_total, 1) * 4);
   c->sp_segtokoff.ensure((n_seg + 1) * 8);
-  enqueue_encode(*c, c->sc, *t, seg_bytes, seg_offsets, n_seg, seg_total, c->sp_segtok.as<uint32_t>(),
-                 c->sp_segtokoff.as<uint64_t>(), s);
-  ck(cudaStreamSynchronize(s), "encode");
   try {
-    check_device_errors(*c, nullptr, n_seg, 0, nullptr, seg_offsets, seg_bytes);
+    encode_device_sync(*c, *t, seg_bytes, seg_offsets, n_seg, seg_total, c->sp_segtok.as<uint32_t>(),
+                       c->sp_segtokoff.as<uint64_t>(), s);
   } catch (const bbpe::Error& e) {
     // "row <segment>: ..." -> the input row holding that segment.
     const std::string m = e.what();
@@ -1538,8 +1551,6 @@ namespace {
 // byte): chunk ids land at d_out_ids + the running token base, the chunk's
 // offsets are moved onto it by k_add_u64; one sync per chunk. Chunk starts
 // prefer 16-byte aligned rows (k_pieces' asynchronous window loads).
-constexpr uint64_t kDeviceChunk = 2ull << 30;
-
 double encode_device_chunked(bbpe_ctx& c, const bbpe_table& t, const uint8_t* d_bytes, const uint64_t* d_offsets,
                              uint64_t n, uint64_t total, uint32_t* d_out_ids, uint64_t* d_out_offsets,
                              cudaStream_t s) {
