@@ -865,3 +865,26 @@ def test_device_call_over_4_gib(gpt2):
     for k in range(R):
         assert torch.equal(ids[k * T:(k + 1) * T], want_ids)
         assert torch.equal(oo[k * n:(k + 1) * n + 1] - k * T, want_oo)
+
+
+def test_pattern_mode_with_specials_vs_reference(gpt2):
+    """gpt2 pattern mode together with special tokens: specials split first,
+    each literal segment pattern-split and encoded (encode_reference,
+    ref_engines.hpp:119-146) -- device split + segment rows in pattern mode."""
+    from oracle.oracle import Reference
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ids_, off_, blob_, m4_ = gpt2.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    enc = bb.Encoder(0, pattern="gpt2")
+    sp = bb.SpecialTokenSet()
+    for b, i in SPECIALS:
+        ref.add_special(b, i)
+        sp.add(b, i)
+    enc.set_specials(sp)
+    rows = _special_rows(gpt2)[:400] + PATTERN_CASES
+    d, o = bb.pack_rows(rows)
+    want_ids, want_off = ref.encode_pattern(d, o, "gpt2", workers=8)
+    ids, oo = enc.encode_batch_packed(gpt2, d, o)
+    assert np.array_equal(oo, want_off)
+    assert np.array_equal(ids, want_ids)
