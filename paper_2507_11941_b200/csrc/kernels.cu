@@ -1210,16 +1210,19 @@ __global__ void __launch_bounds__(256) k_refs(EncodeArgs a) {
         d1 = __ldcg(de + 1);
       }
     }
-    const unsigned rm = __ballot_sync(kFull, ref);
-    for (int it = 0; it < 16; ++it) {
-      if (!((rm >> (2 * it)) & 3u)) continue;  // warp-uniform
-      const int src = 2 * it + h;
+    // References two at a time (the two lowest left in `m`): half-warp h
+    // takes the (h+1)-th; iterations = ceil(references / 2), warp-uniform.
+    for (unsigned m = __ballot_sync(kFull, ref); m;) {
+      const unsigned m2 = m & (m - 1);
+      const int s0 = __ffs(m) - 1, s1 = m2 ? __ffs(m2) - 1 : -1;
+      m = m2 ? m2 & (m2 - 1) : 0u;
+      const int src = h ? (s1 < 0 ? s0 : s1) : s0;
       const uint64_t rh = __shfl_sync(kFull, hdr, src);
       const uint64_t e0 = __shfl_sync(kFull, d0.x, src);
       const uint64_t t01 = __shfl_sync(kFull, d0.y, src);
       const uint64_t t23 = __shfl_sync(kFull, d1.x, src);
       const uint64_t t45 = __shfl_sync(kFull, d1.y, src);
-      if (!((rm >> src) & 1u)) continue;
+      if (h && s1 < 0) continue;
       const int len = int(rh & 63), cnt = int(e0 >> 48);
       const uint64_t start = rh >> 16;
       uint32_t* dst = a.staging + (start / kTile) * kStage + ((rh >> 6) & 1023);
