@@ -173,6 +173,17 @@ int bbpe_decode_device(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* d_ids
                        size_t n_rows, uint64_t n_ids, uint8_t* d_out_bytes, uint64_t cap,
                        uint64_t* d_out_byte_offsets, uint64_t* total);
 
+/* The same with the ctx's special-token set (bbpe_ctx_set_specials): ids the
+ * table lacks decode to their special's bytes (decode, merge_table.hpp:565-579);
+ * skip_specials != 0 drops special ids first (decode_batch, batch.hpp:128-154).
+ * (The two calls above are these with skip_specials = 0.) */
+int bbpe_decode_batch_ex(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* ids, const uint64_t* tok_offsets,
+                         size_t n_rows, int skip_specials, uint8_t* out_bytes, uint64_t cap,
+                         uint64_t* out_byte_offsets, uint64_t* total);
+int bbpe_decode_device_ex(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* d_ids, const uint64_t* d_tok_offsets,
+                          size_t n_rows, uint64_t n_ids, int skip_specials, uint8_t* d_out_bytes, uint64_t cap,
+                          uint64_t* d_out_byte_offsets, uint64_t* total);
+
 /* ---- JSON-lines text of a device CSR batch (
  * write_batch_jsonl, batch.hpp:157-166): {"ids":[...],"len":n}\n per row,
  * byte-identical to the compact nlohmann dump. Writes at most cap bytes;

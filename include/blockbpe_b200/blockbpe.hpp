@@ -305,9 +305,8 @@ class Encoder {
   }
   // encode_batch's rows as CSR: split at `specials` on the device, BOS/EOS
   // added (bbpe_ctx_set_specials + bbpe_encode_batch).
-  void encode_rows_csr(const MergeTable& t, const SpecialTokenSet& specials, bool add_bos, bool add_eos,
-                       const std::string& bytes, const std::vector<std::uint64_t>& offsets, std::vector<TokenId>& ids,
-                       std::vector<std::uint64_t>& out_offsets) {
+  // The ctx's special-token set (split by encode, resolved by decode).
+  void set_specials(const SpecialTokenSet& specials) {
     std::string blob;
     std::vector<std::uint64_t> so{0};
     std::vector<std::uint32_t> sid;
@@ -318,6 +317,11 @@ class Encoder {
     }
     detail::check(bbpe_ctx_set_specials(h_.get(), sid.size(), reinterpret_cast<const std::uint8_t*>(blob.data()),
                                         so.data(), sid.data()));
+  }
+  void encode_rows_csr(const MergeTable& t, const SpecialTokenSet& specials, bool add_bos, bool add_eos,
+                       const std::string& bytes, const std::vector<std::uint64_t>& offsets, std::vector<TokenId>& ids,
+                       std::vector<std::uint64_t>& out_offsets) {
+    set_specials(specials);
     const std::size_t n = offsets.size() - 1;
     ids.resize(offsets.back() - offsets.front() + 2 * n + 1);
     out_offsets.resize(n + 1);
@@ -505,54 +509,33 @@ inline std::string decode(const MergeTable& table, const SpecialTokenSet& specia
 // decode_batch (batch.hpp:128-154). With an Encoder, rows without special
 // ids (or with skip_specials) decode on its GPU (bbpe_decode_batch, SURVEY
 // §8f(2)); the result and the row-tagged DecodeError are the same.
+// decode_batch (batch.hpp:128-154) on the GPU: the rows' ids as CSR, ids the
+// table lacks resolved through the special tokens, skip_specials dropping
+// special ids (bbpe_decode_batch_ex); "row r: unknown token id ..." errors.
 inline std::vector<std::string> decode_batch(const BatchEncoding& enc, const MergeTable& table,
                                              const SpecialTokenSet& specials, bool skip_specials,
                                              Encoder* gpu = nullptr) {
-  std::vector<std::string> out(enc.batch_size);
-  if (gpu) {
-    std::vector<std::uint32_t> ids;
-    std::vector<std::uint64_t> off{0};
-    bool host_only = false;
-    for (std::size_t r = 0; r < enc.batch_size && !host_only; ++r) {
-      for (TokenId id : enc.row(r)) {
-        if (specials.contains_id(id)) {
-          if (skip_specials) continue;
-          host_only = true;  // special bytes are not table tokens
-          break;
-        }
-        ids.push_back(id);
-      }
-      off.push_back(ids.size());
-    }
-    if (!host_only) {
-      // First call sizes the output (cap 0), second fills it.
-      std::vector<std::uint8_t> bytes;
-      std::vector<std::uint64_t> boff(enc.batch_size + 1);
-      std::uint64_t total = 0;
-      detail::check(bbpe_decode_batch(gpu->handle(), table.handle(), ids.data(), off.data(), enc.batch_size,
-                                      nullptr, 0, boff.data(), &total));
-      bytes.resize(std::max<std::uint64_t>(total, 1));
-      detail::check(bbpe_decode_batch(gpu->handle(), table.handle(), ids.data(), off.data(), enc.batch_size,
-                                      bytes.data(), total, boff.data(), &total));
-      for (std::size_t r = 0; r < enc.batch_size; ++r)
-        out[r].assign(reinterpret_cast<const char*>(bytes.data()) + boff[r], boff[r + 1] - boff[r]);
-      return out;
-    }
-  }
+  Encoder& e = gpu ? *gpu : default_encoder();
+  e.set_specials(specials);
+  std::vector<std::uint32_t> ids;
+  std::vector<std::uint64_t> off{0};
   for (std::size_t r = 0; r < enc.batch_size; ++r) {
-    TokenSeq ids = enc.row(r);
-    if (skip_specials) {
-      TokenSeq kept;
-      for (TokenId id : ids)
-        if (!specials.contains_id(id)) kept.push_back(id);
-      ids.swap(kept);
-    }
-    try {
-      out[r] = decode(table, specials, ids);
-    } catch (const DecodeError& e) {
-      throw DecodeError("row " + std::to_string(r) + ": " + e.what());
-    }
+    const TokenSeq row = enc.row(r);
+    ids.insert(ids.end(), row.begin(), row.end());
+    off.push_back(ids.size());
   }
+  // First call sizes the output (cap 0), second fills it.
+  std::vector<std::uint8_t> bytes;
+  std::vector<std::uint64_t> boff(enc.batch_size + 1);
+  std::uint64_t total = 0;
+  detail::check(bbpe_decode_batch_ex(e.handle(), table.handle(), ids.data(), off.data(), enc.batch_size,
+                                     skip_specials ? 1 : 0, nullptr, 0, boff.data(), &total));
+  bytes.resize(std::max<std::uint64_t>(total, 1));
+  detail::check(bbpe_decode_batch_ex(e.handle(), table.handle(), ids.data(), off.data(), enc.batch_size,
+                                     skip_specials ? 1 : 0, bytes.data(), total, boff.data(), &total));
+  std::vector<std::string> out(enc.batch_size);
+  for (std::size_t r = 0; r < enc.batch_size; ++r)
+    out[r].assign(reinterpret_cast<const char*>(bytes.data()) + boff[r], boff[r + 1] - boff[r]);
   return out;
 }
 

@@ -79,6 +79,10 @@ SIGNATURES = {
     "bbpe_decode_batch": (C.c_int, [C.c_void_p, C.c_void_p, u32p, u64p, C.c_size_t, u8p, C.c_uint64, u64p, u64p]),
     "bbpe_decode_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64,
                                      C.c_void_p, C.c_uint64, C.c_void_p, u64p]),
+    "bbpe_decode_batch_ex": (C.c_int, [C.c_void_p, C.c_void_p, u32p, u64p, C.c_size_t, C.c_int, u8p, C.c_uint64,
+                                       u64p, u64p]),
+    "bbpe_decode_device_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64,
+                                        C.c_int, C.c_void_p, C.c_uint64, C.c_void_p, u64p]),
     "bbpe_jsonl_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64, C.c_void_p,
                                     C.c_uint64, u64p]),
     "bbpe_batch_widest_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int, u64p]),

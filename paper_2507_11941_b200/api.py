@@ -553,21 +553,25 @@ class Encoder:
         return nout.value
 
     def decode_packed(self, table: MergeTable, ids: np.ndarray, offsets: np.ndarray,
-                      out: Optional[np.ndarray] = None, out_offsets: Optional[np.ndarray] = None):
+                      out: Optional[np.ndarray] = None, out_offsets: Optional[np.ndarray] = None,
+                      skip_specials: bool = False):
         """Device batch decode (decode / decode_batch, merge_table.hpp:565-579,
-        batch.hpp:128-154): CSR ids -> (bytes u8, byte offsets u64[n+1])."""
+        batch.hpp:128-154): CSR ids -> (bytes u8, byte offsets u64[n+1]). Ids the
+        table lacks decode through this encoder's special tokens (set_specials);
+        skip_specials drops special ids."""
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
         offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
         n = offsets.size - 1
         if out is None:
-            # Upper bound: the longest token times the number of ids.
-            out = np.empty(max(int(offsets[-1] - offsets[0]) * table.max_token_bytes(), 1), dtype=np.uint8)
+            # Upper bound: the longest token (or special) times the number of ids.
+            widest = max([table.max_token_bytes()] + [len(b) for b, _ in self._sp_key])
+            out = np.empty(max(int(offsets[-1] - offsets[0]) * widest, 1), dtype=np.uint8)
         if out_offsets is None:
             out_offsets = np.empty(n + 1, dtype=np.uint64)
         total = C.c_uint64()
-        _check(LIB.bbpe_decode_batch(self._h, table.handle, _p(ids, C.c_uint32) if ids.size else None,
-                                     _p(offsets, C.c_uint64), n, _p(out, C.c_uint8), out.size,
-                                     _p(out_offsets, C.c_uint64), C.byref(total)))
+        _check(LIB.bbpe_decode_batch_ex(self._h, table.handle, _p(ids, C.c_uint32) if ids.size else None,
+                                        _p(offsets, C.c_uint64), n, int(skip_specials), _p(out, C.c_uint8), out.size,
+                                        _p(out_offsets, C.c_uint64), C.byref(total)))
         if total.value > out.size:
             raise UsageError(f"decode output capacity {out.size} is smaller than the {total.value} bytes produced")
         return out[: total.value], out_offsets
@@ -581,11 +585,12 @@ class Encoder:
         return total.value
 
     def decode_device(self, table: MergeTable, d_ids, d_offsets, n_rows: int, n_ids: int, d_out, cap: int,
-                      d_out_offsets) -> int:
+                      d_out_offsets, skip_specials: bool = False) -> int:
         """Device pointers: CSR ids -> CSR bytes on device; returns the byte total."""
         total = C.c_uint64()
-        _check(LIB.bbpe_decode_device(self._h, table.handle, C.c_void_p(d_ids), C.c_void_p(d_offsets), n_rows,
-                                      n_ids, C.c_void_p(d_out), cap, C.c_void_p(d_out_offsets), C.byref(total)))
+        _check(LIB.bbpe_decode_device_ex(self._h, table.handle, C.c_void_p(d_ids), C.c_void_p(d_offsets), n_rows,
+                                         n_ids, int(skip_specials), C.c_void_p(d_out), cap,
+                                         C.c_void_p(d_out_offsets), C.byref(total)))
         return total.value
 
     def block_bpe(self, table: MergeTable, tokens: Sequence[int], trace: bool = False):
@@ -918,18 +923,23 @@ def decode(table: MergeTable, specials: SpecialTokenSet, ids: Sequence[int]) -> 
 
 
 def decode_batch(encoding: BatchEncoding, table: MergeTable, specials: SpecialTokenSet,
-                 skip_specials: bool) -> List[bytes]:
-    """batch.hpp:128-154."""
-    out = []
-    for r in range(encoding.batch_size):
-        ids = encoding.row(r)
-        if skip_specials:
-            ids = [i for i in ids if not specials.contains_id(i)]
-        try:
-            out.append(decode(table, specials, ids))
-        except DecodeError as e:
-            raise DecodeError(f"row {r}: {e}") from None
-    return out
+                 skip_specials: bool, encoder: Optional[Encoder] = None) -> List[bytes]:
+    """batch.hpp:128-154, on the GPU: the rows' ids as CSR, decoded through the
+    table and the special tokens (bbpe_decode_batch_ex), "row r: " errors."""
+    n = encoding.batch_size
+    lens = np.asarray(encoding.lengths[:n], dtype=np.int64)
+    offsets = np.zeros(n + 1, np.uint64)
+    np.cumsum(lens, out=offsets[1:])
+    L = int(encoding.max_len)
+    if n and L:
+        mask = np.arange(L)[None, :] < lens[:, None]
+        ids = np.ascontiguousarray(np.asarray(encoding.ids, dtype=np.uint32).reshape(n, L)[mask])
+    else:
+        ids = np.zeros(0, np.uint32)
+    enc = encoder or default_encoder()
+    enc.set_specials(specials)
+    data, boff = enc.decode_packed(table, ids, offsets, skip_specials=skip_specials)
+    return [data[int(boff[r]):int(boff[r + 1])].tobytes() for r in range(n)]
 
 
 def write_batch_jsonl(encoding: BatchEncoding) -> str:

@@ -202,6 +202,9 @@ struct bbpe_ctx {
   // of bbpe_encode_batch_device.
   uint32_t sp_n = 0;
   DevBuf sp_blob, sp_off, sp_id, sp_first;
+  DevBuf sp_dec;                  // decode: ids ascending | byte starts | lengths (u32 x 3 sp_dn)
+  uint32_t sp_dn = 0;
+  std::vector<uint32_t> sp_dec_ids;  // host copy (error-index rebasing under skip)
   DevBuf sp_cand, sp_cnt, sp_lit, sp_sums, sp_segoff, sp_segsrc, sp_ids, sp_compact, sp_segtok, sp_segtokoff;
 };
 
@@ -1030,7 +1033,7 @@ const bbpe::DeviceReplica& decode_table(bbpe_ctx& c, const bbpe_table& t) {
 // raises the reference's DecodeError for the first unknown id.
 uint64_t decode_on_device(bbpe_ctx& c, const bbpe_table& t, const uint32_t* d_ids, const uint64_t* d_toff,
                           uint64_t n_rows, uint64_t n_ids, uint8_t* d_out, uint64_t cap, uint64_t* d_ooff,
-                          const uint64_t* h_toff) {
+                          const uint64_t* h_toff, int skip = 0) {
   using namespace bbpe;
   const DeviceReplica& rep = decode_table(c, t);
   DecodeArgs a{};
@@ -1051,6 +1054,14 @@ uint64_t decode_on_device(bbpe_ctx& c, const bbpe_table& t, const uint32_t* d_id
   a.out = d_out;
   a.cap = cap;
   a.out_off = d_ooff;
+  a.sp_n = c.sp_dn;
+  a.skip = skip;
+  if (c.sp_dn) {
+    a.sp_ids = c.sp_dec.as<uint32_t>();
+    a.sp_off = a.sp_ids + c.sp_dn;
+    a.sp_len = a.sp_ids + 2 * c.sp_dn;
+    a.sp_blob = c.sp_blob.as<uint8_t>();
+  }
   ck(cudaMemsetAsync(a.err, 0xFF, 8, c.stream), "memset");
   launch_decode(a, c.stream);
   c.launches += n_ids ? 4 : 1;
@@ -1074,8 +1085,15 @@ uint64_t decode_on_device(bbpe_ctx& c, const bbpe_table& t, const uint32_t* d_id
     }
     uint32_t id = 0;
     ck(cudaMemcpy(&id, d_ids + i, 4, cudaMemcpyDeviceToHost), "D2H");
+    uint64_t at = i - (h_toff[lo] - base);  // index within the row (after skipped specials)
+    if (skip && c.sp_dn && at) {
+      std::vector<uint32_t> head(at);
+      ck(cudaMemcpy(head.data(), d_ids + (h_toff[lo] - base), at * 4, cudaMemcpyDeviceToHost), "D2H");
+      for (uint32_t v : head)
+        if (std::binary_search(c.sp_dec_ids.begin(), c.sp_dec_ids.end(), v)) --at;
+    }
     throw Error(BBPE_DECODE, "row " + std::to_string(lo) + ": unknown token id " + std::to_string(id) +
-                                 " at index " + std::to_string(i - (h_toff[lo] - base)));
+                                 " at index " + std::to_string(at));
   }
   return res[1];
 }
@@ -1087,12 +1105,19 @@ extern "C" {
 int bbpe_decode_device(bbpe_ctx* c, const bbpe_table* t, const uint32_t* d_ids, const uint64_t* d_tok_offsets,
                        size_t n_rows, uint64_t n_ids, uint8_t* d_out_bytes, uint64_t cap,
                        uint64_t* d_out_byte_offsets, uint64_t* total) {
+  return bbpe_decode_device_ex(c, t, d_ids, d_tok_offsets, n_rows, n_ids, 0, d_out_bytes, cap, d_out_byte_offsets,
+                               total);
+}
+
+int bbpe_decode_device_ex(bbpe_ctx* c, const bbpe_table* t, const uint32_t* d_ids, const uint64_t* d_tok_offsets,
+                          size_t n_rows, uint64_t n_ids, int skip_specials, uint8_t* d_out_bytes, uint64_t cap,
+                          uint64_t* d_out_byte_offsets, uint64_t* total) {
   BBPE_TRY
   if (!c || !t || !d_tok_offsets || !d_out_byte_offsets) throw bbpe::usage_error("null argument");
   if (n_ids && (!d_ids || (cap && !d_out_bytes))) throw bbpe::usage_error("null buffer");
   DeviceGuard g(c->device);
   const uint64_t tot = decode_on_device(*c, *t, d_ids, d_tok_offsets, n_rows, n_ids, d_out_bytes, cap,
-                                        d_out_byte_offsets, nullptr);
+                                        d_out_byte_offsets, nullptr, skip_specials);
   if (total) *total = tot;
   return BBPE_OK;
   BBPE_CATCH
@@ -1101,6 +1126,12 @@ int bbpe_decode_device(bbpe_ctx* c, const bbpe_table* t, const uint32_t* d_ids, 
 int bbpe_decode_batch(bbpe_ctx* c, const bbpe_table* t, const uint32_t* ids, const uint64_t* tok_offsets,
                       size_t n_rows, uint8_t* out_bytes, uint64_t cap, uint64_t* out_byte_offsets,
                       uint64_t* total) {
+  return bbpe_decode_batch_ex(c, t, ids, tok_offsets, n_rows, 0, out_bytes, cap, out_byte_offsets, total);
+}
+
+int bbpe_decode_batch_ex(bbpe_ctx* c, const bbpe_table* t, const uint32_t* ids, const uint64_t* tok_offsets,
+                         size_t n_rows, int skip_specials, uint8_t* out_bytes, uint64_t cap,
+                         uint64_t* out_byte_offsets, uint64_t* total) {
   BBPE_TRY
   if (!c || !t || !tok_offsets || !out_byte_offsets) throw bbpe::usage_error("null argument");
   const uint64_t base = tok_offsets[0], n_ids = tok_offsets[n_rows] - base;
@@ -1121,7 +1152,7 @@ int bbpe_decode_batch(bbpe_ctx* c, const bbpe_table* t, const uint32_t* ids, con
   c->dec_out.ensure(std::max<uint64_t>(cap, 1));
   const uint64_t tot = decode_on_device(*c, *t, c->dec_ids.as<uint32_t>(), c->dec_toff.as<uint64_t>(), n_rows,
                                         n_ids, c->dec_out.as<uint8_t>(), cap, c->dec_ooff.as<uint64_t>(),
-                                        tok_offsets);
+                                        tok_offsets, skip_specials);
   const uint64_t ncopy = std::min(tot, cap);
   if (ncopy) ck(cudaMemcpyAsync(out_bytes, c->dec_out.p, ncopy, cudaMemcpyDeviceToHost, c->stream), "D2H bytes");
   ck(cudaMemcpyAsync(out_byte_offsets, c->dec_ooff.p, (n_rows + 1) * 8, cudaMemcpyDeviceToHost, c->stream),
@@ -1248,6 +1279,8 @@ int bbpe_ctx_set_specials(bbpe_ctx* c, size_t n, const uint8_t* blob, const uint
   }
   DeviceGuard g(c->device);
   c->sp_n = 0;
+  c->sp_dn = 0;
+  c->sp_dec_ids.clear();
   if (es.empty()) return BBPE_OK;
   c->sp_blob.ensure(hb.size());
   c->sp_off.ensure(ho.size() * 4);
@@ -1257,6 +1290,25 @@ int bbpe_ctx_set_specials(bbpe_ctx* c, size_t n, const uint8_t* blob, const uint
   ck(cudaMemcpy(c->sp_off.p, ho.data(), ho.size() * 4, cudaMemcpyHostToDevice), "specials upload");
   ck(cudaMemcpy(c->sp_id.p, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice), "specials upload");
   ck(cudaMemcpy(c->sp_first.p, hf.data(), 32, cudaMemcpyHostToDevice), "specials upload");
+  // Decode view by id; for an id held by several strings the one latest in
+  // the longest-first order wins (SpecialTokenSet::rebuild_index, merge_table.hpp:357-360).
+  std::vector<std::pair<uint32_t, size_t>> by_id;
+  for (size_t k = 0; k < es.size(); ++k) by_id.push_back({es[k].id, k});
+  std::stable_sort(by_id.begin(), by_id.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+  std::vector<uint32_t> d_id, d_off, d_len;
+  for (size_t k = 0; k < by_id.size(); ++k) {
+    if (k + 1 < by_id.size() && by_id[k + 1].first == by_id[k].first) continue;  // keep the last
+    d_id.push_back(by_id[k].first);
+    d_off.push_back(ho[by_id[k].second]);
+    d_len.push_back(ho[by_id[k].second + 1] - ho[by_id[k].second]);
+  }
+  std::vector<uint32_t> packed(d_id);
+  packed.insert(packed.end(), d_off.begin(), d_off.end());
+  packed.insert(packed.end(), d_len.begin(), d_len.end());
+  c->sp_dec.ensure(packed.size() * 4);
+  ck(cudaMemcpy(c->sp_dec.p, packed.data(), packed.size() * 4, cudaMemcpyHostToDevice), "specials upload");
+  c->sp_dn = uint32_t(d_id.size());
+  c->sp_dec_ids = d_id;
   c->sp_n = uint32_t(es.size());
   return BBPE_OK;
   BBPE_CATCH
@@ -1462,7 +1514,7 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     c->sc.release();
     for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_sums,
                       &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar,
-                      &c->sp_blob, &c->sp_off, &c->sp_id, &c->sp_first, &c->sp_cand, &c->sp_cnt, &c->sp_lit,
+                      &c->sp_blob, &c->sp_off, &c->sp_id, &c->sp_first, &c->sp_dec, &c->sp_cand, &c->sp_cnt, &c->sp_lit,
                       &c->sp_sums, &c->sp_segoff, &c->sp_segsrc, &c->sp_ids, &c->sp_compact, &c->sp_segtok,
                       &c->sp_segtokoff})
       b->release();

@@ -21,18 +21,47 @@ namespace {
 
 constexpr int kDecThreads = 256;
 
+// decode (merge_table.hpp:565-579) of one id: the table's bytes, else the
+// special's; decode_batch's skip_specials drops special ids first
+// (batch.hpp:134-139). Returns false for an unknown id.
+__device__ __forceinline__ bool dec_entry(const DecodeArgs& a, uint32_t id, const uint8_t*& src, uint64_t& len) {
+  int k = -1;
+  if (a.sp_n) {
+    uint32_t lo = 0, hi = a.sp_n;
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (a.sp_ids[m] < id) lo = m + 1;
+      else hi = m;
+    }
+    if (lo < a.sp_n && a.sp_ids[lo] == id) k = int(lo);
+    if (k >= 0 && a.skip) {
+      len = 0;
+      src = nullptr;
+      return true;
+    }
+  }
+  const uint64_t e = id < a.dec_n ? __ldg(a.dec + id) : ~0ull;
+  if (e != ~0ull) {
+    len = e & 0xFFFFFF;
+    src = a.dec_bytes + (e >> 24);
+    return true;
+  }
+  if (k < 0) return false;
+  len = a.sp_len[k];
+  src = a.sp_blob + a.sp_off[k];
+  return true;
+}
+
 __global__ void __launch_bounds__(kDecThreads) k_dec_len(DecodeArgs a) {
   __shared__ uint64_t s_warp[kDecThreads / 32];
   const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t len = 0;
   if (i < a.n_ids) {
-    const uint32_t id = a.ids[i];
-    const uint64_t e = id < a.dec_n ? __ldg(a.dec + id) : ~0ull;
-    if (e == ~0ull) {
+    const uint8_t* src;
+    if (!dec_entry(a, a.ids[i], src, len)) {
+      len = 0;
       atomicMin(reinterpret_cast<unsigned long long*>(a.err), (unsigned long long)i);
-    } else {
-      len = e & 0xFFFFFF;
     }
   }
   uint64_t inc = len;
@@ -99,12 +128,10 @@ __global__ void __launch_bounds__(1024) k_dec_scan(uint64_t* sums, uint64_t n_bl
 __global__ void __launch_bounds__(kDecThreads) k_dec_copy(DecodeArgs a) {
   const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
   if (i >= a.n_ids) return;
-  const uint32_t id = a.ids[i];
-  const uint64_t e = id < a.dec_n ? __ldg(a.dec + id) : ~0ull;
-  if (e == ~0ull) return;
+  const uint8_t* src;
+  uint64_t len;
+  if (!dec_entry(a, a.ids[i], src, len)) return;
   const uint64_t pos = a.block_sums[blockIdx.x] + a.pos[i];
-  const uint64_t len = e & 0xFFFFFF;
-  const uint8_t* src = a.dec_bytes + (e >> 24);
   for (uint64_t k = 0; k < len && pos + k < a.cap; ++k) a.out[pos + k] = __ldg(src + k);
 }
 

@@ -22,6 +22,14 @@ struct DecodeArgs {
   uint64_t cap;
   uint64_t* out_off;         // n_rows + 1 row byte offsets
   uint64_t* err;             // min index of an unknown id (~0 = none)
+  // Special tokens (the ctx's set), sorted by id: ids the table lacks decode
+  // to their bytes; with skip, special ids are dropped (decode_batch).
+  const uint32_t* sp_ids;    // sp_n, ascending
+  const uint32_t* sp_off;    // sp_n: byte start of each in sp_blob
+  const uint32_t* sp_len;    // sp_n
+  const uint8_t* sp_blob;
+  uint32_t sp_n;
+  int skip;
 };
 
 void launch_decode(const DecodeArgs& a, cudaStream_t s);

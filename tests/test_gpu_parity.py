@@ -888,3 +888,31 @@ def test_pattern_mode_with_specials_vs_reference(gpt2):
     ids, oo = enc.encode_batch_packed(gpt2, d, o)
     assert np.array_equal(oo, want_off)
     assert np.array_equal(ids, want_ids)
+
+
+@pytest.mark.parametrize("skip", [False, True])
+def test_device_decode_batch_with_specials(gpt2, skip):
+    """decode_batch (batch.hpp:128-154) on the GPU with special tokens: ids the
+    table lacks decode to their special's bytes, skip_specials drops special
+    ids (a special id that is also a table token -- GPT-2's end of text -- is
+    dropped too); the unknown-id error counts the index among kept ids."""
+    sp = bb.SpecialTokenSet()
+    for b, i in SPECIALS:
+        sp.add(b, i)
+    rows = _special_rows(gpt2)[:300]
+    cfg = bb.BlockConfig(256, None)
+    be = bb.encode_batch(rows, gpt2, sp, cfg, 0)
+    got = bb.decode_batch(be, gpt2, sp, skip)
+    for r in range(0, be.batch_size, 5):  # the host mirror of decode, merge_table.hpp:565-579
+        ids = be.row(r)
+        if skip:
+            ids = [i for i in ids if not sp.contains_id(i)]
+        assert got[r] == bb.decode(gpt2, sp, ids), r
+    if not skip:
+        assert got == [bytes(x) for x in rows]  # lossless round trip through the specials
+    bad = bb.BatchEncoding(batch_size=2, max_len=4, pad_id=0)
+    bad.ids = np.array([31373, 0, 0, 0, 50300, 60001, 70000, 995], np.uint32)
+    bad.lengths = np.array([1, 4], np.uint32)
+    bad.mask = np.ones(8, np.uint8)
+    with pytest.raises(bb.DecodeError, match=f"row 1: unknown token id 70000 at index {0 if skip else 2}"):
+        bb.decode_batch(bad, gpt2, sp, skip)
