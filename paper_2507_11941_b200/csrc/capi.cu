@@ -1375,25 +1375,38 @@ uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t*
     encode_device_sync(*c, *t, d_bytes, d_offsets, n, total_bytes, d_out_ids, d_out_offsets, s);
     return read_u64(d_out_offsets + n);
   }
-  // (2) literal segments: r + match_base[r] + j, j = 0..matches(r), compacted.
+  // (2) segments. When every byte value has a token (and no pass cap is set),
+  // special bytes can be encoded harmlessly: the segments tile the input in place (literal,
+  // special, ..., literal; the specials' tokens are dropped by the stitch).
+  // Otherwise the literal bytes are compacted (r + match_base[r] + j).
+  // (A pass cap could fail on a special's bytes, which the reference never encodes.)
+  const bool inplace = c->cfg.max_passes <= 0 &&
+                       std::none_of(t->lut.begin(), t->lut.end(), [](uint32_t v) { return v == bbpe::kInvalidToken; });
+  const int stride = inplace ? 2 : 1;
   const uint8_t* seg_bytes = d_bytes;
   const uint64_t* seg_offsets = d_offsets;
   uint64_t n_seg = n, seg_total = total_bytes;
   if (M) {
-    bbpe::launch_scan_u64(c->sp_lit.as<uint64_t>(), n, c->sp_sums.as<uint64_t>(), s);
-    seg_total = read_u64(c->sp_lit.as<uint64_t>() + n);
-    n_seg = n + M;
+    n_seg = n + stride * M;
     c->sp_segoff.ensure((n_seg + 1) * 8);
-    c->sp_segsrc.ensure(n_seg * 8);
     c->sp_ids.ensure(M * 4);
-    c->sp_compact.ensure(seg_total + 16);
-    bbpe::launch_sp_emit(d_bytes, d_offsets, n, sp, c->sp_cand.as<uint32_t>(), match_base,
-                         c->sp_lit.as<uint64_t>(), c->sp_segoff.as<uint64_t>(), c->sp_segsrc.as<uint64_t>(),
-                         c->sp_ids.as<uint32_t>(), s);
-    bbpe::launch_sp_copy(d_bytes, n_seg, c->sp_segoff.as<uint64_t>(), c->sp_segsrc.as<uint64_t>(),
-                         c->sp_compact.as<uint8_t>(), sm, s);
-    c->launches += 5;
-    seg_bytes = c->sp_compact.as<uint8_t>();
+    if (inplace) {
+      bbpe::launch_sp_emit(d_bytes, d_offsets, n, sp, c->sp_cand.as<uint32_t>(), match_base, nullptr,
+                           c->sp_segoff.as<uint64_t>(), nullptr, c->sp_ids.as<uint32_t>(), 1, s);
+      c->launches += 1;
+    } else {
+      bbpe::launch_scan_u64(c->sp_lit.as<uint64_t>(), n, c->sp_sums.as<uint64_t>(), s);
+      seg_total = read_u64(c->sp_lit.as<uint64_t>() + n);
+      c->sp_segsrc.ensure(n_seg * 8);
+      c->sp_compact.ensure(seg_total + 16);
+      bbpe::launch_sp_emit(d_bytes, d_offsets, n, sp, c->sp_cand.as<uint32_t>(), match_base,
+                           c->sp_lit.as<uint64_t>(), c->sp_segoff.as<uint64_t>(), c->sp_segsrc.as<uint64_t>(),
+                           c->sp_ids.as<uint32_t>(), 0, s);
+      bbpe::launch_sp_copy(d_bytes, n_seg, c->sp_segoff.as<uint64_t>(), c->sp_segsrc.as<uint64_t>(),
+                           c->sp_compact.as<uint8_t>(), sm, s);
+      c->launches += 5;
+      seg_bytes = c->sp_compact.as<uint8_t>();
+    }
     seg_offsets = c->sp_segoff.as<uint64_t>();
   }
   // (3) encode the literal segments as rows.
@@ -1410,15 +1423,16 @@ uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t*
     const uint64_t seg = std::stoull(m.substr(4, colon - 4));
     std::vector<uint64_t> mb(n + 1);
     ck(cudaMemcpy(mb.data(), match_base, (n + 1) * 8, cudaMemcpyDeviceToHost), "D2H");
-    uint64_t lo = 0, hi = n - 1;  // max r with r + mb[r] <= seg
+    uint64_t lo = 0, hi = n - 1;  // max r with r + stride * mb[r] <= seg
     while (lo < hi) {
       const uint64_t mid = (lo + hi + 1) / 2;
-      if (mid + mb[mid] <= seg) lo = mid; else hi = mid - 1;
+      if (mid + stride * mb[mid] <= seg) lo = mid; else hi = mid - 1;
     }
     throw bbpe::Error(e.code, "row " + std::to_string(lo) + m.substr(colon));
   }
   // (4) stitch: BOS, segment tokens, special ids, EOS.
-  bbpe::launch_sp_lengths(n, match_base, c->sp_segtokoff.as<uint64_t>(), add_bos, add_eos, d_out_offsets, s);
+  bbpe::launch_sp_lengths(n, match_base, c->sp_segtokoff.as<uint64_t>(), add_bos, add_eos, M ? stride : 1,
+                          d_out_offsets, s);
   bbpe::launch_scan_u64(d_out_offsets, n, c->sp_sums.as<uint64_t>(), s);
   const uint64_t out_total = read_u64(d_out_offsets + n);
   if (out_total > out_capacity)
@@ -1426,7 +1440,7 @@ uint64_t encode_batch_on_device(bbpe_ctx* c, const bbpe_table* t, const uint8_t*
                             std::to_string(out_total) + " ids");
   if (out_total && !d_out_ids) throw bbpe::usage_error("null output ids");
   bbpe::launch_sp_stitch(n, match_base, c->sp_segtokoff.as<uint64_t>(), c->sp_segtok.as<uint32_t>(),
-                         c->sp_ids.as<uint32_t>(), d_out_offsets, bos_id, eos_id, d_out_ids, sm, s);
+                         c->sp_ids.as<uint32_t>(), d_out_offsets, bos_id, eos_id, M ? stride : 1, d_out_ids, sm, s);
   c->launches += n ? 5 : 1;
   ck(cudaStreamSynchronize(s), "stitch");
   return out_total;

@@ -118,14 +118,26 @@ __global__ void __launch_bounds__(256) k_sp_cand(const uint8_t* bytes, uint64_t 
   if (threadIdx.x < 8) s_first[threadIdx.x] = sp.first[threadIdx.x];
   __syncthreads();
   const uint64_t nw = (total + 31) / 32, stride = uint64_t(gridDim.x) * blockDim.x;
+  const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
   for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < nw; w += stride) {
     uint32_t bits = 0;
     const uint64_t p0 = w * 32, p1 = min(total, p0 + 32);
-    for (uint64_t p = p0; p < p1; ++p) {
-      const uint8_t c = __ldg(bytes + p);
-      if ((s_first[c >> 5] >> (c & 31)) & 1u) {
+    uint32_t v[8];
+    if (aligned && p1 - p0 == 32) {  // two 16-byte loads
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(bytes + p0));
+      const uint4 y = __ldg(reinterpret_cast<const uint4*>(bytes + p0 + 16));
+      v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w, v[4] = y.x, v[5] = y.y, v[6] = y.z, v[7] = y.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = 0;
+      for (uint64_t p = p0; p < p1; ++p) v[(p - p0) >> 2] |= uint32_t(__ldg(bytes + p)) << (8 * ((p - p0) & 3));
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t c = (v[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+      if (((s_first[c >> 5] >> (c & 31)) & 1u) && p0 + k < p1) {
         uint32_t id;
-        if (sp_match(sp, bytes, p, total, id)) bits |= 1u << (p - p0);
+        if (sp_match(sp, bytes, p0 + k, total, id)) bits |= 1u << k;
       }
     }
     cand[w] = bits;
@@ -170,11 +182,23 @@ __global__ void k_sp_rows(const uint8_t* bytes, const uint64_t* offsets, uint64_
 
 __global__ void k_sp_emit(const uint8_t* bytes, const uint64_t* offsets, uint64_t n_rows, SpecArgs sp,
                           const uint32_t* cand, const uint64_t* match_base, const uint64_t* lit_base,
-                          uint64_t* seg_off, uint64_t* seg_src, uint32_t* sp_ids) {
+                          uint64_t* seg_off, uint64_t* seg_src, uint32_t* sp_ids, int inplace) {
   const uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (r >= n_rows) return;
   const uint64_t rs = offsets[r], re = offsets[r + 1];
   const uint64_t mb = match_base[r];
+  if (inplace) {  // segments tile the input: literal, special, literal, ..., literal
+    uint64_t seg = r + 2 * mb, src = rs, j = 0;
+    sp_walk(sp, bytes, cand, rs, re, [&](uint64_t p, uint32_t len, uint32_t id) {
+      seg_off[seg++] = src;
+      seg_off[seg++] = p;
+      sp_ids[mb + j++] = id;
+      src = p + len;
+    });
+    seg_off[seg] = src;
+    if (r + 1 == n_rows) seg_off[seg + 1] = re;
+    return;
+  }
   uint64_t seg = r + mb, at = lit_base[r], src = rs, j = 0;
   sp_walk(sp, bytes, cand, rs, re, [&](uint64_t p, uint32_t len, uint32_t id) {
     seg_off[seg] = at;  // literal segment [src, p)
@@ -201,37 +225,60 @@ __global__ void __launch_bounds__(256) k_sp_copy(const uint8_t* bytes, uint64_t 
 }
 
 __global__ void k_sp_len(uint64_t n_rows, const uint64_t* match_base, const uint64_t* seg_tok_off, int add_bos,
-                         int add_eos, uint64_t* out_len) {
+                         int add_eos, int stride, uint64_t* out_len) {
   const uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (r >= n_rows) return;
-  const uint64_t k = match_base[r + 1] - match_base[r], s0 = r + match_base[r];
-  out_len[r] = uint64_t(add_bos) + uint64_t(add_eos) + k + (seg_tok_off[s0 + k + 1] - seg_tok_off[s0]);
+  const uint64_t k = match_base[r + 1] - match_base[r], s0 = r + stride * match_base[r];
+  uint64_t lit = 0;
+  if (stride == 1) {
+    lit = seg_tok_off[s0 + k + 1] - seg_tok_off[s0];  // the row's literal segments are contiguous
+  } else {
+    for (uint64_t j = 0; j <= k; ++j) lit += seg_tok_off[s0 + 2 * j + 1] - seg_tok_off[s0 + 2 * j];
+  }
+  out_len[r] = uint64_t(add_bos) + uint64_t(add_eos) + k + lit;
 }
 
-// Warp per row (grid-stride).
+// Warp per 32 rows (grid-stride): lane l loads row l's metadata (match base,
+// output offset, the first segments' token ranges) so the rows' dependent
+// loads overlap; the warp then copies row by row, lanes along the tokens.
 __global__ void __launch_bounds__(256) k_sp_stitch(uint64_t n_rows, const uint64_t* match_base,
                                                    const uint64_t* seg_tok_off, const uint32_t* seg_ids,
                                                    const uint32_t* sp_ids, const uint64_t* out_off, uint32_t bos_id,
-                                                   uint32_t eos_id, uint32_t* out_ids) {
+                                                   uint32_t eos_id, int stride, uint32_t* out_ids) {
   const int lane = threadIdx.x & 31;
   const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x / 32);
-  for (uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); r < n_rows; r += nw) {
-    const uint64_t mb = match_base[r], k = match_base[r + 1] - mb, s0 = r + mb;
-    uint64_t at = out_off[r];
-    if (bos_id != 0xFFFFFFFFu) {
-      if (lane == 0) out_ids[at] = bos_id;
-      ++at;
+  for (uint64_t r0 = (blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5)) * 32; r0 < n_rows; r0 += nw * 32) {
+    const uint64_t r = r0 + lane;
+    uint64_t mb = 0, k = 0, at = 0, t0 = 0, t1 = 0;
+    if (r < n_rows) {
+      mb = match_base[r];
+      k = match_base[r + 1] - mb;
+      at = out_off[r];
+      const uint64_t s0 = r + stride * mb;
+      t0 = seg_tok_off[s0];
+      t1 = seg_tok_off[s0 + 1];
     }
-    for (uint64_t j = 0; j <= k; ++j) {
-      const uint64_t t0 = seg_tok_off[s0 + j], n = seg_tok_off[s0 + j + 1] - t0;
-      for (uint64_t i = lane; i < n; i += 32) out_ids[at + i] = seg_ids[t0 + i];
-      at += n;
-      if (j < k) {
-        if (lane == 0) out_ids[at] = sp_ids[mb + j];
-        ++at;
+    const uint32_t live = __ballot_sync(0xFFFFFFFFu, r < n_rows);
+    for (int i = 0; i < 32 && ((live >> i) & 1u); ++i) {
+      const uint64_t rmb = __shfl_sync(0xFFFFFFFFu, mb, i), rk = __shfl_sync(0xFFFFFFFFu, k, i);
+      uint64_t o = __shfl_sync(0xFFFFFFFFu, at, i);
+      uint64_t a = __shfl_sync(0xFFFFFFFFu, t0, i), b = __shfl_sync(0xFFFFFFFFu, t1, i);
+      const uint64_t s0 = (r0 + i) + stride * rmb;
+      if (bos_id != 0xFFFFFFFFu) {
+        if (lane == 0) out_ids[o] = bos_id;
+        ++o;
       }
+      for (uint64_t j = 0;; ++j) {  // literal segment j: tokens [a, b)
+        for (uint64_t q = lane; q < b - a; q += 32) out_ids[o + q] = seg_ids[a + q];
+        o += b - a;
+        if (j == rk) break;
+        if (lane == 0) out_ids[o] = sp_ids[rmb + j];
+        ++o;
+        a = seg_tok_off[s0 + stride * (j + 1)];
+        b = seg_tok_off[s0 + stride * (j + 1) + 1];
+      }
+      if (eos_id != 0xFFFFFFFFu && lane == 0) out_ids[o] = eos_id;
     }
-    if (eos_id != 0xFFFFFFFFu && lane == 0) out_ids[at] = eos_id;
   }
 }
 
@@ -267,10 +314,10 @@ void launch_sp_rows(const uint8_t* bytes, const uint64_t* offsets, uint64_t n_ro
 
 void launch_sp_emit(const uint8_t* bytes, const uint64_t* offsets, uint64_t n_rows, SpecArgs sp,
                     const uint32_t* cand, const uint64_t* match_base, const uint64_t* lit_base, uint64_t* seg_off,
-                    uint64_t* seg_src, uint32_t* sp_ids, cudaStream_t s) {
+                    uint64_t* seg_src, uint32_t* sp_ids, int inplace, cudaStream_t s) {
   if (n_rows)
     k_sp_emit<<<blocks_for(n_rows, 128), 128, 0, s>>>(bytes, offsets, n_rows, sp, cand, match_base, lit_base,
-                                                     seg_off, seg_src, sp_ids);
+                                                     seg_off, seg_src, sp_ids, inplace);
 }
 
 void launch_sp_copy(const uint8_t* bytes, uint64_t n_seg, const uint64_t* seg_off, const uint64_t* seg_src,
@@ -279,17 +326,18 @@ void launch_sp_copy(const uint8_t* bytes, uint64_t n_seg, const uint64_t* seg_of
 }
 
 void launch_sp_lengths(uint64_t n_rows, const uint64_t* match_base, const uint64_t* seg_tok_off, int add_bos,
-                       int add_eos, uint64_t* out_len, cudaStream_t s) {
+                       int add_eos, int stride, uint64_t* out_len, cudaStream_t s) {
   if (n_rows)
-    k_sp_len<<<blocks_for(n_rows, 256), 256, 0, s>>>(n_rows, match_base, seg_tok_off, add_bos, add_eos, out_len);
+    k_sp_len<<<blocks_for(n_rows, 256), 256, 0, s>>>(n_rows, match_base, seg_tok_off, add_bos, add_eos, stride,
+                                                    out_len);
 }
 
 void launch_sp_stitch(uint64_t n_rows, const uint64_t* match_base, const uint64_t* seg_tok_off,
                       const uint32_t* seg_ids, const uint32_t* sp_ids, const uint64_t* out_off, uint32_t bos_id,
-                      uint32_t eos_id, uint32_t* out_ids, int sm_count, cudaStream_t s) {
+                      uint32_t eos_id, int stride, uint32_t* out_ids, int sm_count, cudaStream_t s) {
   if (n_rows)
     k_sp_stitch<<<unsigned(sm_count * 8), 256, 0, s>>>(n_rows, match_base, seg_tok_off, seg_ids, sp_ids, out_off,
-                                                       bos_id, eos_id, out_ids);
+                                                       bos_id, eos_id, stride, out_ids);
 }
 
 }  // namespace bbpe
