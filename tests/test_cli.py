@@ -129,3 +129,83 @@ def test_cli_compare_matches_reference(tmp_path, gpt2, as_json):
     assert want.returncode == 0, want.stderr.decode()
     assert r.stdout == want.stdout
     assert (b'"divergent": true' if as_json else b"DIVERGE [") in r.stdout  # items that differ are reported
+
+
+# ---- the reference's own CLI tests (proj/tests/test_cli.cpp), same inputs and
+# expectations; the GPT-2 table comes from tests/golden/gpt2.bbpt (--format binary).
+
+def gpt2_args():
+    return ["--vocab", os.path.join(GOLDEN, "gpt2.bbpt"), "--format", "binary"]
+
+
+def test_ref_cli_exit_codes_and_eval(tmp_path):
+    """test_cli.cpp: ExitCodeOneOnUsageErrors, ExitCodeTwoOnIntegrityErrors,
+    EvalComputesSimilarity (no GPU involved)."""
+    build_cli()
+    inp = tmp_path / "in6.txt"
+    inp.write_text("x\n")
+    assert run("tokenize").returncode == 1
+    assert run("tokenize", "--vocab", "/nonexistent.json", "--merges", "/nonexistent.txt", str(inp)).returncode == 1
+    assert run("nonsense-subcommand").returncode == 1
+    refs = tmp_path / "refs2.jsonl"
+    refs.write_text('{"ids":[1]}\n')
+    lens0 = tmp_path / "lens2.txt"
+    lens0.write_text("0\n")
+    assert run("eval", "--refs", str(refs), "--cands", str(refs), "--source-lens", str(lens0)).returncode == 1
+    (tmp_path / "dv.json").write_text('{"a":0,"b":1,"ab":2}')
+    (tmp_path / "dm.txt").write_text("#version: 0.2\na b\na b\n")
+    (tmp_path / "in7.txt").write_text("ab\n")
+    r = run("tokenize", "--vocab", str(tmp_path / "dv.json"), "--merges", str(tmp_path / "dm.txt"),
+            str(tmp_path / "in7.txt"))
+    assert r.returncode == 2
+    (tmp_path / "refs.jsonl").write_text('{"ids":[1,2]}\n{"ids":[3]}\n')
+    (tmp_path / "cands.jsonl").write_text('{"ids":[1]}\n{"ids":[3]}\n')
+    (tmp_path / "lens.txt").write_text("4\n2\n")
+    r = run("eval", "--json", "--refs", str(tmp_path / "refs.jsonl"), "--cands", str(tmp_path / "cands.jsonl"),
+            "--source-lens", str(tmp_path / "lens.txt"))
+    assert r.returncode == 0
+    j = json.loads(r.stdout)
+    assert j["count"] == 2 and abs(j["aggregate_sim"] - 0.875) < 1e-12
+
+
+@pytest.mark.gpu
+def test_ref_cli_tokenize_cases(tmp_path):
+    """test_cli.cpp: TokenizeJsonl, TokenizeBinary, TokenizeWithSpecialsAndBosEos,
+    TokenizeCanonicalJsonFormat."""
+    build_cli()
+    (tmp_path / "in.txt").write_text("hello world\n....\n")
+    r = run("tokenize", *gpt2_args(), str(tmp_path / "in.txt"))
+    assert r.returncode == 0
+    assert r.stdout == b'{"ids":[31373,995],"len":2}\n{"ids":[1106],"len":1}\n'
+    (tmp_path / "in3.txt").write_text("hi\n")
+    out = tmp_path / "out.bbpe"
+    assert run("tokenize", "--out", "bin", "--output", str(out), *gpt2_args(), str(tmp_path / "in3.txt")).returncode == 0
+    blob = out.read_bytes()
+    assert len(blob) >= 16 and blob[:4] == b"BBPE"
+    (tmp_path / "sp.json").write_text('{"specials": [["<|endoftext|>", 50256]], '
+                                      '"bos": "<|endoftext|>", "eos": "<|endoftext|>"}')
+    r = run("tokenize", "--bos", "--eos", "--specials", str(tmp_path / "sp.json"), *gpt2_args(),
+            str(tmp_path / "in3.txt"))
+    assert r.returncode == 0 and r.stdout == b'{"ids":[50256,5303,50256],"len":3}\n'
+    (tmp_path / "canon.json").write_text('{"tokens": [[0, [97]], [1, [98]], [2, [99]], [3, [97, 98]], '
+                                         '[4, [97, 98, 99]]], "merges": [[0, 0, 1, 3], [1, 3, 2, 4]]}')
+    (tmp_path / "in5.txt").write_text("abc\nab\n")
+    r = run("tokenize", "--vocab", str(tmp_path / "canon.json"), "--format", "json", str(tmp_path / "in5.txt"))
+    assert r.returncode == 0 and r.stdout == b'{"ids":[4],"len":1}\n{"ids":[3],"len":1}\n'
+
+
+@pytest.mark.gpu
+def test_ref_cli_compare_cases(tmp_path):
+    """test_cli.cpp: CompareReportsDivergence, CompareTextOutput."""
+    build_cli()
+    (tmp_path / "cmp.txt").write_text(".'t\nhello\n")
+    r = run("compare", "--pattern", "gpt2", "--json", *gpt2_args(), str(tmp_path / "cmp.txt"))
+    assert r.returncode == 0
+    j = json.loads(r.stdout)
+    assert j["count"] == 2 and j["divergent_count"] == 1
+    assert j["items"][0]["divergent"] is True
+    assert j["items"][0]["reference_tokens"] == [2637, 83] and j["items"][0]["block_tokens"] == [13, 470]
+    assert j["items"][1]["divergent"] is False
+    (tmp_path / "cmp2.txt").write_text(".'t\n")
+    r = run("compare", "--pattern", "gpt2", *gpt2_args(), str(tmp_path / "cmp2.txt"))
+    assert r.returncode == 0 and b"DIVERGE" in r.stdout

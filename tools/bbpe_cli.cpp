@@ -13,6 +13,8 @@
 //            [--pad-id N] [--workers N] [--device N] input
 //   bbpe_cli compare --vocab V ... --pattern gpt2 [--block-size N] [--json]
 //            [--output F] [--device N] input
+//   bbpe_cli eval --refs R.jsonl --cands C.jsonl --source-lens L [--json]
+//            (the similarity report, eval.hpp:43-72, 207-230; host only)
 #include <blockbpe_b200/blockbpe.hpp>
 
 #include <nlohmann/json.hpp>
@@ -73,12 +75,13 @@ const char* kUsage =
     "                [--bos-token T] [--eos-token T] [--engine cuda] [--block-size N] [--bos] [--eos]\n"
     "                [--out jsonl|bin] [--output F] [--pad-id N] [--workers N] [--device N] input\n"
     "       bbpe_cli compare --vocab V [vocab options] --pattern gpt2 [--block-size N] [--json]\n"
-    "                [--output F] [--device N] input\n";
+    "                [--output F] [--device N] input\n"
+    "       bbpe_cli eval --refs R.jsonl --cands C.jsonl --source-lens L [--json]\n";
 
 struct Args {
   std::string cmd;
   std::string vocab, merges, format = "gpt2", specials, bos_token, eos_token, engine = "cuda";
-  std::string out = "jsonl", output, input, pattern;
+  std::string out = "jsonl", output, input, pattern, refs, cands, lens;
   std::uint32_t block_size = 256;
   bool bos = false, eos = false, json = false;
   std::optional<bb::TokenId> pad_id;
@@ -97,8 +100,9 @@ std::uint64_t to_u64(const std::string& opt, const std::string& v) {
 }
 
 Args parse(int argc, char** argv) {
-  if (argc < 2 || (std::string(argv[1]) != "tokenize" && std::string(argv[1]) != "compare"))
-    throw bb::UsageError("expected the tokenize or compare subcommand");
+  if (argc < 2 || (std::string(argv[1]) != "tokenize" && std::string(argv[1]) != "compare" &&
+                    std::string(argv[1]) != "eval"))
+    throw bb::UsageError("expected the tokenize, compare or eval subcommand");
   Args a;
   a.cmd = argv[1];
   for (int i = 2; i < argc; ++i) {
@@ -123,10 +127,18 @@ Args parse(int argc, char** argv) {
     else if (k == "--workers") (void)to_u64(k, val());  // host threads: not used by the device path
     else if (k == "--device") a.device = static_cast<int>(to_u64(k, val()));
     else if (k == "--pattern" && a.cmd == "compare") a.pattern = val();
-    else if (k == "--json" && a.cmd == "compare") a.json = true;
+    else if (k == "--json" && a.cmd != "tokenize") a.json = true;
+    else if (k == "--refs" && a.cmd == "eval") a.refs = val();
+    else if (k == "--cands" && a.cmd == "eval") a.cands = val();
+    else if (k == "--source-lens" && a.cmd == "eval") a.lens = val();
     else if (!k.empty() && k[0] == '-') throw bb::UsageError("unknown option " + k);
     else if (a.input.empty()) a.input = k;
     else throw bb::UsageError("unexpected argument " + k);
+  }
+  if (a.cmd == "eval") {
+    if (a.refs.empty() || a.cands.empty() || a.lens.empty())
+      throw bb::UsageError("--refs, --cands and --source-lens are required");
+    return a;
   }
   if (a.vocab.empty()) throw bb::UsageError("--vocab is required");
   if (a.input.empty()) throw bb::UsageError("the input file is required");
@@ -283,6 +295,78 @@ int run_compare(const Args& a) {
   return 0;
 }
 
+// read_jsonl_token_seqs (batch.hpp:170-189): the "ids" array of every object line.
+std::vector<bb::TokenSeq> read_jsonl_ids(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw bb::UsageError("cannot open " + path);
+  std::vector<bb::TokenSeq> out;
+  std::string line;
+  std::size_t no = 0;
+  while (std::getline(in, line)) {
+    ++no;
+    if (line.empty()) continue;
+    nlohmann::json row;
+    try {
+      row = nlohmann::json::parse(line);
+    } catch (const nlohmann::json::exception& e) {
+      throw bb::ParseError(path + ":" + std::to_string(no) + ": " + e.what());
+    }
+    if (!row.is_object() || !row.contains("ids") || !row["ids"].is_array())
+      throw bb::ParseError(path + ":" + std::to_string(no) + ": expected an object with an \"ids\" array");
+    out.push_back(row["ids"].get<bb::TokenSeq>());
+  }
+  return out;
+}
+
+// run_eval (blockbpe_cli.cpp:172-202) with similarity (eval.hpp:43-72):
+// sim = (1/n) sum(1 - d_L(ref_i, cand_i) / |s_i|).
+int run_eval(const Args& a) {
+  const std::vector<bb::TokenSeq> refs = read_jsonl_ids(a.refs), cands = read_jsonl_ids(a.cands);
+  std::ifstream lin(a.lens, std::ios::binary);
+  if (!lin) throw bb::UsageError("cannot open source-lens file " + a.lens);
+  std::vector<std::size_t> lens;
+  std::string line;
+  std::size_t no = 0;
+  while (std::getline(lin, line)) {
+    ++no;
+    if (line.empty()) continue;
+    try {
+      lens.push_back(std::stoull(line));
+    } catch (const std::exception&) {
+      throw bb::ParseError(a.lens + ":" + std::to_string(no) + ": expected an integer");
+    }
+  }
+  if (refs.size() != cands.size() || refs.size() != lens.size())
+    throw bb::UsageError("similarity inputs must have equal lengths (refs " + std::to_string(refs.size()) +
+                         ", cands " + std::to_string(cands.size()) + ", lens " + std::to_string(lens.size()) + ")");
+  std::vector<std::uint32_t> dist(refs.size());
+  std::vector<double> sims(refs.size());
+  double total = 0.0;
+  for (std::size_t i = 0; i < refs.size(); ++i) {
+    if (lens[i] == 0)
+      throw bb::UsageError("source length 0 at index " + std::to_string(i) + "; the similarity formula is undefined");
+    dist[i] = levenshtein(refs[i], cands[i]);
+    sims[i] = 1.0 - static_cast<double>(dist[i]) / static_cast<double>(lens[i]);
+    total += sims[i];
+  }
+  const double agg = refs.empty() ? 1.0 : total / static_cast<double>(refs.size());
+  if (a.json) {  // to_json(SimilarityReport) (eval.hpp:208-215), dump(2)
+    nlohmann::json items = nlohmann::json::array();
+    for (std::size_t i = 0; i < refs.size(); ++i)
+      items.push_back({{"source_len", lens[i]}, {"distance", dist[i]}, {"item_sim", sims[i]}});
+    std::cout << nlohmann::json{{"count", refs.size()}, {"aggregate_sim", agg}, {"items", items}}.dump(2) << '\n';
+    return 0;
+  }
+  // write_text(SimilarityReport) (eval.hpp:239-249)
+  std::cout << "items: " << refs.size() << "  aggregate_sim: " << std::setprecision(6) << std::fixed << agg << "\n";
+  std::cout << std::setw(6) << "item" << std::setw(12) << "source_len" << std::setw(10) << "distance" << std::setw(12)
+            << "item_sim" << "\n";
+  for (std::size_t i = 0; i < refs.size(); ++i)
+    std::cout << std::setw(6) << i << std::setw(12) << lens[i] << std::setw(10) << dist[i] << std::setw(12) << sims[i]
+              << "\n";
+  return 0;
+}
+
 int run_tokenize(const Args& a) {
   const bb::MergeTable table = load_table(a);
   const bb::SpecialTokenSet specials = load_specials_arg(a, table);
@@ -309,7 +393,7 @@ int main(int argc, char** argv) {
   }
   try {
     const Args a = parse(argc, argv);
-    return a.cmd == "compare" ? run_compare(a) : run_tokenize(a);
+    return a.cmd == "compare" ? run_compare(a) : a.cmd == "eval" ? run_eval(a) : run_tokenize(a);
   } catch (const bb::UsageError& e) {
     std::cerr << "error: " << e.what() << '\n' << kUsage;
     return 1;
