@@ -611,6 +611,11 @@ PATTERN_CASES = [
     "café naïve Ångström".encode(), "αβγ абв 中文 가나".encode(),
     "١٢ ²³  thin　ideo".encode(), b"\xaa\xb5\xba\x80\xff\xfe broken utf8 \xe2\x82",
     b"...!!!???", b"'", b" ", b"'ll", b"", b"don't stop-believin' 2023/24 $5.00",
+    # the reference's pattern_pretokenize KAT inputs (test_pretokenize.cpp:114-150)
+    b"1000", b"hello world", b"can't", b"a\n\nb", b"hi  ", b"hello  world", b"I'll be 42 today!", b" leading",
+    b"tab\there", b"...wait", b"$3.14", "naïve café".encode(), b"a\r\nb", b"it's'll", b"don''t", b"100abc",
+    b"A1b2", "a\xa0b".encode(), "a\xa0\xa0b".encode(), "a \xa0b".encode(), "a\xa0".encode(), "1½2".encode(),
+    "x\u2003\u2003y".encode(),
 ]
 
 
