@@ -202,6 +202,14 @@ int bbpe_pad_device(bbpe_ctx* ctx, const uint32_t* d_ids, const uint64_t* d_tok_
                     uint32_t pad_id, uint32_t bos_id, uint32_t eos_id, uint64_t max_len, uint32_t* d_out_ids,
                     uint32_t* d_lengths, uint8_t* d_mask, uint64_t* truncated_rows);
 
+/* The gpt2 split pattern's chunk starts (pattern_pretokenize, pretokenize.hpp:
+ * 79-264, applied to every row; row starts included) as a bitmap of
+ * (total_bytes + 31) / 32 u32 words at d_chunk_bits (bit p: a chunk starts at
+ * byte p). The splitter that bbpe_config.pattern = 1 runs; device buffers,
+ * synchronous. */
+int bbpe_pretokenize_device(bbpe_ctx* ctx, const uint8_t* d_bytes, const uint64_t* d_offsets, size_t n_rows,
+                            uint64_t total_bytes, uint32_t* d_chunk_bits);
+
 /* ---- special tokens on the device ----
  * bbpe_ctx_set_specials replaces the ctx's special-token set (SpecialTokenSet,
  * merge_table.hpp:309-369): n byte strings blob[offsets[i], offsets[i+1]) with

@@ -88,6 +88,7 @@ SIGNATURES = {
     "bbpe_batch_widest_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int, u64p]),
     "bbpe_pad_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint32,
                                   C.c_uint32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, u64p]),
+    "bbpe_pretokenize_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64, C.c_void_p]),
     "bbpe_ctx_set_specials": (C.c_int, [C.c_void_p, C.c_size_t, u8p, u64p, u32p]),
     "bbpe_encode_batch_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_uint64,
                                            C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint64, C.c_void_p, u64p]),

@@ -484,6 +484,12 @@ class Encoder:
     def sync(self):
         _check(LIB.bbpe_ctx_sync(self._h))
 
+    def pretokenize_device(self, d_bytes, d_offsets, n: int, total: int, d_chunk_bits):
+        """The gpt2 splitter's chunk starts (row starts included) as a bitmap of
+        (total + 31) // 32 u32 words (bbpe_pretokenize_device)."""
+        _check(LIB.bbpe_pretokenize_device(self._h, C.c_void_p(d_bytes), C.c_void_p(d_offsets), n, total,
+                                           C.c_void_p(d_chunk_bits)))
+
     def encode_tensors(self, table: MergeTable, data, offsets):
         """Zero-copy hand-off: device tensors in, device tensors
         out -- uint8 bytes and int64 row offsets on this encoder's GPU -> (ids

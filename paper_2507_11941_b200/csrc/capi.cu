@@ -1245,6 +1245,36 @@ int bbpe_pad_device(bbpe_ctx* c, const uint32_t* d_ids, const uint64_t* d_tok_of
   BBPE_CATCH
 }
 
+int bbpe_pretokenize_device(bbpe_ctx* c, const uint8_t* d_bytes, const uint64_t* d_offsets, size_t n,
+                            uint64_t total_bytes, uint32_t* d_chunk_bits) {
+  BBPE_TRY
+  if (!c || !d_offsets || (total_bytes && (!d_bytes || !d_chunk_bits))) throw bbpe::usage_error("null argument");
+  DeviceGuard g(c->device);
+  ensure_plan(*c);
+  if (!total_bytes) return BBPE_OK;
+  const int saved = c->cfg.pattern;
+  c->cfg.pattern = 1;
+  bbpe::EncodeArgs a;
+  try {
+    a = prepare_args(*c, c->sc, d_bytes, d_offsets, n, total_bytes, nullptr, nullptr, c->stream);
+  } catch (...) {
+    c->cfg.pattern = saved;
+    throw;
+  }
+  c->cfg.pattern = saved;
+  c->launches += bbpe::launch_pretok_only(a, c->plan, d_chunk_bits, c->stream);
+  // k_gather did not run: the row / chunk bitmaps and counters are not zero.
+  c->sc.rowbits_zeroed = 0;
+  c->sc.chunkbits_zeroed = 0;
+  c->sc.ctrl_dirty = true;
+  ck(cudaStreamSynchronize(c->stream), "pretokenize");
+  uint64_t err[bbpe::ERR_N];
+  ck(cudaMemcpy(err, a.err, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
+  if (err[bbpe::ERR_BAD_OFFSETS] != ~0ull) throw bbpe::usage_error("offsets must be non-decreasing");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
 int bbpe_ctx_set_specials(bbpe_ctx* c, size_t n, const uint8_t* blob, const uint64_t* offsets,
                           const uint32_t* ids) {
   BBPE_TRY

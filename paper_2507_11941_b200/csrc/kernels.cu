@@ -1604,6 +1604,23 @@ LaunchPlan plan_launch(int device) {
   return p;
 }
 
+namespace {
+__global__ void k_or_words(uint32_t* out, const uint32_t* x, const uint32_t* y, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = x[i] | y[i];
+}
+}  // namespace
+
+int launch_pretok_only(const EncodeArgs& a, const LaunchPlan& p, uint32_t* d_out_bits, cudaStream_t stream) {
+  const unsigned threads = 256, blocks = unsigned((a.n_rows + 1 + threads - 1) / threads);
+  k_tile_first<<<blocks, threads, 0, stream>>>(a);
+  launch_pretok_gpt2(a.bytes, a.offsets, a.tile_first, a.n_rows, a.total, a.rowbits, a.chunkbits,
+                     a.counters + CNT_PRETOK, p.sm_count, stream);
+  const uint64_t words = (a.total + 31) / 32;
+  if (words) k_or_words<<<unsigned(std::max(p.sm_count, 1) * 2), 256, 0, stream>>>(d_out_bits, a.rowbits, a.chunkbits, words);
+  return 4;
+}
+
 int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, cudaStream_t stream,
                   cudaEvent_t* ev) {
   int launched = 0;

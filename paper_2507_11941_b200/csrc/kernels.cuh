@@ -127,6 +127,9 @@ struct LaunchPlan {
 LaunchPlan plan_launch(int device);
 // Enqueues the full encode on `stream`; returns the number of kernels launched.
 // ev (optional): BBPE_N_KERNELS + 1 events, before the first and after each kernel.
+// Row starts + the gpt2 splitter only: chunk starts (row starts included) as a
+// bitmap of (total + 31) / 32 words into d_out_bits. Returns the launch count.
+int launch_pretok_only(const EncodeArgs& a, const LaunchPlan& p, uint32_t* d_out_bits, cudaStream_t stream);
 int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, cudaStream_t stream,
                   cudaEvent_t* ev = nullptr);
 // Copies one wave's results into the caller's device-mapped pinned buffers:

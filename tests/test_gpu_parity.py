@@ -921,3 +921,44 @@ def test_device_decode_batch_with_specials(gpt2, skip):
     bad.mask = np.ones(8, np.uint8)
     with pytest.raises(bb.DecodeError, match=f"row 1: unknown token id 70000 at index {0 if skip else 2}"):
         bb.decode_batch(bad, gpt2, sp, skip)
+
+
+def test_gpt2_splitter_chunk_starts_vs_reference(gpt2):
+    """The device splitter itself (bbpe_pretokenize_device): chunk starts equal
+    pattern_pretokenize("gpt2")'s (pretokenize.hpp:79-264, oracle/_ref) on the
+    reference's KAT strings, mixed-alphabet rows, and long rows (> 4 KiB, the
+    span kernel) interleaved with short ones; an encode on the same ctx after
+    it still matches (the splitter's scratch is re-zeroed)."""
+    import torch
+    from oracle.oracle import Reference
+    from paper_2507_11941_b200 import synth
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ids_, off_, blob_, m4_ = gpt2.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    rng = np.random.default_rng(29)
+    alphabet = [bytes([c]) for c in b"ab cd\n\n\r\t'sll.,!0123 "] + ["é".encode(), "αβ".encode(), b"\xe3\x80\x80",
+                                                                    b"\xc2\xa0", b"\xe2\x80\x83", b"\xff"]
+    rows = list(PATTERN_CASES)
+    for n in rng.integers(0, 9000, 60):
+        rows.append(b"".join(alphabet[j] for j in rng.integers(0, len(alphabet), int(n) // 2)))
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off = synth.rows_fixed(gen, 30, 7000, seed=30)
+    rows += [bytes(data[int(off[i]):int(off[i + 1])]) for i in range(30)]
+    d, o = bb.pack_rows(rows)
+    total = int(o[-1])
+    enc = bb.Encoder(0)
+    dd = torch.from_numpy(d.copy()).cuda()
+    do = torch.from_numpy(o.view(np.int64).copy()).cuda()
+    bits = torch.zeros((total + 31) // 32, dtype=torch.int32, device="cuda")
+    enc.pretokenize_device(dd.data_ptr(), do.data_ptr(), len(rows), total, bits.data_ptr())
+    b = bits.cpu().numpy().view(np.uint32)
+    flags = ((b[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(-1)[:total]
+    starts = np.nonzero(flags)[0]
+    for r, s in enumerate(rows):
+        lo, hi = int(o[r]), int(o[r + 1])
+        got = (starts[(starts >= lo) & (starts < hi)] - lo).tolist()
+        assert got == list(ref.pretokenize(s, "gpt2")), (r, s[:60])
+    ids, oo, _ = enc.encode_packed(gpt2, d, o)
+    want, wo, _ = bb.Encoder(0).encode_packed(gpt2, d, o)
+    assert np.array_equal(ids, want) and np.array_equal(oo, wo)
