@@ -423,6 +423,37 @@ def main():
                    "note": "k_tile_first includes the gpt2 splitter (k_pretok_rows + k_pretok_spans)"}
         enc.set_config(pattern=None)
 
+    # ---- special tokens + BOS on the device (bbpe_encode_batch_device) ----
+    specials_line = None
+    if args.engine == "pieces" and args.config == 2 and n and total == 256 * n:
+        sp = bb.SpecialTokenSet()
+        sp.add("<|endoftext|>", 50256)
+        d_sp = d_data.clone().view(n, 256)
+        d_sp[:, -13:] = torch.tensor(list(b"<|endoftext|>"), dtype=torch.uint8, device="cuda")
+        enc.set_specials(sp)
+        cap = total + 2 * n
+        d_sp_ids = torch.empty(cap, dtype=torch.int32, device="cuda")
+
+        def sp_step():
+            return enc.encode_batch_device(table, d_sp.data_ptr(), d_off.data_ptr(), n, total, d_sp_ids.data_ptr(),
+                                           cap, d_oo.data_ptr(), bos_id=50256)
+
+        for _ in range(args.warmup):
+            sp_step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            n_sp = sp_step()
+        e1.record()
+        torch.cuda.synchronize()
+        sp_ms = e0.elapsed_time(e1) / args.steps
+        specials_line = {"value": n_sp / (sp_ms / 1e3), "unit": "tokens/s", "ms_per_step": sp_ms,
+                         "workload": "cfg2 rows ending in <|endoftext|> (a special), BOS added",
+                         "timing": "CUDA events around synchronous calls (split, encode, stitch)"}
+        enc.set_specials(None)
+        del d_sp, d_sp_ids
+
     # ---- roofline of the dominant kernel ----
     k_ms = {k: v / max(kcalls, 1) for k, v in ktimes.items()}
     dom = max(k_ms, key=k_ms.get)
@@ -493,6 +524,7 @@ def main():
             "epilogue": epilogue,
             "jsonl": jsonl,
             "pattern_mode": pattern,
+            "specials_mode": specials_line,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
