@@ -962,3 +962,41 @@ def test_gpt2_splitter_chunk_starts_vs_reference(gpt2):
     ids, oo, _ = enc.encode_packed(gpt2, d, o)
     want, wo, _ = bb.Encoder(0).encode_packed(gpt2, d, o)
     assert np.array_equal(ids, want) and np.array_equal(oo, wo)
+
+
+def test_splitter_unaligned_and_decode_device_skip(gpt2):
+    """bbpe_pretokenize_device on an unaligned byte pointer (plain-load kernels)
+    equals the aligned result; bbpe_decode_device_ex with skip_specials on
+    device buffers equals the host-buffer decode."""
+    import torch
+    rows = list(PATTERN_CASES) + [b"word " * 1200, b"x\n" * 3000]
+    d, o = bb.pack_rows(rows)
+    total = int(o[-1])
+    enc = bb.Encoder(0)
+    do = torch.from_numpy(o.view(np.int64).copy()).cuda()
+    outs = []
+    for shift in (0, 5):
+        buf = torch.zeros(total + 16, dtype=torch.uint8, device="cuda")
+        buf[shift:shift + total] = torch.from_numpy(d.copy()).cuda()
+        bits = torch.zeros((total + 31) // 32, dtype=torch.int32, device="cuda")
+        enc.pretokenize_device(buf.data_ptr() + shift, do.data_ptr(), len(rows), total, bits.data_ptr())
+        outs.append(bits.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    sp = bb.SpecialTokenSet()
+    for b, i in SPECIALS:
+        sp.add(b, i)
+    sp.set_bos("<|endoftext|>")
+    srows = _special_rows(gpt2)[:200]
+    ids, oo = bb.encode_batch_csr(srows, gpt2, sp, bb.BlockConfig(256, None), True, False)
+    enc.set_specials(sp)
+    want, woff = enc.decode_packed(gpt2, ids, oo, skip_specials=True)
+    d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+    d_oo = torch.from_numpy(oo.view(np.int64)).cuda()
+    cap = int(woff[-1]) + 64
+    d_out = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    d_boff = torch.empty(len(srows) + 1, dtype=torch.int64, device="cuda")
+    n = enc.decode_device(gpt2, d_ids.data_ptr(), d_oo.data_ptr(), len(srows), ids.size, d_out.data_ptr(), cap,
+                          d_boff.data_ptr(), skip_specials=True)
+    assert n == int(woff[-1])
+    assert bytes(d_out[:n].cpu().numpy()) == bytes(want)
+    assert np.array_equal(d_boff.cpu().numpy().view(np.uint64), woff)
