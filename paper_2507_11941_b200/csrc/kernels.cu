@@ -433,13 +433,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
       const uint32_t y[5] = {y0, yv.x, yv.y, yv.z, yv.w};
       uint32_t jm = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int r = j + 3;
-        const uint32_t lo = y[r >> 2];
-        const uint32_t hi = ((r & 3) == 3) ? y[(r >> 2) + 1] : lo;
-        const uint32_t v = __byte_perm(lo, hi, uint32_t((r & 3) | (((r & 3) + 1) << 4)));
-        const uint32_t wd = s_jt[((v >> 5) ^ v) & 0x7FF];
-        jm |= (__funnelshift_r(wd, wd, v) & 1u) << j;
+      for (int j = 0; j < 16; j += 2) {
+        // Pairs j and j+1 at once: V = a1 | c1 << 8 | a2 << 16 | c2 << 24
+        // (bytes j+3, j+4, j+4, j+5), both swizzled word indices from one
+        // shift + mask (the shift's bleed from the upper half lands in bits
+        // 11-15 of the lower half, which the mask clears).
+        const int r = j + 3, b = r & 3;
+        const uint32_t V = __byte_perm(y[r >> 2], y[(r >> 2) + 1],
+                                       uint32_t(b | ((b + 1) << 4) | ((b + 1) << 8) | ((b + 2) << 12)));
+        const uint32_t idx = ((V >> 5) ^ V) & 0x07FF07FFu;
+        const uint32_t w1 = s_jt[idx & 0xFFFFu], w2 = s_jt[idx >> 16];
+        jm |= ((__funnelshift_r(w1, w1, V) & 1u) << j) | ((__funnelshift_r(w2, w2, V >> 16) & 1u) << (j + 1));
       }
       uint32_t m = (~jm) & 0xFFFFu;  // not a junction: boundary
       if (chk) {
