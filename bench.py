@@ -258,10 +258,11 @@ def main():
     if args.scale is None:
         args.scale = 1 / 8 if args.config == 5 else 1.0  # cfg5: 16 GB over 8 GPUs = 2 GB per GPU
 
-    rank, world, local = dist_init(args.gpus)
     if args.impl == "reference":
-        reference_arm(args, rank, world)
+        # CPU only, rank 0 alone: no process group (the other ranks exit 0 at once).
+        reference_arm(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return
+    rank, world, local = dist_init(args.gpus)
 
     import torch
     import paper_2507_11941_b200 as bb
