@@ -8,13 +8,14 @@
 // Device table: dec[id] = byte start << 24 | byte length (~0: no such token),
 // dense over ids 0..max_id, and the token bytes; built once per device.
 // Kernels: k_dec_len (token lengths, block-local exclusive scan, first bad
-// token), k_dec_scan (block totals -> block bases, one CTA), k_dec_copy
+// token), k_scan_totals (scan.cuh: block totals -> block bases, one CTA), k_dec_copy
 // (bytes gathered to their output position), k_dec_rows (row byte offsets).
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "decode.cuh"
+#include "scan.cuh"
 
 namespace bbpe {
 namespace {
@@ -85,44 +86,6 @@ __global__ void __launch_bounds__(kDecThreads) k_dec_len(DecodeArgs a) {
   }
   __syncthreads();
   if (i < a.n_ids) a.pos[i] = s_warp[wid] + inc - len;
-}
-
-// One CTA: exclusive scan of the block totals in place, total at [n_blocks].
-__global__ void __launch_bounds__(1024) k_dec_scan(uint64_t* sums, uint64_t n_blocks) {
-  __shared__ uint64_t s_warp[32];
-  __shared__ uint64_t s_carry;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint64_t b0 = 0; b0 < n_blocks; b0 += 1024) {
-    const uint64_t b = b0 + threadIdx.x;
-    const uint64_t v = b < n_blocks ? sums[b] : 0;
-    uint64_t inc = v;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-      if (lane >= d) inc += u;
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const uint64_t x = s_warp[lane];
-      uint64_t xi = x;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, xi, d);
-        if (lane >= d) xi += u;
-      }
-      s_warp[lane] = xi - x;
-    }
-    __syncthreads();
-    const uint64_t carry = s_carry;
-    if (b < n_blocks) sums[b] = carry + s_warp[wid] + inc - v;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = carry + s_warp[wid] + inc;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) sums[n_blocks] = s_carry;
 }
 
 __global__ void __launch_bounds__(kDecThreads) k_dec_copy(DecodeArgs a) {
@@ -249,13 +212,13 @@ __global__ void k_json_write(JsonArgs a) {
 void launch_jsonl(const JsonArgs& a, int sm_count, cudaStream_t s) {
   if (a.n_ids) {
     k_json_tok<<<unsigned(a.n_tok_blocks), kDecThreads, 0, s>>>(a);
-    k_dec_scan<<<1, 1024, 0, s>>>(a.tok_sums, a.n_tok_blocks);
+    k_scan_totals<<<1, 1024, 0, s>>>(a.tok_sums, a.n_tok_blocks);
   } else {
     cudaMemsetAsync(a.tok_sums, 0, 8, s);
   }
   if (a.n_rows) {
     k_json_row<<<unsigned(a.n_row_blocks), kDecThreads, 0, s>>>(a);
-    k_dec_scan<<<1, 1024, 0, s>>>(a.row_sums, a.n_row_blocks);
+    k_scan_totals<<<1, 1024, 0, s>>>(a.row_sums, a.n_row_blocks);
     k_json_write<<<unsigned(sm_count * 8), 256, 0, s>>>(a);
   } else {
     cudaMemsetAsync(a.row_sums, 0, 8, s);
@@ -265,7 +228,7 @@ void launch_jsonl(const JsonArgs& a, int sm_count, cudaStream_t s) {
 void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   if (a.n_ids) {
     k_dec_len<<<unsigned(a.n_blocks), kDecThreads, 0, s>>>(a);
-    k_dec_scan<<<1, 1024, 0, s>>>(a.block_sums, a.n_blocks);
+    k_scan_totals<<<1, 1024, 0, s>>>(a.block_sums, a.n_blocks);
     k_dec_copy<<<unsigned(a.n_blocks), kDecThreads, 0, s>>>(a);
   } else {
     cudaMemsetAsync(a.block_sums, 0, 8, s);

@@ -18,6 +18,8 @@
 //   k_sp_stitch  warp per row: BOS, segment tokens, special ids, EOS
 #include "specials.cuh"
 
+#include "scan.cuh"
+
 namespace bbpe {
 namespace {
 
@@ -49,44 +51,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_blocks(uint64_t* v, uint6
   }
   __syncthreads();
   if (i < n) v[i] = s_warp[wid] + inc - x;
-}
-
-// One CTA: exclusive scan of the block totals in place, total at [nb].
-__global__ void __launch_bounds__(1024) k_scan_sums(uint64_t* sums, uint64_t nb) {
-  __shared__ uint64_t s_warp[32];
-  __shared__ uint64_t s_carry;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
-  for (uint64_t b0 = 0; b0 < nb; b0 += 1024) {
-    const uint64_t b = b0 + threadIdx.x;
-    const uint64_t x = b < nb ? sums[b] : 0;
-    uint64_t inc = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-      if (lane >= d) inc += u;
-    }
-    if (lane == 31) s_warp[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const uint64_t w = s_warp[lane];
-      uint64_t wi = w;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, wi, d);
-        if (lane >= d) wi += u;
-      }
-      s_warp[lane] = wi - w;
-    }
-    __syncthreads();
-    const uint64_t carry = s_carry;
-    if (b < nb) sums[b] = carry + s_warp[wid] + inc - x;
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = carry + s_warp[wid] + inc;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) sums[nb] = s_carry;
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_add(uint64_t* v, uint64_t n, const uint64_t* sums,
@@ -295,7 +259,7 @@ void launch_scan_u64(uint64_t* v, uint64_t n, uint64_t* sums, cudaStream_t s) {
     return;
   }
   k_scan_blocks<<<unsigned(nb), kScanThreads, 0, s>>>(v, n, sums);
-  k_scan_sums<<<1, 1024, 0, s>>>(sums, nb);
+  k_scan_totals<<<1, 1024, 0, s>>>(sums, nb);
   k_scan_add<<<unsigned(nb), kScanThreads, 0, s>>>(v, n, sums, nb);
 }
 
