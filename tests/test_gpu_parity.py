@@ -1000,3 +1000,32 @@ def test_splitter_unaligned_and_decode_device_skip(gpt2):
     assert n == int(woff[-1])
     assert bytes(d_out[:n].cpu().numpy()) == bytes(want)
     assert np.array_equal(d_boff.cpu().numpy().view(np.uint64), woff)
+
+
+def test_splitter_full_size_cfg3_vs_reference(gpt2):
+    """The gpt2 splitter at full cfg3 size (16,384 rows of U[8, 64] KiB, the
+    span kernel): chunk starts of 120 random rows equal the reference
+    pattern_pretokenize's."""
+    import torch
+    from oracle.oracle import Reference
+    from paper_2507_11941_b200 import synth
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ids_, off_, blob_, m4_ = gpt2.export()
+    ref = Reference.from_arrays(ids_, off_, blob_, m4_)
+    gen = synth.TextGen(synth.word_list(gpt2))
+    data, off, _ = synth.config_rows(gen, 3, seed=3000)
+    n, total = off.size - 1, int(off[-1])
+    enc = bb.Encoder(0)
+    dd = torch.from_numpy(data).cuda()
+    do = torch.from_numpy(off.view(np.int64)).cuda()
+    bits = torch.zeros((total + 31) // 32, dtype=torch.int32, device="cuda")
+    enc.pretokenize_device(dd.data_ptr(), do.data_ptr(), n, total, bits.data_ptr())
+    b = bits.cpu().numpy().view(np.uint32)
+    rng = np.random.default_rng(3)
+    for r in rng.integers(0, n, 120):
+        lo, hi = int(off[r]), int(off[r + 1])
+        w0, w1 = lo // 32, (hi + 31) // 32
+        flags = ((b[w0:w1, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(-1)
+        got = (np.nonzero(flags[lo - 32 * w0:hi - 32 * w0])[0]).tolist()
+        assert got == list(ref.pretokenize(data[lo:hi].tobytes(), "gpt2")), int(r)
