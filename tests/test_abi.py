@@ -59,3 +59,21 @@ def test_bad_block_size_is_usage_error():
     assert b"block_size" in _lib.LIB.bbpe_last_error()
     assert bb.coarsening_factor(2048, bb.BlockConfig(256)) == 8
     assert bb.coarsening_factor(1025, bb.BlockConfig(1024)) == 2
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/bbpe_b200.h is the FFI boundary for any language: it compiles as
+    pedantic C99, links against libbbpe_b200.so and runs (no GPU call)."""
+    import subprocess
+    from conftest import ROOT
+    src = tmp_path / "c_abi.c"
+    src.write_text('#include "bbpe_b200.h"\n'
+                   "int main(void) { bbpe_config c = {256, 0, BBPE_ENGINE_PIECES, 0, 1, 0, 0}; (void)c;\n"
+                   "  return bbpe_abi_version() > 0 ? 0 : 1; }\n")
+    lib = os.path.join(ROOT, "paper_2507_11941_b200")
+    exe = tmp_path / "c_abi"
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                        str(src), "-L" + lib, "-lbbpe_b200", "-Wl,-rpath," + lib, "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert subprocess.run([str(exe)]).returncode == 0
