@@ -123,6 +123,7 @@ struct bbpe_table {
   // Device layout, built once on the host.
   uint32_t id_bits = 0, rank_bits = 0;
   bool remap = false;
+  uint32_t max_dev_id = 0;  // largest id a byte token or merge mentions (non-remapped device ids)
   bool narrow = false;  // 16-bit device working arrays and 32-bit pair keys suffice
   std::unordered_map<uint32_t, uint32_t> dense_of;  // only when remap
   std::vector<uint32_t> dense_to_id;                // only when remap

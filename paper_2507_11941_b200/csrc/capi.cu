@@ -422,7 +422,8 @@ void raise_device_errors(bbpe_ctx& c, const uint64_t* err, const uint64_t* host_
                          uint64_t row_base, const uint8_t* host_bytes, const uint64_t* d_offsets,
                          const uint8_t* d_bytes) {
   const uint64_t none = ~0ull;
-  if (err[bbpe::ERR_BAD_OFFSETS] != none) throw bbpe::usage_error("offsets must be non-decreasing");
+  if (err[bbpe::ERR_BAD_OFFSETS] != none)
+    throw bbpe::usage_error("offsets must start at 0, be non-decreasing and end at total_bytes");
   if (err[bbpe::ERR_BAD_BYTE_POS] == none && err[bbpe::ERR_MAXPASS_ROW] == none) return;
   std::vector<uint64_t> tmp;
   if (!host_offsets) {
@@ -713,7 +714,8 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
   };
 
   auto raise_wave_errors = [&](const uint64_t* err, size_t k) {
-    if (err[ERR_BAD_OFFSETS] != ~0ull) throw usage_error("offsets must be non-decreasing");
+    if (err[ERR_BAD_OFFSETS] != ~0ull)
+      throw usage_error("offsets must start at 0, be non-decreasing and end at total_bytes");
     if (err[ERR_BAD_BYTE_POS] != ~0ull || err[ERR_MAXPASS_ROW] != ~0ull) {
       const uint64_t r0 = waves[k].first, nr = waves[k].second - r0, base = offsets[r0];
       std::vector<uint64_t> rel(nr + 1);
@@ -1270,7 +1272,8 @@ int bbpe_pretokenize_device(bbpe_ctx* c, const uint8_t* d_bytes, const uint64_t*
   ck(cudaStreamSynchronize(c->stream), "pretokenize");
   uint64_t err[bbpe::ERR_N];
   ck(cudaMemcpy(err, a.err, sizeof(err), cudaMemcpyDeviceToHost), "read error slots");
-  if (err[bbpe::ERR_BAD_OFFSETS] != ~0ull) throw bbpe::usage_error("offsets must be non-decreasing");
+  if (err[bbpe::ERR_BAD_OFFSETS] != ~0ull)
+    throw bbpe::usage_error("offsets must start at 0, be non-decreasing and end at total_bytes");
   return BBPE_OK;
   BBPE_CATCH
 }
@@ -1799,23 +1802,21 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   DeviceGuard g(c->device);
   const DevTable& dt = table_on_device(*t, c->device);
   ensure_plan(*c);
-  // Dense ids for the device. Ids the table never mentions cannot pair; under
-  // a remapped table they get private placeholder ids (mapped back below).
+  // Dense ids for the device. Ids the table never mentions never pair
+  // (find_pair misses, merge_table.hpp:237), but a raw id past the device key
+  // width would alias a real pair (l << id_bits | r). All of them become one
+  // placeholder id P that no merge mentions; P is never produced by a merge
+  // either, so the output's placeholders are the input's outside ids in
+  // their input order (mapped back below).
   std::vector<uint64_t> x(n);
-  std::vector<uint32_t> extra;  // placeholder dense id -> original id
-  std::unordered_map<uint32_t, uint32_t> extra_of;
+  std::vector<uint32_t> outside;  // outside ids, in input order
   const uint32_t n_dense = t->remap ? static_cast<uint32_t>(t->dense_to_id.size()) : 0;
+  const uint32_t P = t->remap ? n_dense : t->max_dev_id + 1;
   for (size_t i = 0; i < n; ++i) {
     uint32_t d = t->dense(tokens[i]);
-    if (t->remap && d == kInvalidToken) {
-      auto it = extra_of.find(tokens[i]);
-      if (it == extra_of.end()) {
-        uint32_t nd = n_dense + static_cast<uint32_t>(extra.size());
-        if (nd + 1 >= (1u << t->id_bits)) throw usage_error("too many token ids outside the table");
-        it = extra_of.emplace(tokens[i], nd).first;
-        extra.push_back(tokens[i]);
-      }
-      d = it->second;
+    if ((t->remap && d == kInvalidToken) || (!t->remap && tokens[i] > t->max_dev_id)) {
+      outside.push_back(tokens[i]);
+      d = P;
     }
     x[i] = uint64_t(d) | (uint64_t(0xFFFFFFFEu) << 32);
   }
@@ -1868,8 +1869,17 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   ck(cudaStreamSynchronize(c->stream), "block_bpe");
   std::vector<uint32_t> res(cnt);
   if (cnt) ck(cudaMemcpy(res.data(), a.lpo + 1, cnt * 4ull, cudaMemcpyDeviceToHost), "D2H");
-  if (t->remap)
-    for (auto& v : res) v = v < n_dense ? t->dense_to_id[v] : extra[v - n_dense];
+  {
+    size_t k = 0;
+    for (auto& v : res) {
+      if (v == P) {
+        if (k >= outside.size()) return fail(BBPE_CONTRACT, "block_bpe: placeholder count changed");
+        v = outside[k++];
+      } else if (t->remap) {
+        v = t->dense_to_id[v];
+      }
+    }
+  }
   std::memcpy(out, res.data(), cnt * 4ull);
   *out_n = cnt;
   if (n_passes) *n_passes = passes;

@@ -139,7 +139,7 @@ __global__ void k_tile_first(EncodeArgs a) {
   const uint64_t* src = a.offsets_raw ? a.offsets_raw : a.offsets;
   uint64_t o = src[s] - a.offsets_base;
   const uint64_t prev = s == 0 ? 0 : src[s - 1] - a.offsets_base;
-  if (o < prev || o > a.total || (s == a.n_rows && o != a.total)) {
+  if (o < prev || o > a.total || (s == a.n_rows && o != a.total) || (s == 0 && o != 0)) {
     // Offsets must be non-decreasing (the host raises UsageError); clamp so
     // that every kernel stays inside its buffers meanwhile.
     atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_BAD_OFFSETS]), (unsigned long long)s);
@@ -150,7 +150,9 @@ __global__ void k_tile_first(EncodeArgs a) {
   if (s == 0) hi = 0;  // offsets[0] == 0
   for (uint64_t t = lo; t <= hi && t < a.num_tiles; ++t) a.tile_first[t] = s;
   if (s == 0) a.tile_first[a.num_tiles] = a.n_rows + 1;
-  if (a.rowbits && s < a.n_rows) atomicOr(&a.rowbits[o >> 5], 1u << (o & 31));
+  // A row starting at `total` has no bytes: no bit (it would land past the
+  // last tile, where k_gather never clears it).
+  if (a.rowbits && s < a.n_rows && o < a.total) atomicOr(&a.rowbits[o >> 5], 1u << (o & 31));
   if (a.offsets_raw) a.offsets_w[s] = o;  // the rebased copy the other kernels read
 }
 

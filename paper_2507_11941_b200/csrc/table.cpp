@@ -249,6 +249,9 @@ bbpe_table* load_binary(const std::string& path) {
   take(&nm, 8);
   if (nt > (1ull << 32) || nb > (1ull << 36) || nm > (1ull << 32))
     throw parse_error(path + ": implausible sizes");
+  // The payload the header announces must be present before anything is
+  // allocated from it (no overflow: the bounds above keep it < 2^40).
+  if (nt * 4 + (nt + 1) * 8 + nb + nm * 16 > blob.size() - pos) throw parse_error(path + ": truncated table file");
   std::vector<uint32_t> ids(nt);
   std::vector<uint64_t> off(nt + 1);
   std::vector<uint8_t> bytes(nb);
@@ -351,6 +354,7 @@ void build_device_layout(bbpe_table& t) {
     if (v != kInvalidToken) max_dev_id = std::max(max_dev_id, v);
   for (size_t i = 0; i < M; ++i)
     max_dev_id = std::max({max_dev_id, t.m_left[i], t.m_right[i], t.m_merged[i]});
+  t.max_dev_id = max_dev_id;
   t.rank_bits = std::max(1, bits_for(M));
   int idb = bits_for(uint64_t(max_dev_id) + 1);  // ids < 2^idb - 1 keeps keys != all-ones
   t.remap = (2 * idb + static_cast<int>(t.rank_bits) > 64);

@@ -31,6 +31,17 @@ def test_gpt2_text_format_loader_matches_fixture(gpt2):
         assert np.array_equal(x, y)
 
 
+def test_binary_header_sizes_checked_before_allocation(tmp_path):
+    """A .bbpt header announcing more payload than the file holds is a
+    ParseError ('truncated'), not a multi-GB allocation."""
+    import struct
+    p = str(tmp_path / "bad.bbpt")
+    with open(p, "wb") as f:
+        f.write(b"BBPT" + struct.pack("<IQQQ", 1, 1 << 31, 1 << 35, 1 << 31) + b"\0" * 64)
+    with pytest.raises(bb.ParseError, match="truncated"):
+        bb.load_merge_table_files(p, None, "binary")
+
+
 def test_binary_round_trip(tmp_path, gpt2):
     p = str(tmp_path / "t.bbpt")
     gpt2.save_binary(p)
