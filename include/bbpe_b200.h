@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define BBPE_ABI_VERSION 1
+#define BBPE_ABI_VERSION 2
 
 typedef enum bbpe_status {
   BBPE_OK = 0,
@@ -264,11 +264,24 @@ int bbpe_ctx_sync(bbpe_ctx* ctx);
 uint64_t bbpe_ctx_kernel_launches(const bbpe_ctx* ctx);
 /* Per-kernel device time (CUDA events recorded between launches on the
  * launching stream) summed over the encodes since the last reset:
- * ms[0] k_tile_first, ms[1] k_pieces (or k_block_rows), ms[2] k_merge,
- * ms[3] k_long_pieces, ms[4] k_tile_scan, ms[5] k_gather. Synchronises the
- * streams used. *calls receives the number of encodes. */
-#define BBPE_N_KERNELS 6
+ * ms[0] k_tile_first (+ the gpt2 splitter in pattern mode), ms[1] k_pieces
+ * (or k_block_rows), ms[2] k_dedup, ms[3] k_merge, ms[4] k_refs,
+ * ms[5] k_long_pieces, ms[6] k_tile_scan, ms[7] k_gather (0 for a kernel
+ * that did not run). Synchronises the streams used. *calls receives the
+ * number of encodes. */
+#define BBPE_N_KERNELS 8
 int bbpe_ctx_kernel_times(bbpe_ctx* ctx, double* ms, uint64_t* calls, int reset);
+
+/* Piece statistics of the encodes on this ctx since the last reset (what the
+ * piece decomposition did with the input; diagnostics for the bench):
+ * out[0] pieces, out[1] pieces resolved from the piece memo / byte LUT,
+ * out[2] pieces sent to the lane-per-piece merge loop, out[3] long pieces
+ * (> 32 bytes, or whole rows under BBPE_ENGINE_BLOCK), out[4] bytes in long
+ * pieces, out[5] distinct merge pieces actually merged after the within-call
+ * dedupe (0 when the dedupe did not run), out[6] input bytes. No reference
+ * counterpart. Synchronises the device. */
+#define BBPE_N_PIECE_STATS 7
+int bbpe_ctx_piece_stats(bbpe_ctx* ctx, uint64_t* out, int reset);
 
 /* block_bpe on explicit initial token ids (one sequence), always the
  * BBPE_ENGINE_BLOCK pass loop. trace (optional): per pass {pass_index (1-based),

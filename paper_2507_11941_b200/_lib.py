@@ -106,6 +106,7 @@ SIGNATURES = {
     "bbpe_ctx_sync": (C.c_int, [C.c_void_p]),
     "bbpe_ctx_kernel_launches": (C.c_uint64, [C.c_void_p]),
     "bbpe_ctx_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), u64p, C.c_int]),
+    "bbpe_ctx_piece_stats": (C.c_int, [C.c_void_p, u64p, C.c_int]),
     "bbpe_block_bpe": (C.c_int, [C.c_void_p, C.c_void_p, u32p, C.c_size_t, u32p, C.POINTER(C.c_size_t),
                                  u64p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "bbpe_partition": (C.c_int, [u64p, C.c_size_t, C.c_int, u64p]),

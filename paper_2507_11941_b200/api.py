@@ -439,7 +439,8 @@ class Encoder:
     def kernel_launches(self) -> int:
         return LIB.bbpe_ctx_kernel_launches(self._h)
 
-    KERNELS = ("k_tile_first", "k_pieces", "k_merge", "k_long_pieces", "k_tile_scan", "k_gather")
+    KERNELS = ("k_tile_first", "k_pieces", "k_dedup", "k_merge", "k_refs", "k_long_pieces", "k_tile_scan",
+               "k_gather")
 
     def kernel_times(self, reset: bool = True) -> Tuple[dict, int]:
         """Per-kernel device ms (CUDA events on the launching stream) summed
@@ -448,6 +449,19 @@ class Encoder:
         calls = C.c_uint64()
         _check(LIB.bbpe_ctx_kernel_times(self._h, ms, C.byref(calls), 1 if reset else 0))
         return dict(zip(self.KERNELS, list(ms))), calls.value
+
+    PIECE_STATS = ("pieces", "memo_hits", "merge_pieces", "long_pieces", "long_bytes", "merged_after_dedupe",
+                   "input_bytes")
+
+    def piece_stats(self, reset: bool = True) -> dict:
+        """What the piece decomposition did over the encodes since the last
+        reset (bbpe_ctx_piece_stats), with memo hit rate and long-byte share."""
+        v = np.zeros(len(self.PIECE_STATS), np.uint64)
+        _check(LIB.bbpe_ctx_piece_stats(self._h, _p(v, C.c_uint64), 1 if reset else 0))
+        d = {k: int(x) for k, x in zip(self.PIECE_STATS, v)}
+        d["memo_hit_rate"] = d["memo_hits"] / d["pieces"] if d["pieces"] else None
+        d["long_byte_fraction"] = d["long_bytes"] / d["input_bytes"] if d["input_bytes"] else None
+        return d
 
     def encode_packed(self, table: MergeTable, data: np.ndarray, offsets: np.ndarray,
                       out_ids: Optional[np.ndarray] = None, out_offsets: Optional[np.ndarray] = None):

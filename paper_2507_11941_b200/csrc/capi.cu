@@ -197,6 +197,7 @@ struct bbpe_ctx {
   // Device decode scratch and host-API staging.
   DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff;
   DevBuf pad_scalar;  // epilogue: widest row / truncated count
+  DevBuf pstats;      // piece statistics (bbpe_ctx_piece_stats), PST_N u64
   DevBuf run_base;
   // Special-token set (bbpe_ctx_set_specials), longest first, and the scratch
   // of bbpe_encode_batch_device.
@@ -315,6 +316,8 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   a.engine = block ? BBPE_ENGINE_BLOCK : BBPE_ENGINE_PIECES;
   a.max_passes = c.cfg.max_passes;
   a.pattern = c.cfg.pattern;
+  if (c.pstats.ensure(PST_N * 8)) ck(cudaMemsetAsync(c.pstats.p, 0, PST_N * 8, s), "memset pstats");
+  a.pstats = c.pstats.as<uint64_t>();
   // Counters and look-back status are left zero by k_gather; rowbits too.
   if (sc.ctrl_dirty) {
     ck(cudaMemsetAsync(a.status, 0, sc.status.cap, s), "memset status");
@@ -1560,7 +1563,7 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaStreamSynchronize(c->stream);
     c->sc.release();
     for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_sums,
-                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar,
+                      &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar, &c->pstats,
                       &c->sp_blob, &c->sp_off, &c->sp_id, &c->sp_first, &c->sp_dec, &c->sp_cand, &c->sp_cnt, &c->sp_lit,
                       &c->sp_sums, &c->sp_segoff, &c->sp_segsrc, &c->sp_ids, &c->sp_compact, &c->sp_segtok,
                       &c->sp_segtokoff})
@@ -1781,6 +1784,21 @@ int bbpe_ctx_kernel_times(bbpe_ctx* c, double* ms, uint64_t* calls, int reset) {
     for (double& v : c->kernel_ms) v = 0;
     c->timed_calls = 0;
   }
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_ctx_piece_stats(bbpe_ctx* c, uint64_t* out, int reset) {
+  BBPE_TRY
+  if (!c || !out) throw bbpe::usage_error("null argument");
+  DeviceGuard g(c->device);
+  for (int i = 0; i < BBPE_N_PIECE_STATS; ++i) out[i] = 0;
+  if (!c->pstats.p) return BBPE_OK;
+  ck(cudaDeviceSynchronize(), "piece stats sync");
+  uint64_t v[bbpe::PST_N];
+  ck(cudaMemcpy(v, c->pstats.p, sizeof(v), cudaMemcpyDeviceToHost), "D2H piece stats");
+  for (int i = 0; i < BBPE_N_PIECE_STATS; ++i) out[i] = v[i];
+  if (reset) ck(cudaMemset(c->pstats.p, 0, sizeof(v)), "memset piece stats");
   return BBPE_OK;
   BBPE_CATCH
 }

@@ -149,7 +149,10 @@ __global__ void k_tile_first(EncodeArgs a) {
   uint64_t lo = (s == 0) ? 0 : min(prev, a.total) / kTile + 1;
   if (s == 0) hi = 0;  // offsets[0] == 0
   for (uint64_t t = lo; t <= hi && t < a.num_tiles; ++t) a.tile_first[t] = s;
-  if (s == 0) a.tile_first[a.num_tiles] = a.n_rows + 1;
+  if (s == 0) {
+    a.tile_first[a.num_tiles] = a.n_rows + 1;
+    if (a.pstats) atomicAdd(reinterpret_cast<unsigned long long*>(a.pstats + PST_BYTES), (unsigned long long)a.total);
+  }
   // A row starting at `total` has no bytes: no bit (it would land past the
   // last tile, where k_gather never clears it).
   if (a.rowbits && s < a.n_rows && o < a.total) atomicOr(&a.rowbits[o >> 5], 1u << (o & 31));
@@ -404,6 +407,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   int buf = 0;
   uint64_t mbase = 0;
   uint32_t mleft = 0;
+  uint32_t st_pieces = 0, st_merge = 0, st_long = 0, st_lbytes = 0;  // piece statistics (warp-uniform)
 
   while (tile < a.num_tiles) {
     // Prefetch: the next tile's window and row range.
@@ -554,6 +558,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         lmu[u] = __ballot_sync(kFull, lg[u]);
         mm_any |= mmu[u];
         lm_any |= lmu[u];
+        st_merge += __popc(mmu[u]);
+        st_long += __popc(lmu[u]);
       }
 #pragma unroll
       for (int u = 0; u < PPL; ++u) {
@@ -623,12 +629,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         const int k = S.lk[i];
         const uint64_t abs = b0 + S.plist[k];
         const uint64_t len = long_piece_length(a.offsets, a.n_rows, a.bytes, s_jt, a.chunkbits, abs, lane);
+        st_lbytes += uint32_t(len);
         if (lane == 0) {
           if (lfirst + i < a.lp_cap) a.lrec[lfirst + i] = LongRec{abs, len, 0, S.cnt[k], 0u};
           if (x0 + i < a.long_cap) a.long_idx[x0 + i] = uint32_t(lfirst + i);
         }
       }
     }
+    st_pieces += uint32_t(npieces);
     if (lane == 0) {
       a.tile_lrec[tile] = nlong ? ((lfirst << 24) | nlong) : 0;
       a.tile_count[tile] = run;
@@ -661,6 +669,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
   cp_async_wait<0>();
   for (uint32_t i = lane; i < mleft; i += 32)
     if (mbase + i < a.mrec_cap) a.mrec[mbase + i] = make_ulonglong2(~0ull, 0);
+  if (a.pstats && lane == 0) {  // piece statistics: one set of atomics per warp
+    auto add = [&](int k, uint64_t v) {
+      if (v) atomicAdd(reinterpret_cast<unsigned long long*>(a.pstats + k), (unsigned long long)v);
+    };
+    add(PST_PIECES, st_pieces);
+    add(PST_MEMO, st_pieces - st_merge - st_long);
+    add(PST_MERGE, st_merge);
+    add(PST_LONG, st_long);
+    add(PST_LONG_BYTES, st_lbytes);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1308,6 +1326,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_block_rows(EncodeArgs a, 
         a.tile_lrec[tile] = ne ? ((first << 24) | ne) : 0;
         a.tile_count[tile] = 0;
         a.tile_slots[tile] = 0;
+        if (a.pstats) {  // every non-empty row is one long piece
+          unsigned long long* ps = reinterpret_cast<unsigned long long*>(a.pstats);
+          if (ne) {
+            atomicAdd(ps + PST_PIECES, (unsigned long long)ne);
+            atomicAdd(ps + PST_LONG, (unsigned long long)ne);
+          }
+          atomicAdd(ps + PST_LONG_BYTES, (unsigned long long)tl);
+        }
       }
         }
 }
@@ -1329,6 +1355,9 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(EncodeArgs a) {
   if (tid == 0) s_cta = atomicAdd(&a.counters[CNT_GROUP_TICKET], 1u);
   __syncthreads();
   const uint64_t cta = s_cta;
+  if (cta == 0 && tid == 0 && a.pstats && a.dmask)  // k_dedup's owners (k_gather zeroes the counters)
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.pstats + PST_OWNERS),
+              (unsigned long long)a.counters[CNT_OWNERS]);
   const uint64_t t0 = cta * kScanTiles + uint64_t(tid) * kScanPer;
   uint64_t v[kScanPer];
   uint64_t sum = 0;
@@ -1646,15 +1675,16 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
   if (a.engine == BBPE_ENGINE_BLOCK) {
     k_block_rows<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
     ++launched;
-    if (ev) cudaEventRecord(ev[2], stream);
+    if (ev) for (int k = 2; k <= 5; ++k) cudaEventRecord(ev[k], stream);
   } else {
     k_pieces<<<p.main_grid, kWarpsPerCta * 32, pieces_smem(), stream>>>(a, t);
     ++launched;
     if (ev) cudaEventRecord(ev[2], stream);
-    if (a.dmask) {  // timed together with k_merge
+    if (a.dmask) {
       k_dedup<<<unsigned(p.sm_count * 8), 256, 0, stream>>>(a);
       ++launched;
     }
+    if (ev) cudaEventRecord(ev[3], stream);
     if (a.narrow)
       k_merge<uint16_t><<<p.merge_grid, kWarpsPerCta * 32, sizeof(MergeSmem<uint16_t>) * kWarpsPerCta,
                           stream>>>(a, t);
@@ -1662,21 +1692,22 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
       k_merge<uint32_t><<<p.merge_grid_wide, kWarpsPerCta * 32, sizeof(MergeSmem<uint32_t>) * kWarpsPerCta,
                           stream>>>(a, t);
     ++launched;
-    if (a.dmask) {  // timed together with k_merge
+    if (ev) cudaEventRecord(ev[4], stream);
+    if (a.dmask) {
       k_refs<<<unsigned(p.sm_count * 8), 256, 0, stream>>>(a);
       ++launched;
     }
+    if (ev) cudaEventRecord(ev[5], stream);
   }
-  if (ev) cudaEventRecord(ev[3], stream);
   k_long_pieces<kLpThreads><<<p.lp_grid, kLpThreads, 0, stream>>>(a, t);
   ++launched;
-  if (ev) cudaEventRecord(ev[4], stream);
+  if (ev) cudaEventRecord(ev[6], stream);
   k_tile_scan<<<unsigned((a.num_tiles + kScanTiles - 1) / kScanTiles), kScanThreads, 0, stream>>>(a);
   ++launched;
-  if (ev) cudaEventRecord(ev[5], stream);
+  if (ev) cudaEventRecord(ev[7], stream);
   k_gather<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
   ++launched;
-  if (ev) cudaEventRecord(ev[6], stream);
+  if (ev) cudaEventRecord(ev[8], stream);
   return launched;
 }
 

@@ -112,7 +112,11 @@ struct EncodeArgs {
   int tokens_input;         // 1: lpx already holds initial tokens (bbpe_block_bpe)
   int pattern;              // 1: gpt2 split pattern chunk starts are piece boundaries (pretok.cu)
   int64_t max_passes;       // <= 0: none
+  uint64_t* pstats;         // PST_N piece statistics, accumulated across encodes (never reset by kernels)
 };
+// Piece statistics (bbpe_ctx_piece_stats): per-warp counts added once per warp.
+enum { PST_PIECES = 0, PST_MEMO = 1, PST_MERGE = 2, PST_LONG = 3, PST_LONG_BYTES = 4, PST_OWNERS = 5,
+       PST_BYTES = 6, PST_N = 8 };
 
 struct LaunchPlan {
   int main_grid = 0;

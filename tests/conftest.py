@@ -53,6 +53,19 @@ def table_from_json(t):
     return MergeTable.build([(i, bytes(b)) for i, b in t["tokens"]], [tuple(m) for m in t["merges"]])
 
 
+def extend_table(table, total_merges):
+    """(MergeTable, arrays) of `table` extended by word-level merges
+    (workloads.tables.extend_wordlevel) to `total_merges` merges."""
+    from paper_2507_11941_b200 import MergeTable
+    from workloads.tables import arrays, extend_wordlevel
+    ids, off, blob, m4 = table.export()
+    raw = blob.tobytes()
+    toks = {int(i): raw[int(off[k]):int(off[k + 1])] for k, i in enumerate(ids)}
+    t, m = extend_wordlevel(toks, [tuple(int(x) for x in r) for r in m4], total_merges)
+    arrs = arrays(t, m)
+    return MergeTable.from_arrays(*arrs), arrs
+
+
 def arrays_from_json(t):
     toks = sorted((i, bytes(b)) for i, b in t["tokens"])
     ids = np.array([x[0] for x in toks], np.uint32)

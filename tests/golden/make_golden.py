@@ -188,7 +188,7 @@ def main():
     save_vectors("gpt2_random", ref, rows, "gpt2")
 
     from paper_2507_11941_b200 import load_merge_table_files
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     t = load_merge_table_files(os.path.join(OUT, "gpt2.bbpt"), None, "binary")
     gen = synth.TextGen(synth.word_list(t))
     d1, o1, _ = synth.config_rows(gen, 1, scale=1 / 16)

@@ -29,7 +29,7 @@ def test_every_declared_symbol_is_exported():
 
 
 def test_abi_version():
-    assert _lib.LIB.bbpe_abi_version() == 1
+    assert _lib.LIB.bbpe_abi_version() == 2
 
 
 def test_library_is_built_for_sm100a():

@@ -46,7 +46,7 @@ def test_cli_builds_and_usage_errors():
 def test_cli_tokenize_matches_reference(tmp_path, gpt2, out, specials, bos_eos):
     from oracle.oracle import Reference
     import paper_2507_11941_b200 as bb
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     if not Reference.available():
         pytest.skip("oracle/_ref not built")
     build_cli()
@@ -101,7 +101,7 @@ def test_cli_compare_matches_reference(tmp_path, gpt2, as_json):
     gpt2 split-pattern mode) prints the reference's divergence report
     (eval.hpp:147-273, oracle/_ref/ref_compare) byte for byte."""
     import paper_2507_11941_b200 as bb
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     ref_bin = os.path.join(ROOT, "oracle", "_ref", "ref_compare")
     if not os.path.exists(ref_bin):
         pytest.skip("oracle/_ref not built")

@@ -51,7 +51,7 @@ def test_gpt2_decomposition(gpt2, oracle_for):
     rng = np.random.default_rng(5)
     for _ in range(300):
         check(orc, J, bytes(rng.integers(0, 256, rng.integers(0, 200)).astype(np.uint8)))
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     text = gen.stream(1 << 15, seed=9).tobytes()
     for i in range(0, len(text), 1024):

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2507_11941_b200 as bb
-from conftest import GOLDEN, VECTOR_SETS, load_vectors, table_from_json
+from conftest import extend_table, GOLDEN, VECTOR_SETS, load_vectors, table_from_json
 
 pytestmark = pytest.mark.gpu
 
@@ -168,7 +168,7 @@ def test_losslessness(enc, gpt2):
 
 
 def test_waves_match_single_pass(gpt2):
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off = synth.rows_fixed(gen, 3000, 256, seed=3)
     a = bb.Encoder(0).encode_packed(gpt2, data, off)
@@ -204,7 +204,7 @@ def test_sharded_single_device_matches(gpt2):
 def test_config_parity_vs_reference_engines(cfg, scale, gpt2, oracle_for):
     """BASELINE configs at sizes the C oracle's heap engine finishes quickly
     (heap == block on the training-consistent GPT-2 table)."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off, _ = synth.config_rows(gen, cfg, scale=scale)
     wi, wo = oracle_for("gpt2").encode_packed(data, off, engine=1)
@@ -215,7 +215,7 @@ def test_config_parity_vs_reference_engines(cfg, scale, gpt2, oracle_for):
 
 def test_full_size_cfg2_properties(gpt2):
     """Full 2^20 x 256 B: round trip, determinism, and a random subsample vs the oracle."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     from oracle.oracle import CRestatement
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off, _ = synth.config_rows(gen, 2)
@@ -272,8 +272,8 @@ def test_remapped_ids_and_sparse_ranks(engine, toy_tables, oracle_for):
 
 @pytest.fixture(scope="module")
 def big_tables(gpt2):
-    from paper_2507_11941_b200 import synth
-    t200, arrs = synth.extend_table(gpt2, 200000)
+    from workloads import text as synth
+    t200, arrs = extend_table(gpt2, 200000)
     ids, off, blob, m4 = arrs
     keep = m4[:, 0] < 128000
     t128 = bb.MergeTable.from_arrays(ids, off, blob, m4[keep])
@@ -287,7 +287,7 @@ def test_large_vocab_cfg4_vs_oracle(which, engine, big_tables):
     hash), log-uniform 128 B-16 KiB rows, against the oracle's heap engine
     (identical to the block engine on these rank-consistent tables)."""
     from oracle.oracle import CRestatement
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     table, m4 = big_tables[which]
     assert table.info()["rank_consistent"] == 1
     gen = synth.TextGen(synth.word_list(table))
@@ -309,7 +309,7 @@ def test_pinned_and_pageable_outputs_match(gpt2, wave_bytes):
     """Pinned outputs take the device-driven copy-out path (k_copy_out into
     the mapped buffer, no host round trip per wave); pageable outputs the
     host-paced path. Both equal the single-wave result and the oracle's."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off = synth.rows_fixed(gen, 6000, 256, seed=11)
     ref_ids, ref_off, _ = bb.Encoder(0).encode_packed(gpt2, data, off)
@@ -327,7 +327,7 @@ def test_pinned_and_pageable_outputs_match(gpt2, wave_bytes):
 def test_ramped_waves_and_odd_alignment(gpt2, oracle_for):
     """Ramped wave plan over rows of mixed length; the output buffer starts at
     an odd u32 offset so k_copy_out's aligning head/tail paths run."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     rng = np.random.default_rng(5)
     lens = rng.integers(0, 3000, 2500)
@@ -392,7 +392,7 @@ def test_dedupe_is_results_neutral(gpt2, oracle_for, memo):
     """Within-call dedupe of merge pieces (default) vs every piece merged on
     its own: identical ids/offsets, and equal to the oracle. Text with heavy
     repetition (numbers, capitalised words) and random bytes."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off = synth.rows_fixed(gen, 4000, 256, seed=21)
     rng = np.random.default_rng(22)
@@ -410,7 +410,7 @@ def test_device_decode_round_trip(gpt2):
     """Device decode inverts the device encode: lossless
     round trip (acceptance_test.cpp:111-129) on Zipf text, random bytes and
     empty rows; row byte offsets equal the input offsets."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off = synth.rows_fixed(gen, 3000, 256, seed=31)
     rng = np.random.default_rng(32)
@@ -460,7 +460,7 @@ def test_device_epilogue_matches_host_padding(gpt2, max_len):
     equals the host padding of the same CSR (batch.hpp:98-125): widest or
     fixed max_len with right truncation, pad ids, lengths, mask, truncated
     row count; empty rows included."""
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     rng = np.random.default_rng(41)
     lens = rng.integers(0, 400, 700)
@@ -515,7 +515,7 @@ def test_full_size_long_row_configs(gpt2, cfg):
     sampled long rows equal the oracle (heap engine = block engine on GPT-2)."""
     torch = pytest.importorskip("torch")
     from oracle.oracle import CRestatement
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off, _ = synth.config_rows(gen, cfg, scale=1.0 if cfg == 3 else 1 / 16)
     e = bb.Encoder(0)
@@ -547,7 +547,7 @@ def test_device_jsonl_matches_reference_format(gpt2):
     row, as the host mirror writes it), including empty rows; a capacity
     shorter than the text reports the full length."""
     torch = pytest.importorskip("torch")
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     rng = np.random.default_rng(51)
     lens = rng.integers(0, 300, 900)
@@ -627,7 +627,7 @@ def test_gpt2_pattern_mode_vs_reference(gpt2, engine):
     runs and backoff, unicode letters/numbers/spaces, broken UTF-8, and Zipf
     text; the chunk starts equal the reference splitter's."""
     from oracle.oracle import Reference
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     if not Reference.available():
         pytest.skip("oracle/_ref not built")
     ids_, off_, blob_, m4_ = gpt2.export()
@@ -675,7 +675,7 @@ def test_gpt2_pattern_mode_long_rows_and_newline_runs(gpt2):
     rows += [b"word " * 2000, b"\n" * 500 + b"x", b"x\n" * 700, b"a" * 5000, b" \n \n  \n\t\n" * 90]
     # Short and long rows (threshold 4 KiB) interleaved so long rows start at
     # arbitrary offsets inside the splitter's 1 KiB spans.
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     tdata, toff = synth.rows_fixed(gen, 40, 9000, seed=72)
     for i in range(40):
@@ -714,7 +714,7 @@ SPECIAL_CASES = [b"", b"<|endoftext|>", b"hi<|endoftext|>there", b"<|a|>x<|a|><|
 
 
 def _special_rows(gpt2):
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     rng = np.random.default_rng(83)
     data, off = synth.rows_fixed(gen, 1500, 256, seed=84)
@@ -823,7 +823,7 @@ def test_encode_tensors_zero_copy(gpt2):
     DLPack export shares the memory; a row window (offsets[0] != 0) works."""
     import torch
     from torch.utils.dlpack import from_dlpack, to_dlpack
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off = synth.rows_fixed(gen, 3000, 200, seed=91)
     enc = bb.Encoder(0)
@@ -848,7 +848,7 @@ def test_device_call_over_4_gib(gpt2):
     no 32-bit tile / slot / record index overflows -- the ids and offsets are
     exactly the single batch's, repeated (rows are independent)."""
     import torch
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     gen = synth.TextGen(synth.word_list(gpt2))
     data, off, _ = synth.config_rows(gen, 2)
     e = bb.Encoder(0)
@@ -931,7 +931,7 @@ def test_gpt2_splitter_chunk_starts_vs_reference(gpt2):
     it still matches (the splitter's scratch is re-zeroed)."""
     import torch
     from oracle.oracle import Reference
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     if not Reference.available():
         pytest.skip("oracle/_ref not built")
     ids_, off_, blob_, m4_ = gpt2.export()
@@ -1008,7 +1008,7 @@ def test_splitter_full_size_cfg3_vs_reference(gpt2):
     pattern_pretokenize's."""
     import torch
     from oracle.oracle import Reference
-    from paper_2507_11941_b200 import synth
+    from workloads import text as synth
     if not Reference.available():
         pytest.skip("oracle/_ref not built")
     ids_, off_, blob_, m4_ = gpt2.export()

@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 import paper_2507_11941_b200 as bb
-from paper_2507_11941_b200 import synth
+from workloads import text as synth
 
 
 def specials():

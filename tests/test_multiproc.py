@@ -17,6 +17,11 @@ def _free_port():
         return s.getsockname()[1]
 
 
+class _Args:
+    def __init__(self, **kw):
+        self.__dict__.update(dict(config=2, text="zipf", table="wordlevel", merges=200000, scale=1 / 4096), **kw)
+
+
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -24,15 +29,20 @@ def _worker(rank, world, port, q):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import bench
     import paper_2507_11941_b200 as bb
-    table = bb.load_merge_table_files(os.path.join(bench.GOLDEN, "gpt2.bbpt"), None, "binary")
-    data, off, _ = bench.make_rows(table, 2, rank, 1 / 4096)
+    w = bench.Workload(_Args(), rank, world)
+    data, off = w.rows()
     # Each rank's shard is its own (weak scaling): seeds differ per rank.
     digest = int(np.frombuffer(data.tobytes()[:4096], np.uint8).astype(np.int64).sum())
+    # cfg5 (strong scaling): ONE corpus, contiguous shards from the encoder's partitioner.
+    w5 = bench.Workload(_Args(config=5, scale=1 / 20000), rank, world)
+    corpus = w5.corpus_offsets()
+    bounds = bb.partition(corpus, world).astype(np.int64)
+    d5, o5 = w5.rows(bounds)
     t = torch.tensor([float(rank + 1)], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # what bench.barrier_max does (nccl on GPU)
-    n = torch.tensor([off.size - 1], dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # what bench.allreduce does (nccl on GPU)
+    n = torch.tensor([off.size - 1, o5.size - 1, int(o5[-1])], dtype=torch.int64)
     dist.all_reduce(n)
-    q.put((rank, digest, float(t.item()), int(n.item())))
+    q.put((rank, digest, float(t.item()), n.tolist(), int(corpus.size - 1), int(corpus[-1]), w5.scaling))
     dist.destroy_process_group()
 
 
@@ -49,7 +59,19 @@ def test_two_rank_gloo_plan():
         assert p.exitcode == 0
     assert res[0][1] != res[1][1]                 # distinct shards
     assert res[0][2] == res[1][2] == 2.0          # max over ranks
-    assert res[0][3] == res[1][3] == 2 * 256      # whole-job row count
+    assert res[0][3][0] == 2 * 256                # whole-job row count (weak scaling)
+    rows5, bytes5 = res[0][4], res[0][5]
+    assert res[0][3][1:] == [rows5, bytes5]       # cfg5 shards partition the one corpus
+    assert res[0][6] == "strong"
+
+
+def test_bench_rank_count_must_match(monkeypatch):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    monkeypatch.setenv("WORLD_SIZE", "1")
+    with pytest.raises(SystemExit, match="--gpus 2 but 1 rank"):
+        bench.dist_init(_Args(gpus=2))
 
 
 def test_partition_shards_cover_rows():

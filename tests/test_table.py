@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2507_11941_b200 as bb
-from conftest import GOLDEN, arrays_from_json, table_from_json
+from conftest import extend_table, GOLDEN, arrays_from_json, table_from_json
 
 REF_GPT2 = "/root/reference/proj/tests/testdata/gpt2/"
 
@@ -122,12 +122,12 @@ def test_decode_and_unknown_ids(gpt2):
 
 
 def test_extended_large_tables(gpt2):
-    from paper_2507_11941_b200 import synth
-    t, (ids, off, blob, m4) = synth.extend_table(gpt2, 200000)
+    from workloads import text as synth
+    t, (ids, off, blob, m4) = extend_table(gpt2, 200000)
     info = t.info()
     assert info["merge_count"] == 200000 and info["rank_consistent"] == 1
     assert info["remapped_ids"] == 0 and info["id_bits"] == 18 and info["hash_slots"] == 524288
     # regex-like: the junction set barely grows
     assert info["junction_bigrams"] < 3000
-    t2, _ = synth.extend_table(gpt2, 200000)
+    t2, _ = extend_table(gpt2, 200000)
     assert np.array_equal(t2.export()[3], m4)  # deterministic

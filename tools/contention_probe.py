@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 import paper_2507_11941_b200 as bb
-from paper_2507_11941_b200 import synth
+from workloads import text as synth
 
 t = bb.load_merge_table_files(os.path.join(ROOT, "tests/golden/gpt2.bbpt"), None, "binary")
 gen = synth.TextGen(synth.word_list(t))

@@ -7,14 +7,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 import paper_2507_11941_b200 as bb
-from paper_2507_11941_b200 import synth
+from workloads import text as synth
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 memo = (sys.argv[2] != "nomemo") if len(sys.argv) > 2 else True
 pattern = sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "none" else None
 dedup = (sys.argv[4] != "nodedup") if len(sys.argv) > 4 else True
 t = bb.load_merge_table_files(os.path.join(ROOT, "tests/golden/gpt2.bbpt"), None, "binary")
 if cfg == 4:
-    t, _ = synth.extend_table(t, 200000)
+    from workloads import tables as WT
+    t = bb.MergeTable.from_arrays(*WT.arrays(*WT.extend_wordlevel(*WT.gpt2_table(), 200000)))
 gen = synth.TextGen(synth.word_list(t))
 data, off, desc = synth.config_rows(gen, cfg, scale=1 / 16 if cfg == 5 else 1.0, seed=cfg * 1000)
 n, total = off.size - 1, int(off[-1])

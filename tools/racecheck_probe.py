@@ -4,7 +4,7 @@ import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np
 import paper_2507_11941_b200 as bb
-from paper_2507_11941_b200 import synth
+from workloads import text as synth
 t = bb.load_merge_table_files("tests/golden/gpt2.bbpt", None, "binary")
 gen = synth.TextGen(synth.word_list(t))
 data, off = synth.rows_fixed(gen, 200, 600, seed=5)
