@@ -198,6 +198,7 @@ struct bbpe_ctx {
   DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff;
   DevBuf pad_scalar;  // epilogue: widest row / truncated count
   DevBuf pstats;      // piece statistics (bbpe_ctx_piece_stats), PST_N u64
+  bool stats_paused = false;  // the memo build's own encodes are not counted
   DevBuf run_base;
   // Special-token set (bbpe_ctx_set_specials), longest first, and the scratch
   // of bbpe_encode_batch_device.
@@ -317,7 +318,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   a.max_passes = c.cfg.max_passes;
   a.pattern = c.cfg.pattern;
   if (c.pstats.ensure(PST_N * 8)) ck(cudaMemsetAsync(c.pstats.p, 0, PST_N * 8, s), "memset pstats");
-  a.pstats = c.pstats.as<uint64_t>();
+  a.pstats = c.stats_paused ? nullptr : c.pstats.as<uint64_t>();
   // Counters and look-back status are left zero by k_gather; rowbits too.
   if (sc.ctrl_dirty) {
     ck(cudaMemsetAsync(a.status, 0, sc.status.cap, s), "memset status");
@@ -804,7 +805,19 @@ uint64_t encode_host_pipelined(bbpe_ctx& c, const bbpe_table& t, const uint8_t* 
 // merge junctions) is encoded by this engine with the memo off; encodings of
 // at most two tokens are stored in an open-addressing table keyed by the
 // bytes. Entries depend on the table only, never on the input being encoded.
+void ensure_memo_impl(bbpe_ctx& c, const bbpe_table& t);
 void ensure_memo(bbpe_ctx& c, const bbpe_table& t) {
+  c.stats_paused = true;
+  try {
+    ensure_memo_impl(c, t);
+  } catch (...) {
+    c.stats_paused = false;
+    throw;
+  }
+  c.stats_paused = false;
+}
+
+void ensure_memo_impl(bbpe_ctx& c, const bbpe_table& t) {
   using namespace bbpe;
   DeviceReplica& rep = replica_of(t, c.device);
   {

@@ -34,6 +34,7 @@
 
 #include "kernels.cuh"
 #include "pretok.cuh"
+#include "probe.cuh"
 
 namespace bbpe {
 namespace {
@@ -47,57 +48,6 @@ constexpr int kTileWords = kTile / 32;
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ uint64_t dmix64(uint64_t h) {
-  h ^= h >> 33;
-  h *= 0xff51afd7ed558ccdULL;
-  h ^= h >> 33;
-  return h;
-}
-
-// Probe results ("rk"): for narrow tables (T.key32) rank << 16 | merged id,
-// for wide tables the dense rank (merged id = r2m[rank]). Both order like the
-// rank (ranks are unique), kNoRank when the pair is not in the table.
-__device__ __forceinline__ uint32_t rk_merged(const DevTable& T, uint32_t rk) {
-  return T.key32 ? (rk & 0xFFFFu) : __ldg(T.r2m + rk);
-}
-__device__ __forceinline__ uint32_t rk_rank(const DevTable& T, uint32_t rk) { return T.key32 ? rk >> 16 : rk; }
-
-// Pair -> rk (kNoRank when absent). One 32-byte bucket per step.
-__device__ __forceinline__ uint32_t probe32(const DevTable& T, uint32_t l, uint32_t r) {
-  const uint32_t key = (l << 16) | r;
-  uint64_t b = mix32(key) & T.bucket_mask;
-  for (;;) {
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + b * kBucketSlots);
-    const ulonglong2 s01 = __ldg(p), s23 = __ldg(p + 1);
-    const uint64_t s[4] = {s01.x, s01.y, s23.x, s23.y};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (s[j] == kEmptySlot) return kNoRank;
-      if (uint32_t(s[j] >> 32) == key) return uint32_t(s[j]);
-    }
-    b = (b + 1) & T.bucket_mask;
-  }
-}
-
-__device__ __forceinline__ uint32_t probe(const DevTable& T, uint32_t l, uint32_t r) {
-  if (T.key32) return probe32(T, l, r);
-  const uint64_t key = (uint64_t(l) << T.id_bits) | uint64_t(r);
-  uint64_t b = dmix64(key) & T.bucket_mask;
-  const uint64_t rmask = (1ull << T.rank_bits) - 1;
-  for (;;) {
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + b * kBucketSlots);
-    ulonglong2 s01 = __ldg(p);
-    ulonglong2 s23 = __ldg(p + 1);
-    uint64_t s[4] = {s01.x, s01.y, s23.x, s23.y};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (s[j] == kEmptySlot) return kNoRank;
-      if ((s[j] >> T.rank_bits) == key) return static_cast<uint32_t>(s[j] & rmask);
-    }
-    b = (b + 1) & T.bucket_mask;
-  }
-}
 
 __device__ __forceinline__ bool is_junction(const uint32_t* junc, uint32_t a, uint32_t c) {
   uint32_t bit = (a << 8) | c;
@@ -680,284 +630,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
     add(PST_LONG_BYTES, st_lbytes);
   }
 }
-
-// ---------------------------------------------------------------------------
-// Block-level helpers for the CTA-per-piece kernel.
-template <int NT>
-struct BlockScratch {
-  uint32_t red_u32[2][32];
-  int32_t red_i32[2][32];
-  uint32_t bcast_u32[4];
-  int32_t bcast_i32[4];
-};
-
-template <int NT>
-__device__ uint32_t block_min_u32(uint32_t v, BlockScratch<NT>& sc, int slot) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = __reduce_min_sync(kFull, v);
-  if (lane == 0) sc.red_u32[slot][wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t x = lane < NT / 32 ? sc.red_u32[slot][lane] : kNoRank;
-    x = __reduce_min_sync(kFull, x);
-    if (lane == 0) sc.bcast_u32[slot] = x;
-  }
-  __syncthreads();
-  return sc.bcast_u32[slot];
-}
-
-// Exclusive scan (sum) of u32 over the block; *total receives the block sum.
-template <int NT>
-__device__ uint32_t block_excl_sum_u32(uint32_t v, BlockScratch<NT>& sc, int slot,
-                                       uint32_t* total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t inc = warp_incl_sum(v, lane);
-  if (lane == 31) sc.red_u32[slot][wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    uint32_t x = lane < NT / 32 ? sc.red_u32[slot][lane] : 0;
-    uint32_t xi = warp_incl_sum(x, lane);
-    if (lane < NT / 32) sc.red_u32[slot][lane] = xi - x;
-    if (lane == 31) sc.bcast_u32[slot] = xi;
-  }
-  __syncthreads();
-  *total = sc.bcast_u32[slot];
-  return sc.red_u32[slot][wid] + inc - v;
-}
-
-// Exclusive max-scan of i32 (identity -1).
-template <int NT>
-__device__ int32_t block_excl_max_i32(int32_t v, BlockScratch<NT>& sc, int slot) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int32_t inc = v;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    int32_t u = __shfl_up_sync(kFull, inc, d);
-    if (lane >= d) inc = max(inc, u);
-  }
-  int32_t exc = __shfl_up_sync(kFull, inc, 1);
-  if (lane == 0) exc = -1;
-  if (lane == 31) sc.red_i32[slot][wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    int32_t x = lane < NT / 32 ? sc.red_i32[slot][lane] : -1;
-    int32_t xi = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      int32_t u = __shfl_up_sync(kFull, xi, d);
-      if (lane >= d) xi = max(xi, u);
-    }
-    int32_t xe = __shfl_up_sync(kFull, xi, 1);
-    if (lane == 0) xe = -1;
-    if (lane < NT / 32) sc.red_i32[slot][lane] = xe;
-  }
-  __syncthreads();
-  return max(sc.red_i32[slot][wid], exc);
-}
-
-__device__ __forceinline__ uint32_t tok_of(uint64_t e) { return static_cast<uint32_t>(e); }
-__device__ __forceinline__ uint32_t rank_of(uint64_t e) { return static_cast<uint32_t>(e >> 32); }
-__device__ __forceinline__ uint64_t pack_tr(uint32_t t, uint32_t r) {
-  return uint64_t(t) | (uint64_t(r) << 32);
-}
-
-// ---------------------------------------------------------------------------
-// k_long_pieces: the block engine (block_engine.hpp:268-310) for one piece per
-// CTA, persistent over the long-piece list. Working set {token, rank} pairs in
-// global memory (L2-resident for pieces of a few MB), double-buffered like the
-// reference (277-283, 306). Exactness-preserving deviations:
-//   * ranks are cached and only pairs touching a merge are re-probed
-//     (a pair whose two tokens are unchanged keeps its rank);
-//   * the merged id of a pass is r2m[min_rank] (ranks are unique per pair,
-//     merge_table.hpp:264-268), not a second probe per merge (173);
-//   * left-greedy marking uses run parity: pair q merges iff rank(q) == m and
-//     q - (start of its run of m's) is even, identical to flags[i+1] =
-//     (ranks[i] == m && !flags[i]) (107-109).
-template <int NT>
-__global__ void __launch_bounds__(NT) k_long_pieces(EncodeArgs a, DevTable T) {
-  __shared__ uint32_t s_lut[256];
-  __shared__ BlockScratch<NT> sc;
-  __shared__ uint32_t s_idx;
-  const int tid = threadIdx.x;
-  if (blockIdx.x >= min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap)) return;  // nothing for this CTA
-  for (int i = threadIdx.x; i < 256; i += NT) s_lut[i] = T.lut[i];
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_idx = atomicAdd(&a.counters[CNT_LP_NEXT], 1u);
-    __syncthreads();
-    const uint32_t idx = s_idx;
-    const uint32_t count = min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap);
-    if (idx >= count) return;
-    const uint32_t ridx = a.long_idx[idx];
-    const LongRec P = a.lrec[ridx];
-    const int32_t len = static_cast<int32_t>(P.len);
-    uint64_t* X = a.lpx + P.start;
-    uint64_t* Y = a.lpy + P.start;
-    if (!a.tokens_input) {
-      for (int32_t i = tid; i < len; i += NT) X[i] = pack_tr(s_lut[a.bytes[P.start + i]], kProbe);
-    }
-    __syncthreads();
-    int32_t n = len;
-    uint64_t pass = 0;
-    bool maxpass_hit = false;
-    while (n >= 2) {
-      const int32_t chunk = (n + NT - 1) / NT;
-      const int32_t c0 = min(n, tid * chunk), c1 = min(n, c0 + chunk);
-      // (1) ranks for unresolved pairs + local min.
-      uint32_t lmin = kNoRank;
-      for (int32_t i = c0; i < c1 && i < n - 1; ++i) {
-        uint64_t e = X[i];
-        uint32_t r = rank_of(e);
-        if (r == kProbe) {
-          r = probe(T, tok_of(e), tok_of(X[i + 1]));
-          X[i] = pack_tr(tok_of(e), r);
-        }
-        lmin = min(lmin, r);
-      }
-      const uint32_t m = block_min_u32<NT>(lmin, sc, 0);
-      if (m == kNoRank) break;
-      if (a.max_passes > 0 && pass >= uint64_t(a.max_passes)) {
-        maxpass_hit = true;
-        break;
-      }
-      // (2) start of the run of m's active at my chunk start.
-      int32_t agg = -1;
-      bool prev_is_m = (c0 > 0 && c0 < n) ? rank_of(X[c0 - 1]) == m : false;
-      {
-        bool pm = prev_is_m;
-        for (int32_t i = c0; i < c1 && i < n - 1; ++i) {
-          bool im = rank_of(X[i]) == m;
-          if (im && !pm) agg = i;
-          pm = im;
-        }
-      }
-      const int32_t carry = block_excl_max_i32<NT>(agg, sc, 0);
-      // (3) mark merges (run parity) and count them.
-      uint32_t my_merges = 0;
-      {
-        int32_t s = carry;
-        bool pm = prev_is_m;
-        for (int32_t i = c0; i < c1 && i < n - 1; ++i) {
-          uint64_t e = X[i];
-          bool im = rank_of(e) == m;
-          if (im) {
-            if (!pm) s = i;
-            if (((i - s) & 1) == 0) {
-              X[i] = pack_tr(tok_of(e), kMergeMark);
-              ++my_merges;
-            }
-          }
-          pm = im;
-        }
-      }
-      uint32_t total_merges;
-      const uint32_t before = block_excl_sum_u32<NT>(my_merges, sc, 1, &total_merges);
-      // (4) compaction into Y (block_engine.hpp:166-182) with cached ranks.
-      const uint32_t M = rk_merged(T, m);
-      {
-        uint32_t run = before;  // merges at pair positions q < i
-        for (int32_t i = c0; i < c1; ++i) {
-          if (i > c0 && rank_of(X[i - 1]) == kMergeMark) ++run;
-          bool removed = i > 0 && rank_of(X[i - 1]) == kMergeMark;
-          if (removed) continue;
-          uint64_t e = X[i];
-          bool mi = (i < n - 1) && rank_of(e) == kMergeMark;
-          bool mnext = (i + 1 < n - 1) && rank_of(X[i + 1]) == kMergeMark;
-          uint32_t t = mi ? M : tok_of(e);
-          uint32_t r = (mi || mnext) ? kProbe : rank_of(e);
-          Y[i - run] = pack_tr(t, r);
-        }
-      }
-      if (a.trace && tid == 0) {
-        if (pass < a.trace_cap) {
-          a.trace[3 * pass] = pass + 1;
-          a.trace[3 * pass + 1] = T.rank_orig[rk_rank(T, m)];
-          a.trace[3 * pass + 2] = total_merges;
-        }
-      }
-      ++pass;
-      n -= static_cast<int32_t>(total_merges);
-      uint64_t* tmp = X;
-      X = Y;
-      Y = tmp;
-      __syncthreads();
-    }
-    __syncthreads();
-    if (maxpass_hit && tid == 0)
-      atomicMin(reinterpret_cast<unsigned long long*>(&a.err[ERR_MAXPASS_ROW]),
-                (unsigned long long)P.row);
-    if (a.trace && tid == 0 && a.trace_count) *a.trace_count = pass;
-    // Result: lpo[start] = count, tokens follow when anything merged (or on token input).
-    uint32_t* O = a.lpo + P.start;
-    if (tid == 0) {
-      O[0] = static_cast<uint32_t>(n) | ((n == len && !a.tokens_input) ? kUnchanged : 0u);
-      a.lrec[ridx].count = static_cast<uint32_t>(n);
-      if (!a.tokens_input) atomicAdd(&a.tile_count[P.start / kTile], static_cast<uint32_t>(n));
-    }
-    if (n < len || a.tokens_input)
-      for (int32_t i = tid; i < n; i += NT) O[1 + i] = tok_of(X[i]);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Batched probe: issue the bucket loads, resolve later. K32: narrow tables
-// (ids < 2^16) with 32-bit keys, slot = key32 << 32 | rank.
-struct ProbeReq {
-  uint64_t key;
-  ulonglong2 s01, s23;
-};
-template <bool K32>
-__device__ __forceinline__ uint64_t probe_bucket(const DevTable& T, uint64_t key) {
-  return (K32 ? uint64_t(mix32(uint32_t(key))) : dmix64(key)) & T.bucket_mask;
-}
-template <bool K32>
-__device__ __forceinline__ void probe_issue(ProbeReq& q, const DevTable& T, uint32_t l, uint32_t r) {
-  q.key = K32 ? uint64_t((l << 16) | r) : ((uint64_t(l) << T.id_bits) | uint64_t(r));
-  const ulonglong2* p = reinterpret_cast<const ulonglong2*>(T.slots + probe_bucket<K32>(T, q.key) * kBucketSlots);
-  q.s01 = __ldg(p);
-  q.s23 = __ldg(p + 1);
-}
-
-// Bucket full without a hit: keep probing linearly (rare at load <= 0.5).
-template <bool K32>
-__device__ __noinline__ uint32_t probe_overflow(const uint64_t* slots, uint64_t bucket_mask, uint32_t rank_bits,
-                                                uint64_t key, uint64_t b) {
-  const uint64_t rmask = (1ull << rank_bits) - 1;
-  for (;;) {
-    b = (b + 1) & bucket_mask;
-    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(slots + b * kBucketSlots);
-    const ulonglong2 x = __ldg(p), y = __ldg(p + 1);
-    const uint64_t t[4] = {x.x, x.y, y.x, y.y};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (t[j] == kEmptySlot) return kNoRank;
-      if (K32 ? (uint32_t(t[j] >> 32) == uint32_t(key)) : ((t[j] >> rank_bits) == key))
-        return K32 ? uint32_t(t[j]) : static_cast<uint32_t>(t[j] & rmask);
-    }
-  }
-}
-
-template <bool K32>
-__device__ __forceinline__ uint32_t probe_resolve(const ProbeReq& q, const DevTable& T) {
-  // Branch-free over the bucket (both halves of the 32-byte load are used
-  // unconditionally, so the compiler cannot sink one behind the other): a key
-  // occupies at most one slot and slots fill left to right, so the result is
-  // the matching slot, else no rank if the bucket has an empty slot, else the
-  // next bucket (rare at load <= 0.5).
-  const uint64_t s[4] = {q.s01.x, q.s01.y, q.s23.x, q.s23.y};
-  uint32_t res = kNoRank;
-  bool any_empty = false;
-#pragma unroll
-  for (int j = 3; j >= 0; --j) {
-    const bool hit = K32 ? (uint32_t(s[j] >> 32) == uint32_t(q.key)) : ((s[j] >> T.rank_bits) == q.key);
-    const uint32_t v = K32 ? uint32_t(s[j]) : static_cast<uint32_t>(s[j] & ((1ull << T.rank_bits) - 1));
-    res = hit ? v : res;
-    any_empty |= s[j] == kEmptySlot;
-  }
-  if (res != kNoRank || any_empty) return res;
-  return probe_overflow<K32>(T.slots, T.bucket_mask, T.rank_bits, q.key, probe_bucket<K32>(T, q.key));
-}
-
 
 // ---------------------------------------------------------------------------
 // k_merge: the deferred 2..kLmax-byte pieces of every tile, lane per piece,
@@ -1634,7 +1306,7 @@ LaunchPlan plan_launch(int device) {
                        int(sizeof(MergeSmem<uint32_t>) * kWarpsPerCta));
   p.merge_grid = grid(k_merge<uint16_t>, kWarpsPerCta * 32, sizeof(MergeSmem<uint16_t>) * kWarpsPerCta);
   p.merge_grid_wide = grid(k_merge<uint32_t>, kWarpsPerCta * 32, sizeof(MergeSmem<uint32_t>) * kWarpsPerCta);
-  p.lp_grid = grid(k_long_pieces<kLpThreads>, kLpThreads, 0);
+  p.lp_grid = long_pieces_grid(device, p.sm_count);
   p.gather_grid = grid(k_gather, kWarpsPerCta * 32, 0);
   return p;
 }
@@ -1699,7 +1371,7 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     }
     if (ev) cudaEventRecord(ev[5], stream);
   }
-  k_long_pieces<kLpThreads><<<p.lp_grid, kLpThreads, 0, stream>>>(a, t);
+  launch_long_pieces(a, t, p.lp_grid, stream);
   ++launched;
   if (ev) cudaEventRecord(ev[6], stream);
   k_tile_scan<<<unsigned((a.num_tiles + kScanTiles - 1) / kScanTiles), kScanThreads, 0, stream>>>(a);
@@ -1714,7 +1386,7 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
 int launch_block_bpe(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p,
                      cudaStream_t stream) {
   (void)p;
-  k_long_pieces<kLpThreads><<<1, kLpThreads, 0, stream>>>(a, t);
+  launch_long_pieces(a, t, 1, stream);
   return 1;
 }
 

@@ -19,7 +19,8 @@ constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece to
 constexpr int kScanTilesPerCta = 4096;  // k_tile_scan: 512 threads x 8 tiles
 constexpr int kWarpsPerCta = 8;
 constexpr int kTilesPerTicket = 4;  // k_pieces: consecutive tiles per ticket
-constexpr int kLpThreads = 512;     // CTA size of the long-piece (block engine) kernel
+constexpr int kLpWarps = 8;         // k_long_pieces: warps per CTA (one piece per warp)
+constexpr int kLpSmemBytes = 8192;  // k_long_pieces: shared-memory positions per warp (2048 narrow / 1024 wide)
 constexpr int kWinVec = (kTile + 48) / 16;  // 16-byte chunks of a tile window: bytes [b0-16, b0+kTile+32)
 constexpr int kRowWords = kTile / 32 + 4;   // row-start bit words copied per tile (whole 16-byte chunks)
 constexpr int kMrecChunk = 256;     // merge records a warp reserves at a time
@@ -144,6 +145,10 @@ void launch_add_u64(uint64_t* d_p, uint64_t n, uint64_t v, int sm_count, cudaStr
 void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t* d_wave_offsets,
                      uint64_t* mapped_offsets, uint64_t nr, uint64_t* run_base, uint64_t cap, int sm_count,
                      cudaStream_t stream);
+// k_long_pieces (longpieces.cu): the warp-per-piece block engine.
+size_t long_pieces_smem(bool narrow);
+int long_pieces_grid(int device, int sm_count);
+void launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);
 // Long-piece kernel only (token input, used by bbpe_block_bpe).
 int launch_block_bpe(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p,
                      cudaStream_t stream);

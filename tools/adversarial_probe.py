@@ -1,38 +1,72 @@
-"""Full-size adversarial batches (256 MiB each): random bytes, 64 KiB runs of
-one byte, digit runs. Checks: decode(encode(x)) == x, ids of sampled rows vs
-the reference (oracle/_ref encode_batch), and the device time."""
-import os, sys, time
+"""Full-size adversarial batches (256 MiB each, SURVEY §8d sidecar set):
+random bytes, 64 KiB runs of one byte, 4 KiB digit rows, 1 KiB rows of
+random CJK. Every row is checked against the compiled reference
+(bench.parity_check: oracle/_ref heap_bpe on every row + the block engine on
+a sample); prints device ms per encode and the per-kernel split.
+
+  python tools/adversarial_probe.py [case ...] [--engine pieces|block]
+"""
+import os, sys, json
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import torch
+import bench
 import paper_2507_11941_b200 as bb
 from oracle.oracle import Reference
-t = bb.load_merge_table_files("tests/golden/gpt2.bbpt", None, "binary")
-ref = Reference.from_arrays(*t.export())
+from workloads import tables as WT
+
+engine = "block" if "--engine=block" in sys.argv else "pieces"
+want = [a for a in sys.argv[1:] if not a.startswith("--")]
+t = bb.load_merge_table_files(WT.GPT2_VOCAB, WT.GPT2_MERGES, "gpt2")
+ref = Reference.load_files(WT.GPT2_VOCAB, WT.GPT2_MERGES)
 rng = np.random.default_rng(7)
 N = 256 << 20
+
+
+def cjk(n):
+    cp = rng.integers(0x4E00, 0xA000, n // 3 + 1)
+    b = np.stack([0xE0 | (cp >> 12), 0x80 | ((cp >> 6) & 0x3F), 0x80 | (cp & 0x3F)], 1).astype(np.uint8).reshape(-1)
+    return b[:n]
+
+
 cases = {
-    "random_bytes_256B_rows": (rng.integers(0, 256, N, dtype=np.uint8), 256),
-    "runs_a_64KiB_rows": (np.full(N, ord("a"), np.uint8), 65536),
-    "digits_4KiB_rows": (rng.integers(ord("0"), ord("9") + 1, N, dtype=np.uint8), 4096),
+    "random_bytes_256B_rows": (lambda: rng.integers(0, 256, N, dtype=np.uint8), 256),
+    "runs_a_64KiB_rows": (lambda: np.full(N, ord("a"), np.uint8), 65536),
+    "runs_dot_64KiB_rows": (lambda: np.full(N, ord("."), np.uint8), 65536),
+    "digits_4KiB_rows": (lambda: rng.integers(ord("0"), ord("9") + 1, N, dtype=np.uint8), 4096),
+    "cjk_1KiB_rows": (lambda: cjk(N), 1023),
 }
-enc = bb.Encoder(0)
-for name, (data, L) in cases.items():
-    off = np.arange(0, N + 1, L, dtype=np.uint64)
-    ids, oo, st = enc.encode_packed(t, data, off)
-    d, bo = enc.decode_packed(t, ids, oo)
-    assert np.array_equal(np.asarray(d), data), name
-    for r in rng.integers(0, off.size - 1, 3):
-        s = slice(int(off[r]), int(off[r + 1]))
-        w, wo = ref.encode_batch(data[s], np.array([0, L], np.uint64), workers=8)
-        assert ids[int(oo[r]):int(oo[r + 1])].tolist() == w.tolist(), (name, int(r))
+enc = bb.Encoder(0, engine=engine)
+for name, (mk, L) in cases.items():
+    if want and name not in want:
+        continue
+    data = mk()
+    n = N // L
+    off = np.arange(0, n + 1, dtype=np.uint64) * np.uint64(L)
+    data = data[: int(off[-1])]
+    tot = int(off[-1])
     dd = torch.from_numpy(data).cuda(); do = torch.from_numpy(off.view(np.int64)).cuda()
-    di = torch.empty(N, dtype=torch.int32, device="cuda"); doo = torch.empty(off.size, dtype=torch.int64, device="cuda")
+    di = torch.empty(tot, dtype=torch.int32, device="cuda"); doo = torch.empty(off.size, dtype=torch.int64, device="cuda")
     for _ in range(2):
-        enc.encode_device(t, dd.data_ptr(), do.data_ptr(), off.size - 1, N, di.data_ptr(), doo.data_ptr())
+        enc.encode_device(t, dd.data_ptr(), do.data_ptr(), n, tot, di.data_ptr(), doo.data_ptr())
+    enc.kernel_times(reset=True)
+    enc.piece_stats(reset=True)
     torch.cuda.synchronize(); e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(3):
-        enc.encode_device(t, dd.data_ptr(), do.data_ptr(), off.size - 1, N, di.data_ptr(), doo.data_ptr())
+        enc.encode_device(t, dd.data_ptr(), do.data_ptr(), n, tot, di.data_ptr(), doo.data_ptr(), sync=False)
     e1.record(); torch.cuda.synchronize()
-    print(name, "tokens", int(oo[-1]), "device ms", round(e0.elapsed_time(e1) / 3, 2), "ok", flush=True)
+    kt, kc = enc.kernel_times(reset=True)
+    ps = enc.piece_stats(reset=True)
+    oo = doo.cpu().numpy().view(np.uint64)
+    ids = di[: int(oo[-1])].cpu().numpy().view(np.uint32)
+    par = bench.parity_check(ref, data, off, ids, oo, 30.0)
+    print(json.dumps({"case": name, "engine": engine, "rows": n, "tokens": int(oo[-1]),
+                      "device_ms": round(e0.elapsed_time(e1) / 3, 3),
+                      "kernel_ms": {k: round(v / kc, 3) for k, v in kt.items() if v},
+                      "long_pieces": ps["long_pieces"] // 3, "long_byte_fraction": ps["long_byte_fraction"],
+                      "parity": {k: par[k] for k in ("rows_checked", "mismatches", "oracle")}}), flush=True)
+    assert par["mismatches"] == 0, par
+    del dd, do, di, doo
+    torch.cuda.empty_cache()
