@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_PIECES_MINB) k_pieces(
         const uint64_t len = long_piece_length(a.offsets, a.n_rows, a.bytes, s_jt, a.chunkbits, abs, lane);
         st_lbytes += uint32_t(len);
         if (lane == 0) {
-          if (lfirst + i < a.lp_cap) a.lrec[lfirst + i] = LongRec{abs, len, 0, S.cnt[k], 0u};
+          if (lfirst + i < a.lp_cap) a.lrec[lfirst + i] = LongRec{abs, len, 0, S.cnt[k], 0u, 0};
           if (x0 + i < a.long_cap) a.long_idx[x0 + i] = uint32_t(lfirst + i);
         }
       }
@@ -989,7 +989,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_block_rows(EncodeArgs a, 
         const uint32_t before = ri + __popc(nm & lanemask_lt(lane));
         if (s < s1 && s <= a.n_rows) a.out_offsets[s] = uint64_t(before) << 40;
         if (ne_row && first + before < a.lp_cap) {
-          a.lrec[first + before] = LongRec{o, e - o, s, 0u, 0u};
+          a.lrec[first + before] = LongRec{o, e - o, s, 0u, 0u, 0};
           if (lfirst + before < a.long_cap) a.long_idx[lfirst + before] = uint32_t(first + before);
         }
         ri += __popc(nm);
@@ -1173,7 +1173,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
     if (s0 + lane < s1 && s0 + lane <= a.n_rows) roff = __ldcg(a.out_offsets + s0 + lane);
     // Leave the look-back status and the counters zero for the next encode.
     if (t < a.num_groups && lane == 0) a.status[t] = 0;
-    if (t == 0 && lane < CNT_N) a.counters[lane] = 0;
+    if (t == 0 && lane < CNT_N && lane != CNT_LREC && lane != CNT_LCOPY && lane != CNT_LDONE) a.counters[lane] = 0;
     // The tile's row-start bits are consumed: leave them zero for the next encode.
     if (a.rowbits && lane < kTile / 32) a.rowbits[t * (kTile / 32) + lane] = 0;
     if (a.chunkbits && lane < kTile / 32) a.chunkbits[t * (kTile / 32) + lane] = 0;
@@ -1210,17 +1210,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
       run += __popc(bal);
     }
     __syncwarp();
-    if (nl) {  // long pieces' tokens (rare path)
+    if (nl) {  // long pieces: their CSR positions (k_long_copy moves the tokens)
       uint32_t before = 0;
       for (uint32_t li = 0; li < nl; ++li) {
-        const LongRec& lr = a.lrec[lfirst + li];
-        const uint32_t o = compact_at(G, lr.spref, nslots, run) + before;
         const uint32_t cnt = LV.cnt(li);
-        const bool unchanged = (__ldcg(a.lpo + lr.start) & kUnchanged) != 0;
-        for (uint32_t i = lane; i < cnt; i += 32) {
-          const uint32_t v = unchanged ? s_lut[a.bytes[lr.start + i]] : __ldcg(a.lpo + lr.start + 1 + i);
-          out[o + i] = d2id ? __ldg(d2id + v) : v;
-        }
+        if (lane == 0) a.lrec[lfirst + li].out = tbase + compact_at(G, LV.sp(li), nslots, run) + before;
         before += cnt;
       }
     }
@@ -1378,6 +1372,8 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
   ++launched;
   if (ev) cudaEventRecord(ev[7], stream);
   k_gather<<<p.gather_grid, kWarpsPerCta * 32, 0, stream>>>(a, t);
+  ++launched;
+  launch_long_copy(a, t, p.gather_grid, stream);
   ++launched;
   if (ev) cudaEventRecord(ev[8], stream);
   return launched;

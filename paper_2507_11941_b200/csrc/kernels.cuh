@@ -19,8 +19,14 @@ constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece to
 constexpr int kScanTilesPerCta = 4096;  // k_tile_scan: 512 threads x 8 tiles
 constexpr int kWarpsPerCta = 8;
 constexpr int kTilesPerTicket = 4;  // k_pieces: consecutive tiles per ticket
-constexpr int kLpWarps = 8;         // k_long_pieces: warps per CTA (one piece per warp)
-constexpr int kLpSmemBytes = 8192;  // k_long_pieces: shared-memory positions per warp (2048 narrow / 1024 wide)
+#ifndef BBPE_LP_WARPS
+#define BBPE_LP_WARPS 4
+#endif
+#ifndef BBPE_LP_SMEM
+#define BBPE_LP_SMEM 16384
+#endif
+constexpr int kLpWarps = BBPE_LP_WARPS;     // k_long_pieces: warps per CTA (one piece per warp)
+constexpr int kLpSmemBytes = BBPE_LP_SMEM;  // k_long_pieces: shared-memory positions per warp (4096 narrow / 2048 wide)
 constexpr int kWinVec = (kTile + 48) / 16;  // 16-byte chunks of a tile window: bytes [b0-16, b0+kTile+32)
 constexpr int kRowWords = kTile / 32 + 4;   // row-start bit words copied per tile (whole 16-byte chunks)
 constexpr int kMrecChunk = 256;     // merge records a warp reserves at a time
@@ -35,7 +41,9 @@ constexpr int kInlineRes = 6;
 
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
-       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_PRETOK = 8, CNT_N = 9 };
+       CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_PRETOK = 8, CNT_LCOPY = 9, CNT_LDONE = 10,
+       CNT_N = 11 };
+// k_gather leaves CNT_LREC / CNT_LCOPY / CNT_LDONE for k_long_copy, which resets them.
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFSETS = 3, ERR_N = 4 };
 
@@ -55,6 +63,7 @@ struct LongRec {
   uint64_t row;    // row index (MaxPassesError reporting)
   uint32_t spref;  // staging slots of the tile before this piece
   uint32_t count;  // tokens out, written by the merging kernel
+  uint64_t out;    // first output position (k_gather), for k_long_copy
 };
 __host__ __device__ inline uint64_t pack_mrec(uint64_t start, uint32_t spref, uint32_t len) {
   return (start << 16) | (uint64_t(spref) << 6) | len;
@@ -149,6 +158,8 @@ void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t
 size_t long_pieces_smem(bool narrow);
 int long_pieces_grid(int device, int sm_count);
 void launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);
+// k_long_copy: long pieces' tokens into their CSR places (after k_gather).
+void launch_long_copy(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);
 // Long-piece kernel only (token input, used by bbpe_block_bpe).
 int launch_block_bpe(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p,
                      cudaStream_t stream);

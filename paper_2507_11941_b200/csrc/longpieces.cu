@@ -26,10 +26,11 @@
 //     later segment, so a run of m-pairs continues correctly across segments.
 //   * the merged id of a pass is r2m[m] (ranks are unique per pair,
 //     merge_table.hpp:264-268), not a probe per merge (compact_into 173).
-// Working set: a piece of <= kLpCap tokens lives in the warp's slice of
-// shared memory; longer ones (64 KiB byte runs, huge rows under the block
-// engine) in the global scratch lpx/lpy (L2-resident), same code through
-// generic pointers.
+// Working set: a piece of <= kLpSmemBytes / record size tokens lives in the
+// warp's slice of shared memory; for longer ones (64 KiB byte runs, long
+// rows under the block engine) the positions move to the global scratch
+// (L2-resident) and, beyond ~64K positions, the metadata too: same code
+// through generic pointers.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -278,21 +279,23 @@ __device__ void run_piece(const EncodeArgs& a, const DevTable& T, const uint32_t
   V.n = n;
   V.nseg = (n + 31) / 32;
   V.ngrp = (V.nseg + 31) / 32;
-  if (n <= lp_cap<NARROW>()) {  // shared memory
+  // Working set: positions and metadata in the warp's shared memory (n <=
+  // cap); positions in the global scratch lpy and metadata in shared memory
+  // (up to ~64K positions); both in global scratch (lpy, lpx) beyond.
+  const uint32_t meta_words = 2 * V.nseg + 2 * V.ngrp;
+  uint32_t* meta;
+  if (n <= lp_cap<NARROW>()) {
     V.P = reinterpret_cast<typename PT::T*>(smem);
-    uint32_t* meta = reinterpret_cast<uint32_t*>(smem + kLpSmemBytes);
-    V.live = meta;
-    V.smin = meta + V.nseg;
-    V.gmin = meta + 2 * V.nseg;
-    V.aff = V.gmin + V.ngrp;
-  } else {  // global scratch: positions in lpy, metadata in lpx (both n x 8 bytes at R.start)
+    meta = reinterpret_cast<uint32_t*>(smem + kLpSmemBytes);
+  } else {
     V.P = reinterpret_cast<typename PT::T*>(a.lpy + R.start);
-    uint32_t* meta = reinterpret_cast<uint32_t*>(a.lpx + R.start);
-    V.live = meta;
-    V.smin = meta + V.nseg;
-    V.gmin = meta + 2 * V.nseg;
-    V.aff = V.gmin + V.ngrp;
+    meta = meta_words * 4 <= uint32_t(kLpSmemBytes) ? reinterpret_cast<uint32_t*>(smem)
+                                                    : reinterpret_cast<uint32_t*>(a.lpx + R.start);
   }
+  V.live = meta;
+  V.smin = meta + V.nseg;
+  V.gmin = meta + 2 * V.nseg;
+  V.aff = V.gmin + V.ngrp;
   // Initial tokens (bytes_to_initial_tokens, pretokenize.hpp:60-71) or the
   // caller's tokens (bbpe_block_bpe: lpx holds them, read before lpx is
   // reused for metadata), every pair pending except the last.
@@ -360,7 +363,7 @@ __device__ void run_piece(const EncodeArgs& a, const DevTable& T, const uint32_t
 
 // Persistent: each warp takes long pieces from the list by ticket.
 template <bool NARROW>
-__global__ void __launch_bounds__(kLpWarps * 32) k_long_pieces(EncodeArgs a, DevTable T) {
+__global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_lp[];
   const uint32_t count = static_cast<uint32_t>(min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap));
@@ -378,7 +381,61 @@ __global__ void __launch_bounds__(kLpWarps * 32) k_long_pieces(EncodeArgs a, Dev
   }
 }
 
+// k_long_copy: warp per long piece (by ticket; a piece's tokens are written
+// with 8 independent loads in flight per lane). The last warp to finish
+// resets the counters k_gather left for it.
+__global__ void __launch_bounds__(256, 4) k_long_copy(EncodeArgs a, DevTable T) {
+  const uint32_t nrec = static_cast<uint32_t>(min((uint64_t)a.counters[CNT_LREC], a.lp_cap));
+  if (a.counters[CNT_LREC] == 0) return;  // nothing to copy, nothing to reset
+  __shared__ uint32_t s_lut[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t* d2id = T.d2id;
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(&a.counters[CNT_LCOPY], 1u);
+    r = __shfl_sync(kFullMask, r, 0);
+    if (r >= nrec) break;
+    const LongRec R = a.lrec[r];
+    const uint32_t* src = a.lpo + R.start;
+    const bool unchanged = (__ldcg(src) & kUnchangedFlag) != 0;
+    uint32_t* dst = a.out_ids + R.out;
+    const uint32_t cnt = R.count;
+    constexpr int U = 8;
+    for (uint32_t i0 = 0; i0 < cnt; i0 += 32 * U) {
+      uint32_t v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + 32 * u + lane;
+        v[u] = i < cnt ? (unchanged ? s_lut[__ldg(a.bytes + R.start + i)] : __ldcs(src + 1 + i)) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = i0 + 32 * u + lane;
+        if (i < cnt) dst[i] = d2id ? __ldg(d2id + v[u]) : v[u];
+      }
+    }
+  }
+  // Last warp out resets the counters (the next encode starts from zero).
+  uint32_t done = 0;
+  if (lane == 0) {
+    __threadfence();
+    done = atomicAdd(&a.counters[CNT_LDONE], 1u);
+  }
+  done = __shfl_sync(kFullMask, done, 0);
+  if (done == gridDim.x * (blockDim.x / 32) - 1 && lane == 0) {
+    a.counters[CNT_LREC] = 0;
+    a.counters[CNT_LCOPY] = 0;
+    a.counters[CNT_LDONE] = 0;
+  }
+}
+
 }  // namespace
+
+void launch_long_copy(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream) {
+  k_long_copy<<<grid, 256, 0, stream>>>(a, t);
+}
 
 size_t long_pieces_smem(bool narrow) {
   return size_t(kLpWarps) * (narrow ? lp_warp_bytes<true>() : lp_warp_bytes<false>());
