@@ -159,7 +159,9 @@ class Workload:
         self.tokens = tokens
         self.merges = merges
         corpus = open(os.path.join(GOLDEN, "corpus.txt"), "rb").read() if args.text == "corpus" else None
-        self.gen = WX.make_gen(args.text, tokens, corpus)
+        # the trained table's text is the GPT-2 Zipf text it was trained on (other seed)
+        words_from = WT.gpt2_table()[0] if (args.config == 4 and args.table == "trained") else tokens
+        self.gen = WX.make_gen(args.text, words_from, corpus)
         self.rank, self.world = rank, world
 
     def rows(self, bounds=None):

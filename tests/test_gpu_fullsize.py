@@ -84,6 +84,21 @@ def test_cfg4_full_size_wordlevel_tables(merges, tmp_path):
     _check(ref, table, data, off)
 
 
+@pytest.mark.parametrize("merges", [128000, 200000])
+def test_cfg4_full_size_trained_tables(merges, tmp_path):
+    """SURVEY §8d's cfg4 table: GPT-2 continued by BPE training without
+    pre-tokenization (cross-word merges: rows become long pieces)."""
+    from workloads import tables as WT, text as WX, train
+    tokens, m, _ = train.trained_table(*WT.gpt2_table(), merges)
+    path = WT.write_canonical(str(tmp_path / "t.json"), tokens, m)
+    table = bb.load_merge_table_files(path, None, "json")
+    ref = Reference.load_files(path, None, canonical=True)
+    data, off, _ = WX.config_rows(WX.TextGen(WX.word_list(WT.gpt2_table()[0])), 4)
+    assert off.size - 1 == 65536
+    par, st = _check(ref, table, data, off)
+    assert st["long_pieces"] > 0
+
+
 def test_cfg5_2gb_shard(gpt2, gpt2_ref, gen):
     """Shard 1 of 8 of the one 16 GB cfg5 corpus (cost-balanced bounds from the
     encoder's partitioner): ~2 GB, bit-exact on every row."""

@@ -131,3 +131,46 @@ def test_extended_large_tables(gpt2):
     assert info["junction_bigrams"] < 3000
     t2, _ = extend_table(gpt2, 200000)
     assert np.array_equal(t2.export()[3], m4)  # deterministic
+
+
+@pytest.fixture(scope="module")
+def trained200k(tmp_path_factory):
+    """GPT-2 continued by BPE training without
+    pre-tokenization (workloads/train.py)."""
+    from workloads import tables as WT, train
+    toks, merges, how = train.trained_table(*WT.gpt2_table(), 200000)
+    path = WT.write_canonical(str(tmp_path_factory.mktemp("tr") / "t.json"), toks, merges)
+    return toks, merges, path
+
+
+def test_trained_cfg4_table(trained200k):
+    toks, merges, path = trained200k
+    t = bb.load_merge_table_files(path, None, "json")
+    info = t.info()
+    assert info["merge_count"] == 200000
+    # cross-word merges add junctions GPT-2 lacks (letter|punctuation, space), so
+    # pieces span words (GPT-2 alone: 2,689 junction bigrams)
+    assert info["junction_bigrams"] > 2689 + 200
+    assert any(toks[m[3]].count(b" ") >= 2 for m in merges[50000:50100])
+    for r, l, rr, m in merges[::997]:
+        assert toks[m] == toks[l] + toks[rr]
+
+
+def test_trained_cfg4_table_oracles_agree(trained200k):
+    """The C restatement's block engine equals the compiled reference's
+    encode_batch on rows of the cfg4 text under the trained table."""
+    from oracle.oracle import CRestatement, Reference
+    from workloads import text as WX
+    toks, merges, path = trained200k
+    if not Reference.available():
+        pytest.skip("oracle/_ref not built")
+    ref = Reference.load_files(path, None, canonical=True)
+    data, off, _ = WX.config_rows(WX.TextGen(WX.word_list(toks)), 4, scale=1 / 2048)
+    ri, ro = ref.encode_batch(data, off, workers=os.cpu_count() or 1)
+    t = bb.load_merge_table_files(path, None, "json")
+    _, _, _, m4 = t.export()
+    orc = CRestatement(m4, [t.byte_token(b) for b in range(256)])
+    ci, co = orc.encode_packed(data, off)
+    assert np.array_equal(ro, co) and np.array_equal(ri, ci)
+    # cross-word merges: far fewer tokens per byte than GPT-2 alone
+    assert int(ro[-1]) < int(off[-1]) / 6
