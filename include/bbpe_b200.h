@@ -292,6 +292,27 @@ int bbpe_block_bpe(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* tokens, s
                    uint32_t* out, size_t* out_n, uint64_t* trace, size_t trace_cap,
                    size_t* n_passes);
 
+/* ---- spec-level operations (block_engine.hpp:189-256) on the device ----
+ * A per-phase replay of one block_bpe pass, with the reference's contract
+ * checks: BBPE_CONTRACT (ContractViolation) with the reference's messages.
+ * Host buffers in and out; each call runs its kernels on the ctx's device.
+ *   bbpe_pair_ranks      <- pair_ranks (189-199): ranks[i] = rank of
+ *                           (tokens[i], tokens[i+1]) or 0xFFFFFFFF, n-1 entries
+ *   bbpe_min_rank_reduce <- min_rank_reduce (201-206): 0xFFFFFFFF = none
+ *   bbpe_mark_merges     <- mark_merges (211-220): n flags, left-greedy
+ *   bbpe_exclusive_scan  <- exclusive_scan (223-235): flags must be 0/1 and
+ *                           never adjacent
+ *   bbpe_compact         <- compact (238-256) and compact_into (166-182):
+ *                           lengths, offsets = exclusive scan of flags, and
+ *                           every flagged pair a merge of the table */
+int bbpe_pair_ranks(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* tokens, size_t n, uint32_t* ranks);
+int bbpe_min_rank_reduce(bbpe_ctx* ctx, const uint32_t* ranks, size_t n, uint32_t* out);
+int bbpe_mark_merges(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* tokens, size_t n, uint32_t min_rank,
+                     uint8_t* flags);
+int bbpe_exclusive_scan(bbpe_ctx* ctx, const uint8_t* flags, size_t n, uint32_t* offsets);
+int bbpe_compact(bbpe_ctx* ctx, const bbpe_table* t, const uint32_t* tokens, size_t n, const uint8_t* flags,
+                 size_t n_flags, const uint32_t* offsets, size_t n_offsets, uint32_t* out, size_t* out_n);
+
 /* ---- multi-GPU ---- */
 /* Splits rows [0, n) into `parts` contiguous shards with near-equal cost,
  * cost(row) = len + 64 (bytes plus a per-row overhead). bounds gets parts+1

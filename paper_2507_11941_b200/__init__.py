@@ -11,5 +11,6 @@ from .api import (  # noqa: F401
     encode_batch, encode_batch_csr, encode_sharded, gather_csr, encode_single, load_merge_table_files, pack_rows,
     parse_vocab_format, partition, read_batch_binary, read_jsonl_token_seqs, split_specials,
     validate_specials, write_batch_binary, write_batch_jsonl,
+    pair_ranks, min_rank_reduce, mark_merges, exclusive_scan, compact, block_bpe_replay,
 )
 from ._lib import LIB_PATH  # noqa: F401

@@ -109,6 +109,12 @@ SIGNATURES = {
     "bbpe_ctx_piece_stats": (C.c_int, [C.c_void_p, u64p, C.c_int]),
     "bbpe_block_bpe": (C.c_int, [C.c_void_p, C.c_void_p, u32p, C.c_size_t, u32p, C.POINTER(C.c_size_t),
                                  u64p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "bbpe_pair_ranks": (C.c_int, [C.c_void_p, C.c_void_p, u32p, C.c_size_t, u32p]),
+    "bbpe_min_rank_reduce": (C.c_int, [C.c_void_p, u32p, C.c_size_t, u32p]),
+    "bbpe_mark_merges": (C.c_int, [C.c_void_p, C.c_void_p, u32p, C.c_size_t, C.c_uint32, u8p]),
+    "bbpe_exclusive_scan": (C.c_int, [C.c_void_p, u8p, C.c_size_t, u32p]),
+    "bbpe_compact": (C.c_int, [C.c_void_p, C.c_void_p, u32p, C.c_size_t, u8p, C.c_size_t, u32p, C.c_size_t, u32p,
+                               C.POINTER(C.c_size_t)]),
     "bbpe_partition": (C.c_int, [u64p, C.c_size_t, C.c_int, u64p]),
     "bbpe_encode_sharded": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_void_p, u8p, u64p, C.c_size_t,
                                       u32p, C.c_uint64, u64p, C.POINTER(Stats)]),

@@ -690,17 +690,21 @@ def gather_csr(ids, offsets, dst: int = 0, group=None):
     return out_ids, out_off
 
 
-def encode_sharded(encoders: Sequence[Encoder], table: MergeTable, data: np.ndarray, offsets: np.ndarray):
+def encode_sharded(encoders: Sequence[Encoder], table: MergeTable, data: np.ndarray, offsets: np.ndarray,
+                   capacity: Optional[int] = None):
+    """Rows split into cost-balanced contiguous shards (bbpe_partition), one
+    per encoder/GPU, each on its own host thread near its GPU; CSR stitched.
+    `capacity`: output ids to allocate (default: input bytes, the upper bound)."""
     data = np.ascontiguousarray(data, dtype=np.uint8)
     offsets = np.ascontiguousarray(offsets, dtype=np.uint64)
     n = offsets.size - 1
-    total = int(offsets[-1] - offsets[0])
+    total = int(offsets[-1] - offsets[0]) if capacity is None else int(capacity)
     out = np.empty(max(total, 1), np.uint32)
     oo = np.empty(n + 1, np.uint64)
     hs = (C.c_void_p * len(encoders))(*[e.handle for e in encoders])
     st = Stats()
     _check(LIB.bbpe_encode_sharded(hs, len(encoders), table.handle, _p(data, C.c_uint8) if data.size else None,
-                                   _p(offsets, C.c_uint64), n, _p(out, C.c_uint32), out.size, _p(oo, C.c_uint64),
+                                   _p(offsets, C.c_uint64), n, _p(out, C.c_uint32), total, _p(oo, C.c_uint64),
                                    C.byref(st)))
     return out[: int(oo[-1])], oo, st.as_dict()
 
@@ -926,6 +930,86 @@ def block_bpe(tokens: Sequence[int], table: MergeTable, config: BlockConfig, enc
         trace.extend(tr)
         return res
     return enc.block_bpe(table, tokens)
+
+
+# ---- spec-level operations (block_engine.hpp:189-256), run on the device ----
+
+def _u32(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.uint32).reshape(-1))
+
+
+def pair_ranks(tokens: Sequence[int], table: MergeTable, encoder: Optional[Encoder] = None) -> List[Optional[int]]:
+    """block_engine.hpp:189-199: rank of each adjacent pair, None if absent."""
+    enc = encoder or default_encoder()
+    t = _u32(tokens)
+    if t.size < 2:
+        return []
+    out = np.zeros(t.size - 1, np.uint32)
+    _check(LIB.bbpe_pair_ranks(enc.handle, table.handle, _p(t, C.c_uint32), t.size, _p(out, C.c_uint32)))
+    return [None if int(r) == NO_RANK else int(r) for r in out]
+
+
+def min_rank_reduce(ranks: Sequence[Optional[int]], encoder: Optional[Encoder] = None) -> Optional[int]:
+    """block_engine.hpp:201-206."""
+    enc = encoder or default_encoder()
+    r = _u32([NO_RANK if x is None else x for x in ranks])
+    out = C.c_uint32(0)
+    _check(LIB.bbpe_min_rank_reduce(enc.handle, _p(r, C.c_uint32) if r.size else None, r.size, C.byref(out)))
+    return None if out.value == NO_RANK else out.value
+
+
+def mark_merges(tokens: Sequence[int], table: MergeTable, min_rank: int, encoder: Optional[Encoder] = None) -> List[int]:
+    """block_engine.hpp:211-220: flags[i+1] = 1 for left-greedy rank-min pairs."""
+    enc = encoder or default_encoder()
+    t = _u32(tokens)
+    f = np.zeros(max(t.size, 1), np.uint8)
+    _check(LIB.bbpe_mark_merges(enc.handle, table.handle, _p(t, C.c_uint32) if t.size else None, t.size,
+                                int(min_rank), _p(f, C.c_uint8)))
+    return f[: t.size].tolist()
+
+
+def exclusive_scan(flags: Sequence[int], encoder: Optional[Encoder] = None) -> List[int]:
+    """block_engine.hpp:223-235 (ContractViolation on values > 1 or adjacent flags)."""
+    enc = encoder or default_encoder()
+    f = np.ascontiguousarray(np.asarray(flags, dtype=np.uint8).reshape(-1))
+    out = np.zeros(max(f.size, 1), np.uint32)
+    _check(LIB.bbpe_exclusive_scan(enc.handle, _p(f, C.c_uint8) if f.size else None, f.size, _p(out, C.c_uint32)))
+    return out[: f.size].tolist()
+
+
+def compact(tokens: Sequence[int], table: MergeTable, flags: Sequence[int], offsets: Sequence[int],
+            encoder: Optional[Encoder] = None) -> List[int]:
+    """block_engine.hpp:238-256 + compact_into 166-182 (ContractViolation on
+    length/offset mismatch or a flagged pair that is not a merge)."""
+    enc = encoder or default_encoder()
+    t = _u32(tokens)
+    f = np.ascontiguousarray(np.asarray(flags, dtype=np.uint8).reshape(-1))
+    o = _u32(offsets)
+    out = np.zeros(max(t.size, 1), np.uint32)
+    n_out = C.c_size_t(0)
+    _check(LIB.bbpe_compact(enc.handle, table.handle, _p(t, C.c_uint32) if t.size else None, t.size,
+                            _p(f, C.c_uint8) if f.size else None, f.size, _p(o, C.c_uint32) if o.size else None,
+                            o.size, _p(out, C.c_uint32), C.byref(n_out)))
+    return out[: n_out.value].tolist()
+
+
+def block_bpe_replay(tokens: Sequence[int], table: MergeTable, encoder: Optional[Encoder] = None,
+                     trace: Optional[list] = None) -> List[int]:
+    """block_bpe (block_engine.hpp:268-310) driven pass by pass through the
+    device spec ops above: the per-phase debug replay of the engine."""
+    t = [int(x) for x in tokens]
+    npass = 0
+    while len(t) >= 2:
+        m = min_rank_reduce(pair_ranks(t, table, encoder), encoder)
+        if m is None:
+            break
+        f = mark_merges(t, table, m, encoder)
+        off = exclusive_scan(f, encoder)
+        t = compact(t, table, f, off, encoder)
+        npass += 1
+        if trace is not None:
+            trace.append((npass, m, int(sum(f))))
+    return t
 
 
 def decode(table: MergeTable, specials: SpecialTokenSet, ids: Sequence[int]) -> bytes:

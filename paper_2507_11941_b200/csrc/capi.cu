@@ -7,8 +7,11 @@
 // encoded on the device into CSR, and errors raised on the device (invalid byte,
 // pass cap) are re-materialised on the host with the reference's messages.
 #include <cuda_runtime.h>
+#include <pthread.h>
+#include <sched.h>
 
 #include <algorithm>
+#include <cctype>
 #include <array>
 #include <atomic>
 #include <chrono>
@@ -1922,6 +1925,217 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   BBPE_CATCH
 }
 
+// ---- spec-level operations (block_engine.hpp:189-256) on the device ----
+}  // extern "C"
+
+namespace {
+// Pins the calling thread to the CPUs local to `device` (sysfs local_cpulist
+// of its PCI function), so pinned staging it allocates and the copies it
+// drives stay on the GPU's NUMA node. Best effort: silently does nothing when
+// the topology is unavailable.
+void bind_thread_near_device(int device) {
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return;
+  std::string id(bus);
+  for (auto& ch : id) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+  FILE* f = std::fopen(("/sys/bus/pci/devices/" + id + "/local_cpulist").c_str(), "r");
+  if (!f) return;
+  char buf[4096] = {0};
+  const size_t k = std::fread(buf, 1, sizeof(buf) - 1, f);
+  std::fclose(f);
+  buf[k] = 0;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  int count = 0;
+  for (char* p = buf; *p && *p != '\n';) {
+    char* e = nullptr;
+    long a = std::strtol(p, &e, 10), b = a;
+    if (e == p) break;
+    if (*e == '-') b = std::strtol(e + 1, &e, 10);
+    for (long c = a; c <= b && c < CPU_SETSIZE; ++c, ++count) CPU_SET(int(c), &set);
+    p = (*e == ',') ? e + 1 : e;
+  }
+  if (count) pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
+}
+
+// dst[0, n) = src[0, n) by `threads` threads (the ranges must not overlap).
+void parallel_copy(uint32_t* dst, const uint32_t* src, uint64_t n, int threads) {
+  const uint64_t per = (n + threads - 1) / threads;
+  if (threads <= 1 || n < (1u << 18)) {
+    std::memcpy(dst, src, n * 4);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int k = 0; k < threads; ++k) {
+    const uint64_t a = k * per, b = std::min<uint64_t>(n, a + per);
+    if (a >= b) break;
+    th.emplace_back([=] { std::memcpy(dst + a, src + a, (b - a) * 4); });
+  }
+  for (auto& x : th) x.join();
+}
+
+// Caller ids -> dense device ids; ids the table never mentions become one
+// placeholder that no merge mentions (as in bbpe_block_bpe).
+std::vector<uint32_t> spec_dense(const bbpe_table* t, const uint32_t* tokens, size_t n) {
+  std::vector<uint32_t> d(n);
+  const uint32_t P = t->remap ? static_cast<uint32_t>(t->dense_to_id.size()) : t->max_dev_id + 1;
+  for (size_t i = 0; i < n; ++i) {
+    uint32_t x = t->dense(tokens[i]);
+    if ((t->remap && x == bbpe::kInvalidToken) || (!t->remap && tokens[i] > t->max_dev_id)) x = P;
+    d[i] = x;
+  }
+  return d;
+}
+
+// Scoped device allocation for the spec ops (test/debug surface).
+struct SpecBuf {
+  void* p = nullptr;
+  explicit SpecBuf(size_t bytes) { ck(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "cudaMalloc (spec op)"); }
+  ~SpecBuf() { cudaFree(p); }
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+void spec_ranks_device(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, size_t n, const SpecBuf& dtok,
+                       const SpecBuf& ranks) {
+  const bbpe::DevTable& dt = bbpe::table_on_device(*t, c->device);
+  const std::vector<uint32_t> d = spec_dense(t, tokens, n);
+  ck(cudaMemcpyAsync(dtok.p, d.data(), n * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  bbpe::launch_spec_ranks(dtok.as<uint32_t>(), n, dt, ranks.as<uint32_t>(), c->stream);
+  c->launches += 1;
+  ck(cudaGetLastError(), "launch");
+}
+}  // namespace
+
+extern "C" {
+
+int bbpe_pair_ranks(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, size_t n, uint32_t* ranks) {
+  BBPE_TRY
+  if (!c || !t || (n && !tokens) || (n > 1 && !ranks)) throw bbpe::usage_error("null argument");
+  if (n < 2) return BBPE_OK;
+  DeviceGuard g(c->device);
+  SpecBuf dtok(n * 4), dr(n * 4);
+  spec_ranks_device(c, t, tokens, n, dtok, dr);
+  ck(cudaMemcpyAsync(ranks, dr.p, (n - 1) * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "pair_ranks");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_min_rank_reduce(bbpe_ctx* c, const uint32_t* ranks, size_t n, uint32_t* out) {
+  BBPE_TRY
+  if (!c || !out || (n && !ranks)) throw bbpe::usage_error("null argument");
+  *out = bbpe::kNoRank;
+  if (!n) return BBPE_OK;
+  DeviceGuard g(c->device);
+  SpecBuf dr(n * 4), dm(4);
+  ck(cudaMemcpyAsync(dr.p, ranks, n * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemsetAsync(dm.p, 0xFF, 4, c->stream), "memset");
+  bbpe::launch_spec_min(dr.as<uint32_t>(), n, dm.as<uint32_t>(), c->stream);
+  c->launches += 1;
+  ck(cudaGetLastError(), "launch");
+  ck(cudaMemcpyAsync(out, dm.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "min_rank_reduce");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_mark_merges(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, size_t n, uint32_t min_rank,
+                     uint8_t* flags) {
+  BBPE_TRY
+  if (!c || !t || (n && (!tokens || !flags))) throw bbpe::usage_error("null argument");
+  if (!n) return BBPE_OK;
+  DeviceGuard g(c->device);
+  SpecBuf dtok(n * 4), dr(n * 4), df(n);
+  ck(cudaMemsetAsync(df.p, 0, n, c->stream), "memset");
+  if (n >= 2) {
+    spec_ranks_device(c, t, tokens, n, dtok, dr);
+    bbpe::launch_spec_runs(dr.as<uint32_t>(), n, min_rank, df.as<uint8_t>(), c->stream);
+    c->launches += 1;
+    ck(cudaGetLastError(), "launch");
+  }
+  ck(cudaMemcpyAsync(flags, df.p, n, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "mark_merges");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_exclusive_scan(bbpe_ctx* c, const uint8_t* flags, size_t n, uint32_t* offsets) {
+  BBPE_TRY
+  if (!c || (n && (!flags || !offsets))) throw bbpe::usage_error("null argument");
+  if (!n) return BBPE_OK;
+  DeviceGuard g(c->device);
+  SpecBuf df(n), doff(n * 4), derr(8), dtot(4);
+  ck(cudaMemcpyAsync(df.p, flags, n, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemsetAsync(derr.p, 0xFF, 8, c->stream), "memset");
+  bbpe::launch_spec_check(df.as<uint8_t>(), n, derr.as<unsigned long long>(), c->stream);
+  bbpe::launch_spec_scan(df.as<uint8_t>(), n, doff.as<uint32_t>(), dtot.as<uint32_t>(), c->stream);
+  c->launches += 2;
+  ck(cudaGetLastError(), "launch");
+  uint64_t err = 0;
+  ck(cudaMemcpyAsync(&err, derr.p, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "exclusive_scan");
+  if (err != ~0ull) {  // block_engine.hpp:225-231, lowest failing index first
+    const uint64_t i = err >> 1;
+    if ((err & 1) == 0)
+      return fail(BBPE_CONTRACT, "merge flags must be 0/1, got " + std::to_string(int(flags[i])) + " at index " +
+                                     std::to_string(i));
+    return fail(BBPE_CONTRACT, "adjacent merge flags at indices " + std::to_string(i - 1) + " and " +
+                                   std::to_string(i) + " are both set; left-greedy marking forbids this");
+  }
+  ck(cudaMemcpy(offsets, doff.p, n * 4, cudaMemcpyDeviceToHost), "D2H");
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
+int bbpe_compact(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, size_t n, const uint8_t* flags,
+                 size_t n_flags, const uint32_t* offsets, size_t n_offsets, uint32_t* out, size_t* out_n) {
+  BBPE_TRY
+  if (!c || !t || !out_n || (n && !tokens) || (n_flags && !flags) || (n_offsets && !offsets) || (n && !out))
+    throw bbpe::usage_error("null argument");
+  *out_n = 0;
+  if (n_flags != n || n_offsets != n)  // block_engine.hpp:242-243
+    return fail(BBPE_CONTRACT, "flags/offsets length does not match token count");
+  if (!n) return BBPE_OK;
+  DeviceGuard g(c->device);
+  const bbpe::DevTable& dt = bbpe::table_on_device(*t, c->device);
+  const std::vector<uint32_t> d = spec_dense(t, tokens, n);
+  SpecBuf dtok(n * 4), dorig(n * 4), df(n), doff(n * 4), dscan(n * 4), dtot(4), derr(16), dout(n * 4);
+  ck(cudaMemcpyAsync(dtok.p, d.data(), n * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemcpyAsync(dorig.p, tokens, n * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemcpyAsync(df.p, flags, n, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemcpyAsync(doff.p, offsets, n * 4, cudaMemcpyHostToDevice, c->stream), "H2D");
+  ck(cudaMemsetAsync(derr.p, 0xFF, 16, c->stream), "memset");
+  unsigned long long* e = derr.as<unsigned long long>();
+  // offsets must be the exclusive scan of flags (244-249)
+  bbpe::launch_spec_scan(df.as<uint8_t>(), n, dscan.as<uint32_t>(), dtot.as<uint32_t>(), c->stream);
+  bbpe::launch_spec_check_offsets(doff.as<uint32_t>(), dscan.as<uint32_t>(), n, e, c->stream);
+  ck(cudaGetLastError(), "launch");
+  uint64_t err[2];
+  uint32_t total = 0;
+  ck(cudaMemcpyAsync(err, e, 16, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaMemcpyAsync(&total, dtot.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "compact");
+  c->launches += 2;
+  if (err[0] != ~0ull)
+    return fail(BBPE_CONTRACT, "offsets are not the exclusive scan of flags at index " + std::to_string(err[0]));
+  // compact_into (166-182): a flagged pair that is not a merge is a ContractViolation
+  bbpe::launch_spec_compact(dtok.as<uint32_t>(), dorig.as<uint32_t>(), df.as<uint8_t>(), doff.as<uint32_t>(), n, dt,
+                            dout.as<uint32_t>(), e + 1, c->stream);
+  c->launches += 1;
+  ck(cudaGetLastError(), "launch");
+  ck(cudaMemcpyAsync(err + 1, e + 1, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+  ck(cudaStreamSynchronize(c->stream), "compact");
+  if (err[1] != ~0ull)
+    return fail(BBPE_CONTRACT, "flags mark a pair that is not in the merge table at index " + std::to_string(err[1]));
+  if (total > n) return fail(BBPE_CONTRACT, "merge flags exceed the token count");
+  const size_t m = n - total;
+  ck(cudaMemcpy(out, dout.p, m * 4, cudaMemcpyDeviceToHost), "D2H");
+  *out_n = m;
+  return BBPE_OK;
+  BBPE_CATCH
+}
+
 int bbpe_partition(const uint64_t* offsets, size_t n, int parts, uint64_t* bounds) {
   BBPE_TRY
   if (!offsets || !bounds || parts < 1) throw bbpe::usage_error("bad partition arguments");
@@ -1945,29 +2159,43 @@ int bbpe_encode_sharded(bbpe_ctx* const* ctxs, int n_devices, const bbpe_table* 
                         uint64_t out_capacity, uint64_t* out_offsets, bbpe_stats* st) {
   BBPE_TRY
   if (!ctxs || n_devices < 1 || !t || !offsets || !out_offsets) throw bbpe::usage_error("null argument");
+  for (int d = 0; d < n_devices; ++d)
+    if (!ctxs[d]) throw bbpe::usage_error("null ctx");
   auto t0 = std::chrono::steady_clock::now();
   std::vector<uint64_t> bounds(n_devices + 1);
   bbpe_partition(offsets, n, n_devices, bounds.data());
-  // Shard k writes at its byte-based upper-bound position, then shards are
-  // packed in order (tokens <= bytes per shard, so regions never overlap).
+  const uint64_t base = offsets[0], total_bytes = offsets[n] - base;
+  // Output regions: shard d writes its ids at at[d], a share of the caller's
+  // capacity proportional to its bytes (tokens <= bytes, so with capacity >=
+  // total bytes no region can overflow; with less, a shard that overflows its
+  // region is re-encoded into a host vector and copied in the stitch).
+  std::vector<uint64_t> at(n_devices + 1);
+  for (int d = 0; d <= n_devices; ++d) {
+    const uint64_t b = offsets[bounds[d]] - base;
+    at[d] = out_capacity >= total_bytes
+                ? b
+                : uint64_t((unsigned __int128)out_capacity * b / std::max<uint64_t>(total_bytes, 1));
+  }
   std::vector<uint64_t> ntok(n_devices, 0);
   std::vector<std::vector<uint64_t>> offs(n_devices);
+  std::vector<std::vector<uint32_t>> spill(n_devices);  // shards that overflowed their region
   std::vector<int> codes(n_devices, BBPE_OK);
   std::vector<std::string> msgs(n_devices);
   std::vector<bbpe_stats> stats(n_devices);
   std::vector<std::thread> th;
-  const uint64_t base = offsets[0];
-  if (out_capacity < offsets[n] - base && offsets[n] > base) {
-    // The staging layout needs the byte-sized upper bound.
-    throw bbpe::usage_error("bbpe_encode_sharded needs out_capacity >= total input bytes");
-  }
   for (int d = 0; d < n_devices; ++d) {
     th.emplace_back([&, d] {
+      bind_thread_near_device(ctxs[d]->device);  // host staging and copies on the GPU's NUMA node
       const uint64_t r0 = bounds[d], r1 = bounds[d + 1];
       offs[d].resize(r1 - r0 + 1);
-      const uint64_t at = offsets[r0] - base;
-      int rc = bbpe_encode(ctxs[d], t, bytes, offsets + r0, r1 - r0, out_ids + at,
-                           out_capacity - at, offs[d].data(), &stats[d]);
+      const uint64_t cap = at[d + 1] - at[d];
+      int rc = bbpe_encode(ctxs[d], t, bytes, offsets + r0, r1 - r0, out_ids ? out_ids + at[d] : nullptr, cap,
+                           offs[d].data(), &stats[d]);
+      if (rc == BBPE_USAGE && cap < offsets[r1] - offsets[r0]) {  // region too small: host vector
+        spill[d].resize(std::max<uint64_t>(offsets[r1] - offsets[r0], 1));
+        rc = bbpe_encode(ctxs[d], t, bytes, offsets + r0, r1 - r0, spill[d].data(), spill[d].size(),
+                         offs[d].data(), &stats[d]);
+      }
       codes[d] = rc;
       if (rc != BBPE_OK) msgs[d] = bbpe_last_error();
       ntok[d] = offs[d].back();
@@ -1985,19 +2213,49 @@ int bbpe_encode_sharded(bbpe_ctx* const* ctxs, int n_devices, const bbpe_table* 
       }
       return fail(codes[d], m);
     }
-  uint64_t pos = 0;
+  std::vector<uint64_t> pos(n_devices + 1, 0);
+  for (int d = 0; d < n_devices; ++d) pos[d + 1] = pos[d] + ntok[d];
+  if (pos[n_devices] > out_capacity)
+    throw bbpe::usage_error("output capacity " + std::to_string(out_capacity) + " is smaller than the " +
+                            std::to_string(pos[n_devices]) + " tokens of the batch");
+  // Stitch. Shards move left in shard order (shard d's destination can only
+  // overlap sources of shards < d, already moved); each move is copied by
+  // several threads in waves no longer than its shift, so no wave writes a
+  // source another thread of the wave still reads.
+  // With a spilled shard, later regions may start before their destination:
+  // every shard then goes through a host vector.
+  const int hw = std::max(1, std::min<int>(16, int(std::thread::hardware_concurrency())));
+  bool any_spill = false;
+  for (int d = 0; d < n_devices; ++d) any_spill |= !spill[d].empty();
+  if (any_spill) {
+    for (int d = 0; d < n_devices; ++d)
+      if (spill[d].empty() && ntok[d]) spill[d].assign(out_ids + at[d], out_ids + at[d] + ntok[d]);
+    for (int d = 0; d < n_devices; ++d)
+      if (ntok[d]) parallel_copy(out_ids + pos[d], spill[d].data(), ntok[d], hw);
+  }
+  for (int d = 0; d < n_devices && !any_spill; ++d) {
+    if (!ntok[d]) continue;
+    uint32_t* dst = out_ids + pos[d];
+    const uint32_t* src = out_ids + at[d];
+    if (src == dst) continue;
+    const uint64_t shift = uint64_t(src - dst);  // pos <= at: every shard before d fits its region
+    const uint64_t wave = std::min<uint64_t>(shift, ntok[d]);
+    if (wave < (1u << 20)) {
+      std::memmove(dst, src, ntok[d] * 4);
+      continue;
+    }
+    for (uint64_t w = 0; w < ntok[d]; w += wave)
+      parallel_copy(dst + w, src + w, std::min<uint64_t>(wave, ntok[d] - w), hw);
+  }
   for (int d = 0; d < n_devices; ++d) {
     const uint64_t r0 = bounds[d], r1 = bounds[d + 1];
-    const uint64_t at = offsets[r0] - base;
-    if (at != pos && ntok[d]) std::memmove(out_ids + pos, out_ids + at, ntok[d] * 4);
-    for (uint64_t i = 0; i <= r1 - r0; ++i) out_offsets[r0 + i] = pos + offs[d][i];
-    pos += ntok[d];
+    for (uint64_t i = 0; i <= r1 - r0; ++i) out_offsets[r0 + i] = pos[d] + offs[d][i];
   }
   if (st) {
     *st = bbpe_stats{};
     st->n_rows = n;
-    st->input_bytes = offsets[n] - base;
-    st->tokens = pos;
+    st->input_bytes = total_bytes;
+    st->tokens = pos[n_devices];
     for (auto& s : stats) {
       st->device_ms = std::max(st->device_ms, s.device_ms);
       st->waves += s.waves;

@@ -158,6 +158,16 @@ void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t
 size_t long_pieces_smem(bool narrow);
 int long_pieces_grid(int device, int sm_count);
 void launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);
+// Spec-level ops (specops.cu): per-phase replay of one block_bpe pass.
+void launch_spec_ranks(const uint32_t* tok, uint64_t n, const DevTable& t, uint32_t* ranks, cudaStream_t s);
+void launch_spec_min(const uint32_t* ranks, uint64_t n, uint32_t* out, cudaStream_t s);
+void launch_spec_runs(const uint32_t* ranks, uint64_t n, uint32_t m, uint8_t* flags, cudaStream_t s);
+void launch_spec_check(const uint8_t* flags, uint64_t n, unsigned long long* err, cudaStream_t s);
+void launch_spec_scan(const uint8_t* flags, uint64_t n, uint32_t* offsets, uint32_t* total, cudaStream_t s);
+void launch_spec_check_offsets(const uint32_t* offsets, const uint32_t* scan, uint64_t n, unsigned long long* err,
+                               cudaStream_t s);
+void launch_spec_compact(const uint32_t* dtok, const uint32_t* orig, const uint8_t* flags, const uint32_t* offsets,
+                         uint64_t n, const DevTable& t, uint32_t* out, unsigned long long* err, cudaStream_t s);
 // k_long_copy: long pieces' tokens into their CSR places (after k_gather).
 void launch_long_copy(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);
 // Long-piece kernel only (token input, used by bbpe_block_bpe).

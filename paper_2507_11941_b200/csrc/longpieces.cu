@@ -215,19 +215,28 @@ __device__ uint32_t merge_pass(const Piece<NARROW>& V, uint32_t m, uint32_t M, i
         const uint32_t p = 32 * s + lane;
         typename PT::T e = p < V.n ? V.P[p] : typename PT::T(0);
         const uint32_t L = V.live[s];
-        const unsigned Mb = __ballot_sync(kFullMask, ((L >> lane) & 1u) && PT::rank(e) == m);
-        // Left-greedy in live order (fill_merge_flags 103-128).
-        uint32_t merged = 0, kill = 0;
-        int64_t out_kill = -1;
-        for (unsigned mm = Mb; mm; mm &= mm - 1) {
-          const uint32_t b = __ffs(mm) - 1;
-          if ((kill >> b) & 1u) continue;  // consumed by the previous merge of the run
-          merged |= 1u << b;
-          const uint32_t nb = L & above(b);
-          if (nb) kill |= 1u << (__ffs(nb) - 1);
-          else out_kill = first_live_from(V, s + 1);  // the pair's right token is in a later segment
-        }
+        const bool lv = (L >> lane) & 1u;
+        const bool isM = lv && PT::rank(e) == m;
+        const unsigned Mb = __ballot_sync(kFullMask, isM);
+        // Left-greedy in live order (fill_merge_flags 103-128) by run parity:
+        // a run is a stretch of consecutive live lanes whose pairs have rank m;
+        // its lanes at even live offsets from the run start are marked, each
+        // consuming the next live token. A run never continues from an earlier
+        // segment: if that segment's last pair was marked, this segment's first
+        // live token is already cleared (out_kill below), otherwise the first
+        // m-pair here is at an even offset anyway.
+        const uint32_t below = L & ((1u << lane) - 1u);
+        const bool prev_m = below && ((Mb >> (31 - __clz(below))) & 1u);
+        const unsigned S = __ballot_sync(kFullMask, isM && !prev_m);  // run starts
+        const uint32_t sb = S & (lane == 31 ? ~0u : ((2u << lane) - 1u));
+        const uint32_t st = sb ? 31 - __clz(sb) : 0;
+        const bool mk = isM && !(__popc(below & ~((1u << st) - 1u)) & 1u);
+        const uint32_t merged = __ballot_sync(kFullMask, mk);
         if (!merged) continue;
+        // consumed tokens: the live successor of every marked lane
+        const uint32_t kill = __ballot_sync(kFullMask, lv && below && ((merged >> (31 - __clz(below))) & 1u));
+        const bool last_marked = (merged >> (31 - __clz(L))) & 1u;  // its right token is in a later segment
+        const int64_t out_kill = last_marked ? first_live_from(V, s + 1) : -1;
         merges += __popc(merged);
         const uint32_t Ln = L & ~kill;
         const bool me = (merged >> lane) & 1u;
@@ -361,6 +370,277 @@ __device__ void run_piece(const EncodeArgs& a, const DevTable& T, const uint32_t
   __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Super-pass engine: many consecutive passes of block_bpe per sweep, exactly.
+//
+// Let the current pairs have ranks r_i (kNoRank = none). Run the passes of
+// block_bpe (block_engine.hpp:286-307) from here, and call a token FRESH if
+// one of these passes created it. As long as no pass merges a pair with a
+// fresh token, the passes only merge current pairs, each in its own rank's
+// pass, so which current pairs merge is decided by rank order alone:
+//   * pair i merges iff it is not consumed first by a lower-ranked neighbour
+//     pair that merges, nor (equal ranks = a run of one repeated pair) by a
+//     left neighbour of the run that merges (left-greedy, fill_merge_flags
+//     103-128). Closed form: with a_i = the number of consecutive
+//     non-decreasing steps r_{i-1} <= r_i ending at i and b_i = the number of
+//     consecutive strictly decreasing steps r_{i+1} < r_i starting at i,
+//     pair i merges iff r_i != none, a_i is even and b_i is even (chains of
+//     decreasing rank alternate from their minimum; a peak merges iff both
+//     lower neighbours do not).
+// The first pass that merges a fresh token: a merge of pair i (at rank
+// tau = r_i, merged token M) creates the pairs (left token at tau, M) and
+// (M, right token at tau), whose ranks x are processed no earlier than
+// max(x, tau + 1). With C = the minimum of that over all merges, every pass
+// below C merges current pairs only, so applying all merges with r_i < C in
+// one sweep is exactly those passes (C > the global minimum rank, so every
+// super-pass makes progress). Conservative in one respect only (a fresh pair
+// that a later merge of the same sweep destroys still bounds C), which costs
+// sweeps, never exactness. Checked against block_bpe on the compiled
+// reference (tests) and on random consistent and inconsistent tables
+// (oracle/bpe_oracle.c restatement, tests/test_superpass.py).
+//
+// Layout: positions in a warp's slice of shared memory (or, for pieces
+// longer than kLpSmemBytes / 8, in the piece's global scratch): X[i] token,
+// R[i] = rk of (X[i], X[i+1]); per 32-position segment a b-parity mask and a
+// merge mask. Every super-pass is four coalesced sweeps (b parity right to
+// left, merge mask left to right, cut, in-place compaction with re-probes of
+// the pairs that changed); positions shrink to the live tokens each time.
+// Used unless a pass cap or a trace asks for pass-by-pass execution.
+
+template <bool NARROW>
+__device__ __forceinline__ uint32_t sp_merged(const DevTable& T, uint32_t rk) {
+  return NARROW ? (rk & 0xFFFFu) : __ldg(T.r2m + rk);
+}
+
+__device__ __forceinline__ uint32_t bit_at(const uint32_t* w, uint32_t i) { return (w[i >> 5] >> (i & 31)) & 1u; }
+
+template <bool NARROW>
+__device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint32_t* s_lut, uint32_t ridx,
+                             unsigned char* smem, int lane) {
+  const LongRec Rec = a.lrec[ridx];
+  const uint32_t n0 = static_cast<uint32_t>(Rec.len);
+  const uint32_t nseg0 = (n0 + 31) / 32;
+  constexpr uint32_t cap = kLpSmemBytes / 8;
+  uint32_t *X, *R, *bm, *mm;
+  if (n0 <= cap) {
+    X = reinterpret_cast<uint32_t*>(smem);
+    R = X + cap;
+    bm = R + cap;
+    mm = bm + cap / 32;
+  } else {
+    X = reinterpret_cast<uint32_t*>(a.lpx + Rec.start);
+    R = X + n0;
+    bm = reinterpret_cast<uint32_t*>(a.lpy + Rec.start);
+    mm = bm + nseg0;
+  }
+  const uint8_t* bytes = a.bytes + Rec.start;
+  constexpr int U = 4;
+  // Initial tokens (bytes_to_initial_tokens, pretokenize.hpp:60-71) and ranks
+  // (fill_pair_ranks, block_engine.hpp:72-79).
+  for (uint32_t s0 = 0; s0 < nseg0; s0 += U) {
+    uint32_t t[U];
+    ProbeReq q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = 32 * (s0 + u) + lane;
+      t[u] = i < n0 ? s_lut[bytes[i]] : 0u;
+      uint32_t nx = __shfl_down_sync(kFullMask, t[u], 1);
+      if (lane == 31 && i + 1 < n0) nx = s_lut[bytes[i + 1]];
+      if (i + 1 < n0) probe_issue<NARROW>(q[u], T, t[u], nx);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = 32 * (s0 + u) + lane;
+      if (i < n0) {
+        X[i] = t[u];
+        R[i] = i + 1 < n0 ? probe_resolve<NARROW>(q[u], T) : kNoRank;
+      }
+    }
+  }
+  __syncwarp();
+  uint32_t n = n0;
+  for (;;) {
+    const uint32_t nseg = (n + 31) / 32;
+    // Sweep 1, right to left: parity of b_i (strictly decreasing run to the right).
+    {
+      uint32_t r_next0 = kNoRank, bp_next0 = 0;
+      for (int s0 = int(nseg) - 1; s0 >= 0; s0 -= U) {
+        uint32_t r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int s = s0 - u;
+          const uint32_t i = 32 * uint32_t(s) + lane;
+          r[u] = (s >= 0 && i < n) ? R[i] : kNoRank;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int s = s0 - u;
+          if (s < 0) break;
+          uint32_t rn = __shfl_down_sync(kFullMask, r[u], 1);
+          if (lane == 31) rn = r_next0;
+          const unsigned D = __ballot_sync(kFullMask, rn < r[u]);
+          const uint32_t Z = ~D & (~0u << lane);  // non-descending steps at or above lane
+          const uint32_t bp = Z ? ((__ffs(Z) - 1 - lane) & 1u) : ((lane + bp_next0) & 1u);
+          const unsigned E = __ballot_sync(kFullMask, bp == 0);
+          if (lane == 0) bm[s] = E;
+          r_next0 = __shfl_sync(kFullMask, r[u], 0);
+          bp_next0 = __shfl_sync(kFullMask, bp, 0);
+        }
+      }
+    }
+    __syncwarp();
+    // Sweep 2, left to right: parity of a_i; merge mask; any merge at all?
+    bool any = false;
+    {
+      uint32_t r_prev = kNoRank, ap_prev = 0;
+      for (uint32_t s0 = 0; s0 < nseg; s0 += U) {
+        uint32_t r[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t s = s0 + u, i = 32 * s + lane;
+          r[u] = i < n ? R[i] : kNoRank;
+          b[u] = s < nseg ? bm[s] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t s = s0 + u;
+          if (s >= nseg) break;
+          uint32_t rp = __shfl_up_sync(kFullMask, r[u], 1);
+          if (lane == 0) rp = r_prev;
+          const unsigned Up = __ballot_sync(kFullMask, rp <= r[u]);
+          const uint32_t Z = ~Up & (lane == 31 ? ~0u : ((2u << lane) - 1u));  // breaks at or below lane
+          const uint32_t ap = Z ? ((lane - (31 - __clz(Z))) & 1u) : ((lane + 1 + ap_prev) & 1u);
+          const bool mg = r[u] != kNoRank && ap == 0 && ((b[u] >> lane) & 1u);
+          const unsigned Mm = __ballot_sync(kFullMask, mg);
+          if (lane == 0) mm[s] = Mm;
+          any |= Mm != 0;
+          r_prev = __shfl_sync(kFullMask, r[u], 31);
+          ap_prev = __shfl_sync(kFullMask, ap, 31);
+        }
+      }
+    }
+    if (!any) break;  // no pair in the table (block_engine.hpp:288-289)
+    __syncwarp();
+    // Sweep 3: the cut C.
+    uint32_t C = kNoRank;
+    for (uint32_t s = 0; s < nseg; ++s) {
+      const uint32_t Mm = mm[s];
+      if (!Mm) continue;
+      const uint32_t i = 32 * s + lane;
+      const bool mg = (Mm >> lane) & 1u;
+      const uint32_t tau = mg ? R[i] : kNoRank;
+      const bool act = mg && tau < C;  // a merge at or above the cut cannot lower it
+      ProbeReq ql, qr;
+      bool hl = false, hr = false;
+      if (act) {
+        const uint32_t M = sp_merged<NARROW>(T, tau);
+        if (i >= 1) {
+          uint32_t lt;
+          if (i >= 2 && bit_at(mm, i - 2) && R[i - 2] <= tau) lt = sp_merged<NARROW>(T, R[i - 2]);
+          else lt = X[i - 1];
+          probe_issue<NARROW>(ql, T, lt, M);
+          hl = true;
+        }
+        if (i + 2 < n) {
+          uint32_t rt;
+          if (bit_at(mm, i + 2) && R[i + 2] <= tau) rt = sp_merged<NARROW>(T, R[i + 2]);
+          else rt = X[i + 2];
+          probe_issue<NARROW>(qr, T, M, rt);
+          hr = true;
+        }
+      }
+      uint32_t c = kNoRank;
+      if (hl) {
+        const uint32_t x = probe_resolve<NARROW>(ql, T);
+        if (x != kNoRank) c = min(c, max(x, tau + 1));
+      }
+      if (hr) {
+        const uint32_t x = probe_resolve<NARROW>(qr, T);
+        if (x != kNoRank) c = min(c, max(x, tau + 1));
+      }
+      C = __reduce_min_sync(kFullMask, min(C, c));
+    }
+    // Sweep 4: apply the merges below C, compact in place, re-rank changed pairs.
+    {
+      uint32_t q0 = 0, applied_prev = 0;
+      for (uint32_t s0 = 0; s0 < nseg; s0 += U) {
+        uint32_t x[U], r[U], outv[U], nt[U], dst[U];
+        bool emit[U], probe_it[U], keep_r[U];
+        ProbeReq q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t s = s0 + u, i = 32 * s + lane;
+          emit[u] = false;
+          probe_it[u] = false;
+          keep_r[u] = false;
+          if (s >= nseg) continue;
+          x[u] = i < n ? X[i] : 0u;
+          r[u] = i < n ? R[i] : kNoRank;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t s = s0 + u, i = 32 * s + lane;
+          if (s >= nseg) break;
+          const uint32_t Mm = mm[s];
+          const bool ap = ((Mm >> lane) & 1u) && r[u] < C;
+          const unsigned A = __ballot_sync(kFullMask, ap);
+          const bool consumed = lane == 0 ? applied_prev != 0 : ((A >> (lane - 1)) & 1u);
+          const bool em = i < n && !consumed;
+          const unsigned Em = __ballot_sync(kFullMask, em);
+          dst[u] = q0 + __popc(Em & ((1u << lane) - 1u));
+          q0 += __popc(Em);
+          applied_prev = (A >> 31) & 1u;
+          emit[u] = em;
+          if (!em) continue;
+          // pair i+1: applied?
+          // (lanes < 31 take pair i+1 from the ballot; lane 31 reads the next segment)
+          bool ap1 = false;
+          if (lane < 31) ap1 = (A >> (lane + 1)) & 1u;
+          else if (i + 1 < n) ap1 = bit_at(mm, i + 1) && R[i + 1] < C;
+          outv[u] = ap ? sp_merged<NARROW>(T, r[u]) : x[u];
+          if (!ap && !ap1) {
+            keep_r[u] = true;  // both tokens unchanged: the pair's rank stays
+            continue;
+          }
+          if (ap) {  // the next live token is at i + 2
+            if (i + 2 < n) {
+              const uint32_t r2 = R[i + 2];
+              const bool ap2 = bit_at(mm, i + 2) && r2 < C;
+              nt[u] = ap2 ? sp_merged<NARROW>(T, r2) : X[i + 2];
+              probe_it[u] = true;
+            }
+          } else {  // pair i+1 merged: the next token is its merged token
+            nt[u] = sp_merged<NARROW>(T, R[i + 1]);
+            probe_it[u] = true;
+          }
+          if (probe_it[u]) probe_issue<NARROW>(q[u], T, outv[u], nt[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!emit[u]) continue;
+          const uint32_t nr = keep_r[u] ? r[u] : (probe_it[u] ? probe_resolve<NARROW>(q[u], T) : kNoRank);
+          X[dst[u]] = keep_r[u] ? x[u] : outv[u];
+          R[dst[u]] = nr;
+        }
+        __syncwarp();
+      }
+      n = q0;
+    }
+    __syncwarp();
+  }
+  // Result: lpo[start] = count (| unchanged), then the tokens in order.
+  uint32_t* O = a.lpo + Rec.start;
+  const bool unchanged = n == n0;
+  if (lane == 0) {
+    O[0] = n | (unchanged ? kUnchangedFlag : 0u);
+    a.lrec[ridx].count = n;
+    atomicAdd(&a.tile_count[Rec.start / kTile], n);
+  }
+  if (!unchanged)
+    for (uint32_t i = lane; i < n; i += 32) O[1 + i] = X[i];
+  __syncwarp();
+}
+
 // Persistent: each warp takes long pieces from the list by ticket.
 template <bool NARROW>
 __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, DevTable T) {
@@ -378,6 +658,27 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
     idx = __shfl_sync(kFullMask, idx, 0);
     if (idx >= count) return;
     run_piece<NARROW>(a, T, s_lut, a.long_idx[idx], smem, lane);
+  }
+}
+
+// The super-pass engine, same ticketing (used unless a pass cap, a trace or
+// caller tokens ask for the pass-by-pass engine above).
+template <bool NARROW>
+__global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_sp(EncodeArgs a, DevTable T) {
+  __shared__ uint32_t s_lut[256];
+  extern __shared__ __align__(16) unsigned char s_lp[];
+  const uint32_t count = static_cast<uint32_t>(min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap));
+  if (count == 0) return;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned char* smem = s_lp + size_t(wid) * lp_warp_bytes<NARROW>();
+  for (;;) {
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(&a.counters[CNT_LP_NEXT], 1u);
+    idx = __shfl_sync(kFullMask, idx, 0);
+    if (idx >= count) return;
+    run_piece_sp<NARROW>(a, T, s_lut, a.long_idx[idx], smem, lane);
   }
 }
 
@@ -446,16 +747,22 @@ int long_pieces_grid(int device, int sm_count) {
   const size_t sn = long_pieces_smem(true), sw = long_pieces_smem(false);
   cudaFuncSetAttribute(k_long_pieces<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
   cudaFuncSetAttribute(k_long_pieces<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
+  cudaFuncSetAttribute(k_long_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
+  cudaFuncSetAttribute(k_long_sp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_long_pieces<true>, kLpWarps * 32, sn);
   return sm_count * (per_sm > 0 ? per_sm : 1);
 }
 
 void launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream) {
-  if (t.key32)  // 16-bit ids and ranks: the u32 position record
-    k_long_pieces<true><<<grid, kLpWarps * 32, long_pieces_smem(true), stream>>>(a, t);
-  else
-    k_long_pieces<false><<<grid, kLpWarps * 32, long_pieces_smem(false), stream>>>(a, t);
+  const bool by_pass = a.trace || a.max_passes > 0 || a.tokens_input;  // PassTrace, MaxPassesError
+  if (t.key32) {  // 16-bit ids and ranks
+    if (by_pass) k_long_pieces<true><<<grid, kLpWarps * 32, long_pieces_smem(true), stream>>>(a, t);
+    else k_long_sp<true><<<grid, kLpWarps * 32, long_pieces_smem(true), stream>>>(a, t);
+  } else {
+    if (by_pass) k_long_pieces<false><<<grid, kLpWarps * 32, long_pieces_smem(false), stream>>>(a, t);
+    else k_long_sp<false><<<grid, kLpWarps * 32, long_pieces_smem(false), stream>>>(a, t);
+  }
 }
 
 }  // namespace bbpe

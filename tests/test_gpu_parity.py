@@ -200,6 +200,31 @@ def test_sharded_single_device_matches(gpt2):
     assert np.array_equal(oo, v["out_offsets"]) and np.array_equal(ids, v["ids"])
 
 
+@pytest.mark.parametrize("n_ctx", [2, 3, 4])
+def test_sharded_partitioned_path(gpt2, n_ctx):
+    """bbpe_encode_sharded over n contexts on device 0 (the multi-GPU path
+    with one GPU): cost-balanced shards, proportional output regions, the
+    ordered parallel stitch (a 64 MiB batch so every move runs in waves), and
+    the exact / too-small capacity cases; equal to the one-context encode."""
+    from workloads import text as WX, tables as WT
+    gen = WX.TextGen(WX.word_list(WT.gpt2_table()[0]))
+    data, off, _ = WX.config_rows(gen, 2, scale=1 / 4)
+    enc = bb.Encoder(0)
+    want_ids, want_off, _ = enc.encode_packed(gpt2, data, off)
+    encs = [bb.Encoder(0) for _ in range(n_ctx)]
+    ids, oo, st = bb.encode_sharded(encs, gpt2, data, off)
+    assert np.array_equal(oo, want_off) and np.array_equal(ids, want_ids)
+    assert st["tokens"] == want_ids.size and st["n_rows"] == off.size - 1
+    # capacity = the exact token count: regions are capacity shares (a shard
+    # that overflows its share re-encodes into a host vector)
+    ids2, oo2, _ = bb.encode_sharded(encs, gpt2, data, off, capacity=int(want_ids.size))
+    assert np.array_equal(oo2, want_off) and np.array_equal(ids2, want_ids)
+    ids3, oo3, _ = bb.encode_sharded(encs, gpt2, data, off, capacity=int(want_ids.size) + 1000)
+    assert np.array_equal(oo3, want_off) and np.array_equal(ids3, want_ids)
+    with pytest.raises(bb.UsageError, match="capacity"):
+        bb.encode_sharded(encs, gpt2, data, off, capacity=int(want_ids.size) - 1)
+
+
 @pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 1 / 128), (3, 1 / 512), (4, 1 / 256)])
 def test_config_parity_vs_reference_engines(cfg, scale, gpt2, oracle_for):
     """BASELINE configs at sizes the C oracle's heap engine finishes quickly
