@@ -412,7 +412,26 @@ __device__ __forceinline__ uint32_t sp_merged(const DevTable& T, uint32_t rk) {
   return NARROW ? (rk & 0xFFFFu) : __ldg(T.r2m + rk);
 }
 
-__device__ __forceinline__ uint32_t bit_at(const uint32_t* w, uint32_t i) { return (w[i >> 5] >> (i & 31)) & 1u; }
+// Value of lane + k of a segment (k = 1, 2), continuing into the next segment.
+__device__ __forceinline__ uint32_t lane_ahead(uint32_t cur, uint32_t nxt, int lane, int k) {
+  const uint32_t a = __shfl_down_sync(kFullMask, cur, k);
+  const uint32_t b = __shfl_sync(kFullMask, nxt, (lane + k) & 31);
+  return lane + k < 32 ? a : b;
+}
+// Value of lane - k (k = 1, 2), continuing into the previous segment.
+__device__ __forceinline__ uint32_t lane_behind(uint32_t cur, uint32_t prv, int lane, int k) {
+  const uint32_t a = __shfl_up_sync(kFullMask, cur, k);
+  const uint32_t b = __shfl_sync(kFullMask, prv, (lane - k) & 31);
+  return lane >= k ? a : b;
+}
+__device__ __forceinline__ uint32_t bit_ahead(uint32_t cur, uint32_t nxt, int lane, int k) {
+  return lane + k < 32 ? (cur >> (lane + k)) & 1u : (nxt >> (lane + k - 32)) & 1u;
+}
+__device__ __forceinline__ uint32_t bit_behind(uint32_t cur, uint32_t prv, int lane, int k) {
+  return lane >= k ? (cur >> (lane - k)) & 1u : (prv >> (lane + 32 - k)) & 1u;
+}
+
+constexpr uint32_t kEvenLanes = 0x55555555u, kOddLanes = 0xAAAAAAAAu;
 
 template <bool NARROW>
 __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint32_t* s_lut, uint32_t ridx,
@@ -434,26 +453,33 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     mm = bm + nseg0;
   }
   const uint8_t* bytes = a.bytes + Rec.start;
-  constexpr int U = 4;
+  const uint32_t lt_mask = (1u << lane) - 1u;
   // Initial tokens (bytes_to_initial_tokens, pretokenize.hpp:60-71) and ranks
   // (fill_pair_ranks, block_engine.hpp:72-79).
-  for (uint32_t s0 = 0; s0 < nseg0; s0 += U) {
-    uint32_t t[U];
-    ProbeReq q[U];
+  {
+    constexpr int U = 4;
+    for (uint32_t s0 = 0; s0 < nseg0; s0 += U) {
+      uint32_t t[U], nx[U];
+      ProbeReq q[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = 32 * (s0 + u) + lane;
-      t[u] = i < n0 ? s_lut[bytes[i]] : 0u;
-      uint32_t nx = __shfl_down_sync(kFullMask, t[u], 1);
-      if (lane == 31 && i + 1 < n0) nx = s_lut[bytes[i + 1]];
-      if (i + 1 < n0) probe_issue<NARROW>(q[u], T, t[u], nx);
-    }
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = 32 * (s0 + u) + lane;
+        t[u] = i < n0 ? s_lut[bytes[i]] : 0u;
+        nx[u] = (lane == 31 && i + 1 < n0) ? s_lut[bytes[i + 1]] : 0u;
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t i = 32 * (s0 + u) + lane;
-      if (i < n0) {
-        X[i] = t[u];
-        R[i] = i + 1 < n0 ? probe_resolve<NARROW>(q[u], T) : kNoRank;
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = 32 * (s0 + u) + lane;
+        const uint32_t d = __shfl_down_sync(kFullMask, t[u], 1);
+        if (i + 1 < n0) probe_issue<NARROW>(q[u], T, t[u], lane == 31 ? nx[u] : d);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t i = 32 * (s0 + u) + lane;
+        if (i < n0) {
+          X[i] = t[u];
+          R[i] = i + 1 < n0 ? probe_resolve<NARROW>(q[u], T) : kNoRank;
+        }
       }
     }
   }
@@ -461,9 +487,12 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
   uint32_t n = n0;
   for (;;) {
     const uint32_t nseg = (n + 31) / 32;
-    // Sweep 1, right to left: parity of b_i (strictly decreasing run to the right).
+    // Phase A, right to left: bm[s] bit = b_i even (b_i = strictly decreasing
+    // steps from i). The carry between segments is one parity bit; the ballots
+    // do not depend on it, so consecutive segments overlap.
     {
-      uint32_t r_next0 = kNoRank, bp_next0 = 0;
+      constexpr int U = 8;
+      uint32_t r_next0 = kNoRank, c = 0;
       for (int s0 = int(nseg) - 1; s0 >= 0; s0 -= U) {
         uint32_t r[U];
 #pragma unroll
@@ -476,151 +505,162 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
         for (int u = 0; u < U; ++u) {
           const int s = s0 - u;
           if (s < 0) break;
-          uint32_t rn = __shfl_down_sync(kFullMask, r[u], 1);
-          if (lane == 31) rn = r_next0;
+          const uint32_t nx0 = u == 0 ? r_next0 : __shfl_sync(kFullMask, r[u > 0 ? u - 1 : 0], 0);
+          const uint32_t rd = __shfl_down_sync(kFullMask, r[u], 1);
+          const uint32_t rn = lane == 31 ? nx0 : rd;
           const unsigned D = __ballot_sync(kFullMask, rn < r[u]);
           const uint32_t Z = ~D & (~0u << lane);  // non-descending steps at or above lane
-          const uint32_t bp = Z ? ((__ffs(Z) - 1 - lane) & 1u) : ((lane + bp_next0) & 1u);
-          const unsigned E = __ballot_sync(kFullMask, bp == 0);
+          const unsigned Eb = __ballot_sync(kFullMask, Z && !((__ffs(Z) - 1 - lane) & 1u));
+          const unsigned Zt = __ballot_sync(kFullMask, Z == 0);  // lanes whose run reaches the next segment
+          const unsigned E = Eb | (Zt & (c ? kOddLanes : kEvenLanes));
           if (lane == 0) bm[s] = E;
-          r_next0 = __shfl_sync(kFullMask, r[u], 0);
-          bp_next0 = __shfl_sync(kFullMask, bp, 0);
+          c = (E & 1u) ^ 1u;  // parity of b at lane 0
         }
+        r_next0 = __shfl_sync(kFullMask, r[U - 1], 0);
       }
     }
     __syncwarp();
-    // Sweep 2, left to right: parity of a_i; merge mask; any merge at all?
+    // Phase B, left to right: a parity and the merge masks, and (one segment
+    // behind, once the next segment's mask is known) the cut C.
     bool any = false;
+    uint32_t C = kNoRank;
     {
-      uint32_t r_prev = kNoRank, ap_prev = 0;
-      for (uint32_t s0 = 0; s0 < nseg; s0 += U) {
-        uint32_t r[U], b[U];
+      constexpr int U = 4;
+      // window: [0] = segment s0-2, [1] = s0-1, [2 + u] = s0 + u
+      uint32_t wx[U + 2], wr[U + 2], wm[U + 2];
+      wx[0] = wx[1] = 0u;
+      wr[0] = wr[1] = kNoRank;
+      wm[0] = wm[1] = 0u;
+      uint32_t c = 0;  // parity of a at lane 31 of the previous segment
+      for (uint32_t s0 = 0; s0 <= nseg; s0 += U) {
+        uint32_t bv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t s = s0 + u, i = 32 * s + lane;
-          r[u] = i < n ? R[i] : kNoRank;
-          b[u] = s < nseg ? bm[s] : 0u;
+          wx[2 + u] = i < n ? X[i] : 0u;
+          wr[2 + u] = i < n ? R[i] : kNoRank;
+          bv[u] = s < nseg ? bm[s] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t s = s0 + u;
-          if (s >= nseg) break;
-          uint32_t rp = __shfl_up_sync(kFullMask, r[u], 1);
-          if (lane == 0) rp = r_prev;
-          const unsigned Up = __ballot_sync(kFullMask, rp <= r[u]);
+          if (s >= nseg) {
+            wm[2 + u] = 0u;
+            continue;
+          }
+          const uint32_t p31 = __shfl_sync(kFullMask, wr[1 + u], 31);
+          const uint32_t ru = __shfl_up_sync(kFullMask, wr[2 + u], 1);
+          const uint32_t rp = lane == 0 ? p31 : ru;
+          const unsigned Up = __ballot_sync(kFullMask, rp <= wr[2 + u]);
           const uint32_t Z = ~Up & (lane == 31 ? ~0u : ((2u << lane) - 1u));  // breaks at or below lane
-          const uint32_t ap = Z ? ((lane - (31 - __clz(Z))) & 1u) : ((lane + 1 + ap_prev) & 1u);
-          const bool mg = r[u] != kNoRank && ap == 0 && ((b[u] >> lane) & 1u);
-          const unsigned Mm = __ballot_sync(kFullMask, mg);
+          const unsigned Ab = __ballot_sync(kFullMask, Z && !((lane - (31 - __clz(Z))) & 1u));
+          const unsigned Zb = __ballot_sync(kFullMask, Z == 0);  // runs from the previous segment
+          const unsigned A = Ab | (Zb & (c ? kEvenLanes : kOddLanes));
+          const unsigned Nn = __ballot_sync(kFullMask, wr[2 + u] != kNoRank);
+          const uint32_t Mm = A & bv[u] & Nn;
+          wm[2 + u] = Mm;
           if (lane == 0) mm[s] = Mm;
           any |= Mm != 0;
-          r_prev = __shfl_sync(kFullMask, r[u], 31);
-          ap_prev = __shfl_sync(kFullMask, ap, 31);
+          c = ((A >> 31) & 1u) ^ 1u;  // parity of a at lane 31
         }
+        // The cut for window segments [1, U] (s0-1 .. s0+U-2).
+        uint32_t cmin = kNoRank;
+#pragma unroll
+        for (int j = 1; j <= U; ++j) {
+          const int64_t s = int64_t(s0) + j - 2;
+          if (s < 0 || s >= int64_t(nseg) || !wm[j]) continue;
+          const uint32_t i = 32 * uint32_t(s) + lane;
+          const uint32_t tau = wr[j];
+          const bool act = ((wm[j] >> lane) & 1u) && tau < C;
+          // left token when pair i merges: M of pair i-2 if it merged first, else X[i-1]
+          const uint32_t xm1 = lane_behind(wx[j], wx[j - 1], lane, 1);
+          const uint32_t rm2 = lane_behind(wr[j], wr[j - 1], lane, 2);
+          const uint32_t mm2 = bit_behind(wm[j], wm[j - 1], lane, 2);
+          // right token: M of pair i+2 if it merged first, else X[i+2]
+          const uint32_t xp2 = lane_ahead(wx[j], wx[j + 1], lane, 2);
+          const uint32_t rp2 = lane_ahead(wr[j], wr[j + 1], lane, 2);
+          const uint32_t mp2 = bit_ahead(wm[j], wm[j + 1], lane, 2);
+          ProbeReq ql, qr;
+          const bool hl = act && i >= 1, hr = act && i + 2 < n;
+          if (act) {
+            const uint32_t M = sp_merged<NARROW>(T, tau);
+            if (hl) probe_issue<NARROW>(ql, T, (i >= 2 && mm2 && rm2 <= tau) ? sp_merged<NARROW>(T, rm2) : xm1, M);
+            if (hr) probe_issue<NARROW>(qr, T, M, (mp2 && rp2 <= tau) ? sp_merged<NARROW>(T, rp2) : xp2);
+          }
+          if (hl) {
+            const uint32_t x = probe_resolve<NARROW>(ql, T);
+            if (x != kNoRank) cmin = min(cmin, max(x, tau + 1));
+          }
+          if (hr) {
+            const uint32_t x = probe_resolve<NARROW>(qr, T);
+            if (x != kNoRank) cmin = min(cmin, max(x, tau + 1));
+          }
+        }
+        C = __reduce_min_sync(kFullMask, min(C, cmin));
+        wx[0] = wx[U];
+        wx[1] = wx[U + 1];
+        wr[0] = wr[U];
+        wr[1] = wr[U + 1];
+        wm[0] = wm[U];
+        wm[1] = wm[U + 1];
       }
     }
     if (!any) break;  // no pair in the table (block_engine.hpp:288-289)
     __syncwarp();
-    // Sweep 3: the cut C.
-    uint32_t C = kNoRank;
-    for (uint32_t s = 0; s < nseg; ++s) {
-      const uint32_t Mm = mm[s];
-      if (!Mm) continue;
-      const uint32_t i = 32 * s + lane;
-      const bool mg = (Mm >> lane) & 1u;
-      const uint32_t tau = mg ? R[i] : kNoRank;
-      const bool act = mg && tau < C;  // a merge at or above the cut cannot lower it
-      ProbeReq ql, qr;
-      bool hl = false, hr = false;
-      if (act) {
-        const uint32_t M = sp_merged<NARROW>(T, tau);
-        if (i >= 1) {
-          uint32_t lt;
-          if (i >= 2 && bit_at(mm, i - 2) && R[i - 2] <= tau) lt = sp_merged<NARROW>(T, R[i - 2]);
-          else lt = X[i - 1];
-          probe_issue<NARROW>(ql, T, lt, M);
-          hl = true;
-        }
-        if (i + 2 < n) {
-          uint32_t rt;
-          if (bit_at(mm, i + 2) && R[i + 2] <= tau) rt = sp_merged<NARROW>(T, R[i + 2]);
-          else rt = X[i + 2];
-          probe_issue<NARROW>(qr, T, M, rt);
-          hr = true;
-        }
-      }
-      uint32_t c = kNoRank;
-      if (hl) {
-        const uint32_t x = probe_resolve<NARROW>(ql, T);
-        if (x != kNoRank) c = min(c, max(x, tau + 1));
-      }
-      if (hr) {
-        const uint32_t x = probe_resolve<NARROW>(qr, T);
-        if (x != kNoRank) c = min(c, max(x, tau + 1));
-      }
-      C = __reduce_min_sync(kFullMask, min(C, c));
-    }
-    // Sweep 4: apply the merges below C, compact in place, re-rank changed pairs.
+    // Phase C, left to right: apply the merges below C, compact in place
+    // (destinations never pass the position being read), re-rank the pairs
+    // whose tokens changed.
     {
-      uint32_t q0 = 0, applied_prev = 0;
+      constexpr int U = 4;
+      uint32_t q0 = 0, ap_prev = 0;
       for (uint32_t s0 = 0; s0 < nseg; s0 += U) {
-        uint32_t x[U], r[U], outv[U], nt[U], dst[U];
-        bool emit[U], probe_it[U], keep_r[U];
+        uint32_t wx[U + 1], wr[U + 1], Aa[U + 1];
+#pragma unroll
+        for (int u = 0; u <= U; ++u) {
+          const uint32_t s = s0 + u, i = 32 * s + lane;
+          wx[u] = i < n ? X[i] : 0u;
+          wr[u] = i < n ? R[i] : kNoRank;
+          const uint32_t m = s < nseg ? mm[s] : 0u;
+          Aa[u] = __ballot_sync(kFullMask, ((m >> lane) & 1u) && wr[u] < C);
+        }
+        uint32_t outv[U], nr[U], dst[U];
+        bool emit[U], prb[U];
         ProbeReq q[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t s = s0 + u, i = 32 * s + lane;
-          emit[u] = false;
-          probe_it[u] = false;
-          keep_r[u] = false;
+          emit[u] = prb[u] = false;
           if (s >= nseg) continue;
-          x[u] = i < n ? X[i] : 0u;
-          r[u] = i < n ? R[i] : kNoRank;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t s = s0 + u, i = 32 * s + lane;
-          if (s >= nseg) break;
-          const uint32_t Mm = mm[s];
-          const bool ap = ((Mm >> lane) & 1u) && r[u] < C;
-          const unsigned A = __ballot_sync(kFullMask, ap);
-          const bool consumed = lane == 0 ? applied_prev != 0 : ((A >> (lane - 1)) & 1u);
+          const bool ap = (Aa[u] >> lane) & 1u;
+          const bool consumed = lane == 0 ? ap_prev != 0 : ((Aa[u] >> (lane - 1)) & 1u);
           const bool em = i < n && !consumed;
           const unsigned Em = __ballot_sync(kFullMask, em);
-          dst[u] = q0 + __popc(Em & ((1u << lane) - 1u));
+          dst[u] = q0 + __popc(Em & lt_mask);
           q0 += __popc(Em);
-          applied_prev = (A >> 31) & 1u;
+          ap_prev = Aa[u] >> 31;
+          const uint32_t x1 = lane_ahead(wx[u], wx[u + 1], lane, 1), r1 = lane_ahead(wr[u], wr[u + 1], lane, 1);
+          const uint32_t x2 = lane_ahead(wx[u], wx[u + 1], lane, 2), r2 = lane_ahead(wr[u], wr[u + 1], lane, 2);
+          const bool ap1 = bit_ahead(Aa[u], Aa[u + 1], lane, 1), ap2 = bit_ahead(Aa[u], Aa[u + 1], lane, 2);
           emit[u] = em;
-          if (!em) continue;
-          // pair i+1: applied?
-          // (lanes < 31 take pair i+1 from the ballot; lane 31 reads the next segment)
-          bool ap1 = false;
-          if (lane < 31) ap1 = (A >> (lane + 1)) & 1u;
-          else if (i + 1 < n) ap1 = bit_at(mm, i + 1) && R[i + 1] < C;
-          outv[u] = ap ? sp_merged<NARROW>(T, r[u]) : x[u];
-          if (!ap && !ap1) {
-            keep_r[u] = true;  // both tokens unchanged: the pair's rank stays
-            continue;
-          }
+          outv[u] = ap ? sp_merged<NARROW>(T, wr[u]) : wx[u];
+          nr[u] = (ap || ap1) ? kNoRank : wr[u];  // unchanged pair: its rank stays
+          if (!em || !(ap || ap1)) continue;
+          uint32_t nt = 0;
           if (ap) {  // the next live token is at i + 2
-            if (i + 2 < n) {
-              const uint32_t r2 = R[i + 2];
-              const bool ap2 = bit_at(mm, i + 2) && r2 < C;
-              nt[u] = ap2 ? sp_merged<NARROW>(T, r2) : X[i + 2];
-              probe_it[u] = true;
-            }
+            prb[u] = i + 2 < n;
+            nt = ap2 ? sp_merged<NARROW>(T, r2) : x2;
           } else {  // pair i+1 merged: the next token is its merged token
-            nt[u] = sp_merged<NARROW>(T, R[i + 1]);
-            probe_it[u] = true;
+            prb[u] = true;
+            nt = sp_merged<NARROW>(T, r1);
           }
-          if (probe_it[u]) probe_issue<NARROW>(q[u], T, outv[u], nt[u]);
+          (void)x1;
+          if (prb[u]) probe_issue<NARROW>(q[u], T, outv[u], nt);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (!emit[u]) continue;
-          const uint32_t nr = keep_r[u] ? r[u] : (probe_it[u] ? probe_resolve<NARROW>(q[u], T) : kNoRank);
-          X[dst[u]] = keep_r[u] ? x[u] : outv[u];
-          R[dst[u]] = nr;
+          X[dst[u]] = outv[u];
+          R[dst[u]] = prb[u] ? probe_resolve<NARROW>(q[u], T) : nr[u];
         }
         __syncwarp();
       }
