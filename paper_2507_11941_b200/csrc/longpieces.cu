@@ -704,7 +704,7 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 // The super-pass engine, same ticketing (used unless a pass cap, a trace or
 // caller tokens ask for the pass-by-pass engine above).
 template <bool NARROW>
-__global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_sp(EncodeArgs a, DevTable T) {
+__global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_lp[];
   const uint32_t count = static_cast<uint32_t>(min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap));
