@@ -203,6 +203,16 @@ L2_NOTE = "inputs larger than L2 (126 MB), else L2 flushed between steps"
 # Distributed plumbing
 
 
+def profile_tag(args):
+    """Name of a workload in profiles/ (r2_<kernel>_<tag>.json ncu summaries)."""
+    tag = f"cfg{args.config}_{args.text}"
+    if args.config == 4 and args.table == "trained":
+        tag += "_trained"
+    if args.engine == "block":
+        tag += "_block"
+    return tag
+
+
 def free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -556,7 +566,7 @@ def main():
     peak, peak_src = peaks()
     achieved = alg_bytes / (k_ms[dom] / 1e3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"r2_{dom}_cfg{args.config}_{args.text}.json")
+    prof = os.path.join(ROOT, "profiles", f"r2_{dom}_{profile_tag(args)}.json")
     if os.path.exists(prof) and args.scale == 1.0:
         with open(prof) as f:
             pj = json.load(f)
@@ -600,7 +610,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": w.scaling,
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": w.config(),
+            "config": dict(w.config(), l2=(f"inputs ({total / 2**20:.0f} MiB per GPU) larger than L2 (126 MB): "
+                                           "no flush" if flush is None else
+                                           f"inputs ({total / 2**20:.1f} MiB) smaller than 2x L2: a 252 MB buffer "
+                                           "written before every step, its time measured alone and subtracted")),
             "engine": args.engine,
             "parallelism": f"rows sharded, {world} independent GPU(s), no collective on the data path",
             "input_GBps": bytes_all / (ms / 1e3) / 1e9,
