@@ -40,19 +40,9 @@ namespace bbpe {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr uint32_t kProbe = 0xFFFFFFFEu;   // rank not yet looked up
-constexpr uint32_t kMergeMark = 0xFFFFFFFDu;
-constexpr uint32_t kUnchanged = 0x80000000u;  // lpo flag: piece merged nothing
-constexpr int kWords = (kWin + 127) / 128 * 4;  // boundary words, whole 128-position chunks
-constexpr int kTileWords = kTile / 32;
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPrefix = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
-
-__device__ __forceinline__ bool is_junction(const uint32_t* junc, uint32_t a, uint32_t c) {
-  uint32_t bit = (a << 8) | c;
-  return (junc[bit >> 5] >> (bit & 31)) & 1u;
-}
 
 __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -1133,13 +1123,10 @@ __device__ __forceinline__ uint32_t compact_at(const GatherSmem& G, uint32_t slo
 #define BBPE_GATHER_MINB 4
 #endif
 __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(EncodeArgs a, DevTable T) {
-  __shared__ uint32_t s_lut[256];
   __shared__ GatherSmem s_g[kWarpsPerCta];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
-  __syncthreads();
+  (void)T;
   const int lane = threadIdx.x & 31;
   GatherSmem& G = s_g[threadIdx.x >> 5];
-  const uint32_t* d2id = T.d2id;
   const uint64_t nwarps = uint64_t(gridDim.x) * kWarpsPerCta;
   // Tile metadata is prefetched one tile ahead; a tile's staged slots and row
   // offsets are all loaded before any is used (one round trip, not one per
