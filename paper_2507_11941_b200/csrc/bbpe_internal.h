@@ -18,6 +18,9 @@ namespace bbpe {
 constexpr uint32_t kNoRank = 0xFFFFFFFFu;     // block_engine.hpp:16
 constexpr uint32_t kInvalidToken = 0xFFFFFFFFu;  // merge_table.hpp:22
 constexpr uint64_t kEmptySlot = ~0ull;
+#ifndef BBPE_PAIR_SLOTS_PER_MERGE
+#define BBPE_PAIR_SLOTS_PER_MERGE 8  // pair-table slots per merge (load <= 1/8: full home buckets are rare, so misses end at one 32-byte load)
+#endif
 constexpr int kBucketSlots = 4;               // 4 x 8 B = one 32 B sector per bucket
 
 // Exceptions mirror the reference taxonomy (types.hpp:32-70); the C-ABI maps

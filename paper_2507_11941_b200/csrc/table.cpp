@@ -383,12 +383,12 @@ void build_device_layout(bbpe_table& t) {
     t.narrow = max_dense < 0xFFFDull && M < 0xFFFDull;
   }
 
-  // Bucketised open addressing, load <= 0.5. Narrow tables (ids and ranks <
+  // Bucketised open addressing, load <= 1 / BBPE_PAIR_SLOTS_PER_MERGE. Narrow tables (ids and ranks <
   // 2^16) use 32-bit keys and carry the merged id in the slot:
   // slot = key32 << 32 | rank << 16 | merged, bucket = mix32(key32), so one
   // probe yields both (merge_table.hpp:142-145 Entry{rank, merged}).
   uint64_t buckets = 1;
-  while (buckets * kBucketSlots < 2 * M + 8) buckets <<= 1;
+  while (buckets * kBucketSlots < uint64_t(BBPE_PAIR_SLOTS_PER_MERGE) * M + 8) buckets <<= 1;
   t.bucket_mask = buckets - 1;
   t.slots.assign(buckets * kBucketSlots, kEmptySlot);
   for (size_t i = 0; i < M; ++i) {

@@ -126,7 +126,7 @@ def test_extended_large_tables(gpt2):
     t, (ids, off, blob, m4) = extend_table(gpt2, 200000)
     info = t.info()
     assert info["merge_count"] == 200000 and info["rank_consistent"] == 1
-    assert info["remapped_ids"] == 0 and info["id_bits"] == 18 and info["hash_slots"] == 524288
+    assert info["remapped_ids"] == 0 and info["id_bits"] == 18 and info["hash_slots"] == 2097152
     # regex-like: the junction set barely grows
     assert info["junction_bigrams"] < 3000
     t2, _ = extend_table(gpt2, 200000)

@@ -1,5 +1,5 @@
 """Long-piece tier probe for ncu: one workload encoded `reps` times on the
-device (digits | runs_a | cfg4t).  python tools/lp_probe.py digits 3"""
+device (digits | runs_a | cfg4t | cfg2 | mixed | block2).  python tools/lp_probe.py digits 3"""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,7 +12,13 @@ case = sys.argv[1] if len(sys.argv) > 1 else "digits"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 rng = np.random.default_rng(7)
 N = 256 << 20
-if case == "cfg4t":
+engine = "pieces"
+if case in ("cfg2", "mixed", "block2"):
+    t = bb.load_merge_table_files(WT.GPT2_VOCAB, WT.GPT2_MERGES, "gpt2")
+    gen = WX.make_gen("mixed" if case == "mixed" else "zipf", WT.gpt2_table()[0])
+    data, off, _ = WX.config_rows(gen, 2, seed=2000)
+    engine = "block" if case == "block2" else "pieces"
+elif case == "cfg4t":
     from workloads import train
     tokens, m, _ = train.trained_table(*WT.gpt2_table(), 200000)
     t = bb.MergeTable.from_arrays(*WT.arrays(tokens, m))
@@ -24,7 +30,7 @@ else:
     else:
         data, L = np.full(N, ord("a"), np.uint8), 65536
     off = np.arange(0, N + 1, L, dtype=np.uint64)
-enc = bb.Encoder(0)
+enc = bb.Encoder(0, engine=engine)
 n, total = off.size - 1, int(off[-1])
 d = torch.from_numpy(data).cuda()
 o = torch.from_numpy(off.view(np.int64)).cuda()
