@@ -1352,8 +1352,7 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
     }
     if (ev) cudaEventRecord(ev[5], stream);
   }
-  launch_long_pieces(a, t, p.lp_grid, stream);
-  ++launched;
+  launched += launch_long_pieces(a, t, p.lp_grid, stream);
   if (ev) cudaEventRecord(ev[6], stream);
   k_tile_scan<<<unsigned((a.num_tiles + kScanTiles - 1) / kScanTiles), kScanThreads, 0, stream>>>(a);
   ++launched;
@@ -1369,8 +1368,7 @@ int launch_encode(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p, c
 int launch_block_bpe(const EncodeArgs& a, const DevTable& t, const LaunchPlan& p,
                      cudaStream_t stream) {
   (void)p;
-  launch_long_pieces(a, t, 1, stream);
-  return 1;
+  return launch_long_pieces(a, t, 1, stream);
 }
 
 }  // namespace bbpe

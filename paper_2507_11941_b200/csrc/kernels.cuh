@@ -46,7 +46,7 @@ constexpr int kInlineRes = 6;
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
        CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_PRETOK = 8, CNT_LCOPY = 9, CNT_LDONE = 10,
-       CNT_N = 11 };
+       CNT_LP_NEXT2 = 11, CNT_N = 12 };
 // k_gather leaves CNT_LREC / CNT_LCOPY / CNT_LDONE for k_long_copy, which resets them.
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFSETS = 3, ERR_N = 4 };
@@ -161,7 +161,7 @@ void launch_copy_out(const uint32_t* d_ids, uint32_t* mapped_out, const uint64_t
 // k_long_pieces (longpieces.cu): the warp-per-piece block engine.
 size_t long_pieces_smem(bool narrow);
 int long_pieces_grid(int device, int sm_count);
-void launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);
+int launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream);  // kernels launched
 // Spec-level ops (specops.cu): per-phase replay of one block_bpe pass.
 void launch_spec_ranks(const uint32_t* tok, uint64_t n, const DevTable& t, uint32_t* ranks, cudaStream_t s);
 void launch_spec_min(const uint32_t* ranks, uint64_t n, uint32_t* out, cudaStream_t s);

@@ -433,7 +433,7 @@ __device__ __forceinline__ uint32_t bit_behind(uint32_t cur, uint32_t prv, int l
 
 constexpr uint32_t kEvenLanes = 0x55555555u, kOddLanes = 0xAAAAAAAAu;
 
-template <bool NARROW>
+template <bool NARROW, bool PIPE>
 __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint32_t* s_lut, uint32_t ridx,
                              unsigned char* smem, int lane) {
   const LongRec Rec = a.lrec[ridx];
@@ -493,13 +493,29 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     {
       constexpr int U = 8;
       uint32_t r_next0 = kNoRank, c = 0;
+      // Software-pipelined: the next batch's loads are in flight while this
+      // one is processed (the L2 path's latency).
+      uint32_t rq[U];
+#pragma unroll
+      for (int u = 0; u < U && PIPE; ++u) {
+        const int s = int(nseg) - 1 - u;
+        const uint32_t i = 32 * uint32_t(s) + lane;
+        rq[u] = (s >= 0 && i < n) ? R[i] : kNoRank;
+      }
       for (int s0 = int(nseg) - 1; s0 >= 0; s0 -= U) {
         uint32_t r[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int s = s0 - u;
-          const uint32_t i = 32 * uint32_t(s) + lane;
-          r[u] = (s >= 0 && i < n) ? R[i] : kNoRank;
+          if (PIPE) {
+            r[u] = rq[u];
+            const int s = s0 - U - u;
+            const uint32_t i = 32 * uint32_t(s) + lane;
+            rq[u] = (s >= 0 && i < n) ? R[i] : kNoRank;
+          } else {
+            const int s = s0 - u;
+            const uint32_t i = 32 * uint32_t(s) + lane;
+            r[u] = (s >= 0 && i < n) ? R[i] : kNoRank;
+          }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -532,14 +548,32 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
       wr[0] = wr[1] = kNoRank;
       wm[0] = wm[1] = 0u;
       uint32_t c = 0;  // parity of a at lane 31 of the previous segment
+      uint32_t qx[U], qr[U], qb[U];  // the next batch, in flight (software pipelining)
+#pragma unroll
+      for (int u = 0; u < U && PIPE; ++u) {
+        const uint32_t s = u, i = 32 * s + lane;
+        qx[u] = i < n ? X[i] : 0u;
+        qr[u] = i < n ? R[i] : kNoRank;
+        qb[u] = s < nseg ? bm[s] : 0u;
+      }
       for (uint32_t s0 = 0; s0 <= nseg; s0 += U) {
         uint32_t bv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const uint32_t s = s0 + u, i = 32 * s + lane;
-          wx[2 + u] = i < n ? X[i] : 0u;
-          wr[2 + u] = i < n ? R[i] : kNoRank;
-          bv[u] = s < nseg ? bm[s] : 0u;
+          if (PIPE) {
+            wx[2 + u] = qx[u];
+            wr[2 + u] = qr[u];
+            bv[u] = qb[u];
+            const uint32_t s = s0 + U + u, i = 32 * s + lane;
+            qx[u] = i < n ? X[i] : 0u;
+            qr[u] = i < n ? R[i] : kNoRank;
+            qb[u] = s < nseg ? bm[s] : 0u;
+          } else {
+            const uint32_t s = s0 + u, i = 32 * s + lane;
+            wx[2 + u] = i < n ? X[i] : 0u;
+            wr[2 + u] = i < n ? R[i] : kNoRank;
+            bv[u] = s < nseg ? bm[s] : 0u;
+          }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -613,15 +647,45 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     {
       constexpr int U = 4;
       uint32_t q0 = 0, ap_prev = 0;
+      // Segments s0..s0+U (one of lookahead); segments s0+U+1.. of the next
+      // batch are loaded before this batch's writes, which only reach
+      // positions below 32 (s0 + U) (in-place compaction never passes its reads).
+      uint32_t px[U + 1], pr[U + 1], pm[U + 1];
+#pragma unroll
+      for (int u = 0; u <= U && PIPE; ++u) {
+        const uint32_t s = u, i = 32 * s + lane;
+        px[u] = i < n ? X[i] : 0u;
+        pr[u] = i < n ? R[i] : kNoRank;
+        pm[u] = s < nseg ? mm[s] : 0u;
+      }
       for (uint32_t s0 = 0; s0 < nseg; s0 += U) {
         uint32_t wx[U + 1], wr[U + 1], Aa[U + 1];
+        if (!PIPE) {
+#pragma unroll
+          for (int u = 0; u <= U; ++u) {
+            const uint32_t s = s0 + u, i = 32 * s + lane;
+            px[u] = i < n ? X[i] : 0u;
+            pr[u] = i < n ? R[i] : kNoRank;
+            pm[u] = s < nseg ? mm[s] : 0u;
+          }
+        }
 #pragma unroll
         for (int u = 0; u <= U; ++u) {
-          const uint32_t s = s0 + u, i = 32 * s + lane;
-          wx[u] = i < n ? X[i] : 0u;
-          wr[u] = i < n ? R[i] : kNoRank;
-          const uint32_t m = s < nseg ? mm[s] : 0u;
-          Aa[u] = __ballot_sync(kFullMask, ((m >> lane) & 1u) && wr[u] < C);
+          wx[u] = px[u];
+          wr[u] = pr[u];
+          Aa[u] = __ballot_sync(kFullMask, ((pm[u] >> lane) & 1u) && wr[u] < C);
+        }
+        if (PIPE) {
+          px[0] = px[U];
+          pr[0] = pr[U];
+          pm[0] = pm[U];
+#pragma unroll
+          for (int u = 1; u <= U; ++u) {
+            const uint32_t s = s0 + U + u, i = 32 * s + lane;
+            px[u] = i < n ? X[i] : 0u;
+            pr[u] = i < n ? R[i] : kNoRank;
+            pm[u] = s < nseg ? mm[s] : 0u;
+          }
         }
         uint32_t outv[U], nr[U], dst[U];
         bool emit[U], prb[U];
@@ -703,7 +767,12 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 
 // The super-pass engine, same ticketing (used unless a pass cap, a trace or
 // caller tokens ask for the pass-by-pass engine above).
-template <bool NARROW>
+// Two instances over the same list: PIPE = pieces longer than kPipeMin
+// positions, which stream from L2 and prefetch the next batch in every sweep;
+// the other instance takes the rest (separate kernels keep each one's
+// register allocation free of the other's prefetch buffers).
+constexpr uint64_t kPipeMin = 4 * (kLpSmemBytes / 8);
+template <bool NARROW, bool PIPE>
 __global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_lp[];
@@ -715,10 +784,12 @@ __global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeA
   unsigned char* smem = s_lp + size_t(wid) * lp_warp_bytes<NARROW>();
   for (;;) {
     uint32_t idx = 0;
-    if (lane == 0) idx = atomicAdd(&a.counters[CNT_LP_NEXT], 1u);
+    if (lane == 0) idx = atomicAdd(&a.counters[PIPE ? CNT_LP_NEXT2 : CNT_LP_NEXT], 1u);
     idx = __shfl_sync(kFullMask, idx, 0);
     if (idx >= count) return;
-    run_piece_sp<NARROW>(a, T, s_lut, a.long_idx[idx], smem, lane);
+    const uint32_t ridx = a.long_idx[idx];
+    if ((a.lrec[ridx].len > kPipeMin) != PIPE) continue;
+    run_piece_sp<NARROW, PIPE>(a, T, s_lut, ridx, smem, lane);
   }
 }
 
@@ -787,22 +858,31 @@ int long_pieces_grid(int device, int sm_count) {
   const size_t sn = long_pieces_smem(true), sw = long_pieces_smem(false);
   cudaFuncSetAttribute(k_long_pieces<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
   cudaFuncSetAttribute(k_long_pieces<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
-  cudaFuncSetAttribute(k_long_sp<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
-  cudaFuncSetAttribute(k_long_sp<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
+  cudaFuncSetAttribute(k_long_sp<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
+  cudaFuncSetAttribute(k_long_sp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
+  cudaFuncSetAttribute(k_long_sp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
+  cudaFuncSetAttribute(k_long_sp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_long_pieces<true>, kLpWarps * 32, sn);
   return sm_count * (per_sm > 0 ? per_sm : 1);
 }
 
-void launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream) {
+int launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream) {
   const bool by_pass = a.trace || a.max_passes > 0 || a.tokens_input;  // PassTrace, MaxPassesError
-  if (t.key32) {  // 16-bit ids and ranks
-    if (by_pass) k_long_pieces<true><<<grid, kLpWarps * 32, long_pieces_smem(true), stream>>>(a, t);
-    else k_long_sp<true><<<grid, kLpWarps * 32, long_pieces_smem(true), stream>>>(a, t);
-  } else {
-    if (by_pass) k_long_pieces<false><<<grid, kLpWarps * 32, long_pieces_smem(false), stream>>>(a, t);
-    else k_long_sp<false><<<grid, kLpWarps * 32, long_pieces_smem(false), stream>>>(a, t);
+  const size_t sm = long_pieces_smem(t.key32 != 0);
+  if (by_pass) {
+    if (t.key32) k_long_pieces<true><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+    else k_long_pieces<false><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+    return 1;
   }
+  if (t.key32) {  // 16-bit ids and ranks
+    k_long_sp<true, false><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+    k_long_sp<true, true><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+  } else {
+    k_long_sp<false, false><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+    k_long_sp<false, true><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+  }
+  return 2;
 }
 
 }  // namespace bbpe
