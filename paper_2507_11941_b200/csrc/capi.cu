@@ -286,7 +286,7 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   // a full neighbourhood just skips the dedupe for that piece).
   if (!block && !c.cfg.no_dedup && total >= kDedupMinBytes) {
     uint64_t slots = 4096;
-    while (slots < total / 128) slots <<= 1;
+    while (slots < total / BBPE_DEDUP_BYTES_PER_SLOT) slots <<= 1;
     sc.dkey.ensure(slots * 16);
     sc.dres.ensure(slots * 32);
     a.dkey = sc.dkey.as<ulonglong2>();

@@ -274,14 +274,14 @@ __device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulon
 // Within-call dedupe of merge pieces: finds or claims the slot of `key`.
 // Returns the slot (the caller owns it: its merge passes run), the slot with
 // bit 63 set (another piece with the same bytes owns it: copy its result),
-// or ~0 after 16 probes (no dedupe for this piece).
+// or ~0 after BBPE_DEDUP_PROBES probes (no dedupe for this piece).
 __device__ __forceinline__ uint64_t dedup_claim(ulonglong2* dkey, uint64_t dmask, ulonglong2 key) {
   uint64_t h = (key.x * 0x9E3779B97F4A7C15ull) ^ (key.y * 0xC2B2AE3D27D4EB4Full);
   h ^= h >> 29;
   h *= 0xBF58476D1CE4E5B9ull;
   h ^= h >> 32;
   uint64_t s = h & dmask;
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < BBPE_DEDUP_PROBES; ++i) {
     ulonglong2 cur = __ldcg(dkey + s);
     if (cur.x == 0 && cur.y == 0) {
       cur = cas128(dkey + s, make_ulonglong2(0, 0), key);
