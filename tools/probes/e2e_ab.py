@@ -1,5 +1,5 @@
 """e2e A/B of two library builds (same C-ABI subset): median bbpe_encode time
-on cfg2 from pinned host buffers.  python tools/e2e_ab.py lib1.so [lib2.so ...]"""
+on cfg2 from pinned host buffers.  python tools/probes/e2e_ab.py lib1.so [lib2.so ...]"""
 import ctypes as C
 import os
 import sys
@@ -7,7 +7,7 @@ import time
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 from workloads import tables as WT, text as WX  # noqa: E402
 

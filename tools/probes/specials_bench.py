@@ -3,7 +3,7 @@
 stitch) vs the plain encode of the same bytes; CUDA-event ms per call."""
 import os, sys, json
 import numpy as np
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 import paper_2507_11941_b200 as bb
