@@ -4,7 +4,7 @@ events: alone, with a concurrent pinned H2D copy, and with a concurrent D2H
 copy. Separates per-wave fixed cost from PCIe-copy contention."""
 import json, os, sys
 import numpy as np
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 import paper_2507_11941_b200 as bb

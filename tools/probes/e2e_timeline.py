@@ -4,7 +4,7 @@ call for several wave sizes; with BBPE_TIMELINE=1 the library prints the
 per-wave copy/kernel timeline to stderr."""
 import os, sys, time, json
 import numpy as np
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 import paper_2507_11941_b200 as bb

@@ -4,7 +4,7 @@ graph, alone and under a concurrent pinned D2H copy (BBPE_NO_KERNEL_TIMING=1).""
 import os, sys
 import numpy as np
 os.environ["BBPE_NO_KERNEL_TIMING"] = "1"
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import torch
 import paper_2507_11941_b200 as bb
