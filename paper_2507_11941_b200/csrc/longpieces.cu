@@ -171,6 +171,7 @@ __device__ void resolve_touched(const Piece<NARROW>& V, const DevTable& T, int l
           }
           if (pend[u] && has_r[u]) probe_issue<NARROW>(q[u], T, PT::tok(e[u]), rt);
         }
+        __syncwarp();  // reads of right neighbours in later segments before this batch's writes
 #pragma unroll
         for (int u = 0; u < B; ++u) {
           if (u >= k) continue;
@@ -243,6 +244,7 @@ __device__ uint32_t merge_pass(const Piece<NARROW>& V, uint32_t m, uint32_t M, i
         // The left neighbour of a merged token: its pair changed.
         const uint32_t nbx = Ln & above(lane);
         const bool left_of_merge = ((Ln >> lane) & 1u) && !me && nbx && ((merged >> (__ffs(nbx) - 1)) & 1u);
+        __syncwarp();  // every lane has read live[s] and its neighbours before they change
         if (me) V.P[p] = PT::make(M, PT::PEND);
         else if (left_of_merge) V.P[p] = PT::make(PT::tok(e), PT::PEND);
         if (lane == 0) {
