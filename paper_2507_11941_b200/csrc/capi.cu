@@ -106,14 +106,14 @@ bool is_pinned(const void* p) {
 // Device scratch of one encode in flight (kernels.cuh EncodeArgs).
 struct Scratch {
   DevBuf tile_first, status, counters, err, lpo, lpx, lpy, trace, trace_count;
-  DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, rowbits, mrec;
+  DevBuf staging, tile_count, tile_slots, tile_lrec, lrec, tile_base, long_idx, long_idx2, rowbits, mrec;
   DevBuf dkey, dres, owners, offs, chunkbits;
   uint64_t rowbits_zeroed = 0;  // words known to be zero (k_gather clears what k_tile_first set)
   uint64_t chunkbits_zeroed = 0;  // the same for the pattern splitter's chunk bits
   bool ctrl_dirty = true;       // counters/status not known to be zero (k_gather resets them)  // words known to be zero (k_pieces clears what it consumes)
   void release() {
     for (DevBuf* b : {&tile_first, &status, &counters, &err, &lpo, &lpx, &lpy, &trace, &trace_count, &staging,
-                      &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &rowbits, &mrec,
+                      &tile_count, &tile_slots, &tile_lrec, &lrec, &tile_base, &long_idx, &long_idx2, &rowbits, &mrec,
                       &dkey, &dres, &owners, &offs, &chunkbits})
       b->release();
     rowbits_zeroed = 0;
@@ -299,6 +299,8 @@ bbpe::EncodeArgs prepare_args(bbpe_ctx& c, Scratch& sc, const uint8_t* d_bytes, 
   sc.lrec.ensure(a.lp_cap * sizeof(LongRec));
   sc.long_idx.ensure(a.long_cap * 4);
   a.long_idx = sc.long_idx.as<uint32_t>();
+  sc.long_idx2.ensure(a.long_cap * 4);
+  a.long_idx2 = sc.long_idx2.as<uint32_t>();
   sc.lpo.ensure((total + 1) * 4);
   sc.lpx.ensure(std::max<uint64_t>(total, 1) * 8);
   sc.lpy.ensure(std::max<uint64_t>(total, 1) * 8);
@@ -1861,6 +1863,7 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   c->sc.err.ensure(ERR_N * 8);
   c->sc.lrec.ensure(sizeof(LongRec));
   c->sc.long_idx.ensure(4);
+  c->sc.long_idx2.ensure(4);
   c->sc.lpo.ensure((n + 1) * 4);
   c->sc.lpx.ensure(n * 8);
   c->sc.lpy.ensure(n * 8);
@@ -1872,6 +1875,7 @@ int bbpe_block_bpe(bbpe_ctx* c, const bbpe_table* t, const uint32_t* tokens, siz
   a.lrec = c->sc.lrec.as<LongRec>();
   a.lp_cap = 1;
   a.long_idx = c->sc.long_idx.as<uint32_t>();
+  a.long_idx2 = c->sc.long_idx2.as<uint32_t>();
   a.long_cap = 1;
   a.lpo = c->sc.lpo.as<uint32_t>();
   a.lpx = c->sc.lpx.as<uint64_t>();

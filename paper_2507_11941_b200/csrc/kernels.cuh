@@ -52,7 +52,7 @@ constexpr int kInlineRes = 6;
 // Counter slots (u32).
 enum { CNT_TILE_TICKET = 0, CNT_LONG = 1, CNT_LP_NEXT = 2, CNT_GROUP_TICKET = 3, CNT_LREC = 4,
        CNT_MERGE_TICKET = 5, CNT_MREC = 6, CNT_OWNERS = 7, CNT_PRETOK = 8, CNT_LCOPY = 9, CNT_LDONE = 10,
-       CNT_LP_NEXT2 = 11, CNT_N = 12 };
+       CNT_LP_NEXT2 = 11, CNT_LONG2 = 12, CNT_N = 13 };
 // k_gather leaves CNT_LREC / CNT_LCOPY / CNT_LDONE for k_long_copy, which resets them.
 // Error slots (u64, initialised to ~0).
 enum { ERR_BAD_BYTE_POS = 0, ERR_MAXPASS_ROW = 1, ERR_CONTRACT = 2, ERR_BAD_OFFSETS = 3, ERR_N = 4 };
@@ -116,6 +116,7 @@ struct EncodeArgs {
   uint64_t* owners;         // mrec_cap: record index | (slot + 1) << 32 for k_merge (CNT_OWNERS used)
   LongRec* lrec;            // lp_cap records (CNT_LREC used)
   uint32_t* long_idx;       // indices of the long records (CNT_LONG used)
+  uint32_t* long_idx2;      // the pieces > kPipeMin positions among them (CNT_LONG2 used; k_long_sp)
   uint64_t long_cap;
   uint32_t* counters;       // CNT_N
   uint64_t* err;            // ERR_N

@@ -769,16 +769,19 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 
 // The super-pass engine, same ticketing (used unless a pass cap, a trace or
 // caller tokens ask for the pass-by-pass engine above).
-// Two instances over the same list: PIPE = pieces longer than kPipeMin
-// positions, which stream from L2 and prefetch the next batch in every sweep;
-// the other instance takes the rest (separate kernels keep each one's
+// Two instances: PIPE = pieces longer than kPipeMin positions, which stream
+// from L2 and prefetch the next batch in every sweep; the other instance
+// takes the rest and lists those for it (separate kernels keep each one's
 // register allocation free of the other's prefetch buffers).
 constexpr uint64_t kPipeMin = 4 * (kLpSmemBytes / 8);
 template <bool NARROW, bool PIPE>
 __global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_lp[];
-  const uint32_t count = static_cast<uint32_t>(min((uint64_t)a.counters[CNT_LONG], (uint64_t)a.long_cap));
+  // PIPE = false: every long piece by ticket; the ones above kPipeMin are
+  // listed for the PIPE instance, which runs after it on the same stream.
+  const uint32_t count =
+      static_cast<uint32_t>(min((uint64_t)a.counters[PIPE ? CNT_LONG2 : CNT_LONG], (uint64_t)a.long_cap));
   if (count == 0) return;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) s_lut[i] = T.lut[i];
   __syncthreads();
@@ -789,8 +792,11 @@ __global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeA
     if (lane == 0) idx = atomicAdd(&a.counters[PIPE ? CNT_LP_NEXT2 : CNT_LP_NEXT], 1u);
     idx = __shfl_sync(kFullMask, idx, 0);
     if (idx >= count) return;
-    const uint32_t ridx = a.long_idx[idx];
-    if ((a.lrec[ridx].len > kPipeMin) != PIPE) continue;
+    const uint32_t ridx = PIPE ? a.long_idx2[idx] : a.long_idx[idx];
+    if (!PIPE && a.lrec[ridx].len > kPipeMin) {
+      if (lane == 0) a.long_idx2[atomicAdd(&a.counters[CNT_LONG2], 1u)] = ridx;
+      continue;
+    }
     run_piece_sp<NARROW, PIPE>(a, T, s_lut, ridx, smem, lane);
   }
 }
