@@ -434,6 +434,17 @@ __device__ __forceinline__ uint32_t bit_behind(uint32_t cur, uint32_t prv, int l
 }
 
 constexpr uint32_t kEvenLanes = 0x55555555u, kOddLanes = 0xAAAAAAAAu;
+// Segments per batch of the sweeps (b parity, merge masks + cut, apply) of
+// the shared-memory instance; the pipelined instance uses 8 / 4 / 4.
+#ifndef BBPE_SP_UA
+#define BBPE_SP_UA 8
+#endif
+#ifndef BBPE_SP_UB
+#define BBPE_SP_UB 4
+#endif
+#ifndef BBPE_SP_UC
+#define BBPE_SP_UC 4
+#endif
 
 template <bool NARROW, bool PIPE>
 __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint32_t* s_lut, uint32_t ridx,
@@ -493,7 +504,7 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     // steps from i). The carry between segments is one parity bit; the ballots
     // do not depend on it, so consecutive segments overlap.
     {
-      constexpr int U = 8;
+      constexpr int U = PIPE ? 8 : BBPE_SP_UA;
       uint32_t r_next0 = kNoRank, c = 0;
       // Software-pipelined: the next batch's loads are in flight while this
       // one is processed (the L2 path's latency).
@@ -543,7 +554,7 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     bool any = false;
     uint32_t C = kNoRank;
     {
-      constexpr int U = 4;
+      constexpr int U = PIPE ? 4 : BBPE_SP_UB;
       // window: [0] = segment s0-2, [1] = s0-1, [2 + u] = s0 + u
       uint32_t wx[U + 2], wr[U + 2], wm[U + 2];
       wx[0] = wx[1] = 0u;
@@ -647,7 +658,7 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     // (destinations never pass the position being read), re-rank the pairs
     // whose tokens changed.
     {
-      constexpr int U = 4;
+      constexpr int U = PIPE ? 4 : BBPE_SP_UC;
       uint32_t q0 = 0, ap_prev = 0;
       // Segments s0..s0+U (one of lookahead); segments s0+U+1.. of the next
       // batch are loaded before this batch's writes, which only reach
