@@ -9,6 +9,7 @@
 //   SpecialTokenSet        merge_table.hpp:309-369, validate_specials 374-385
 //   split_specials         pretokenize.hpp:32-57
 //   BlockConfig, block_bpe block_engine.hpp:18-32, 268-310 (PassTrace 42-47)
+//   pair_ranks ... compact block_engine.hpp:189-256 (spec-level ops, on the GPU)
 //   BatchEncoding/Limits   batch.hpp:21-42
 //   encode_single/batch    batch.hpp:46-126
 //   decode/decode_batch    merge_table.hpp:565-579, batch.hpp:128-154
@@ -489,6 +490,55 @@ inline TokenSeq block_bpe(const TokenSeq& tokens, const MergeTable& table, const
     for (std::size_t p = 0; p < passes && p <= tokens.size(); ++p)
       trace->push_back({static_cast<std::size_t>(tr[3 * p]), static_cast<Rank>(tr[3 * p + 1]),
                         static_cast<std::size_t>(tr[3 * p + 2])});
+  return out;
+}
+
+// ---- spec-level operations (block_engine.hpp:189-256), run on the GPU ----
+inline std::vector<std::optional<Rank>> pair_ranks(const TokenSeq& tokens, const MergeTable& table,
+                                                   Encoder* encoder = nullptr) {
+  if (tokens.size() < 2) return {};
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  std::vector<Rank> raw(tokens.size() - 1);
+  detail::check(bbpe_pair_ranks(enc.handle(), table.handle(), tokens.data(), tokens.size(), raw.data()));
+  std::vector<std::optional<Rank>> out(raw.size());
+  for (std::size_t i = 0; i < raw.size(); ++i)
+    if (raw[i] != 0xFFFFFFFFu) out[i] = raw[i];
+  return out;
+}
+
+inline std::optional<Rank> min_rank_reduce(const std::vector<std::optional<Rank>>& ranks,
+                                           Encoder* encoder = nullptr) {
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  std::vector<Rank> raw(ranks.size());
+  for (std::size_t i = 0; i < ranks.size(); ++i) raw[i] = ranks[i] ? *ranks[i] : 0xFFFFFFFFu;
+  Rank m = 0;
+  detail::check(bbpe_min_rank_reduce(enc.handle(), raw.data(), raw.size(), &m));
+  return m == 0xFFFFFFFFu ? std::nullopt : std::optional<Rank>(m);
+}
+
+inline std::vector<std::uint8_t> mark_merges(const TokenSeq& tokens, const MergeTable& table, Rank min_rank,
+                                             Encoder* encoder = nullptr) {
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  std::vector<std::uint8_t> flags(tokens.size(), 0);
+  detail::check(bbpe_mark_merges(enc.handle(), table.handle(), tokens.data(), tokens.size(), min_rank, flags.data()));
+  return flags;
+}
+
+inline std::vector<std::uint32_t> exclusive_scan(const std::vector<std::uint8_t>& flags, Encoder* encoder = nullptr) {
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  std::vector<std::uint32_t> offsets(flags.size(), 0);
+  detail::check(bbpe_exclusive_scan(enc.handle(), flags.data(), flags.size(), offsets.data()));
+  return offsets;
+}
+
+inline TokenSeq compact(const TokenSeq& tokens, const MergeTable& table, const std::vector<std::uint8_t>& flags,
+                        const std::vector<std::uint32_t>& offsets, Encoder* encoder = nullptr) {
+  Encoder& enc = encoder ? *encoder : default_encoder();
+  TokenSeq out(tokens.size() + 1);
+  std::size_t n = 0;
+  detail::check(bbpe_compact(enc.handle(), table.handle(), tokens.data(), tokens.size(), flags.data(), flags.size(),
+                             offsets.data(), offsets.size(), out.data(), &n));
+  out.resize(n);
   return out;
 }
 

@@ -111,6 +111,30 @@ int main(int argc, char** argv) {
   }
   EXPECT(threw);
 
+  // spec-level ops (test_block_engine.cpp:27-112) through the drop-in header
+  {
+    auto r = bb::pair_ranks({0, 1, 2}, toy);
+    EXPECT(r.size() == 2 && r[0] && *r[0] == 0 && !r[1]);
+    EXPECT(bb::min_rank_reduce({bb::Rank{5}, std::nullopt, bb::Rank{2}}) == std::optional<bb::Rank>(2));
+    EXPECT((bb::mark_merges({0, 1, 0, 1}, toy, 0) == std::vector<std::uint8_t>{0, 1, 0, 1}));
+    EXPECT((bb::exclusive_scan({0, 1, 0, 1}) == std::vector<std::uint32_t>{0, 0, 1, 1}));
+    EXPECT((bb::compact({0, 1, 0, 1}, toy, {0, 1, 0, 1}, {0, 0, 1, 1}) == bb::TokenSeq{3, 3}));
+    threw = false;
+    try {
+      bb::exclusive_scan({0, 1, 1});
+    } catch (const bb::ContractViolation&) {
+      threw = true;
+    }
+    EXPECT(threw);
+    threw = false;
+    try {
+      bb::compact({2, 2}, toy, {0, 1}, {0, 0});  // compact_into's missing-pair check
+    } catch (const bb::ContractViolation&) {
+      threw = true;
+    }
+    EXPECT(threw);
+  }
+
   std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
   return failures ? 1 : 0;
 }
