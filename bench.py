@@ -236,6 +236,10 @@ def dist_init(args):
     if world > 1:
         import torch
         import torch.distributed as dist
+        if SHARED_GPU:  # test mode: every rank on GPU 0, gloo for the barriers and the max over ranks
+            local = 0
+            dist.init_process_group("gloo")
+            return rank, world, local
         if torch.cuda.device_count() < world:
             raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} GPU(s) visible")
         torch.cuda.set_device(local)
@@ -243,12 +247,18 @@ def dist_init(args):
     return rank, world, local
 
 
+# BBPE_BENCH_SHARED_GPU=1: run the N-rank path with every rank on device 0
+# (checks the sharding, aggregation and reporting of --gpus N on a one-GPU
+# box; the numbers are not a scaling measurement and the line says so).
+SHARED_GPU = os.environ.get("BBPE_BENCH_SHARED_GPU") == "1"
+
+
 def allreduce(world, value, op="max"):
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([float(value)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([float(value)], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -524,9 +534,39 @@ def main():
     rows_all = int(allreduce(world, n, "sum"))
     value = tokens_all / (ms / 1e3)
 
-    # ---- parity: the step's whole output vs the compiled reference ----
     ids_h = d_ids[:ntok].cpu().numpy().view(np.uint32)
     oo_h = d_oo.cpu().numpy().view(np.uint64)
+
+    # ---- end to end through the host API (pinned host buffers), right after
+    # the device timing and before the CPU-heavy legs ----
+    e2e = None
+    if not args.no_e2e:
+        h_data = torch.from_numpy(data).pin_memory()
+        h_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
+        h_ids = torch.empty(max(total, 1), dtype=torch.int32).pin_memory()
+        h_oo = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        hd, ho = h_data.numpy(), h_off.numpy().view(np.uint64)
+        hi, hoo = h_ids.numpy().view(np.uint32), h_oo.numpy().view(np.uint64)
+        tw, k = time.perf_counter(), 0
+        while k < max(5, args.warmup) or time.perf_counter() - tw < 0.5:
+            enc.encode_packed(table, hd, ho, hi, hoo)
+            k += 1
+        barrier(world)
+        times = []
+        for _ in range(max(10, args.steps)):
+            t0 = time.perf_counter()
+            enc.encode_packed(table, hd, ho, hi, hoo)
+            times.append(time.perf_counter() - t0)
+        assert np.array_equal(hoo, oo_h) and np.array_equal(hi[:ntok], ids_h), "e2e output differs from device"
+        e_ms = allreduce(world, float(np.median(times)) * 1e3, "max")
+        e2e = {"value": tokens_all / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(allreduce(world, total + (n + 1) * 8, "sum")),
+               "d2h_bytes_per_step": int(allreduce(world, ntok * 4 + (n + 1) * 8, "sum")),
+               "input_GBps": bytes_all / (e_ms / 1e3) / 1e9,
+               "timing": "median wall time of bbpe_encode (pinned host in, pinned host out), max over ranks"}
+        del h_data, h_off, h_ids, h_oo
+
+    # ---- parity: the step's whole output vs the compiled reference ----
     parity = None
     ref = None
     try:
@@ -573,34 +613,6 @@ def main():
         if pj.get("engine", "pieces") == args.engine:
             traffic = pj.get("traffic_bytes")
 
-    # ---- end to end through the host API (pinned host buffers) ----
-    e2e = None
-    if not args.no_e2e:
-        h_data = torch.from_numpy(data).pin_memory()
-        h_off = torch.from_numpy(offsets.view(np.int64)).pin_memory()
-        h_ids = torch.empty(max(total, 1), dtype=torch.int32).pin_memory()
-        h_oo = torch.empty(n + 1, dtype=torch.int64).pin_memory()
-        hd, ho = h_data.numpy(), h_off.numpy().view(np.uint64)
-        hi, hoo = h_ids.numpy().view(np.uint32), h_oo.numpy().view(np.uint64)
-        tw, k = time.perf_counter(), 0
-        while k < max(5, args.warmup) or time.perf_counter() - tw < 0.5:
-            enc.encode_packed(table, hd, ho, hi, hoo)
-            k += 1
-        barrier(world)
-        times = []
-        for _ in range(max(10, args.steps)):
-            t0 = time.perf_counter()
-            enc.encode_packed(table, hd, ho, hi, hoo)
-            times.append(time.perf_counter() - t0)
-        assert np.array_equal(hoo, oo_h) and np.array_equal(hi[:ntok], ids_h), "e2e output differs from device"
-        e_ms = allreduce(world, float(np.median(times)) * 1e3, "max")
-        e2e = {"value": tokens_all / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": int(allreduce(world, total + (n + 1) * 8, "sum")),
-               "d2h_bytes_per_step": int(allreduce(world, ntok * 4 + (n + 1) * 8, "sum")),
-               "input_GBps": bytes_all / (e_ms / 1e3) / 1e9,
-               "timing": "median wall time of bbpe_encode (pinned host in, pinned host out), max over ranks"}
-        del h_data, h_off, h_ids, h_oo
-
     cpu = None
     if rank == 0 and ref is not None and not args.no_cpu_baseline:
         cpu = cpu_baseline(w, ref, data, offsets, args.ref_seconds)
@@ -615,7 +627,8 @@ def main():
                                            f"inputs ({total / 2**20:.1f} MiB) smaller than 2x L2: a 252 MB buffer "
                                            "written before every step, its time measured alone and subtracted")),
             "engine": args.engine,
-            "parallelism": f"rows sharded, {world} independent GPU(s), no collective on the data path",
+            "parallelism": (f"rows sharded, {world} independent GPU(s), no collective on the data path" if not SHARED_GPU
+                            else f"TEST MODE: {world} ranks sharing GPU 0 (BBPE_BENCH_SHARED_GPU), not a scaling number"),
             "input_GBps": bytes_all / (ms / 1e3) / 1e9,
             "tokens_per_step": tokens_all, "rows_per_step": rows_all, "bytes_per_step": bytes_all,
             "gpu_launches": launches,
