@@ -200,6 +200,16 @@ def test_sharded_single_device_matches(gpt2):
     assert np.array_equal(oo, v["out_offsets"]) and np.array_equal(ids, v["ids"])
 
 
+def test_sharded_edge_cases(gpt2):
+    """Empty batch, empty rows only, fewer rows than contexts, one long row."""
+    encs = [bb.Encoder(0) for _ in range(3)]
+    for rows in ([], [b""], [b"", b"", b""], [b"hello"], [b"x" * 70000, b"", b"ab"]):
+        data, off = bb.pack_rows(rows)
+        want_ids, want_off, _ = bb.Encoder(0).encode_packed(gpt2, data, off)
+        ids, oo, _ = bb.encode_sharded(encs, gpt2, data, off)
+        assert np.array_equal(oo, want_off) and np.array_equal(ids, want_ids), rows[:2]
+
+
 @pytest.mark.parametrize("n_ctx", [2, 3, 4])
 def test_sharded_partitioned_path(gpt2, n_ctx):
     """bbpe_encode_sharded over n contexts on device 0 (the multi-GPU path

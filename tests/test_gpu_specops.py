@@ -27,6 +27,16 @@ def test_pair_ranks_toy(toy):  # test_block_engine.cpp:27-32
     assert bb.pair_ranks([], toy) == []
 
 
+def test_single_token_and_empty(toy):
+    assert bb.pair_ranks([3], toy) == []
+    assert bb.mark_merges([3], toy, 0) == [0]
+    assert bb.mark_merges([], toy, 0) == []
+    assert bb.exclusive_scan([0]) == [0]
+    assert bb.compact([3], toy, [0], [0]) == [3]
+    assert bb.compact([], toy, [], []) == []
+    assert bb.block_bpe_replay([], toy) == [] and bb.block_bpe_replay([2], toy) == [2]
+
+
 def test_min_rank_reduce():  # :34-41
     assert bb.min_rank_reduce([5, None, 2]) == 2
     assert bb.min_rank_reduce([None, None]) is None
