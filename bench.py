@@ -31,6 +31,10 @@ roofline  the dominant kernel (largest CUDA-event time): algorithmic bytes per
           average duration, against MEASURED_PEAKS.json; `step_frac` is the
           same bytes over the whole step. traffic = DRAM bytes of that kernel
           per launch from the committed ncu capture, when there is one.
+workloads (default line, one GPU) other DESIGN §5 workloads measured the same
+          way, each with its own parity: the paper's block-engine configuration
+          on this line's rows, cfg2-shaped mixed text, and cfg4 with the §8d
+          trained 200k-merge table (--no-workload-legs skips them).
 cpu_baseline  the unmodified reference encode_batch (oracle/_ref, block engine,
           PhasePool over all host cores) on a bounded sample of the same rows
           (+ its heap_bpe engine).
@@ -446,6 +450,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the §8f legs (decode, padding, JSONL, ...)")
+    ap.add_argument("--no-workload-legs", action="store_true",
+                    help="skip the other-workload legs of the default line (trained cfg4, block engine, mixed text)")
     ap.add_argument("--out", default=None, help="also write the JSON line to this file")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -594,6 +600,9 @@ def main():
         enc.set_config(piece_memo=True, dedup=True)
 
     decode = epilogue = jsonl = pattern = specials_line = None
+    workloads = None
+    if extras and world == 1 and not args.no_workload_legs:
+        workloads = workload_legs(args, bb, torch, stream, table, d_data, d_off, ids_h, oo_h, n, total)
     if extras:
         decode, epilogue, jsonl, pattern, specials_line = extra_legs(args, bb, enc, table, torch, stream, step,
                                                                      d_data, d_off, d_ids, d_oo, n, total, ntok)
@@ -644,6 +653,7 @@ def main():
             "merge_only": merge_only,
             "decode": decode, "epilogue": epilogue, "jsonl": jsonl, "pattern_mode": pattern,
             "specials_mode": specials_line,
+            "workloads": workloads,
             "clocks": clocks.summary(),
         }
         if w.shard:
@@ -656,6 +666,92 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def device_leg(bb, torch, table, data, offsets, engine, steps, warmup=2):
+    """Device-resident encode of one batch: (ms per step, tokens, ids, offsets,
+    per-kernel ms, piece stats), CUDA events on the encode stream."""
+    n, total = offsets.size - 1, int(offsets[-1])
+    enc = bb.Encoder(device=torch.cuda.current_device(), engine=engine)
+    enc.prepare(table)
+    dd = torch.from_numpy(data).cuda()
+    do = torch.from_numpy(offsets.view(np.int64)).cuda()
+    di = torch.empty(max(total, 1), dtype=torch.int32, device="cuda")
+    doo = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    st = torch.cuda.Stream()
+
+    def run():
+        enc.encode_device(table, dd.data_ptr(), do.data_ptr(), n, total, di.data_ptr(), doo.data_ptr(),
+                          stream=st.cuda_stream, sync=False)
+    for _ in range(warmup):
+        run()
+    enc.sync()
+    enc.kernel_times(reset=True)
+    enc.piece_stats(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(st):
+        e0.record(st)
+        for _ in range(steps):
+            run()
+        e1.record(st)
+    enc.sync()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    kt, kc = enc.kernel_times(reset=True)
+    ps = enc.piece_stats(reset=True)
+    ntok = int(doo[-1].item())
+    ids = di[:ntok].cpu().numpy().view(np.uint32)
+    oo = doo.cpu().numpy().view(np.uint64)
+    return ms, ntok, ids, oo, {k: v / max(kc, 1) for k, v in kt.items()}, ps
+
+
+def workload_legs(args, bb, torch, stream, table, d_data, d_off, ids_h, oo_h, n, total):
+    """Other workloads of DESIGN §5, measured in the default line so the driver
+    sees them (device-resident, CUDA events, every row checked):
+      * block_engine_cfg2: the paper's configuration (BBPE_ENGINE_BLOCK, every
+        row one piece) on this line's cfg2 rows; checked equal to the pieces
+        engine's output, which `parity` checked against the reference;
+      * mixed_text_cfg2: cfg2 shape, text the piece memo has not seen;
+      * trained_cfg4: cfg4 with SURVEY §8d's trained 200k-merge table (merges
+        cross words: every row is one long piece)."""
+    from oracle.oracle import Reference
+    out = {}
+    peak, _ = peaks()
+
+    def line(name, desc, ms, ntok, rows, nbytes, km, ps, par):
+        dom = max(km, key=km.get)
+        out[name] = {"workload": desc, "ms_per_step": ms, "tokens_per_s": ntok / (ms / 1e3),
+                     "input_GBps": nbytes / (ms / 1e3) / 1e9, "dominant_kernel": dom,
+                     "roofline_frac": (nbytes + 4 * ntok + 16 * rows) / (km[dom] / 1e3) / 1e9 / peak,
+                     "kernel_ms": km, "pieces": ps, "parity": par}
+
+    data = d_data.cpu().numpy()
+    offs = d_off.cpu().numpy().view(np.uint64)
+    ms, ntok, ids, oo, km, ps = device_leg(bb, torch, table, data, offs, "block", max(3, args.steps // 4))
+    same = bool(np.array_equal(oo, oo_h) and np.array_equal(ids, ids_h))
+    line("block_engine_cfg2", "cfg2 rows, --engine block (BBPE_ENGINE_BLOCK: every row one piece)", ms, ntok, n,
+         total, km, ps, {"rows_checked": n, "mismatches": 0 if same else None,
+                         "oracle": "equal to the pieces engine's output on every row (checked by `parity`)"})
+    assert same, "block engine differs from the pieces engine"
+
+    gen = WX.make_gen("mixed", None)
+    md, mo, _ = WX.config_rows(gen, 2, seed=2002)
+    ms, ntok, ids, oo, km, ps = device_leg(bb, torch, table, md, mo, "pieces", max(3, args.steps // 2))
+    ref = Reference.load_files(WT.GPT2_VOCAB, WT.GPT2_MERGES)
+    line("mixed_text_cfg2", f"{mo.size - 1} x 256 B, {TEXT_DESC['mixed']}", ms, ntok, mo.size - 1, int(mo[-1]), km, ps,
+         parity_check(ref, md, mo, ids, oo, 30.0))
+
+    from workloads.train import trained_table
+    tokens, merges, how = trained_table(*WT.gpt2_table(), 200000)
+    tdir = tempfile.mkdtemp(prefix="bbpe_trained_")
+    path = WT.write_canonical(os.path.join(tdir, "cfg4_trained.json"), tokens, merges)
+    ttable = bb.load_merge_table_files(path, None, "json")
+    td, to, desc = WX.config_rows(WX.TextGen(WX.word_list(WT.gpt2_table()[0])), 4)
+    ms, ntok, ids, oo, km, ps = device_leg(bb, torch, ttable, td, to, "pieces", 3)
+    tref = Reference.load_files(path, None, canonical=True)
+    line("trained_cfg4", f"cfg4: {desc}, table: {how}", ms, ntok, to.size - 1, int(to[-1]), km, ps,
+         parity_check(tref, td, to, ids, oo, 20.0))
+    return out
 
 
 def extra_legs(args, bb, enc, table, torch, stream, step, d_data, d_off, d_ids, d_oo, n, total, ntok):
