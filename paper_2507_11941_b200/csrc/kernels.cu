@@ -802,23 +802,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
     m = NONE;
     uint32_t hold = NONE;  // rank of pair (j-1, j) if it survives
     bool prev_merged = false;
+    // Branch-free (lanes sweep different pieces): selects and predicated
+    // stores instead of an if/else per position.
     while (i < n) {
       const uint32_t ri = (i < n - 1) ? rnk[i][lane] : NONE;
-      if (ri == mm) {
-        tok[j][lane] = M;
-        if (j > 0 && !prev_merged) pq[np++][lane] = static_cast<uint8_t>(j - 1);
-        pq[np++][lane] = static_cast<uint8_t>(j);
-        prev_merged = true;
-        hold = NONE;
-        i += 2;
-      } else {
-        m = min(m, hold);  // pair (j-1, j) keeps its rank
-        tok[j][lane] = tok[i][lane];
-        rnk[j][lane] = ri;
-        hold = ri;  // rank of pair (j, j+1), kept unless the next output is a merge
-        prev_merged = false;
-        i += 1;
-      }
+      const bool mg = ri == mm;
+      const Tk ti = tok[i][lane];
+      tok[j][lane] = mg ? M : ti;
+      if (mg && j > 0 && !prev_merged) pq[np++][lane] = static_cast<uint8_t>(j - 1);
+      if (mg) pq[np++][lane] = static_cast<uint8_t>(j);
+      if (!mg) rnk[j][lane] = ri;
+      m = mg ? m : min(m, hold);  // pair (j-1, j) keeps its rank
+      hold = mg ? NONE : ri;      // rank of pair (j, j+1), kept unless the next output is a merge
+      prev_merged = mg;
+      i += mg ? 2 : 1;
       ++j;
     }
     m = min(m, hold);
