@@ -784,7 +784,10 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 // from L2 and prefetch the next batch in every sweep; the other instance
 // takes the rest and lists those for it (separate kernels keep each one's
 // register allocation free of the other's prefetch buffers).
-constexpr uint64_t kPipeMin = 4 * (kLpSmemBytes / 8);
+#ifndef BBPE_PIPE_MIN_SEGS
+#define BBPE_PIPE_MIN_SEGS 4
+#endif
+constexpr uint64_t kPipeMin = BBPE_PIPE_MIN_SEGS * (kLpSmemBytes / 8);
 template <bool NARROW, bool PIPE>
 __global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
