@@ -198,7 +198,7 @@ struct bbpe_ctx {
   uint64_t* h_errs = nullptr;  // pinned: error slots of every wave of the last host encode
   size_t h_errs_cap = 0;
   // Device decode scratch and host-API staging.
-  DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff;
+  DevBuf dec_pos, dec_sums, dec_err, dec_ids, dec_toff, dec_out, dec_ooff, dec_rowbits;
   DevBuf pad_scalar;  // epilogue: widest row / truncated count
   DevBuf pstats;      // piece statistics (bbpe_ctx_piece_stats), PST_N u64
   bool stats_paused = false;  // the memo build's own encodes are not counted
@@ -1067,10 +1067,12 @@ uint64_t decode_on_device(bbpe_ctx& c, const bbpe_table& t, const uint32_t* d_id
   a.dec = static_cast<const uint64_t*>(rep.dec);
   a.dec_n = rep.dec_n;
   a.dec_bytes = static_cast<const uint8_t*>(rep.dec) + rep.dec_n * 8;
-  a.n_blocks = (n_ids + 255) / 256;
+  a.n_blocks = (n_ids + kDecodeBlockTokens - 1) / kDecodeBlockTokens;
   c.dec_pos.ensure(std::max<uint64_t>(n_ids, 1) * 8);
   c.dec_sums.ensure((a.n_blocks + 1) * 8);
   c.dec_err.ensure(8);
+  c.dec_rowbits.ensure(((n_ids + 31) / 32 + 1) * 4);
+  a.rowstart = c.dec_rowbits.as<uint32_t>();
   a.pos = c.dec_pos.as<uint64_t>();
   a.block_sums = c.dec_sums.as<uint64_t>();
   a.err = c.dec_err.as<uint64_t>();
@@ -1087,7 +1089,7 @@ uint64_t decode_on_device(bbpe_ctx& c, const bbpe_table& t, const uint32_t* d_id
   }
   ck(cudaMemsetAsync(a.err, 0xFF, 8, c.stream), "memset");
   launch_decode(a, c.stream);
-  c.launches += n_ids ? 4 : 1;
+  c.launches += n_ids ? (n_rows ? 5 : 4) : 1;
   ck(cudaGetLastError(), "decode launch");
   uint64_t res[2];
   ck(cudaMemcpyAsync(&res[0], a.err, 8, cudaMemcpyDeviceToHost, c.stream), "D2H");
@@ -1580,7 +1582,7 @@ int bbpe_ctx_destroy(bbpe_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->sc.release();
-    for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_sums,
+    for (DevBuf* b : {&c->in_bytes, &c->in_offsets, &c->out_ids, &c->out_offsets, &c->dec_pos, &c->dec_rowbits, &c->dec_sums,
                       &c->dec_err, &c->dec_ids, &c->dec_toff, &c->dec_out, &c->dec_ooff, &c->pad_scalar, &c->pstats,
                       &c->sp_blob, &c->sp_off, &c->sp_id, &c->sp_first, &c->sp_dec, &c->sp_cand, &c->sp_cnt, &c->sp_lit,
                       &c->sp_sums, &c->sp_segoff, &c->sp_segsrc, &c->sp_ids, &c->sp_compact, &c->sp_segtok,

@@ -7,9 +7,11 @@
 //
 // Device table: dec[id] = byte start << 24 | byte length (~0: no such token),
 // dense over ids 0..max_id, and the token bytes; built once per device.
-// Kernels: k_dec_len (token lengths, block-local exclusive scan, first bad
-// token), k_scan_totals (scan.cuh: block totals -> block bases, one CTA), k_dec_copy
-// (bytes gathered to their output position), k_dec_rows (row byte offsets).
+// Kernels: k_dec_mark (row-start tokens as bits), k_dec_len (block byte
+// totals, first bad token), k_scan_totals (scan.cuh: block totals -> block
+// bases, one CTA), k_dec_copy (block-local scan again; the block's bytes
+// assembled in shared memory and written with aligned 16-byte stores;
+// row-start tokens record their byte position), k_dec_rows (row byte offsets).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -25,7 +27,9 @@ constexpr int kDecThreads = 256;
 // decode (merge_table.hpp:565-579) of one id: the table's bytes, else the
 // special's; decode_batch's skip_specials drops special ids first
 // (batch.hpp:134-139). Returns false for an unknown id.
-__device__ __forceinline__ bool dec_entry(const DecodeArgs& a, uint32_t id, const uint8_t*& src, uint64_t& len) {
+__device__ __forceinline__ bool dec_entry(const DecodeArgs& a, uint32_t id, const uint8_t*& src, uint64_t& len,
+                                          bool& from_table) {
+  from_table = false;
   int k = -1;
   if (a.sp_n) {
     uint32_t lo = 0, hi = a.sp_n;
@@ -45,6 +49,7 @@ __device__ __forceinline__ bool dec_entry(const DecodeArgs& a, uint32_t id, cons
   if (e != ~0ull) {
     len = e & 0xFFFFFF;
     src = a.dec_bytes + (e >> 24);
+    from_table = true;
     return true;
   }
   if (k < 0) return false;
@@ -53,57 +58,151 @@ __device__ __forceinline__ bool dec_entry(const DecodeArgs& a, uint32_t id, cons
   return true;
 }
 
-__global__ void __launch_bounds__(kDecThreads) k_dec_len(DecodeArgs a) {
-  __shared__ uint64_t s_warp[kDecThreads / 32];
-  const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint64_t len = 0;
-  if (i < a.n_ids) {
-    const uint8_t* src;
-    if (!dec_entry(a, a.ids[i], src, len)) {
-      len = 0;
-      atomicMin(reinterpret_cast<unsigned long long*>(a.err), (unsigned long long)i);
-    }
-  }
-  uint64_t inc = len;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
-    if (lane >= d) inc += u;
-  }
-  if (lane == 31) s_warp[wid] = inc;
-  __syncthreads();
-  if (wid == 0) {
-    uint64_t x = lane < kDecThreads / 32 ? s_warp[lane] : 0;
-    uint64_t xi = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint64_t u = __shfl_up_sync(0xFFFFFFFFu, xi, d);
-      if (lane >= d) xi += u;
-    }
-    if (lane < kDecThreads / 32) s_warp[lane] = xi - x;
-    if (lane == 31) a.block_sums[blockIdx.x] = xi;
-  }
-  __syncthreads();
-  if (i < a.n_ids) a.pos[i] = s_warp[wid] + inc - len;
+// Row starts as token bits (k_dec_copy records their byte positions).
+__global__ void k_dec_mark(DecodeArgs a) {
+  const uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (r >= a.n_rows) return;
+  const uint64_t t = a.tok_off[r] - a.tok_off[0];
+  if (t < a.n_ids) atomicOr(a.rowstart + (t >> 5), 1u << (t & 31));
 }
 
+// A block decodes kDecBlockTok tokens: warp w takes tokens [256 w, 256 w +
+// 256) of the block in kDecTok rounds of 32 consecutive tokens (lane l: token
+// 32 k + l), so id loads are coalesced and the lanes of a round write
+// neighbouring bytes; the table lookups of a lane's rounds are in flight
+// together.
+constexpr int kDecTok = 8;
+constexpr int kDecBlockTok = kDecThreads * kDecTok;
+static_assert(kDecBlockTok == kDecodeBlockTokens, "host block count");
+
+__device__ __forceinline__ void dec_round_lengths(const DecodeArgs& a, uint64_t wbase, int lane,
+                                                  uint32_t (&len)[kDecTok], const uint8_t* (&src)[kDecTok],
+                                                  bool record_err, bool (&tabk)[kDecTok]) {
+  uint32_t id[kDecTok];
+#pragma unroll
+  for (int k = 0; k < kDecTok; ++k) {
+    const uint64_t t = wbase + 32 * k + lane;
+    id[k] = t < a.n_ids ? __ldg(a.ids + t) : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < kDecTok; ++k) {
+    const uint64_t t = wbase + 32 * k + lane;
+    uint64_t l = 0;
+    bool tab = false;
+    src[k] = nullptr;
+    if (t < a.n_ids && !dec_entry(a, id[k], src[k], l, tab)) {
+      l = 0;
+      if (record_err) atomicMin(reinterpret_cast<unsigned long long*>(a.err), (unsigned long long)t);
+    }
+    len[k] = uint32_t(l);
+    tabk[k] = tab;
+  }
+}
+
+__device__ __forceinline__ uint32_t warp_sum32(uint32_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+  return v;
+}
+
+// Token lengths -> block byte totals, and the first unknown id.
+__global__ void __launch_bounds__(kDecThreads) k_dec_len(DecodeArgs a) {
+  __shared__ uint64_t s_w[kDecThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t wbase = blockIdx.x * uint64_t(kDecBlockTok) + uint64_t(wid) * (32 * kDecTok);
+  uint32_t len[kDecTok];
+  bool tab[kDecTok];
+  const uint8_t* src[kDecTok];
+  dec_round_lengths(a, wbase, lane, len, src, true, tab);
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kDecTok; ++k) sum += len[k];
+  sum = warp_sum32(sum);
+  if (lane == 0) s_w[wid] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kDecThreads / 32; ++w) tot += s_w[w];
+    a.block_sums[blockIdx.x] = tot;
+  }
+}
+
+// The block's bytes: assembled in shared memory, then written as aligned
+// 16-byte stores (byte stores for the unaligned head and tail); blocks with
+// more than kDecStage bytes (very long tokens or specials) copy byte by byte.
+constexpr int kDecStage = 24576;
 __global__ void __launch_bounds__(kDecThreads) k_dec_copy(DecodeArgs a) {
-  const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
-  if (i >= a.n_ids) return;
-  const uint8_t* src;
-  uint64_t len;
-  if (!dec_entry(a, a.ids[i], src, len)) return;
-  const uint64_t pos = a.block_sums[blockIdx.x] + a.pos[i];
-  for (uint64_t k = 0; k < len && pos + k < a.cap; ++k) a.out[pos + k] = __ldg(src + k);
+  __shared__ uint64_t s_w[kDecThreads / 32 + 1];
+  __shared__ __align__(16) uint8_t s_out[kDecStage + 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t wbase = blockIdx.x * uint64_t(kDecBlockTok) + uint64_t(wid) * (32 * kDecTok);
+  uint32_t len[kDecTok];
+  bool tab[kDecTok];
+  const uint8_t* src[kDecTok];
+  dec_round_lengths(a, wbase, lane, len, src, false, tab);
+  uint32_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kDecTok; ++k) sum += len[k];
+  sum = warp_sum32(sum);
+  if (lane == 0) s_w[wid] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive warp bases, block total last
+    uint64_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kDecThreads / 32; ++w) {
+      const uint64_t v = s_w[w];
+      s_w[w] = run;
+      run += v;
+    }
+    s_w[kDecThreads / 32] = run;
+  }
+  __syncthreads();
+  const uint64_t btot = s_w[kDecThreads / 32];
+  const uint64_t base = a.block_sums[blockIdx.x];
+  const bool stage = btot <= kDecStage;
+  uint64_t off = s_w[wid];  // this round's first byte, block-relative
+#pragma unroll
+  for (int k = 0; k < kDecTok; ++k) {
+    uint32_t inc = len[k];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+      if (lane >= d) inc += u;
+    }
+    const uint64_t o = off + inc - len[k];
+    off += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    const uint64_t t = wbase + 32 * k + lane;
+    if (t < a.n_ids && ((a.rowstart[t >> 5] >> (t & 31)) & 1u)) a.pos[t] = base + o;
+    if (stage) {
+      for (uint32_t j = 0; j < len[k]; ++j) s_out[o + j] = __ldg(src[k] + j);
+    } else {
+      for (uint32_t j = 0; j < len[k] && base + o + j < a.cap; ++j) a.out[base + o + j] = __ldg(src[k] + j);
+    }
+  }
+  if (!stage) return;
+  __syncthreads();
+  const uint64_t end = min(base + btot, a.cap);
+  if (end <= base) return;
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(a.out);
+  const uint64_t a0 = min(end, base + ((16 - ((addr + base) & 15)) & 15));  // first 16-byte aligned position
+  const uint64_t a1 = a0 + ((end - a0) & ~uint64_t(15));                     // end of the aligned body
+  for (uint64_t p = base + threadIdx.x; p < a0; p += kDecThreads) a.out[p] = s_out[p - base];
+  for (uint64_t p = a1 + threadIdx.x; p < end; p += kDecThreads) a.out[p] = s_out[p - base];
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(s_out);
+  for (uint64_t p = a0 + 16 * uint64_t(threadIdx.x); p < a1; p += 16 * uint64_t(kDecThreads)) {
+    const uint32_t q = uint32_t(p - base), k = q >> 2, sh = (q & 3) * 8;
+    const uint32_t x0 = w[k], x1 = w[k + 1], x2 = w[k + 2], x3 = w[k + 3], x4 = w[k + 4];
+    *reinterpret_cast<uint4*>(a.out + p) = make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh),
+                                                      __funnelshift_r(x2, x3, sh), __funnelshift_r(x3, x4, sh));
+  }
 }
 
 __global__ void k_dec_rows(DecodeArgs a) {
   const uint64_t r = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (r > a.n_rows) return;
   const uint64_t t = a.tok_off[r] - a.tok_off[0];
-  const uint64_t b = t / kDecThreads;
-  a.out_off[r] = t >= a.n_ids ? a.block_sums[a.n_blocks] : a.block_sums[b] + a.pos[t];
+  a.out_off[r] = t >= a.n_ids ? a.block_sums[a.n_blocks] : a.pos[t];
 }
 
 // ---- JSON-lines text (write_batch_jsonl, batch.hpp:157-166): per row
@@ -227,6 +326,8 @@ void launch_jsonl(const JsonArgs& a, int sm_count, cudaStream_t s) {
 
 void launch_decode(const DecodeArgs& a, cudaStream_t s) {
   if (a.n_ids) {
+    cudaMemsetAsync(a.rowstart, 0, ((a.n_ids + 31) / 32) * 4, s);
+    if (a.n_rows) k_dec_mark<<<unsigned((a.n_rows + 255) / 256), 256, 0, s>>>(a);
     k_dec_len<<<unsigned(a.n_blocks), kDecThreads, 0, s>>>(a);
     k_scan_totals<<<1, 1024, 0, s>>>(a.block_sums, a.n_blocks);
     k_dec_copy<<<unsigned(a.n_blocks), kDecThreads, 0, s>>>(a);

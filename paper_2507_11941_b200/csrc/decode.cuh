@@ -7,6 +7,8 @@
 
 namespace bbpe {
 
+constexpr uint64_t kDecodeBlockTokens = 2048;  // tokens per k_dec_len / k_dec_copy block (256 threads x 8)
+
 struct DecodeArgs {
   const uint32_t* ids;       // n_ids token ids
   const uint64_t* tok_off;   // n_rows + 1 row offsets into ids (relative to tok_off[0])
@@ -15,7 +17,8 @@ struct DecodeArgs {
   const uint64_t* dec;       // dec_n entries: byte start << 24 | length, ~0 = unknown id
   uint64_t dec_n;
   const uint8_t* dec_bytes;
-  uint64_t* pos;             // n_ids: byte offset of each token within its block of 256
+  uint64_t* pos;             // n_ids: byte position of the row-start tokens (k_dec_copy)
+  uint32_t* rowstart;        // (n_ids + 31) / 32 words: bit t = token t starts a row
   uint64_t* block_sums;      // n_blocks + 1: block byte totals -> exclusive bases, total last
   uint64_t n_blocks;
   uint8_t* out;              // cap bytes
