@@ -1213,7 +1213,7 @@ int bbpe_jsonl_device(bbpe_ctx* c, const uint32_t* d_ids, const uint64_t* d_tok_
   a.out = d_out;
   a.cap = cap;
   bbpe::launch_jsonl(a, c->plan.sm_count, c->stream);
-  c->launches += (n_ids ? 2 : 0) + (n_rows ? 3 : 0);
+  c->launches += n_rows ? 4 : 0;
   ck(cudaGetLastError(), "jsonl launch");
   uint64_t t[2];
   ck(cudaMemcpyAsync(&t[0], a.tok_sums + a.n_tok_blocks, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");

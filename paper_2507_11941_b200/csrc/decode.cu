@@ -257,51 +257,98 @@ __device__ __forceinline__ uint64_t block_excl(uint64_t v, uint64_t* sums) {
   return s_warp[wid] + inc - v;
 }
 
-__global__ void __launch_bounds__(kDecThreads) k_json_tok(JsonArgs a) {
-  const uint64_t i = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
-  const uint64_t v = i < a.n_ids ? ndigits(a.ids[i]) + 1 : 0;
-  const uint64_t e = block_excl(v, a.tok_sums);
-  if (i < a.n_ids) a.tok_pos[i] = e;
+// Decimal digits of a u32 id (branch-free compares).
+__device__ __forceinline__ uint32_t ndigits32(uint32_t v) {
+  return 1u + (v >= 10u) + (v >= 100u) + (v >= 1000u) + (v >= 10000u) + (v >= 100000u) + (v >= 1000000u) +
+         (v >= 10000000u) + (v >= 100000000u) + (v >= 1000000000u);
 }
 
-__global__ void __launch_bounds__(kDecThreads) k_json_row(JsonArgs a) {
-  const uint64_t r = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
-  uint64_t v = 0;
-  if (r < a.n_rows) {
-    const uint64_t len = a.tok_off[r + 1] - a.tok_off[r];
-    v = 18 + ndigits(len) - (len > 0 ? 1 : 0);
-  }
-  const uint64_t e = block_excl(v, a.row_sums);
-  if (r < a.n_rows) a.row_pos[r] = e;
-}
-
-__device__ __forceinline__ uint64_t tok_text_pos(const JsonArgs& a, uint64_t i) {  // exclusive, i <= n_ids
-  return i >= a.n_ids ? a.tok_sums[a.n_tok_blocks] : a.tok_sums[i / kDecThreads] + a.tok_pos[i];
-}
-
-// Warp per row: lane per token; lane 0 writes the frame.
-__global__ void k_json_write(JsonArgs a) {
+// Row text lengths (warp per row): the frame plus every token's digits and comma.
+__global__ void __launch_bounds__(256) k_json_rowlen(JsonArgs a) {
   const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x / 32);
   const int lane = threadIdx.x & 31;
   for (uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5); r < a.n_rows; r += nw) {
     const uint64_t t0 = a.tok_off[r] - a.tok_off[0], t1 = a.tok_off[r + 1] - a.tok_off[0];
+    uint64_t s = 0;
+    for (uint64_t i = t0 + lane; i < t1; i += 32) s += ndigits32(__ldg(a.ids + i)) + 1;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, d);
     const uint64_t len = t1 - t0;
-    const uint64_t p0 = tok_text_pos(a, t0);
-    const uint64_t start = a.row_sums[r / kDecThreads] + a.row_pos[r] + p0;
-    for (uint64_t i = t0 + lane; i < t1; i += 32) {
-      const uint32_t id = a.ids[i];
-      const uint32_t d = ndigits(id);
-      const uint64_t pos = start + 8 + (tok_text_pos(a, i) - p0);
-      put_digits(a.out, pos, a.cap, id, d);
-      if (i + 1 < t1 && pos + d < a.cap) a.out[pos + d] = ',';
+    if (lane == 0) a.row_pos[r] = 18 + ndigits(len) - (len > 0 ? 1 : 0) + s;
+  }
+}
+
+// Row lengths -> exclusive positions within blocks of 256 rows, block totals.
+__global__ void __launch_bounds__(kDecThreads) k_json_rowscan(JsonArgs a) {
+  const uint64_t r = blockIdx.x * uint64_t(kDecThreads) + threadIdx.x;
+  const uint64_t v = r < a.n_rows ? a.row_pos[r] : 0;
+  const uint64_t e = block_excl(v, a.row_sums);
+  if (r < a.n_rows) a.row_pos[r] = e;
+}
+
+// The text (warp per row): tokens 32 at a time, their digits and commas laid
+// out in a per-warp shared buffer by a warp scan, then written with
+// consecutive lanes on consecutive bytes.
+__global__ void __launch_bounds__(256) k_json_write(JsonArgs a) {
+  __shared__ uint8_t s_buf[8][32 * 11 + 8];
+  const uint64_t nw = uint64_t(gridDim.x) * (blockDim.x / 32);
+  const int lane = threadIdx.x & 31;
+  uint8_t* buf = s_buf[threadIdx.x >> 5];
+  const uint64_t tb = a.tok_off[0];
+  // The next row's offsets and position are loaded while this row is written.
+  uint64_t r = blockIdx.x * uint64_t(blockDim.x / 32) + (threadIdx.x >> 5);
+  uint64_t n_o0 = 0, n_o1 = 0, n_s = 0, n_p = 0;
+  if (r < a.n_rows) {
+    n_o0 = a.tok_off[r];
+    n_o1 = a.tok_off[r + 1];
+    n_s = a.row_sums[r / kDecThreads];
+    n_p = a.row_pos[r];
+  }
+  for (; r < a.n_rows; r += nw) {
+    const uint64_t t0 = n_o0 - tb, t1 = n_o1 - tb;
+    const uint64_t len = t1 - t0;
+    const uint64_t start = n_s + n_p;
+    const uint64_t rn = r + nw;
+    if (rn < a.n_rows) {
+      n_o0 = a.tok_off[rn];
+      n_o1 = a.tok_off[rn + 1];
+      n_s = a.row_sums[rn / kDecThreads];
+      n_p = a.row_pos[rn];
+    }
+    if (lane == 0) put_str(a.out, start, a.cap, "{\"ids\":[", 8);
+    uint64_t pos = start + 8;
+    for (uint64_t c0 = t0; c0 < t1; c0 += 32) {
+      const uint64_t i = c0 + lane;
+      const bool valid = i < t1;
+      const uint32_t id = valid ? __ldg(a.ids + i) : 0u;
+      const uint32_t d = valid ? ndigits32(id) : 0u;
+      const bool comma = valid && i + 1 < t1;
+      const uint32_t w = d + (comma ? 1u : 0u);
+      uint32_t inc = w;
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, inc, k);
+        if (lane >= k) inc += u;
+      }
+      const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      const uint32_t o = inc - w;
+      uint32_t v = id;
+      for (int k = int(d) - 1; k >= 0; --k) {
+        buf[o + k] = uint8_t('0' + v % 10);
+        v /= 10;
+      }
+      if (comma) buf[o + d] = ',';
+      __syncwarp();
+      for (uint32_t b = lane; b < total; b += 32)
+        if (pos + b < a.cap) a.out[pos + b] = buf[b];
+      __syncwarp();
+      pos += total;
     }
     if (lane == 0) {
-      put_str(a.out, start, a.cap, "{\"ids\":[", 8);
-      const uint64_t q = start + 8 + (tok_text_pos(a, t1) - p0) - (len > 0 ? 1 : 0);
-      put_str(a.out, q, a.cap, "],\"len\":", 8);
+      put_str(a.out, pos, a.cap, "],\"len\":", 8);
       const uint32_t d = ndigits(len);
-      put_digits(a.out, q + 8, a.cap, len, d);
-      put_str(a.out, q + 8 + d, a.cap, "}\n", 2);
+      put_digits(a.out, pos + 8, a.cap, len, d);
+      put_str(a.out, pos + 8 + d, a.cap, "}\n", 2);
     }
   }
 }
@@ -309,14 +356,11 @@ __global__ void k_json_write(JsonArgs a) {
 }  // namespace
 
 void launch_jsonl(const JsonArgs& a, int sm_count, cudaStream_t s) {
-  if (a.n_ids) {
-    k_json_tok<<<unsigned(a.n_tok_blocks), kDecThreads, 0, s>>>(a);
-    k_scan_totals<<<1, 1024, 0, s>>>(a.tok_sums, a.n_tok_blocks);
-  } else {
-    cudaMemsetAsync(a.tok_sums, 0, 8, s);
-  }
+  // Row positions carry the whole text: the token-level total stays zero.
+  cudaMemsetAsync(a.tok_sums + a.n_tok_blocks, 0, 8, s);
   if (a.n_rows) {
-    k_json_row<<<unsigned(a.n_row_blocks), kDecThreads, 0, s>>>(a);
+    k_json_rowlen<<<unsigned(sm_count * 8), 256, 0, s>>>(a);
+    k_json_rowscan<<<unsigned(a.n_row_blocks), kDecThreads, 0, s>>>(a);
     k_scan_totals<<<1, 1024, 0, s>>>(a.row_sums, a.n_row_blocks);
     k_json_write<<<unsigned(sm_count * 8), 256, 0, s>>>(a);
   } else {
