@@ -1119,6 +1119,9 @@ __device__ __forceinline__ uint32_t compact_at(const GatherSmem& G, uint32_t slo
 #ifndef BBPE_GATHER_MINB
 #define BBPE_GATHER_MINB 4
 #endif
+#ifndef BBPE_GATHER_EAGER
+#define BBPE_GATHER_EAGER 6  // 32-slot steps loaded before the tile's slot count is known to need more
+#endif
 __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(EncodeArgs a, DevTable T) {
   __shared__ GatherSmem s_g[kWarpsPerCta];
   (void)T;
@@ -1147,11 +1150,26 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_GATHER_MINB) k_gather(
     meta(t + nwarps);
     const uint32_t* stage = a.staging + t * kStage;
     uint32_t* out = a.out_ids + tbase;
+    // Typical tiles use ~130 slots: the first kGatherEager steps are loaded
+    // unconditionally (all in flight at once), the rest only when the tile
+    // has that many slots (warp-uniform branch), so rare full tiles do not
+    // cost every tile their load instructions.
+    constexpr int kGatherEager = BBPE_GATHER_EAGER;
     uint32_t xs[kStageIt];
 #pragma unroll
-    for (int j = 0; j < kStageIt; ++j) {
+    for (int j = 0; j < kGatherEager; ++j) {
       const uint32_t v = 32 * j + lane;
       xs[j] = v < nslots ? __ldcs(stage + v) : kSentinel;
+    }
+    if (nslots > 32u * kGatherEager) {
+#pragma unroll
+      for (int j = kGatherEager; j < kStageIt; ++j) {
+        const uint32_t v = 32 * j + lane;
+        xs[j] = v < nslots ? __ldcs(stage + v) : kSentinel;
+      }
+    } else {
+#pragma unroll
+      for (int j = kGatherEager; j < kStageIt; ++j) xs[j] = kSentinel;
     }
     uint64_t roff = 0;
     if (s0 + lane < s1 && s0 + lane <= a.n_rows) roff = __ldcg(a.out_offsets + s0 + lane);
