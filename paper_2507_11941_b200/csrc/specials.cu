@@ -79,8 +79,21 @@ __device__ __forceinline__ uint32_t sp_match(const SpecArgs& S, const uint8_t* b
 __global__ void __launch_bounds__(256) k_sp_cand(const uint8_t* bytes, uint64_t total, SpecArgs sp,
                                                  uint32_t* cand) {
   __shared__ uint32_t s_first[8];
+  __shared__ uint32_t s_fb[4];  // up to 4 distinct first bytes, each replicated into the 4 byte lanes
+  __shared__ int s_nfb;         // their number, or -1 for more (bitmap test per byte)
   if (threadIdx.x < 8) s_first[threadIdx.x] = sp.first[threadIdx.x];
   __syncthreads();
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int c = 0; c < 256; ++c)
+      if ((s_first[c >> 5] >> (c & 31)) & 1u) {
+        if (k < 4) s_fb[k] = uint32_t(c) * 0x01010101u;
+        ++k;
+      }
+    s_nfb = k <= 4 ? k : -1;
+  }
+  __syncthreads();
+  const int nfb = s_nfb;
   const uint64_t nw = (total + 31) / 32, stride = uint64_t(gridDim.x) * blockDim.x;
   const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
   for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < nw; w += stride) {
@@ -96,13 +109,26 @@ __global__ void __launch_bounds__(256) k_sp_cand(const uint8_t* bytes, uint64_t 
       for (int k = 0; k < 8; ++k) v[k] = 0;
       for (uint64_t p = p0; p < p1; ++p) v[(p - p0) >> 2] |= uint32_t(__ldg(bytes + p)) << (8 * ((p - p0) & 3));
     }
+    uint32_t maybe = 0;  // bit k: byte k is a special's first byte
+    if (nfb >= 0) {      // few first bytes: 4-byte SIMD compares
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const uint32_t c = (v[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-      if (((s_first[c >> 5] >> (c & 31)) & 1u) && p0 + k < p1) {
-        uint32_t id;
-        if (sp_match(sp, bytes, p0 + k, total, id)) bits |= 1u << k;
+      for (int k = 0; k < 8; ++k) {
+        uint32_t m = 0;
+        for (int f = 0; f < nfb; ++f) m |= __vcmpeq4(v[k], s_fb[f]);
+        maybe |= (((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u)) << (4 * k);
       }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t c = (v[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        maybe |= ((s_first[c >> 5] >> (c & 31)) & 1u) << k;
+      }
+    }
+    if (p1 - p0 < 32) maybe &= (1u << (p1 - p0)) - 1u;
+    for (; maybe; maybe &= maybe - 1) {  // rare: the full match at each candidate
+      const int k = __ffs(maybe) - 1;
+      uint32_t id;
+      if (sp_match(sp, bytes, p0 + k, total, id)) bits |= 1u << k;
     }
     cand[w] = bits;
   }
