@@ -60,12 +60,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_add(uint64_t* v, uint64_t
   if (i == 0) v[n] = sums[nb];
 }
 
+// The 4 bytes at b[p..p+4) as a little-endian word (byte loads: p is unaligned).
+__device__ __forceinline__ uint32_t load4(const uint8_t* b) {
+  return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+}
+
 __device__ __forceinline__ uint32_t sp_match(const SpecArgs& S, const uint8_t* b, uint64_t p, uint64_t end,
                                              uint32_t& id) {
   for (uint32_t i = 0; i < S.n; ++i) {
     const uint32_t o = S.off[i], len = S.off[i + 1] - o;
     if (len > end - p) continue;
     uint32_t k = 0;
+    // four bytes per step (all loads of a step independent), then the tail
+    while (k + 4 <= len && load4(b + p + k) == load4(S.blob + o + k)) k += 4;
+    if (k + 4 <= len) continue;  // a word differed
     while (k < len && b[p + k] == S.blob[o + k]) ++k;
     if (k == len) {
       id = S.id[i];
@@ -94,6 +102,9 @@ __global__ void __launch_bounds__(256) k_sp_cand(const uint8_t* bytes, uint64_t 
   }
   __syncthreads();
   const int nfb = s_nfb;
+  // the first bytes in registers; unused ones repeat the first (no effect on the OR)
+  const uint32_t fb0 = nfb > 0 ? s_fb[0] : 0u, fb1 = nfb > 1 ? s_fb[1] : fb0, fb2 = nfb > 2 ? s_fb[2] : fb0,
+                 fb3 = nfb > 3 ? s_fb[3] : fb0;
   const uint64_t nw = (total + 31) / 32, stride = uint64_t(gridDim.x) * blockDim.x;
   const bool aligned = (reinterpret_cast<uintptr_t>(bytes) & 15) == 0;
   for (uint64_t w = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; w < nw; w += stride) {
@@ -110,14 +121,13 @@ __global__ void __launch_bounds__(256) k_sp_cand(const uint8_t* bytes, uint64_t 
       for (uint64_t p = p0; p < p1; ++p) v[(p - p0) >> 2] |= uint32_t(__ldg(bytes + p)) << (8 * ((p - p0) & 3));
     }
     uint32_t maybe = 0;  // bit k: byte k is a special's first byte
-    if (nfb >= 0) {      // few first bytes: 4-byte SIMD compares
+    if (nfb > 0) {       // few first bytes: 4-byte SIMD compares
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        uint32_t m = 0;
-        for (int f = 0; f < nfb; ++f) m |= __vcmpeq4(v[k], s_fb[f]);
+        const uint32_t m = __vcmpeq4(v[k], fb0) | __vcmpeq4(v[k], fb1) | __vcmpeq4(v[k], fb2) | __vcmpeq4(v[k], fb3);
         maybe |= (((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u)) << (4 * k);
       }
-    } else {
+    } else if (nfb < 0) {
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const uint32_t c = (v[k >> 2] >> (8 * (k & 3))) & 0xFFu;
