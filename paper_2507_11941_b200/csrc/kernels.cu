@@ -271,6 +271,33 @@ __device__ __forceinline__ ulonglong2 cas128(ulonglong2* p, ulonglong2 cmp, ulon
   return old;
 }
 
+// Bytes [p, p + 8k) of the input as k little-endian u64 words (k <= 3),
+// from the aligned 8-byte words that cover them: independent loads in flight
+// together, instead of one dependent byte load per position. Words wholly
+// inside [bytes, bytes + total) only; the rare span whose last word would
+// reach past the end (the input's final bytes) is read byte by byte. Bytes at
+// or past `total` read as 0 on that path; callers use the first len bytes.
+template <int K>
+__device__ __forceinline__ void ld_span(const uint8_t* __restrict__ bytes, uint64_t total, uint64_t p, uint64_t (&v)[K]) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(bytes + p);
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(addr & ~uintptr_t(7));
+  const int sh = int(addr & 7) * 8;
+  if (reinterpret_cast<uintptr_t>(w + K + 1) <= reinterpret_cast<uintptr_t>(bytes + total)) {
+    uint64_t x[K + 1];
+#pragma unroll
+    for (int k = 0; k <= K; ++k) x[k] = __ldg(w + k);
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = sh ? (x[k] >> sh) | (x[k + 1] << (64 - sh)) : x[k];
+  } else {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k] = 0;
+      for (int j = 0; j < 8; ++j)
+        if (p + 8 * k + j < total) v[k] |= uint64_t(__ldg(bytes + p + 8 * k + j)) << (8 * j);
+    }
+  }
+}
+
 // Within-call dedupe of merge pieces: finds or claims the slot of `key`.
 // Returns the slot (the caller owns it: its merge passes run), the slot with
 // bit 63 set (another piece with the same bytes owns it: copy its result),
@@ -730,7 +757,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
           if (i < n) tok[i][lane] = Tk(s_lut[(b8 >> (8 * i)) & 0xFF]);
           pq[i][lane] = static_cast<uint8_t>(i);
         }
-        if (n > 8) {  // bytes past the record's 8 (rare)
+        if (n > 8) {  // bytes past the record's 8: word loads, then the lut
+          static_assert(kLmax <= 32, "three words past the record's 8 bytes");
           const uint8_t* src = a.bytes + (rec >> 16);
           for (int i = 8; i < n; ++i) {
             tok[i][lane] = Tk(s_lut[__ldg(src + i)]);
@@ -831,12 +859,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, BBPE_MERGE_MINB) k_merge(En
 // owner and is listed for k_merge, the others become references (k_refs copies
 // the owner's tokens). Exact: a piece's encoding depends on its bytes only.
 // Longer pieces (and full neighbourhoods) are listed as owners of themselves.
-__global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
+// Owners are listed through one atomicAdd per CTA and step (warp counts
+// scanned in shared memory), not one per warp on the shared counter.
+constexpr int kDedupThreads = 256;
+__global__ void __launch_bounds__(kDedupThreads) k_dedup(EncodeArgs a) {
+  __shared__ uint32_t s_cnt[kDedupThreads / 32 + 1];
   const uint64_t nrec = min((uint64_t)a.counters[CNT_MREC], a.mrec_cap);
-  const int lane = threadIdx.x & 31;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  const uint64_t i0 = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  for (uint64_t i = i0; i - lane < nrec; i += stride) {  // warp-uniform trip count
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t stride = uint64_t(gridDim.x) * kDedupThreads;
+  for (uint64_t b0 = blockIdx.x * uint64_t(kDedupThreads); b0 < nrec; b0 += stride) {  // CTA-uniform trip count
+    const uint64_t i = b0 + threadIdx.x;
     bool owner = false;
     uint64_t oslot = 0;
     if (i < nrec) {
@@ -847,8 +879,12 @@ __global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
         if (len <= kDedupMax) {
           const uint64_t k0 = len >= 8 ? r.y : (r.y & ((1ull << (8 * len)) - 1));
           uint64_t k1 = 0;
-          const uint8_t* src = a.bytes + (r.x >> 16);
-          for (int j = 8; j < len; ++j) k1 |= uint64_t(__ldg(src + j)) << (8 * (j - 8));
+          if (len > 8) {  // bytes 8 .. len-1 (<= 7 of them)
+            static_assert(kDedupMax < 16, "one word past the record's 8 bytes");
+            uint64_t v[1];
+            ld_span<1>(a.bytes, a.total, (r.x >> 16) + 8, v);
+            k1 = v[0] & ((1ull << (8 * (len - 8))) - 1);
+          }
           res = dedup_claim(a.dkey, a.dmask, make_ulonglong2(k0, k1 | (uint64_t(len) << 56)));
         }
         if (res != ~0ull && (res >> 63)) {
@@ -860,10 +896,25 @@ __global__ void __launch_bounds__(256) k_dedup(EncodeArgs a) {
       }
     }
     const unsigned om = __ballot_sync(kFull, owner);
-    uint32_t b = 0;
-    if (lane == 0 && om) b = atomicAdd(&a.counters[CNT_OWNERS], uint32_t(__popc(om)));
-    b = __shfl_sync(kFull, b, 0);
-    if (owner) a.owners[b + __popc(om & lanemask_lt(lane))] = i | (oslot << 32);
+    if (lane == 0) s_cnt[wid] = __popc(om);
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t c = lane < kDedupThreads / 32 ? s_cnt[lane] : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int d = 1; d < kDedupThreads / 32; d <<= 1) {
+        const uint32_t u = __shfl_up_sync(kFull, inc, d);
+        if (lane >= d) inc += u;
+      }
+      const uint32_t tot = __shfl_sync(kFull, inc, kDedupThreads / 32 - 1);
+      uint32_t b = 0;
+      if (lane == 0 && tot) b = atomicAdd(&a.counters[CNT_OWNERS], tot);
+      b = __shfl_sync(kFull, b, 0);
+      if (lane < kDedupThreads / 32) s_cnt[lane] = b + inc - c;
+    }
+    __syncthreads();
+    if (owner) a.owners[s_cnt[wid] + __popc(om & lanemask_lt(lane))] = i | (oslot << 32);
+    __syncthreads();  // s_cnt is rewritten by the next step
   }
 }
 

@@ -1,5 +1,5 @@
 """Long-piece tier probe for ncu: one workload encoded `reps` times on the
-device (digits | runs_a | cfg4t | cfg2 | mixed | block2).  python tools/lp_probe.py digits 3"""
+device (digits | runs_a | cfg4t | cfg4w | mixed4w | cfg2 | mixed | block2).  python tools/lp_probe.py digits 3"""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -18,6 +18,11 @@ if case in ("cfg2", "mixed", "block2"):
     gen = WX.make_gen("mixed" if case == "mixed" else "zipf", WT.gpt2_table()[0])
     data, off, _ = WX.config_rows(gen, 2, seed=2000)
     engine = "block" if case == "block2" else "pieces"
+elif case in ("cfg4w", "mixed4w"):  # the word-level 200k table (wide keys): zipf / mixed text
+    tokens, m = WT.extend_wordlevel(*WT.gpt2_table(), 200000)
+    t = bb.MergeTable.from_arrays(*WT.arrays(tokens, m))
+    gen = WX.make_gen("mixed", WT.gpt2_table()[0]) if case == "mixed4w" else WX.TextGen(WX.word_list(tokens))
+    data, off, _ = WX.config_rows(gen, 4 if case == "cfg4w" else 2, seed=2000)
 elif case == "cfg4t":
     from workloads import train
     tokens, m, _ = train.trained_table(*WT.gpt2_table(), 200000)
