@@ -33,6 +33,7 @@
 // through generic pointers.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "kernels.cuh"
@@ -442,6 +443,15 @@ constexpr uint32_t kEvenLanes = 0x55555555u, kOddLanes = 0xAAAAAAAAu;
 #ifndef BBPE_SP_UB
 #define BBPE_SP_UB 4
 #endif
+#ifndef BBPE_PIPE_UA
+#define BBPE_PIPE_UA 8
+#endif
+#ifndef BBPE_PIPE_UB
+#define BBPE_PIPE_UB 2
+#endif
+#ifndef BBPE_PIPE_UC
+#define BBPE_PIPE_UC 2
+#endif
 #ifndef BBPE_SP_UC
 #define BBPE_SP_UC 4
 #endif
@@ -504,7 +514,7 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     // steps from i). The carry between segments is one parity bit; the ballots
     // do not depend on it, so consecutive segments overlap.
     {
-      constexpr int U = PIPE ? 8 : BBPE_SP_UA;
+      constexpr int U = PIPE ? BBPE_PIPE_UA : BBPE_SP_UA;
       uint32_t r_next0 = kNoRank, c = 0;
       // Software-pipelined: the next batch's loads are in flight while this
       // one is processed (the L2 path's latency).
@@ -554,7 +564,7 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     bool any = false;
     uint32_t C = kNoRank;
     {
-      constexpr int U = PIPE ? 4 : BBPE_SP_UB;
+      constexpr int U = PIPE ? BBPE_PIPE_UB : BBPE_SP_UB;
       // window: [0] = segment s0-2, [1] = s0-1, [2 + u] = s0 + u
       uint32_t wx[U + 2], wr[U + 2], wm[U + 2];
       wx[0] = wx[1] = 0u;
@@ -658,7 +668,7 @@ __device__ void run_piece_sp(const EncodeArgs& a, const DevTable& T, const uint3
     // (destinations never pass the position being read), re-rank the pairs
     // whose tokens changed.
     {
-      constexpr int U = PIPE ? 4 : BBPE_SP_UC;
+      constexpr int U = PIPE ? BBPE_PIPE_UC : BBPE_SP_UC;
       uint32_t q0 = 0, ap_prev = 0;
       // Segments s0..s0+U (one of lookahead); segments s0+U+1.. of the next
       // batch are loaded before this batch's writes, which only reach
@@ -780,16 +790,22 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 
 // The super-pass engine, same ticketing (used unless a pass cap, a trace or
 // caller tokens ask for the pass-by-pass engine above).
-// Two instances: PIPE = pieces longer than kPipeMin positions, which stream
-// from L2 and prefetch the next batch in every sweep; the other instance
-// takes the rest and lists those for it (separate kernels keep each one's
-// register allocation free of the other's prefetch buffers).
+// Two instances: PIPE = pieces longer than kPipeMin positions (by default
+// the shared working set's capacity), which stream from L2 and prefetch the
+// next batch in every sweep; the other instance takes the rest and lists
+// those for it. Separate kernels keep each one's register allocation free of
+// the other's prefetch buffers, and give PIPE its own residency: no shared
+// working set, so BBPE_PIPE_MINB CTAs per SM (5: 20 warps, 96 registers,
+// phases B/C unrolled 2 segments deep) against the shared-memory instance's 3.
 #ifndef BBPE_PIPE_MIN_SEGS
-#define BBPE_PIPE_MIN_SEGS 4
+#define BBPE_PIPE_MIN_SEGS 1
 #endif
 constexpr uint64_t kPipeMin = BBPE_PIPE_MIN_SEGS * (kLpSmemBytes / 8);
+#ifndef BBPE_PIPE_MINB
+#define BBPE_PIPE_MINB 5
+#endif
 template <bool NARROW, bool PIPE>
-__global__ void __launch_bounds__(kLpWarps * 32, kLpMinBlocks) k_long_sp(EncodeArgs a, DevTable T) {
+__global__ void __launch_bounds__(kLpWarps * 32, PIPE ? BBPE_PIPE_MINB : kLpMinBlocks) k_long_sp(EncodeArgs a, DevTable T) {
   __shared__ uint32_t s_lut[256];
   extern __shared__ __align__(16) unsigned char s_lp[];
   // PIPE = false: every long piece by ticket; the ones above kPipeMin are
@@ -875,6 +891,10 @@ size_t long_pieces_smem(bool narrow) {
   return size_t(kLpWarps) * (narrow ? lp_warp_bytes<true>() : lp_warp_bytes<false>());
 }
 
+// Resident CTAs per SM of the PIPE instance (no shared working set: its
+// pieces stream from the global scratch, so only registers bound it).
+static int g_pipe_per_sm = 0, g_sm_count = 0;
+
 int long_pieces_grid(int device, int sm_count) {
   (void)device;
   const size_t sn = long_pieces_smem(true), sw = long_pieces_smem(false);
@@ -884,9 +904,14 @@ int long_pieces_grid(int device, int sm_count) {
   cudaFuncSetAttribute(k_long_sp<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
   cudaFuncSetAttribute(k_long_sp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
   cudaFuncSetAttribute(k_long_sp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
-  int per_sm = 0;
+  int per_sm = 0, pn = 0, pw = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_long_pieces<true>, kLpWarps * 32, sn);
-  return sm_count * (per_sm > 0 ? per_sm : 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pn, k_long_sp<true, true>, kLpWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k_long_sp<false, true>, kLpWarps * 32, 0);
+  per_sm = per_sm > 0 ? per_sm : 1;
+  g_pipe_per_sm = std::max(1, std::min(pn, pw));
+  g_sm_count = sm_count;
+  return sm_count * per_sm;
 }
 
 int launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStream_t stream) {
@@ -897,12 +922,14 @@ int launch_long_pieces(const EncodeArgs& a, const DevTable& t, int grid, cudaStr
     else k_long_pieces<false><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
     return 1;
   }
+  // The PIPE instance: same SMs, its own residency (grid = SMs x its CTAs per SM).
+  const int pgrid = g_sm_count > 0 ? g_sm_count * g_pipe_per_sm : grid;
   if (t.key32) {  // 16-bit ids and ranks
     k_long_sp<true, false><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
-    k_long_sp<true, true><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+    k_long_sp<true, true><<<pgrid, kLpWarps * 32, 0, stream>>>(a, t);
   } else {
     k_long_sp<false, false><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
-    k_long_sp<false, true><<<grid, kLpWarps * 32, sm, stream>>>(a, t);
+    k_long_sp<false, true><<<pgrid, kLpWarps * 32, 0, stream>>>(a, t);
   }
   return 2;
 }

@@ -55,7 +55,8 @@ for name, (mk, L) in cases.items():
     torch.cuda.synchronize(); e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(3):
-        enc.encode_device(t, dd.data_ptr(), do.data_ptr(), n, tot, di.data_ptr(), doo.data_ptr(), sync=False)
+        enc.encode_device(t, dd.data_ptr(), do.data_ptr(), n, tot, di.data_ptr(), doo.data_ptr(), sync=False,
+                          stream=torch.cuda.current_stream().cuda_stream)
     e1.record(); torch.cuda.synchronize()
     kt, kc = enc.kernel_times(reset=True)
     ps = enc.piece_stats(reset=True)
