@@ -23,14 +23,14 @@ constexpr int kTilesPerTicket = 4;  // k_pieces: consecutive tiles per ticket
 #define BBPE_LP_WARPS 4
 #endif
 #ifndef BBPE_LP_MINB
-#define BBPE_LP_MINB 3
+#define BBPE_LP_MINB 6
 #endif
 #ifndef BBPE_LP_SMEM
-#define BBPE_LP_SMEM 16384
+#define BBPE_LP_SMEM 8192
 #endif
-constexpr int kLpMinBlocks = BBPE_LP_MINB;  // k_long_pieces / k_long_sp: resident CTAs per SM (register cap)
+constexpr int kLpMinBlocks = BBPE_LP_MINB;  // k_long_sp (shared-memory instance): resident CTAs per SM (register cap)
 constexpr int kLpWarps = BBPE_LP_WARPS;     // k_long_pieces: warps per CTA (one piece per warp)
-constexpr int kLpSmemBytes = BBPE_LP_SMEM;  // k_long_pieces: shared-memory positions per warp (4096 narrow / 2048 wide)
+constexpr int kLpSmemBytes = BBPE_LP_SMEM;  // long pieces: shared-memory bytes per warp (k_long_sp: 1024 positions)
 constexpr int kWinVec = (kTile + 48) / 16;  // 16-byte chunks of a tile window: bytes [b0-16, b0+kTile+32)
 constexpr int kRowWords = kTile / 32 + 4;   // row-start bit words copied per tile (whole 16-byte chunks)
 constexpr int kMrecChunk = 256;     // merge records a warp reserves at a time

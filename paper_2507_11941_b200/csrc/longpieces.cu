@@ -441,7 +441,7 @@ constexpr uint32_t kEvenLanes = 0x55555555u, kOddLanes = 0xAAAAAAAAu;
 #define BBPE_SP_UA 8
 #endif
 #ifndef BBPE_SP_UB
-#define BBPE_SP_UB 4
+#define BBPE_SP_UB 2
 #endif
 #ifndef BBPE_PIPE_UA
 #define BBPE_PIPE_UA 8
@@ -453,7 +453,7 @@ constexpr uint32_t kEvenLanes = 0x55555555u, kOddLanes = 0xAAAAAAAAu;
 #define BBPE_PIPE_UC 2
 #endif
 #ifndef BBPE_SP_UC
-#define BBPE_SP_UC 4
+#define BBPE_SP_UC 2
 #endif
 
 template <bool NARROW, bool PIPE>
@@ -796,7 +796,8 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 // those for it. Separate kernels keep each one's register allocation free of
 // the other's prefetch buffers, and give PIPE its own residency: no shared
 // working set, so BBPE_PIPE_MINB CTAs per SM (5: 20 warps, 96 registers,
-// phases B/C unrolled 2 segments deep) against the shared-memory instance's 3.
+// phases B/C unrolled 2 segments deep); the shared-memory instance runs
+// kLpMinBlocks (6: 24 warps, 80 registers, 8 KB slices).
 #ifndef BBPE_PIPE_MIN_SEGS
 #define BBPE_PIPE_MIN_SEGS 1
 #endif
@@ -905,7 +906,7 @@ int long_pieces_grid(int device, int sm_count) {
   cudaFuncSetAttribute(k_long_sp<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn));
   cudaFuncSetAttribute(k_long_sp<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sw));
   int per_sm = 0, pn = 0, pw = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_long_pieces<true>, kLpWarps * 32, sn);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_long_sp<true, false>, kLpWarps * 32, sn);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pn, k_long_sp<true, true>, kLpWarps * 32, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pw, k_long_sp<false, true>, kLpWarps * 32, 0);
   per_sm = per_sm > 0 ? per_sm : 1;
