@@ -23,7 +23,7 @@ constexpr int kTilesPerTicket = 4;  // k_pieces: consecutive tiles per ticket
 #define BBPE_LP_WARPS 4
 #endif
 #ifndef BBPE_LP_MINB
-#define BBPE_LP_MINB 6
+#define BBPE_LP_MINB 4
 #endif
 #ifndef BBPE_LP_SMEM
 #define BBPE_LP_SMEM 8192

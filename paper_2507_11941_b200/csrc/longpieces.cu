@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(kLpWarps * 32, 3) k_long_pieces(EncodeArgs a, 
 // the other's prefetch buffers, and give PIPE its own residency: no shared
 // working set, so BBPE_PIPE_MINB CTAs per SM (5: 20 warps, 96 registers,
 // phases B/C unrolled 2 segments deep); the shared-memory instance runs
-// kLpMinBlocks (6: 24 warps, 80 registers, 8 KB slices).
+// kLpMinBlocks (4: 16 warps, 128 registers, 8 KB slices).
 #ifndef BBPE_PIPE_MIN_SEGS
 #define BBPE_PIPE_MIN_SEGS 1
 #endif

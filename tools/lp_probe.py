@@ -1,5 +1,5 @@
 """Long-piece tier probe for ncu: one workload encoded `reps` times on the
-device (digits | runs_a | cfg4t | cfg4w | mixed4w | cfg2 | mixed | block2).  python tools/lp_probe.py digits 3"""
+device (digits | runs_a | cfg4t | cfg4w | mixed4w | cfg2 | mixed | block1 | block2).  python tools/lp_probe.py digits 3"""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -13,11 +13,11 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 rng = np.random.default_rng(7)
 N = 256 << 20
 engine = "pieces"
-if case in ("cfg2", "mixed", "block2"):
+if case in ("cfg2", "mixed", "block2", "block1"):
     t = bb.load_merge_table_files(WT.GPT2_VOCAB, WT.GPT2_MERGES, "gpt2")
     gen = WX.make_gen("mixed" if case == "mixed" else "zipf", WT.gpt2_table()[0])
-    data, off, _ = WX.config_rows(gen, 2, seed=2000)
-    engine = "block" if case == "block2" else "pieces"
+    data, off, _ = WX.config_rows(gen, 1 if case == "block1" else 2, seed=2000)
+    engine = "block" if case.startswith("block") else "pieces"
 elif case in ("cfg4w", "mixed4w"):  # the word-level 200k table (wide keys): zipf / mixed text
     tokens, m = WT.extend_wordlevel(*WT.gpt2_table(), 200000)
     t = bb.MergeTable.from_arrays(*WT.arrays(tokens, m))
