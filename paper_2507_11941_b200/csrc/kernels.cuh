@@ -18,7 +18,10 @@ constexpr int kWin = kTile + kLmax + 1;  // window positions [0, kWin) after b0
 constexpr int kStage = kTile + kLmax;  // staging slots per tile (short-piece tokens)
 constexpr int kScanTilesPerCta = 4096;  // k_tile_scan: 512 threads x 8 tiles
 constexpr int kWarpsPerCta = 8;
-constexpr int kTilesPerTicket = 4;  // k_pieces: consecutive tiles per ticket
+#ifndef BBPE_TILES_PER_TICKET
+#define BBPE_TILES_PER_TICKET 4
+#endif
+constexpr int kTilesPerTicket = BBPE_TILES_PER_TICKET;  // k_pieces: consecutive tiles per ticket
 #ifndef BBPE_LP_WARPS
 #define BBPE_LP_WARPS 4
 #endif
